@@ -1,0 +1,410 @@
+"""Benchmark: PIPECG iterations/s and HBM GB/s vs roofline on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config 3d7-256] [--no-north-star] [--no-e2e]
+
+A *step* is one PIPECG iteration (solvers.py:346-372) over the whole
+problem.  Workload (BASELINE.json configs[1]): 3D 7-point Poisson 256^3
+(N = 16,777,216, nnz = 117,047,296), manufactured solution x = 1/sqrt(N),
+b = A x, x0 = 0, Jacobi, fp64.  The matrix is generated in HBM.  Inputs
+(4.4 GB/iteration) are far larger than the 126 MB L2, so no L2 flush is
+needed between iterations.
+
+JSON line fields (rank 0):
+  value        iterations/s over exactly K timed iterations (CUDA events on
+               the solver stream, inputs resident in HBM), max over ranks
+  roofline     canonical bytes/iteration B = 176N + 12nnz + 4(N+1)
+                / measured iteration time, vs the measured
+               HBM copy peak (MEASURED_PEAKS.json)
+  e2e          the reference-facing call pipecg_solve(A_host, b, x0, pc, cfg)
+               with HOST numpy inputs, uploads and the x download inside the
+               timed region, solved to the recipe tolerance: iterations /
+               wall seconds
+  cpu_baseline the oracle port (oracle/, the reference's algorithm in C)
+               timed on this box's host cores on a bounded sample
+  north_star   the headline 3D 7-pt 400^3 (64M rows) iteration rate
+  clocks       NVML samples during the timed region
+--impl reference: the oracle port on all host threads, same config/metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "PIPECG iters/sec & HBM GB/s vs roofline at 1/2/4/8 B200, 3D Poisson"
+UNIT = "iterations/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="3d7-256")
+    ap.add_argument("--no-north-star", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def parse_config(cfg: str):
+    kind, n = cfg.split("-")
+    return kind, int(n)
+
+
+def canonical_bytes(N: int, nnz: int) -> int:
+    """22 fp64 vector streams + int32 CSR (int64 rowptr past 2^31)."""
+    rp = 8 if nnz >= 2**31 else 4
+    return 176 * N + 12 * nnz + rp * (N + 1)
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """NVML SM-clock / throttle-reason sampling during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int = 0, period: float = 0.005):
+        self.ok = False
+        self.samples = []
+        self.reasons = 0
+        self.period = period
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - informational only
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._stop = threading.Event()
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        s = sorted(self.samples)
+        med = s[len(s) // 2] if s else None
+        reasons = [name for bit, name in self.REASONS.items() if self.reasons & bit and bit != 0x1]
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(s)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle port) -- checker code, used here only as the baseline
+# ---------------------------------------------------------------------------
+def cpu_baseline(kind: str, n: int, seconds: float, warmup: int = 1, steps: int | None = None):
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle
+
+    oracle.build()
+    threads = os.cpu_count() or 1
+    oracle.set_threads(threads)
+    A = oracle.stencil(kind, n)
+    x_true, b, x0, d = oracle.manufactured(A)
+    st = oracle.Stepper(A, b, d)
+    st.steps(max(warmup, 1))
+    t0 = time.perf_counter()
+    done = 0
+    if steps is not None:
+        per = []
+        for _ in range(steps):
+            t1 = time.perf_counter()
+            st.steps(1)
+            per.append(time.perf_counter() - t1)
+            done += 1
+        dt = sum(per)
+    else:
+        while time.perf_counter() - t0 < seconds or done < 2:
+            st.steps(1)
+            done += 1
+        dt = time.perf_counter() - t0
+    st.close()
+    oracle.set_threads(1)
+    return {
+        "value": done / dt, "unit": UNIT, "cores": threads, "kind": "port",
+        "sample": f"oracle/pipecg_oracle.c (reference algorithm, kernels.py/solvers.py restated "
+                  f"in C, -ffp-contract=off) {kind} n={n}: {done} full PIPECG iterations after "
+                  f"pipecg_init, {threads} pthreads (row-parallel SpMV/update, chunked dots)",
+        "seconds": dt, "iterations": done,
+    }
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    kind, n = parse_config(args.config)
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle
+
+    oracle.build()
+    threads = os.cpu_count() or 1
+    oracle.set_threads(threads)
+    A = oracle.stencil(kind, n)
+    x_true, b, x0, d = oracle.manufactured(A)
+    st = oracle.Stepper(A, b, d)
+    st.steps(args.warmup)
+    t0 = time.perf_counter()
+    st.steps(args.steps)
+    dt = time.perf_counter() - t0
+    st.close()
+    N, nnz = A.n_rows, A.nnz
+    v = args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (manufactured solution x=1/sqrt(N))",
+        "config": {"workload": f"{kind} Poisson n={n} (N={N}, nnz={nnz}), Jacobi PIPECG fp64",
+                   "N": N, "nnz": nnz},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} full PIPECG iterations of {kind} n={n} after "
+                                   f"{args.warmup} warm-up iterations; oracle/pipecg_oracle.c "
+                                   f"on {threads} host threads"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def problem_device(pb, torch, kind, n, row_begin=0, row_end=None):
+    A = pb.stencil_device(kind, n, row_begin, row_end)
+    return A
+
+
+def time_iterations(pb, torch, A, pc_d, warmup: int, steps: int, options=None):
+    """Exactly `steps` PIPECG iterations timed with CUDA events on the solver
+    stream (tolerance 0: the stop test never fires, every iteration runs)."""
+    N = A.n_rows
+    x_true = torch.full((N,), 1.0 / math.sqrt(N), dtype=torch.float64, device="cuda")
+    b = pb.spmv(A, x_true)
+    x0 = torch.zeros_like(b)
+    solver = pb.PipecgSolver(A, pc_d, options or pb.DeviceOptions())
+    solver.init(b, x0, 0.0, warmup + steps + 1, 0)
+    solver.enqueue(warmup)
+    torch.cuda.synchronize()
+    stream = torch.cuda.ExternalStream(solver.stream)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    solver.enqueue(steps)
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    res = solver.poll()
+    ok = res.status == 0 and res.iterations == warmup + steps
+    info = {"engine": res.engine, "graph_launches": res.graph_launches, "ok": bool(ok),
+            "status": res.status, "iterations_run": res.iterations}
+    solver.close()
+    del b, x0, x_true
+    return ms, info
+
+
+def time_to_solution(pb, torch, A, pc_d):
+    N = A.n_rows
+    x_true = torch.full((N,), 1.0 / math.sqrt(N), dtype=torch.float64, device="cuda")
+    b = pb.spmv(A, x_true)
+    u0 = pb.jacobi_apply(pb.JacobiPreconditioner(pc_d), b)
+    tol = 1e-8 * math.sqrt(pb.dot(u0, u0, mode="tree"))
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=20000)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    x, rep = pb.pipecg_solve(A, b, torch.zeros_like(b), pb.JacobiPreconditioner(pc_d), cfg)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    err = float((x - x_true).abs().max())
+    return {"iterations": rep.iterations, "converged": rep.converged, "seconds": dt,
+            "setup_s": rep.phase_times["setup"], "iterations_s": rep.phase_times["iterations"],
+            "tolerance": tol, "verify_inf_err": err}
+
+
+def e2e_host(pb, torch, kind, n, reps: int = 1):
+    """The reference-facing drop-in call with host numpy buffers."""
+    import numpy as np
+
+    Ad = pb.stencil_device(kind, n)
+    Ah = Ad.to_host()  # host int64/float64 arrays (reference layout)
+    N, nnz = Ah.n_rows, Ah.nnz
+    ro, ci, va = Ah.row_offsets, Ah.col_indices, Ah.values
+    del Ad
+    torch.cuda.empty_cache()
+    x_true = np.full(N, 1.0 / math.sqrt(N))
+    b = pb.spmv(Ah, x_true)
+    d = pb.jacobi_setup(Ah).inv_diag
+    u0 = d * b
+    tol = 1e-8 * math.sqrt(float(np.dot(u0, u0)))
+    del Ah
+    torch.cuda.empty_cache()
+    x0 = np.zeros(N)
+    total_it, total_s = 0, 0.0
+    for _ in range(reps):
+        # a fresh CsrMatrix each call: nothing cached on the device
+        A = pb.CsrMatrix.__new__(pb.CsrMatrix)
+        for k, v in (("n_rows", N), ("n_cols", N), ("row_offsets", ro), ("col_indices", ci),
+                     ("values", va)):
+            object.__setattr__(A, k, v)
+        pc = pb.JacobiPreconditioner(d)
+        cfg = pb.SolverConfig(tolerance=tol, max_iterations=20000)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        x, rep = pb.pipecg_solve(A, b, x0, pc, cfg)
+        dt = time.perf_counter() - t0
+        total_it += rep.iterations
+        total_s += dt
+        del A
+        torch.cuda.empty_cache()
+    h2d = 8 * (N + 1) + 16 * nnz + 3 * 8 * N
+    d2h = 8 * N
+    per_call_it = total_it / reps
+    return {"value": total_it / total_s, "unit": UNIT,
+            "h2d_bytes_per_step": int(h2d / per_call_it), "d2h_bytes_per_step": int(d2h / per_call_it),
+            "h2d_bytes_per_call": h2d, "d2h_bytes_per_call": d2h,
+            "iterations_per_call": per_call_it, "seconds_per_call": total_s / reps,
+            "call": "paper_2105_06176_b200.pipecg_solve(A host CsrMatrix int64, b, x0 numpy, "
+                    "JacobiPreconditioner(numpy), SolverConfig(tol=1e-8*norm0)) -> (x numpy, report)",
+            "host_memory": "pageable numpy (the reference's own arrays); CSR uploaded as int64 and "
+                           "narrowed to int32 on the device"}
+
+
+def run_b200(args):
+    import torch
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        from paper_2105_06176_b200 import distributed as dist_bench
+
+        return dist_bench.bench_main(args, METRIC, UNIT)
+    torch.cuda.set_device(local)
+    import paper_2105_06176_b200 as pb
+
+    kind, n = parse_config(args.config)
+    peak, peak_src = measured_peak()
+    A = problem_device(pb, torch, kind, n)
+    N, nnz = A.n_rows, A.nnz
+    pc = pb.jacobi_setup(A)
+    pc_d = pc.inv_diag
+    B = canonical_bytes(N, nnz)
+
+    # timed region: exactly K iterations
+    with ClockSampler(local) as clk:
+        ms, info = time_iterations(pb, torch, A, pc_d, args.warmup, args.steps)
+    t_iter = ms / 1e3 / args.steps
+    value = args.steps / (ms / 1e3)
+    achieved = B / t_iter / 1e9
+    chunk = 16
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: stencil matrix generated in HBM, manufactured solution x=1/sqrt(N)",
+        "config": {"workload": f"{kind} Poisson n={n} (N={N}, nnz={nnz}), Jacobi PIPECG fp64 "
+                               "(BASELINE.json configs[1])",
+                   "N": N, "nnz": nnz, "parallelism": "single GPU",
+                   "l2": "inputs (4.4 GB/iteration) >> 126 MB L2; no flush needed",
+                   "engine": {1: "fused", 2: "two-kernel"}.get(info["engine"], "?")},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "bytes_per_iteration": B,
+                     "bytes_formula": "176N + 12nnz + 4(N+1) (canonical, SURVEY.md §8(d))",
+                     "peak_source": peak_src,
+                     "frac_of_8TBs_spec": achieved / 8000.0,
+                     "kernel": "pipecg_fused_kernel (one launch per iteration)"},
+        "gpu_launches": args.steps + math.ceil(args.steps / chunk),
+        "timing_ok": info["ok"],
+        "clocks": clk.summary(),
+    }
+    del A
+    torch.cuda.empty_cache()
+    A = problem_device(pb, torch, kind, n)
+    tts = time_to_solution(pb, torch, A, pc_d)
+    line["time_to_solution"] = tts
+    del A
+    torch.cuda.empty_cache()
+    if not args.no_north_star:
+        try:
+            A4 = problem_device(pb, torch, "3d7", 400)
+            pc4 = pb.jacobi_setup(A4).inv_diag
+            ms4, info4 = time_iterations(pb, torch, A4, pc4, 3, 40)
+            B4 = canonical_bytes(A4.n_rows, A4.nnz)
+            t4 = ms4 / 1e3 / 40
+            line["north_star"] = {"workload": "3d7 Poisson n=400 (N=64,000,000, nnz=447,040,000)",
+                                  "iters_per_s": 1 / t4, "ms_per_iter": t4 * 1e3,
+                                  "achieved_gbs": B4 / t4 / 1e9, "frac": B4 / t4 / 1e9 / peak,
+                                  "target_frac": 0.75, "ok": info4["ok"]}
+            del A4, pc4
+            torch.cuda.empty_cache()
+        except Exception as e:  # report, do not hide
+            line["north_star"] = {"error": repr(e)}
+    if not args.no_e2e:
+        line["e2e"] = e2e_host(pb, torch, kind, n)
+    if not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(kind, n, args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

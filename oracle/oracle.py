@@ -80,6 +80,13 @@ def lib():
         L.or_max_threads.restype = ctypes.c_int
         L.or_gen_csr.argtypes = [ctypes.c_int, ctypes.c_int64, _p_i64, _p_i64, _p_f64]
         L.or_gen_csr.restype = ctypes.c_int
+        L.or_stepper_begin.argtypes = [ctypes.c_int64, _p_i64, _p_i64, _p_f64, _p_f64, _p_f64]
+        L.or_stepper_begin.restype = ctypes.c_void_p
+        L.or_stepper_steps.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+        L.or_stepper_steps.restype = ctypes.c_int
+        L.or_stepper_norm.argtypes = [ctypes.c_void_p]
+        L.or_stepper_norm.restype = ctypes.c_double
+        L.or_stepper_end.argtypes = [ctypes.c_void_p]
         _lib = L
     return _lib
 
@@ -308,6 +315,36 @@ def history_gap(h_test, h_ref) -> float:
     a = np.asarray(h_test[:k])
     r = np.asarray(h_ref[:k])
     return float(np.max(np.abs(a - r)) / h_ref[0]) if k else 0.0
+
+
+class Stepper:
+    """pipecg_init once, then fixed-count iterations (CPU baseline timing only)."""
+
+    def __init__(self, A, b, inv_diag):
+        self.A = as_csr(A)
+        self.b = _f64(b)
+        self.d = _f64(inv_diag)
+        self.h = lib().or_stepper_begin(
+            self.A.n_rows, _ptr(self.A.row_offsets, _p_i64), _ptr(self.A.col_indices, _p_i64),
+            _ptr(self.A.values), _ptr(self.b), _ptr(self.d))
+        if not self.h:
+            raise MemoryError("oracle stepper allocation failed")
+
+    def steps(self, count: int) -> None:
+        rc = lib().or_stepper_steps(self.h, int(count))
+        if rc:
+            raise RuntimeError(f"oracle breakdown {BREAKDOWN_NAMES.get(rc, rc)}")
+
+    def norm(self) -> float:
+        return float(lib().or_stepper_norm(self.h))
+
+    def close(self):
+        if self.h:
+            lib().or_stepper_end(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
 
 
 def lib_path() -> str:

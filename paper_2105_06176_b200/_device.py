@@ -1,0 +1,67 @@
+"""Device plumbing: torch CUDA tensors as the memory of the C-ABI kernels.
+
+PyTorch is used only for device memory, streams and host<->device copies;
+all arithmetic on the solve path runs in the sm_100a kernels of
+``_lib/libpipecg_b200.so``.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+_F64 = torch.float64
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "paper_2105_06176_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback"
+        )
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def is_device_tensor(v) -> bool:
+    return isinstance(v, torch.Tensor) and v.is_cuda
+
+
+def host_f64(v) -> np.ndarray:
+    """Reference coercion (kernels.py:145-149): contiguous float64 ndarray."""
+    if isinstance(v, torch.Tensor):
+        v = v.detach().cpu().numpy()
+    return np.ascontiguousarray(v, dtype=np.float64)
+
+
+def to_device_f64(v, pad: int = 0) -> torch.Tensor:
+    """Copy a host vector (or reuse a CUDA float64 tensor) on the device."""
+    dev = require_cuda()
+    if is_device_tensor(v):
+        t = v if v.dtype == _F64 else v.to(_F64)
+        t = t.contiguous()
+        if pad:
+            out = torch.zeros(t.numel() + pad, dtype=_F64, device=t.device)
+            out[: t.numel()].copy_(t)
+            return out
+        return t
+    a = host_f64(v).reshape(-1)
+    out = torch.empty(a.size + pad, dtype=_F64, device=dev)
+    if pad:
+        out[a.size:].zero_()
+    if a.size:
+        out[: a.size].copy_(torch.from_numpy(a), non_blocking=False)
+    return out
+
+
+def vec_len(v) -> int:
+    if isinstance(v, torch.Tensor):
+        return v.numel() if v.dim() == 1 else -1
+    a = np.asarray(v)
+    return a.size if a.ndim == 1 else -1

@@ -1,0 +1,141 @@
+// common.cuh -- device helpers shared by the PIPECG sm_100a kernels.
+//
+// Everything here is plain CUDA C++ plus inline PTX for the Blackwell
+// asynchronous bulk-copy engine (cp.async.bulk -> SASS UBLKCP) and mbarriers.
+// The whole library is compiled with -fmad=false: the reference's numba
+// kernels contain no FMA, and every elementwise /
+// per-row result must round exactly like kernels.py:64-111.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define PCG_WARP 32
+
+namespace pcg {
+
+// ----------------------------------------------------------------------------
+// cache-hinted global accesses
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ double ldg_nc(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ldg_nc(const int* p) {
+  int v;
+  asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ long long ldg_nc(const long long* p) {
+  long long v;
+  asm volatile("ld.global.nc.s64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+// streaming load (read once this iteration): evict-first in L1/L2
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.cs.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_stream(double* p, double v) {
+  asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+// ----------------------------------------------------------------------------
+// exact-rounding arithmetic (belt and braces on top of -fmad=false)
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+
+// ----------------------------------------------------------------------------
+// shared-memory addressing, mbarrier and bulk copy (TMA engine, 1-D)
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "PCG_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra PCG_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0,
+// both addresses 16-byte aligned).  L2 policy: evict_first for streams that
+// are read exactly once per iteration.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// ----------------------------------------------------------------------------
+// deterministic reductions (fixed shuffle tree, fixed smem order)
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v = add(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Sum NV values over the NT threads [first, first+NT) of a block (NT % 32 ==
+// 0).  `red` needs NV*NT/32 doubles.  Every participating thread gets the
+// result.  Uses named barrier `bar_id`.  Order is fixed -> deterministic.
+template <int NV, int NT>
+__device__ __forceinline__ void group_sum(double (&v)[NV], int lt, double* red, int bar_id) {
+  constexpr int NW = NT / PCG_WARP;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
+  const int w = lt / PCG_WARP, lane = lt % PCG_WARP;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) red[k * NW + w] = v[k];
+  }
+  bar_sync(bar_id, NT);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < NW; ++j) s = add(s, red[k * NW + j]);
+    v[k] = s;
+  }
+  bar_sync(bar_id, NT);  // red may be reused right after
+}
+
+__host__ __device__ __forceinline__ int64_t round_up(int64_t a, int64_t b) {
+  return (a + b - 1) / b * b;
+}
+
+}  // namespace pcg

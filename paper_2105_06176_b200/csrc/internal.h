@@ -1,0 +1,30 @@
+// internal.h -- declarations shared by the translation units of the library.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pcg {
+
+constexpr int kNumSMs = 148;               // B200
+constexpr int kDotGrid = 4 * kNumSMs;      // fixed grid for deterministic dots
+constexpr int64_t kGridCap = 64 * kNumSMs; // grid-stride cap for row kernels
+constexpr int64_t kLongRow = 256;          // rows longer than this use the block path
+
+int set_error(int code, const char* what);
+int cuda_status(cudaError_t e, const char* where);
+
+inline unsigned elementwise_grid(int64_t n) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > kGridCap) blocks = kGridCap;
+  if (blocks < 1) blocks = 1;
+  return (unsigned)blocks;
+}
+
+int spmv_any(int64_t n_rows, int rp64, const void* rowptr, const int* col, const double* val,
+             const double* x, const double* b, double* y, const int* long_rows, int64_t n_long,
+             int mode, cudaStream_t st);
+int dots_any(int64_t n, int npairs, const double* const* a, const double* const* b, int mode,
+             double* out, double* workspace, cudaStream_t st);
+
+}  // namespace pcg

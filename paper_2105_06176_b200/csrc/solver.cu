@@ -1,0 +1,1255 @@
+// solver.cu -- the PIPECG iteration on B200 (solvers.py:297-387).
+//
+// Two engines share one device-side control block (Ctrl) and one prologue:
+//
+//  Engine 1 ("fused", the hot path): ONE persistent kernel per iteration.
+//    Iteration `it` of the reference does
+//        scalars(it) -> fused update -> 3 dots -> guards -> m = M^-1 w -> n = A m
+//    and iteration it+1 consumes n and m.  Kernel F(it) therefore computes,
+//    per row i, n_i = sum_k a_ik * (dinv[c_k] * w_old[c_k]) on the fly from
+//    the *previous* w (ping-pong buffers, so neighbours' w is never
+//    overwritten in flight), m_i = dinv_i * w_old_i, and then the eight
+//    recurrences and the three dot partials.  m and n never touch HBM:
+//    17 vector streams + CSR per iteration instead of the canonical 22.
+//    Every rounding matches the reference (mul/add separately, CSR order).
+//    CSR tiles and the 7 streamed vectors are staged into shared memory by
+//    the bulk-copy (TMA) engine from a producer warp, S-stage mbarrier ring.
+//
+//  Engine 2 ("two-kernel", general matrices, e.g. hub rows): K1 = fused
+//    update + Jacobi + dot partials, K2 = SpMV n = A m (thread-per-row for
+//    rows <= 256 nnz, block-per-row tree for longer rows).
+//
+// Control: no host synchronisation per iteration.  Each kernel reads the
+// iteration index from Ctrl (base + graph step), re-derives gamma, delta and
+// norm from the previous kernel's block partials in a fixed order (every
+// block computes identical values), applies the reference's guards and stop
+// test in the reference's order, and block 0 records history / status.
+// Kernels after a stop are no-ops.  Iterations are launched as CUDA-graph
+// chunks; the host reads one small record per chunk while the next chunk
+// is already queued.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <vector>
+
+#include "../../include/pipecg_b200.h"
+#include "common.cuh"
+#include "internal.h"
+
+namespace pcg {
+
+constexpr int kHistRing = 1024;  // history / drift ring (power of two)
+constexpr int kMaxChunk = 256;   // 2*kMaxChunk <= kHistRing
+
+struct Slot {
+  double gamma, delta, alpha, norm;
+};
+
+struct Ctrl {
+  // solve constants (set by init)
+  double tol;
+  long long max_it;
+  long long drift_k;
+  double b_norm;
+  Slot init;  // gamma0, delta0, -, norm0
+  // progress
+  long long base_it;
+  int status;
+  int bd_code;
+  long long bd_it;
+  double bd_val;
+  long long final_it;
+  double final_norm;
+  Slot slot[2];
+  double pad_[4];
+};
+static_assert(sizeof(Ctrl) <= 256, "Ctrl must fit its 256-byte record slot");
+
+// host-visible record = Ctrl | hist ring | drift-value ring | drift-it ring
+constexpr size_t kRecCtrl = 256;
+constexpr size_t kRecBytes = kRecCtrl + 3 * kHistRing * sizeof(double);
+
+struct Record {
+  Ctrl* C;
+  double* hist;
+  double* dval;
+  long long* dit;
+};
+
+__host__ __device__ inline Record record_at(char* base) {
+  Record r;
+  r.C = reinterpret_cast<Ctrl*>(base);
+  r.hist = reinterpret_cast<double*>(base + kRecCtrl);
+  r.dval = r.hist + kHistRing;
+  r.dit = reinterpret_cast<long long*>(r.dval + kHistRing);
+  return r;
+}
+
+struct Step {
+  int go;
+  double alpha, beta;
+};
+
+__device__ __forceinline__ int read_status(const Ctrl* C) {
+  return *reinterpret_cast<const volatile int*>(&C->status);
+}
+
+// The reference's loop head + tail, solvers.py:346-372, for iteration `it`.
+// NT threads (local id lt) participate; `leader` is one thread of block 0.
+template <int NT>
+__device__ Step prologue(Ctrl* C, double* hist, const double* partials, int n_partials,
+                         long long it, int lt, double* red, int bar_id, bool leader) {
+  Step st{0, 0.0, 0.0};
+  double gamma, delta, norm, gamma_prev = 0.0, alpha_prev = 0.0;
+  if (it == 0) {
+    gamma = C->init.gamma;
+    delta = C->init.delta;
+    norm = C->init.norm;
+  } else {
+    const double* P = partials + (size_t)((it - 1) & 1) * (size_t)n_partials * 4;
+    double v[3] = {0.0, 0.0, 0.0};
+    for (int j = lt; j < n_partials; j += NT) {
+      v[0] = add(v[0], P[j * 4 + 0]);
+      v[1] = add(v[1], P[j * 4 + 1]);
+      v[2] = add(v[2], P[j * 4 + 2]);
+    }
+    group_sum<3, NT>(v, lt, red, bar_id);
+    gamma = v[0];
+    delta = v[1];
+    norm = sqrt(v[2]);
+    const Slot prev = C->slot[(it - 1) & 1];
+    gamma_prev = prev.gamma;
+    alpha_prev = prev.alpha;
+    // solvers.py:354-357 (iteration it-1's guards)
+    if (gamma < 0.0 || !isfinite(gamma)) {
+      if (leader) {
+        C->bd_code = PCG_BD_GAMMA;
+        C->bd_it = it - 1;
+        C->bd_val = gamma;
+        C->status = PCG_BREAKDOWN;
+      }
+      return st;
+    }
+    if (!isfinite(delta)) {
+      if (leader) {
+        C->bd_code = PCG_BD_DELTA;
+        C->bd_it = it - 1;
+        C->bd_val = delta;
+        C->status = PCG_BREAKDOWN;
+      }
+      return st;
+    }
+    if (leader) hist[it & (kHistRing - 1)] = norm;  // solvers.py:369-370
+  }
+  // solvers.py:346 loop condition (NaN norm exits unconverged)
+  if (!(norm >= C->tol && it < C->max_it)) {
+    if (leader) {
+      C->final_it = it;
+      C->final_norm = norm;
+      C->status = PCG_STOPPED;
+    }
+    return st;
+  }
+  // solvers.py:276-294 pipecg_scalars
+  double beta, denom;
+  if (it == 0) {
+    beta = 0.0;
+    denom = delta;
+  } else {
+    beta = gamma / gamma_prev;
+    denom = sub(delta, mul(beta, gamma) / alpha_prev);
+  }
+  if (denom == 0.0 || !isfinite(denom)) {
+    if (leader) {
+      C->bd_code = PCG_BD_ALPHA;
+      C->bd_it = it;
+      C->bd_val = denom;
+      C->status = PCG_BREAKDOWN;
+    }
+    return st;
+  }
+  const double alpha = gamma / denom;
+  if (leader) C->slot[it & 1] = Slot{gamma, delta, alpha, norm};
+  st.go = 1;
+  st.alpha = alpha;
+  st.beta = beta;
+  return st;
+}
+
+// ===========================================================================
+// Engine 1: fused iteration kernel
+// ===========================================================================
+template <typename RP>
+struct FusedParams {
+  long long n;
+  long long n_tiles;
+  const RP* rp;
+  const int* col;
+  const double* val;
+  const double* dinv;
+  double* vec[7];  // z q s p x r u (in place)
+  double* w[2];    // ping-pong: read w[it&1], write w[(it+1)&1]
+  Ctrl* C;
+  double* hist;
+  double* partials;  // [2][n_partials][4]
+  int n_partials;
+  int stages;
+  int cap_val;  // doubles per stage
+  int cap_col;  // ints per stage
+};
+
+template <typename RP, int TR>
+struct FusedLayout {
+  static constexpr int kRpBytes = (int)(((TR + 1) * sizeof(RP) + 15) / 16 * 16);
+  static constexpr int kVecBytes = TR * 8;
+  __host__ __device__ static int stage_bytes(int cap_val, int cap_col) {
+    return kRpBytes + 7 * kVecBytes + cap_val * 8 + (cap_col * 4 + 15) / 16 * 16;
+  }
+  // barriers + reduction scratch + decision, in front of the stages
+  static constexpr int kHeader = 1024;
+};
+
+template <typename RP, int TR>
+__global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel(FusedParams<RP> P, int step) {
+  using L = FusedLayout<RP, TR>;
+  constexpr int NT = TR;  // consumer threads
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);       // [stages]
+  uint64_t* empty = full + 8;                                // [stages]
+  double* red = reinterpret_cast<double*>(smem + 256);       // 3*8 (+)
+  volatile int* decision = reinterpret_cast<volatile int*>(smem + 512);
+  double* sc = reinterpret_cast<double*>(smem + 768);        // alpha, beta
+  unsigned char* stage0 = smem + L::kHeader;
+  const int SB = L::stage_bytes(P.cap_val, P.cap_col);
+  const int S = P.stages;
+
+  Ctrl* C = P.C;
+  if (read_status(C) != PCG_RUNNING) return;
+  const long long it = C->base_it + step;
+  const double* w_old = P.w[it & 1];
+  double* w_new = P.w[(it + 1) & 1];
+
+  const int tid = threadIdx.x;
+  const bool producer = tid < 32;
+  const long long my_tiles =
+      blockIdx.x < P.n_tiles ? (P.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NT / 32);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  // ---- producer: stage tile j of this block into stage j % S -------------
+  uint64_t pol = 0;
+  auto issue = [&](long long j) {
+    const int s = (int)(j % S);
+    const long long t = blockIdx.x + j * gridDim.x;
+    const long long t0 = t * TR;
+    const long long rows = min((long long)TR, P.n - t0);
+    const long long e0 = P.rp[t0], e1 = P.rp[t0 + rows];
+    const long long cb = e0 & ~3LL, ce = (e1 + 3) & ~3LL;
+    const long long vb = e0 & ~1LL, ve = (e1 + 1) & ~1LL;
+    const uint32_t b_rp = (uint32_t)((((rows + 1) * sizeof(RP)) + 15) / 16 * 16);
+    const uint32_t b_vec = (uint32_t)((rows * 8 + 15) / 16 * 16);
+    const uint32_t b_val = (uint32_t)((ve - vb) * 8);
+    const uint32_t b_col = (uint32_t)((ce - cb) * 4);
+    unsigned char* sb = stage0 + (size_t)s * SB;
+    mbar_arrive_expect_tx(&full[s], b_rp + 7 * b_vec + b_val + b_col);
+    bulk_g2s(sb, P.rp + t0, b_rp, &full[s], pol);
+#pragma unroll
+    for (int k = 0; k < 7; ++k)
+      bulk_g2s(sb + L::kRpBytes + k * L::kVecBytes, P.vec[k] + t0, b_vec, &full[s], pol);
+    unsigned char* sval = sb + L::kRpBytes + 7 * L::kVecBytes;
+    if (b_val) bulk_g2s(sval, P.val + vb, b_val, &full[s], pol);
+    if (b_col) bulk_g2s(sval + (size_t)P.cap_val * 8, P.col + cb, b_col, &full[s], pol);
+  };
+
+  if (producer && tid == 0) {
+    pol = policy_evict_first();
+    for (long long j = 0; j < my_tiles && j < S; ++j) issue(j);
+  }
+
+  // ---- prologue (consumers): entry scalars, guards, stop test ------------
+  if (!producer) {
+    const Step stp = prologue<NT>(C, P.hist, P.partials, P.n_partials, it, tid - 32, red, 1,
+                                  blockIdx.x == 0 && tid == 32);
+    if (tid == 32) {
+      sc[0] = stp.alpha;
+      sc[1] = stp.beta;
+      *decision = stp.go;
+    }
+  }
+  __syncthreads();
+  const int go = *decision;
+  if (!go) {
+    // drain the copies already in flight before the CTA retires
+    if (tid == 0)
+      for (long long j = 0; j < my_tiles && j < S; ++j) mbar_wait(&full[j], 0);
+    return;
+  }
+  const double alpha = sc[0], beta = sc[1];
+
+  if (producer) {
+    if (tid == 0) {
+      for (long long j = S; j < my_tiles; ++j) {
+        const int s = (int)(j % S);
+        mbar_wait(&empty[s], (uint32_t)((j / S - 1) & 1));
+        issue(j);
+      }
+    }
+    return;
+  }
+
+  // ---- consumers ----------------------------------------------------------
+  const int lt = tid - 32;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (long long j = 0; j < my_tiles; ++j) {
+    const int s = (int)(j % S);
+    const long long t = blockIdx.x + j * gridDim.x;
+    const long long t0 = t * TR;
+    const long long rows = min((long long)TR, P.n - t0);
+    unsigned char* sb = stage0 + (size_t)s * SB;
+    const RP* rp_s = reinterpret_cast<const RP*>(sb);
+    const double* v_s = reinterpret_cast<const double*>(sb + L::kRpBytes);
+    const double* val_s = reinterpret_cast<const double*>(sb + L::kRpBytes + 7 * L::kVecBytes);
+    const int* col_s = reinterpret_cast<const int*>(val_s + P.cap_val);
+    const long long i = t0 + lt;
+    // own w / dinv: issue before waiting on the stage
+    double wi = 0.0, di = 0.0;
+    if (lt < rows) {
+      wi = ldg_nc(w_old + i);
+      di = ldg_nc(P.dinv + i);
+    }
+    mbar_wait(&full[s], (uint32_t)((j / S) & 1));
+    if (lt < rows) {
+      const long long e0 = rp_s[0];
+      const long long cb = e0 & ~3LL, vb = e0 & ~1LL;
+      const long long lo = rp_s[lt], hi = rp_s[lt + 1];
+      // n_i = sum_k a_ik * m_ck with m = M^-1 w_old, in CSR order.  Gathers
+      // of a batch of 8 entries are issued before the ordered accumulation.
+      double nacc = 0.0;
+      for (long long k0 = lo; k0 < hi; k0 += 8) {
+        double av[8], mv[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const long long k = k0 + t;
+          if (k < hi) {
+            const int c = col_s[k - cb];
+            av[t] = val_s[k - vb];
+            mv[t] = mul(ldg_nc(P.dinv + c), ldg_nc(w_old + c));  // m = M^-1 w
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if (k0 + t < hi) nacc = add(nacc, mul(av[t], mv[t]));  // n = A m
+      }
+      const double mi = mul(di, wi);
+      const double zi = add(nacc, mul(beta, v_s[0 * TR + lt]));
+      const double qi = add(mi, mul(beta, v_s[1 * TR + lt]));
+      const double si = add(wi, mul(beta, v_s[2 * TR + lt]));
+      const double ui = v_s[6 * TR + lt];
+      const double pi = add(ui, mul(beta, v_s[3 * TR + lt]));
+      const double xi = add(v_s[4 * TR + lt], mul(alpha, pi));
+      const double ri = sub(v_s[5 * TR + lt], mul(alpha, si));
+      const double un = sub(ui, mul(alpha, qi));
+      const double wn = sub(wi, mul(alpha, zi));
+      st_stream(P.vec[0] + i, zi);
+      st_stream(P.vec[1] + i, qi);
+      st_stream(P.vec[2] + i, si);
+      st_stream(P.vec[3] + i, pi);
+      st_stream(P.vec[4] + i, xi);
+      st_stream(P.vec[5] + i, ri);
+      st_stream(P.vec[6] + i, un);
+      st_stream(w_new + i, wn);
+      acc[0] = add(acc[0], mul(ri, un));
+      acc[1] = add(acc[1], mul(wn, un));
+      acc[2] = add(acc[2], mul(un, un));
+    }
+    __syncwarp();
+    if ((lt & 31) == 0) mbar_arrive(&empty[s]);
+  }
+  group_sum<3, NT>(acc, lt, red, 1);
+  if (lt == 0) {
+    double* out = P.partials + (size_t)(it & 1) * (size_t)P.n_partials * 4 + (size_t)blockIdx.x * 4;
+    out[0] = acc[0];
+    out[1] = acc[1];
+    out[2] = acc[2];
+    out[3] = 0.0;
+  }
+}
+
+// ===========================================================================
+// Engine 2: K1 (update + Jacobi + dot partials) and K2 (gated SpMV)
+// ===========================================================================
+struct TwoParams {
+  long long n;
+  double *z, *q, *s, *p, *x, *r, *u, *w, *m, *nv;
+  const double* dinv;
+  Ctrl* C;
+  double* hist;
+  double* partials;
+  int n_partials;
+};
+
+__global__ void __launch_bounds__(256) pipecg_k1_kernel(TwoParams P, int step) {
+  __shared__ double red[3 * 8];
+  Ctrl* C = P.C;
+  if (read_status(C) != PCG_RUNNING) return;
+  const long long it = C->base_it + step;
+  const Step stp = prologue<256>(C, P.hist, P.partials, P.n_partials, it, threadIdx.x, red, 1,
+                                 blockIdx.x == 0 && threadIdx.x == 0);
+  if (!stp.go) return;
+  const double alpha = stp.alpha, beta = stp.beta;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < P.n; i += (long long)gridDim.x * 256) {
+    const double zi = add(P.nv[i], mul(beta, P.z[i]));
+    const double qi = add(P.m[i], mul(beta, P.q[i]));
+    const double wi = P.w[i], ui = P.u[i];
+    const double si = add(wi, mul(beta, P.s[i]));
+    const double pi = add(ui, mul(beta, P.p[i]));
+    const double xi = add(P.x[i], mul(alpha, pi));
+    const double ri = sub(P.r[i], mul(alpha, si));
+    const double un = sub(ui, mul(alpha, qi));
+    const double wn = sub(wi, mul(alpha, zi));
+    P.z[i] = zi;
+    P.q[i] = qi;
+    P.s[i] = si;
+    P.p[i] = pi;
+    P.x[i] = xi;
+    P.r[i] = ri;
+    P.u[i] = un;
+    P.w[i] = wn;
+    P.m[i] = mul(P.dinv[i], wn);  // solvers.py:358
+    acc[0] = add(acc[0], mul(ri, un));
+    acc[1] = add(acc[1], mul(wn, un));
+    acc[2] = add(acc[2], mul(un, un));
+  }
+  group_sum<3, 256>(acc, threadIdx.x, red, 1);
+  if (threadIdx.x == 0) {
+    double* out = P.partials + (size_t)(it & 1) * (size_t)P.n_partials * 4 + (size_t)blockIdx.x * 4;
+    out[0] = acc[0];
+    out[1] = acc[1];
+    out[2] = acc[2];
+    out[3] = 0.0;
+  }
+}
+
+template <typename RP>
+__global__ void __launch_bounds__(256) gated_spmv_rows(const Ctrl* C, long long n, const RP* __restrict__ rp,
+                                                        const int* __restrict__ col,
+                                                        const double* __restrict__ val,
+                                                        const double* __restrict__ x,
+                                                        double* __restrict__ y, long long thr) {
+  if (read_status(C) != PCG_RUNNING) return;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+    const long long lo = rp[i], hi = rp[i + 1];
+    if (hi - lo > thr) continue;
+    double acc = 0.0;
+    for (long long k = lo; k < hi; ++k) acc = add(acc, mul(ldg_nc(val + k), ldg_nc(x + ldg_nc(col + k))));
+    y[i] = acc;
+  }
+}
+
+template <typename RP>
+__global__ void __launch_bounds__(256) gated_spmv_long(const Ctrl* C, const int* __restrict__ rows,
+                                                        const RP* __restrict__ rp,
+                                                        const int* __restrict__ col,
+                                                        const double* __restrict__ val,
+                                                        const double* __restrict__ x,
+                                                        double* __restrict__ y) {
+  __shared__ double red[8];
+  if (read_status(C) != PCG_RUNNING) return;
+  const long long i = rows[blockIdx.x];
+  const long long lo = rp[i], hi = rp[i + 1];
+  double v[1] = {0.0};
+  for (long long k = lo + threadIdx.x; k < hi; k += 256)
+    v[0] = add(v[0], mul(ldg_nc(val + k), ldg_nc(x + ldg_nc(col + k))));
+  group_sum<1, 256>(v, threadIdx.x, red, 1);
+  if (threadIdx.x == 0) y[i] = v[0];
+}
+
+// ===========================================================================
+// sequential-dot mode (bitwise reference order) and drift samples
+// ===========================================================================
+// After F(it)/K1(it): overwrite partial 0 with the three strictly sequential
+// dots; the next prologue then reduces exactly one partial.
+__global__ void __launch_bounds__(32) seq_dots_kernel(const Ctrl* C, long long n, const double* r,
+                                                       const double* u, const double* w0,
+                                                       const double* w1, int pingpong,
+                                                       double* partials, int n_partials, int step) {
+  constexpr int CH = 256;
+  __shared__ double prod[3][CH];
+  if (read_status(C) != PCG_RUNNING) return;
+  const long long it = C->base_it + step;
+  const double* w = pingpong ? (((it + 1) & 1) ? w1 : w0) : w0;
+  double acc[3] = {0.0, 0.0, 0.0};
+  const int lane = threadIdx.x;
+  for (long long base = 0; base < n; base += CH) {
+#pragma unroll
+    for (int j = 0; j < CH / 32; ++j) {
+      const long long i = base + j * 32 + lane;
+      const double ui = i < n ? u[i] : 0.0;
+      prod[0][j * 32 + lane] = i < n ? mul(r[i], ui) : 0.0;
+      prod[1][j * 32 + lane] = i < n ? mul(w[i], ui) : 0.0;
+      prod[2][j * 32 + lane] = i < n ? mul(ui, ui) : 0.0;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const int cnt = (int)((n - base) < CH ? (n - base) : CH);
+      for (int j = 0; j < cnt; ++j) {
+        acc[0] = add(acc[0], prod[0][j]);
+        acc[1] = add(acc[1], prod[1][j]);
+        acc[2] = add(acc[2], prod[2][j]);
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    double* out = partials + (size_t)(it & 1) * (size_t)n_partials * 4;
+    out[0] = acc[0];
+    out[1] = acc[1];
+    out[2] = acc[2];
+    out[3] = 0.0;
+  }
+}
+
+// drift (solvers.py:190-192): || (b - A x) - r || / ||b|| at entry of `it`
+template <typename RP>
+__global__ void __launch_bounds__(256) drift_partial_kernel(const Ctrl* C, int step, long long n,
+                                                             const RP* __restrict__ rp,
+                                                             const int* __restrict__ col,
+                                                             const double* __restrict__ val,
+                                                             const double* __restrict__ x,
+                                                             const double* __restrict__ b,
+                                                             const double* __restrict__ r,
+                                                             double* __restrict__ dpart) {
+  __shared__ double red[8];
+  if (read_status(C) != PCG_RUNNING) return;
+  const long long it = C->base_it + step;
+  if (it < 1 || C->drift_k <= 0 || it % C->drift_k != 0) return;
+  double v[1] = {0.0};
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+    double acc = 0.0;
+    for (long long k = rp[i]; k < rp[i + 1]; ++k) acc = add(acc, mul(val[k], x[col[k]]));
+    const double e = sub(sub(b[i], acc), r[i]);
+    v[0] = add(v[0], mul(e, e));
+  }
+  group_sum<1, 256>(v, threadIdx.x, red, 1);
+  if (threadIdx.x == 0) dpart[blockIdx.x] = v[0];
+}
+
+__global__ void __launch_bounds__(256) drift_finish_kernel(const Ctrl* C, int step, const double* dpart,
+                                                            int count, double* dval, long long* dit) {
+  __shared__ double red[8];
+  if (read_status(C) != PCG_RUNNING) return;
+  const long long it = C->base_it + step;
+  if (it < 1 || C->drift_k <= 0 || it % C->drift_k != 0) return;
+  double v[1] = {0.0};
+  for (int j = threadIdx.x; j < count; j += 256) v[0] = add(v[0], dpart[j]);
+  group_sum<1, 256>(v, threadIdx.x, red, 1);
+  if (threadIdx.x == 0) {
+    const double nn = sqrt(v[0]);
+    const double bn = C->b_norm;
+    dval[it & (kHistRing - 1)] = bn > 0 ? nn / bn : nn;
+    dit[it & (kHistRing - 1)] = it;
+  }
+}
+
+__global__ void advance_kernel(Ctrl* C, int k) {
+  if (threadIdx.x == 0) C->base_it += k;
+}
+
+// pipecg_init tail: read the four init dots, reset the control block
+__global__ void init_ctrl_kernel(Ctrl* C, const double* dots4, double tol, long long max_it,
+                                 long long drift_k, double* hist, long long* dit) {
+  if (threadIdx.x == 0) {
+    C->tol = tol;
+    C->max_it = max_it;
+    C->drift_k = drift_k;
+    C->b_norm = sqrt(dots4[3]);
+    C->init = Slot{dots4[0], dots4[1], 0.0, sqrt(dots4[2])};
+    C->base_it = 0;
+    C->status = PCG_RUNNING;
+    C->bd_code = PCG_BD_NONE;
+    C->bd_it = -1;
+    C->bd_val = 0.0;
+    C->final_it = -1;
+    C->final_norm = 0.0;
+    C->slot[0] = Slot{0, 0, 0, 0};
+    C->slot[1] = Slot{0, 0, 0, 0};
+    hist[0] = C->init.norm;
+  }
+  for (int j = threadIdx.x; j < kHistRing; j += blockDim.x) dit[j] = -1;
+}
+
+// block-wide max (one atomic per block: a single-address atomic per row
+// serialises ~10^7 updates in L2)
+__device__ __forceinline__ void block_max_atomic(unsigned long long v, unsigned long long* out) {
+  __shared__ unsigned long long sm[32];
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const unsigned long long t = __shfl_xor_sync(0xffffffffu, v, o);
+    v = t > v ? t : v;
+  }
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (lane == 0) sm[w] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long m = 0;
+    for (int j = 0; j < (int)(blockDim.x / 32); ++j) m = sm[j] > m ? sm[j] : m;
+    atomicMax(out, m);
+  }
+}
+
+// per-tile staged span (cols rounded to 4, vals rounded to 2)
+template <typename RP>
+__global__ void __launch_bounds__(256) tile_span_kernel(long long n, long long n_tiles, int tr,
+                                                         const RP* rp, unsigned long long* max_col,
+                                                         unsigned long long* max_val) {
+  unsigned long long mc = 0, mv = 0;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n_tiles;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long t0 = t * tr;
+    const long long rows = min((long long)tr, n - t0);
+    const long long e0 = rp[t0], e1 = rp[t0 + rows];
+    const unsigned long long c = (unsigned long long)(((e1 + 3) & ~3LL) - (e0 & ~3LL));
+    const unsigned long long v = (unsigned long long)(((e1 + 1) & ~1LL) - (e0 & ~1LL));
+    mc = c > mc ? c : mc;
+    mv = v > mv ? v : mv;
+  }
+  block_max_atomic(mc, max_col);
+  __syncthreads();
+  block_max_atomic(mv, max_val);
+}
+
+__global__ void __launch_bounds__(256) max_row_kernel(long long n, const void* rp, int rp64,
+                                                       unsigned long long* out) {
+  unsigned long long m = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long len = rp64 ? ((const long long*)rp)[i + 1] - ((const long long*)rp)[i]
+                         : (long long)(((const int*)rp)[i + 1] - ((const int*)rp)[i]);
+    m = (unsigned long long)len > m ? (unsigned long long)len : m;
+  }
+  block_max_atomic(m, out);
+}
+
+}  // namespace pcg
+
+using namespace pcg;
+
+// ===========================================================================
+// host runtime
+// ===========================================================================
+struct pcg_solver {
+  pcg_matrix A{};
+  pcg_options opt{};
+  int engine = 0;
+  int tr = 256;
+  int stages = 0;
+  int cap_val = 0, cap_col = 0;
+  size_t smem = 0;
+  int grid = 0;
+  int n_partials = 0;
+  int num_sms = 148;
+  long long n_tiles = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_rec[2] = {nullptr, nullptr};
+  double* vbuf = nullptr;
+  size_t ld = 0;  // padded vector length
+  double *z = nullptr, *q = nullptr, *s = nullptr, *p = nullptr, *x = nullptr, *r = nullptr,
+         *u = nullptr, *w[2] = {nullptr, nullptr}, *m = nullptr, *nv = nullptr, *b = nullptr;
+  double* partials = nullptr;
+  double* dpart = nullptr;
+  double* dots_ws = nullptr;
+  double* dots4 = nullptr;
+  char* rec_dev = nullptr;
+  char* rec_host[2] = {nullptr, nullptr};
+  int* long_rows = nullptr;
+  long long n_long = 0;
+  std::map<int, cudaGraphExec_t> graphs[2];
+  long long host_base = 0;  // iterations enqueued so far
+  bool initialized = false;
+  long long max_it = 0, drift_k = 0;
+  double tol = 0;
+  long long graph_launches = 0;
+  int rec_parity = 0;
+  bool mn_valid = false;
+};
+
+namespace {
+
+struct FusedPlan {
+  int tr = 0, stages = 0, bps = 0, cap_val = 0, cap_col = 0;
+  size_t smem = 0;
+};
+
+// Staged span of the widest tile of `tr` rows -> the shared-memory plan
+// (stages, CTAs/SM) for that tile height, or an empty plan if it cannot fit.
+template <typename RP, int TR>
+int plan_tr(pcg_solver* S, FusedPlan* plan) {
+  using L = FusedLayout<RP, TR>;
+  const long long n = S->A.n_rows;
+  const long long n_tiles = (n + TR - 1) / TR;
+  unsigned long long* mx = nullptr;
+  cudaError_t e = cudaMallocAsync(&mx, 2 * sizeof(unsigned long long), S->stream);
+  if (e != cudaSuccess) return cuda_status(e, "tile span alloc");
+  cudaMemsetAsync(mx, 0, 2 * sizeof(unsigned long long), S->stream);
+  tile_span_kernel<RP><<<elementwise_grid(n_tiles), 256, 0, S->stream>>>(
+      n, n_tiles, TR, static_cast<const RP*>(S->A.rowptr), mx, mx + 1);
+  unsigned long long h[2] = {0, 0};
+  cudaMemcpyAsync(h, mx, sizeof(h), cudaMemcpyDeviceToHost, S->stream);
+  cudaFreeAsync(mx, S->stream);
+  e = cudaStreamSynchronize(S->stream);
+  if (e != cudaSuccess) return cuda_status(e, "tile span");
+  FusedPlan p;
+  p.tr = TR;
+  p.cap_col = (int)std::max<unsigned long long>(h[0], 4);
+  p.cap_val = (int)((std::max<unsigned long long>(h[1], 2) + 1) & ~1ULL);
+  const size_t sb = (size_t)L::stage_bytes(p.cap_val, p.cap_col);
+  const size_t sm_budget = 228 * 1024, cta_max = 227 * 1024;
+  for (int bps = 2; bps >= 1 && !p.stages; --bps) {
+    for (int st = 4; st >= 2; --st) {
+      const size_t need = L::kHeader + st * sb;
+      if (need <= cta_max && (need + 1024) * bps <= sm_budget) {
+        p.stages = st;
+        p.bps = bps;
+        p.smem = need;
+        break;
+      }
+    }
+  }
+  *plan = p;
+  return PCG_OK;
+}
+
+template <typename RP, int TR>
+int finish_plan(pcg_solver* S, const FusedPlan& p) {
+  auto kfn = pipecg_fused_kernel<RP, TR>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+  if (e != cudaSuccess) return cuda_status(e, "fused smem attribute");
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, TR + 32, p.smem);
+  if (e != cudaSuccess) return cuda_status(e, "fused occupancy");
+  if (occ < 1) return PCG_EINVAL;
+  occ = std::min(occ, p.bps);
+  S->tr = TR;
+  S->n_tiles = (S->A.n_rows + TR - 1) / TR;
+  S->stages = p.stages;
+  S->cap_val = p.cap_val;
+  S->cap_col = p.cap_col;
+  S->smem = p.smem;
+  long long g = (long long)occ * S->num_sms;
+  if (g > S->n_tiles) g = S->n_tiles;
+  S->grid = (int)std::max<long long>(g, 1);
+  S->n_partials = S->grid;
+  return PCG_OK;
+}
+
+// Pick the tile height (256/128/64 rows) that keeps the most consumer
+// threads resident per SM with >= 2 bulk-copy stages; ties -> taller tiles.
+template <typename RP>
+int fused_setup(pcg_solver* S) {
+  FusedPlan p256, p128, p64;
+  int rc = plan_tr<RP, 256>(S, &p256);
+  if (!rc) rc = plan_tr<RP, 128>(S, &p128);
+  if (!rc) rc = plan_tr<RP, 64>(S, &p64);
+  if (rc) return rc;
+  const FusedPlan* best = nullptr;
+  int best_score = 0;
+  for (const FusedPlan* p : {&p256, &p128, &p64}) {
+    const int score = p->stages ? p->tr * p->bps : 0;
+    if (score > best_score) {
+      best = p;
+      best_score = score;
+    }
+  }
+  if (!best) return PCG_EINVAL;  // rows too wide for shared memory -> engine 2
+  if (best->tr == 256) return finish_plan<RP, 256>(S, *best);
+  if (best->tr == 128) return finish_plan<RP, 128>(S, *best);
+  return finish_plan<RP, 64>(S, *best);
+}
+
+int alloc_state(pcg_solver* S) {
+  const long long n = S->A.n_rows;
+  S->ld = (size_t)round_up(n + 32, 256);
+  const int nvec = 13;  // z q s p x r u w0 w1 m n b + spare
+  cudaError_t e = cudaMalloc(&S->vbuf, S->ld * nvec * sizeof(double));
+  if (e != cudaSuccess) return set_error(PCG_ENOMEM, "solver: vector allocation failed");
+  cudaMemsetAsync(S->vbuf, 0, S->ld * nvec * sizeof(double), S->stream);
+  double* v = S->vbuf;
+  S->z = v + 0 * S->ld;
+  S->q = v + 1 * S->ld;
+  S->s = v + 2 * S->ld;
+  S->p = v + 3 * S->ld;
+  S->x = v + 4 * S->ld;
+  S->r = v + 5 * S->ld;
+  S->u = v + 6 * S->ld;
+  S->w[0] = v + 7 * S->ld;
+  S->w[1] = v + 8 * S->ld;
+  S->m = v + 9 * S->ld;
+  S->nv = v + 10 * S->ld;
+  S->b = v + 11 * S->ld;
+  const int maxp = std::max(S->n_partials, 1);
+  e = cudaMalloc(&S->partials, (size_t)2 * maxp * 4 * sizeof(double));
+  if (e != cudaSuccess) return set_error(PCG_ENOMEM, "solver: partials allocation failed");
+  cudaMemsetAsync(S->partials, 0, (size_t)2 * maxp * 4 * sizeof(double), S->stream);
+  if (cudaMalloc(&S->dpart, kDotGrid * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&S->dots_ws, (size_t)kDotGrid * 4 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&S->dots4, 4 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&S->rec_dev, kRecBytes) != cudaSuccess)
+    return set_error(PCG_ENOMEM, "solver: workspace allocation failed");
+  cudaMemsetAsync(S->rec_dev, 0, kRecBytes, S->stream);
+  for (int k = 0; k < 2; ++k)
+    if (cudaMallocHost(&S->rec_host[k], kRecBytes) != cudaSuccess)
+      return set_error(PCG_ENOMEM, "solver: pinned record allocation failed");
+  return PCG_OK;
+}
+
+template <typename RP>
+FusedParams<RP> fused_params(pcg_solver* S) {
+  FusedParams<RP> P;
+  P.n = S->A.n_rows;
+  P.n_tiles = S->n_tiles;
+  P.rp = static_cast<const RP*>(S->A.rowptr);
+  P.col = S->A.col;
+  P.val = S->A.val;
+  P.dinv = S->A.inv_diag;
+  P.vec[0] = S->z;
+  P.vec[1] = S->q;
+  P.vec[2] = S->s;
+  P.vec[3] = S->p;
+  P.vec[4] = S->x;
+  P.vec[5] = S->r;
+  P.vec[6] = S->u;
+  P.w[0] = S->w[0];
+  P.w[1] = S->w[1];
+  Record R = record_at(S->rec_dev);
+  P.C = R.C;
+  P.hist = R.hist;
+  P.partials = S->partials;
+  P.n_partials = S->opt.dot_mode == PCG_DOT_SEQ ? 1 : S->n_partials;
+  P.stages = S->stages;
+  P.cap_val = S->cap_val;
+  P.cap_col = S->cap_col;
+  return P;
+}
+
+template <typename RP>
+void launch_fused(pcg_solver* S, int k) {
+  const FusedParams<RP> P = fused_params<RP>(S);
+  switch (S->tr) {
+    case 256: pipecg_fused_kernel<RP, 256><<<S->grid, 256 + 32, S->smem, S->stream>>>(P, k); break;
+    case 128: pipecg_fused_kernel<RP, 128><<<S->grid, 128 + 32, S->smem, S->stream>>>(P, k); break;
+    default: pipecg_fused_kernel<RP, 64><<<S->grid, 64 + 32, S->smem, S->stream>>>(P, k); break;
+  }
+}
+
+// enqueue graph step k (drift? -> iteration -> seq dots?)
+int enqueue_step(pcg_solver* S, int k) {
+  Record R = record_at(S->rec_dev);
+  cudaStream_t st = S->stream;
+  const long long n = S->A.n_rows;
+  if (S->drift_k > 0) {
+    if (S->A.rp64)
+      drift_partial_kernel<long long><<<kDotGrid, 256, 0, st>>>(
+          R.C, k, n, static_cast<const long long*>(S->A.rowptr), S->A.col, S->A.val, S->x, S->b,
+          S->r, S->dpart);
+    else
+      drift_partial_kernel<int><<<kDotGrid, 256, 0, st>>>(R.C, k, n,
+                                                           static_cast<const int*>(S->A.rowptr),
+                                                           S->A.col, S->A.val, S->x, S->b, S->r,
+                                                           S->dpart);
+    drift_finish_kernel<<<1, 256, 0, st>>>(R.C, k, S->dpart, kDotGrid, R.dval, R.dit);
+  }
+  if (S->engine == 1) {
+    if (S->A.rp64) launch_fused<long long>(S, k);
+    else launch_fused<int>(S, k);
+  } else {
+    TwoParams P;
+    P.n = n;
+    P.z = S->z; P.q = S->q; P.s = S->s; P.p = S->p; P.x = S->x;
+    P.r = S->r; P.u = S->u; P.w = S->w[0]; P.m = S->m; P.nv = S->nv;
+    P.dinv = S->A.inv_diag;
+    P.C = R.C;
+    P.hist = R.hist;
+    P.partials = S->partials;
+    P.n_partials = S->opt.dot_mode == PCG_DOT_SEQ ? 1 : S->n_partials;
+    pipecg_k1_kernel<<<S->grid, 256, 0, st>>>(P, k);
+  }
+  if (S->opt.dot_mode == PCG_DOT_SEQ)
+    seq_dots_kernel<<<1, 32, 0, st>>>(R.C, n, S->r, S->u, S->w[0], S->w[1], S->engine == 1,
+                                      S->partials, 1, k);
+  if (S->engine == 2) {
+    const long long thr = S->n_long > 0 ? kLongRow : INT64_MAX;
+    if (S->A.rp64) {
+      gated_spmv_rows<long long><<<elementwise_grid(n), 256, 0, st>>>(
+          R.C, n, static_cast<const long long*>(S->A.rowptr), S->A.col, S->A.val, S->m, S->nv, thr);
+      if (S->n_long > 0)
+        gated_spmv_long<long long><<<(unsigned)S->n_long, 256, 0, st>>>(
+            R.C, S->long_rows, static_cast<const long long*>(S->A.rowptr), S->A.col, S->A.val, S->m,
+            S->nv);
+    } else {
+      gated_spmv_rows<int><<<elementwise_grid(n), 256, 0, st>>>(
+          R.C, n, static_cast<const int*>(S->A.rowptr), S->A.col, S->A.val, S->m, S->nv, thr);
+      if (S->n_long > 0)
+        gated_spmv_long<int><<<(unsigned)S->n_long, 256, 0, st>>>(
+            R.C, S->long_rows, static_cast<const int*>(S->A.rowptr), S->A.col, S->A.val, S->m,
+            S->nv);
+    }
+  }
+  return PCG_OK;
+}
+
+int enqueue_chunk_body(pcg_solver* S, int K, int parity) {
+  for (int k = 0; k < K; ++k) enqueue_step(S, k);
+  advance_kernel<<<1, 32, 0, S->stream>>>(record_at(S->rec_dev).C, K);
+  cudaMemcpyAsync(S->rec_host[parity], S->rec_dev, kRecBytes, cudaMemcpyDeviceToHost, S->stream);
+  return cuda_status(cudaGetLastError(), "chunk launch");
+}
+
+int launch_chunk(pcg_solver* S, int K, int parity) {
+  S->host_base += K;
+  if (!S->opt.use_graphs) {
+    int rc = enqueue_chunk_body(S, K, parity);
+    if (rc) return rc;
+  } else {
+    auto it = S->graphs[parity].find(K);
+    cudaGraphExec_t exec = nullptr;
+    if (it == S->graphs[parity].end()) {
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamBeginCapture(S->stream, cudaStreamCaptureModeThreadLocal);
+      if (e != cudaSuccess) return cuda_status(e, "begin capture");
+      int rc = enqueue_chunk_body(S, K, parity);
+      e = cudaStreamEndCapture(S->stream, &g);
+      if (rc) return rc;
+      if (e != cudaSuccess) return cuda_status(e, "end capture");
+      e = cudaGraphInstantiate(&exec, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return cuda_status(e, "graph instantiate");
+      S->graphs[parity][K] = exec;
+    } else {
+      exec = it->second;
+    }
+    cudaError_t e = cudaGraphLaunch(exec, S->stream);
+    if (e != cudaSuccess) return cuda_status(e, "graph launch");
+    S->graph_launches++;
+  }
+  return cuda_status(cudaEventRecord(S->ev_rec[parity], S->stream), "record event");
+}
+
+int auto_chunk(pcg_solver* S) {
+  if (S->opt.chunk > 0) return std::min(S->opt.chunk, kMaxChunk);
+  // aim for ~2 ms of GPU work per chunk (HBM estimate at ~5 TB/s)
+  const double bytes = 136.0 * S->A.n_rows + 12.0 * S->A.nnz + 4.0 * S->A.n_rows;
+  const double t_iter = bytes / 5.0e12 + 4e-6;
+  int K = (int)(2e-3 / t_iter);
+  int p = 4;
+  while (p * 2 <= K && p < kMaxChunk) p *= 2;
+  return std::max(4, std::min(p, kMaxChunk));
+}
+
+void fill_result(pcg_solver* S, const Ctrl& c, pcg_result* res) {
+  res->status = c.status;
+  res->engine = S->engine;
+  res->graph_launches = S->graph_launches;
+  res->norm0 = c.init.norm;
+  res->breakdown_quantity = c.bd_code;
+  res->breakdown_iteration = c.bd_it;
+  res->breakdown_value = c.bd_val;
+  if (c.status == PCG_STOPPED) {
+    res->iterations = c.final_it;
+    res->final_norm = c.final_norm;
+    res->converged = c.final_norm < S->tol;
+  } else {
+    res->iterations = c.base_it;
+    res->final_norm = NAN;
+    res->converged = 0;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_solver** out) {
+  if (!A || !out || A->n_rows <= 0 || !A->rowptr || !A->inv_diag || (A->nnz > 0 && (!A->col || !A->val)))
+    return set_error(PCG_EINVAL, "solver_create: bad matrix");
+  if (A->n_rows >= (1LL << 31) || A->n_cols >= (1LL << 31))
+    return set_error(PCG_ERANGE, "solver_create: >= 2^31 rows per device; shard the matrix");
+  if (!A->rp64 && A->nnz >= (1LL << 31))
+    return set_error(PCG_ERANGE, "solver_create: nnz >= 2^31 needs int64 row pointers");
+  pcg_solver* S = new pcg_solver();
+  S->A = *A;
+  if (opts) S->opt = *opts;
+  else {
+    S->opt.dot_mode = PCG_DOT_TREE;
+    S->opt.engine = 0;
+    S->opt.chunk = 0;
+    S->opt.use_graphs = 1;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&S->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  int rc = cuda_status(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking), "stream");
+  if (!rc) rc = cuda_status(cudaEventCreateWithFlags(&S->ev_in, cudaEventDisableTiming), "event");
+  for (int k = 0; k < 2 && !rc; ++k)
+    rc = cuda_status(cudaEventCreateWithFlags(&S->ev_rec[k], cudaEventDisableTiming), "event");
+  if (rc) {
+    pipecg_b200_solver_destroy(S);
+    return rc;
+  }
+  // long rows (> kLongRow entries) -> engine 2 with the block-per-row path
+  unsigned long long* mx = nullptr;
+  cudaMallocAsync(&mx, sizeof(unsigned long long), S->stream);
+  cudaMemsetAsync(mx, 0, sizeof(unsigned long long), S->stream);
+  max_row_kernel<<<elementwise_grid(A->n_rows), 256, 0, S->stream>>>(A->n_rows, A->rowptr, A->rp64, mx);
+  unsigned long long max_row = 0;
+  cudaMemcpyAsync(&max_row, mx, sizeof(max_row), cudaMemcpyDeviceToHost, S->stream);
+  cudaFreeAsync(mx, S->stream);
+  rc = cuda_status(cudaStreamSynchronize(S->stream), "max row");
+  if (rc) {
+    pipecg_b200_solver_destroy(S);
+    return rc;
+  }
+  int engine = S->opt.engine;
+  if (engine == 0) engine = max_row > (unsigned long long)kLongRow ? 2 : 1;
+  if (engine == 1) {
+    rc = A->rp64 ? fused_setup<long long>(S) : fused_setup<int>(S);
+    if (rc == PCG_EINVAL && S->opt.engine == 0) engine = 2;  // too wide -> general engine
+    else if (rc) {
+      pipecg_b200_solver_destroy(S);
+      return rc == PCG_EINVAL ? set_error(rc, "fused engine: tiles exceed shared memory") : rc;
+    }
+  }
+  S->engine = engine;
+  if (engine == 2) {
+    S->grid = kDotGrid;
+    S->n_partials = kDotGrid;
+    if (max_row > (unsigned long long)kLongRow) {
+      int64_t cnt = 0;
+      // count first, then fill
+      rc = pipecg_b200_find_long_rows(A->n_rows, A->rp64, A->rowptr, kLongRow, nullptr, 0, &cnt,
+                                      S->stream);
+      if (!rc && cnt > 0) {
+        if (cudaMalloc(&S->long_rows, cnt * sizeof(int)) != cudaSuccess)
+          rc = set_error(PCG_ENOMEM, "long rows alloc");
+        else
+          rc = pipecg_b200_find_long_rows(A->n_rows, A->rp64, A->rowptr, kLongRow, S->long_rows,
+                                          cnt, &cnt, S->stream);
+        S->n_long = cnt;
+      }
+      if (rc) {
+        pipecg_b200_solver_destroy(S);
+        return rc;
+      }
+    }
+  }
+  rc = alloc_state(S);
+  if (rc) {
+    pipecg_b200_solver_destroy(S);
+    return rc;
+  }
+  *out = S;
+  return PCG_OK;
+}
+
+int pipecg_b200_solver_destroy(pcg_solver* S) {
+  if (!S) return PCG_OK;
+  if (S->stream) cudaStreamSynchronize(S->stream);
+  for (int k = 0; k < 2; ++k) {
+    for (auto& kv : S->graphs[k]) cudaGraphExecDestroy(kv.second);
+    if (S->rec_host[k]) cudaFreeHost(S->rec_host[k]);
+    if (S->ev_rec[k]) cudaEventDestroy(S->ev_rec[k]);
+  }
+  cudaFree(S->vbuf);
+  cudaFree(S->partials);
+  cudaFree(S->dpart);
+  cudaFree(S->dots_ws);
+  cudaFree(S->dots4);
+  cudaFree(S->rec_dev);
+  cudaFree(S->long_rows);
+  if (S->ev_in) cudaEventDestroy(S->ev_in);
+  if (S->stream) cudaStreamDestroy(S->stream);
+  delete S;
+  return PCG_OK;
+}
+
+int pipecg_b200_solver_init(pcg_solver* S, const double* b, const double* x0, double tolerance,
+                            int64_t max_iterations, int64_t drift_check_interval, void* stream) {
+  if (!S || !b || !x0) return set_error(PCG_EINVAL, "solver_init: bad arguments");
+  if (max_iterations < 1) return set_error(PCG_EINVAL, "solver_init: max_iterations < 1");
+  cudaStream_t st = S->stream;
+  cudaEventRecord(S->ev_in, (cudaStream_t)stream);
+  cudaStreamWaitEvent(st, S->ev_in, 0);
+  const long long n = S->A.n_rows;
+  const size_t bytes = (size_t)n * sizeof(double);
+  S->tol = tolerance;
+  S->max_it = max_iterations;
+  S->drift_k = drift_check_interval;
+  // solvers.py:305-321
+  cudaMemcpyAsync(S->b, b, bytes, cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyAsync(S->x, x0, bytes, cudaMemcpyDeviceToDevice, st);
+  int rc = spmv_any(n, S->A.rp64, S->A.rowptr, S->A.col, S->A.val, S->x, S->b, S->r,
+                    S->long_rows, S->n_long, 1, st);  // r = b - A x
+  if (rc) return rc;
+  rc = pipecg_b200_jacobi_apply(n, S->A.inv_diag, S->r, S->u, st);  // u = M^-1 r
+  if (rc) return rc;
+  rc = spmv_any(n, S->A.rp64, S->A.rowptr, S->A.col, S->A.val, S->u, nullptr, S->w[0],
+                S->long_rows, S->n_long, 0, st);  // w = A u
+  if (rc) return rc;
+  if (S->engine == 2) {
+    rc = pipecg_b200_jacobi_apply(n, S->A.inv_diag, S->w[0], S->m, st);  // m = M^-1 w
+    if (rc) return rc;
+    rc = spmv_any(n, S->A.rp64, S->A.rowptr, S->A.col, S->A.val, S->m, nullptr, S->nv,
+                  S->long_rows, S->n_long, 0, st);  // n = A m
+    if (rc) return rc;
+  }
+  S->mn_valid = S->engine == 2;
+  cudaMemsetAsync(S->z, 0, bytes, st);
+  cudaMemsetAsync(S->q, 0, bytes, st);
+  cudaMemsetAsync(S->s, 0, bytes, st);
+  cudaMemsetAsync(S->p, 0, bytes, st);
+  const double* da[4] = {S->r, S->w[0], S->u, S->b};
+  const double* db[4] = {S->u, S->u, S->u, S->b};
+  rc = dots_any(n, 4, da, db, S->opt.dot_mode, S->dots4, S->dots_ws, st);
+  if (rc) return rc;
+  Record R = record_at(S->rec_dev);
+  init_ctrl_kernel<<<1, 256, 0, st>>>(R.C, S->dots4, tolerance, max_iterations,
+                                      drift_check_interval, R.hist, R.dit);
+  S->host_base = 0;
+  S->initialized = true;
+  return cuda_status(cudaGetLastError(), "solver_init");
+}
+
+int pipecg_b200_solver_run(pcg_solver* S, pcg_result* res, double* history_host, int64_t hist_cap,
+                           int64_t* drift_it_host, double* drift_val_host, int64_t drift_cap) {
+  if (!S || !res) return set_error(PCG_EINVAL, "solver_run: bad arguments");
+  if (!S->initialized) return set_error(PCG_ESTATE, "solver_run before solver_init");
+  memset(res, 0, sizeof(*res));
+  const int K = auto_chunk(S);
+  long long hist_n = 0, drift_n = 0;
+  long long next_hist = 1;  // next history index to collect (0 = init norm)
+  long long chunk_lo[2] = {0, 0};
+  int cur = S->rec_parity;
+  chunk_lo[cur] = S->host_base;
+  int rc = launch_chunk(S, K, cur);
+  if (rc) return rc;
+  Ctrl c{};
+  bool first = true;
+  while (true) {
+    const int nxt = cur ^ 1;
+    const bool more = S->host_base < S->max_it + 1;  // F(max_it) must run to stop
+    if (more) {
+      chunk_lo[nxt] = S->host_base;
+      rc = launch_chunk(S, K, nxt);
+      if (rc) return rc;
+    }
+    cudaError_t e = cudaEventSynchronize(S->ev_rec[cur]);
+    if (e != cudaSuccess) return cuda_status(e, "chunk wait");
+    const Record R = record_at(S->rec_host[cur]);
+    c = *R.C;
+    if (first) {
+      if (history_host && hist_cap > 0) history_host[0] = c.init.norm;
+      hist_n = 1;
+      first = false;
+    }
+    long long hi = chunk_lo[cur] + K - 1;  // last iteration whose entry this chunk ran
+    if (c.status == PCG_STOPPED) hi = std::min(hi, c.final_it);
+    if (c.status == PCG_BREAKDOWN) hi = std::min(hi, c.bd_it);
+    for (long long itx = next_hist; itx <= hi; ++itx) {
+      if (history_host && hist_n < hist_cap) history_host[hist_n] = R.hist[itx & (kHistRing - 1)];
+      hist_n++;
+    }
+    if (S->drift_k > 0) {
+      for (long long itx = std::max(chunk_lo[cur], 1LL); itx <= hi; ++itx) {
+        if (itx % S->drift_k) continue;
+        const int slot = (int)(itx & (kHistRing - 1));
+        if (R.dit[slot] != itx) continue;
+        if (drift_n < drift_cap) {
+          if (drift_it_host) drift_it_host[drift_n] = itx;
+          if (drift_val_host) drift_val_host[drift_n] = R.dval[slot];
+        }
+        drift_n++;
+      }
+    }
+    next_hist = std::max(next_hist, hi + 1);
+    if (c.status != PCG_RUNNING || !more) break;
+    cur = nxt;
+  }
+  {
+    cudaError_t e = cudaStreamSynchronize(S->stream);
+    if (e != cudaSuccess) return cuda_status(e, "solve sync");
+  }
+  S->rec_parity = cur ^ 1;
+  fill_result(S, c, res);
+  res->n_history = hist_n;
+  res->n_drift = drift_n;
+  S->mn_valid = false;
+  return PCG_OK;
+}
+
+int pipecg_b200_solver_enqueue(pcg_solver* S, int64_t count) {
+  if (!S || !S->initialized) return set_error(PCG_ESTATE, "solver_enqueue before init");
+  const int K = auto_chunk(S);
+  while (count > 0) {
+    const int k = (int)std::min<int64_t>(count, K);
+    int rc = launch_chunk(S, k, S->rec_parity);
+    if (rc) return rc;
+    S->rec_parity ^= 1;
+    count -= k;
+  }
+  S->mn_valid = false;
+  return PCG_OK;
+}
+
+double* pipecg_b200_solver_x(pcg_solver* S) { return S ? S->x : nullptr; }
+
+void* pipecg_b200_solver_stream(pcg_solver* S) { return S ? (void*)S->stream : nullptr; }
+
+int pipecg_b200_solver_poll(pcg_solver* S, pcg_result* res) {
+  if (!S || !res) return set_error(PCG_EINVAL, "solver_poll: bad arguments");
+  cudaError_t e = cudaStreamSynchronize(S->stream);
+  if (e != cudaSuccess) return cuda_status(e, "poll sync");
+  Ctrl c{};
+  e = cudaMemcpy(&c, S->rec_dev, sizeof(Ctrl), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_status(e, "poll copy");
+  memset(res, 0, sizeof(*res));
+  fill_result(S, c, res);
+  return PCG_OK;
+}
+
+int pipecg_b200_solver_state(pcg_solver* S, double** ptrs) {
+  if (!S || !ptrs) return set_error(PCG_EINVAL, "solver_state: bad arguments");
+  Ctrl c{};
+  cudaError_t e = cudaStreamSynchronize(S->stream);
+  if (e == cudaSuccess) e = cudaMemcpy(&c, S->rec_dev, sizeof(Ctrl), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_status(e, "solver_state");
+  const long long done = c.status == PCG_STOPPED ? c.final_it : c.base_it;
+  double* w = S->engine == 1 ? S->w[done & 1] : S->w[0];
+  const long long n = S->A.n_rows;
+  if (!S->mn_valid) {
+    int rc = pipecg_b200_jacobi_apply(n, S->A.inv_diag, w, S->m, S->stream);
+    if (!rc)
+      rc = spmv_any(n, S->A.rp64, S->A.rowptr, S->A.col, S->A.val, S->m, nullptr, S->nv,
+                    S->long_rows, S->n_long, 0, S->stream);
+    if (rc) return rc;
+    e = cudaStreamSynchronize(S->stream);
+    if (e != cudaSuccess) return cuda_status(e, "solver_state m/n");
+    S->mn_valid = true;
+  }
+  double* v[10] = {S->x, S->r, S->u, w, S->m, S->nv, S->z, S->q, S->s, S->p};
+  for (int k = 0; k < 10; ++k) ptrs[k] = v[k];
+  return PCG_OK;
+}
+
+}  // extern "C"

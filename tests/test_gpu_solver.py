@@ -1,0 +1,249 @@
+"""GPU parity of pipecg_solve against the reference's goldens and the oracle.
+
+Gates (BASELINE.md "Parity gates"):
+  1. iteration count within +-1 of the oracle,
+  2. G = max_k |h_k - h_k^ref| / h_0 <= max(1e-10, 3E)  (E: dot-reorder envelope),
+  3. final x within 1e-8 relative,
+  4. dot_mode="seq": history and x bitwise identical to the reference.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import GOLDEN, golden_matrix, load_golden
+
+pytestmark = pytest.mark.gpu
+
+pb = pytest.importorskip("paper_2105_06176_b200")
+torch = pytest.importorskip("torch")
+
+META = json.loads((GOLDEN / "golden_meta.json").read_text())
+SEQ = pb.DeviceOptions(dot_mode="seq")
+
+
+def _cfg(g, record=True):
+    return pb.SolverConfig(tolerance=float(g["tol"]), max_iterations=int(g["max_iterations"]),
+                           record_history=record, drift_check_interval=int(g["drift_k"]))
+
+
+CASES = [c for c in META["cases"] if c != "p125n6_pcg"]
+
+
+@pytest.mark.parametrize("engine", ["fused", "two"])
+@pytest.mark.parametrize("case", CASES)
+def test_golden_bitwise_seq_mode(cuda, case, engine):
+    """dot_mode='seq' reproduces the reference solve bit for bit."""
+    g = load_golden(f"solve_{case}.npz")
+    m = META["cases"][case]
+    A = golden_matrix(g)
+    pc = pb.JacobiPreconditioner(g["inv_diag"])
+    opts = pb.DeviceOptions(dot_mode="seq", engine=engine)
+    if "breakdown" in m:
+        with pytest.raises(pb.SolverBreakdown) as exc:
+            pb.pipecg_solve(A, g["b"], g["x0"], pc, _cfg(g, False), options=opts)
+        assert exc.value.quantity == m["breakdown"]
+        assert exc.value.iteration == m["iteration"]
+        return
+    x, rep = pb.pipecg_solve(A, g["b"], g["x0"], pc, _cfg(g), options=opts)
+    assert rep.iterations == m["iterations"]
+    assert rep.converged == m["converged"]
+    assert rep.final_norm == m["final_norm"]
+    assert rep.strategy == "pipecg"
+    np.testing.assert_array_equal(np.array(rep.history), g["history"])
+    np.testing.assert_array_equal(x, g["x"])
+    if int(g["drift_k"]) > 0:
+        assert [d[0] for d in rep.drift_history] == [int(d) for d in g["drift"][:, 0]]
+        np.testing.assert_allclose(np.array(rep.drift_history)[:, 1], g["drift"][:, 1],
+                                   rtol=1e-6, atol=1e-15)
+
+
+def envelope(A, b, x0, d, tol, max_iterations, drift_k=0):
+    """The oracle's own parity noise floor at this config: the reference
+    algorithm with only its dot order changed (256 sequential partials +
+    pairwise tree).  Returns (iteration gap, h0-normalised history gap E,
+    x relative gap) between the two oracle runs (BASELINE.md gate 2)."""
+    r1 = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=max_iterations)
+    r2 = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=max_iterations,
+                             dot_mode="blocked")
+    scale = max(np.max(np.abs(r1.x)), 1e-300)
+    return (abs(r1.iterations - r2.iterations), oracle.history_gap(r2.history, r1.history),
+            float(np.max(np.abs(r1.x - r2.x)) / scale))
+
+
+def assert_within_envelope(x, rep, ref_iters, ref_hist, ref_x, env):
+    it_gap, E, x_gap = env
+    assert abs(rep.iterations - ref_iters) <= max(1, it_gap), (rep.iterations, ref_iters, env)
+    G = oracle.history_gap(rep.history, list(ref_hist))
+    assert G <= max(1e-10, 3 * E), (G, env)
+    scale = max(np.max(np.abs(ref_x)), 1e-300)
+    rel = float(np.max(np.abs(x - ref_x)) / scale)
+    assert rel <= max(1e-8, 3 * x_gap), (rel, env)
+
+
+@pytest.mark.parametrize("engine", ["fused", "two"])
+@pytest.mark.parametrize("case", CASES)
+def test_golden_tree_mode_tolerance(cuda, case, engine):
+    """Default (tree dots): iterations, history and x within the larger of the
+    BASELINE.md gates (+-1, 1e-10, 1e-8) and 3x the oracle's reorder envelope."""
+    g = load_golden(f"solve_{case}.npz")
+    m = META["cases"][case]
+    A = golden_matrix(g)
+    pc = pb.JacobiPreconditioner(g["inv_diag"])
+    opts = pb.DeviceOptions(engine=engine)
+    if "breakdown" in m:
+        with pytest.raises(pb.SolverBreakdown) as exc:
+            pb.pipecg_solve(A, g["b"], g["x0"], pc, _cfg(g, False), options=opts)
+        assert exc.value.quantity == m["breakdown"]
+        return
+    x, rep = pb.pipecg_solve(A, g["b"], g["x0"], pc, _cfg(g), options=opts)
+    env = envelope(A, g["b"], g["x0"], g["inv_diag"], float(g["tol"]), int(g["max_iterations"]))
+    assert_within_envelope(x, rep, m["iterations"], g["history"], g["x"], env)
+
+
+def test_config1_2d5_512_parity(cuda):
+    """BASELINE config 1 vs the reference's own 894-iteration run."""
+    g = load_golden("config1_2d5_512.npz")
+    A = pb.stencil_host("2d5", 512)
+    x_true = np.full(A.n_rows, 1.0 / math.sqrt(A.n_rows))
+    b = pb.spmv(A, x_true)
+    pc = pb.jacobi_setup(A)
+    tol = float(g["tol"])
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=20000, record_history=True)
+    x, rep = pb.pipecg_solve(A, b, np.zeros(A.n_rows), pc, cfg)
+    assert abs(rep.iterations - 894) <= 1
+    G = oracle.history_gap(rep.history, list(g["history"]))
+    assert G <= max(1e-10, 3 * 3.0e-12), G
+    rel = np.max(np.abs(x - g["x"])) / np.max(np.abs(g["x"]))
+    assert rel <= 1e-8, rel
+    # bitwise mode on the same config
+    x2, rep2 = pb.pipecg_solve(A, b, np.zeros(A.n_rows), pc, cfg, options=SEQ)
+    assert rep2.iterations == 894
+    np.testing.assert_array_equal(np.array(rep2.history), g["history"])
+    np.testing.assert_array_equal(x2, g["x"])
+
+
+@pytest.mark.parametrize("kind,n", [("3d7", 32), ("3d27", 20), ("p125", 12), ("2d5", 100)])
+def test_stencils_vs_oracle(cuda, kind, n):
+    A = pb.stencil_host(kind, n)
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=20000)
+    pc = pb.jacobi_setup(A)
+    np.testing.assert_array_equal(pc.inv_diag, d)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=20000, record_history=True)
+    x, rep = pb.pipecg_solve(A, b, x0, pc, cfg)
+    env = envelope(A, b, x0, d, tol, 20000)
+    assert_within_envelope(x, rep, ref.iterations, ref.history, ref.x, env)
+    xs, reps = pb.pipecg_solve(A, b, x0, pc, cfg, options=SEQ)
+    assert reps.history == ref.history
+    np.testing.assert_array_equal(xs, ref.x)
+
+
+def test_determinism_bitwise(cuda):
+    """Acceptance #10 (test_acceptance.py:328-358): repeated runs identical."""
+    A = pb.stencil_host("3d7", 40)
+    x_true = np.full(A.n_rows, 1 / math.sqrt(A.n_rows))
+    b = pb.spmv(A, x_true)
+    pc = pb.jacobi_setup(A)
+    cfg = pb.SolverConfig(tolerance=1e-9, record_history=True)
+    x1, r1 = pb.pipecg_solve(A, b, np.zeros(A.n_rows), pc, cfg)
+    x2, r2 = pb.pipecg_solve(A, b, np.zeros(A.n_rows), pc, cfg)
+    assert r1.history == r2.history
+    np.testing.assert_array_equal(x1, x2)
+
+
+def test_device_tensor_inputs(cuda):
+    Ad = pb.stencil_device("3d7", 30)
+    n = Ad.n_rows
+    x_true = torch.full((n,), 1 / math.sqrt(n), dtype=torch.float64, device="cuda")
+    b = pb.spmv(Ad, x_true)
+    pc = pb.jacobi_setup(Ad)
+    x, rep = pb.pipecg_solve(Ad, b, torch.zeros_like(b), pc, pb.SolverConfig(tolerance=1e-10))
+    assert isinstance(x, torch.Tensor) and x.is_cuda
+    assert rep.converged
+    assert float((x - x_true).abs().max()) < 1e-7
+
+
+def test_max_iterations_and_chunk_boundaries(cuda):
+    A = pb.stencil_host("3d7", 16)
+    x_true, b, x0, d = oracle.manufactured(A)
+    pc = pb.JacobiPreconditioner(d)
+    for maxit in (1, 2, 3, 4, 5, 7, 8, 9, 31, 64):
+        for chunk in (4, 8, 16):
+            cfg = pb.SolverConfig(max_iterations=maxit, tolerance=1e-300, record_history=True)
+            x, rep = pb.pipecg_solve(A, b, x0, pc, cfg,
+                                     options=pb.DeviceOptions(dot_mode="seq", chunk=chunk))
+            ref = oracle.pipecg_solve(A, b, x0, d, tol=1e-300, max_iterations=maxit)
+            assert rep.iterations == maxit == ref.iterations
+            assert not rep.converged
+            assert rep.history == ref.history
+            np.testing.assert_array_equal(x, ref.x)
+
+
+def test_no_graphs_path(cuda):
+    A = pb.stencil_host("2d5", 40)
+    x_true, b, x0, d = oracle.manufactured(A)
+    pc = pb.JacobiPreconditioner(d)
+    cfg = pb.SolverConfig(tolerance=1e-9, record_history=True)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=1e-9)
+    x, rep = pb.pipecg_solve(A, b, x0, pc, cfg,
+                             options=pb.DeviceOptions(dot_mode="seq", use_graphs=False))
+    assert rep.history == ref.history
+
+
+def test_host_abi_solve(cuda):
+    """pipecg_b200_solve_host: the one-call C-ABI drop-in with host buffers."""
+    import ctypes
+
+    from paper_2105_06176_b200 import _lib
+
+    A = oracle.stencil("3d7", 20)
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=5000)
+    x = np.empty(A.n_rows)
+    hist = np.empty(5001)
+    res = _lib.PcgResult()
+    P = lambda a, t=ctypes.c_double: a.ctypes.data_as(ctypes.POINTER(t))  # noqa: E731
+    _lib.call("pipecg_b200_solve_host", A.n_rows, P(A.row_offsets, ctypes.c_int64),
+              P(A.col_indices, ctypes.c_int64), P(A.values), P(b), P(x0), P(d), tol, 5000, 0,
+              _lib.PCG_DOT_SEQ, P(x), P(hist), hist.size, None, None, 0, ctypes.byref(res))
+    assert res.status == _lib.PCG_STOPPED and res.converged
+    assert res.iterations == ref.iterations
+    np.testing.assert_array_equal(hist[: res.n_history], np.array(ref.history))
+    np.testing.assert_array_equal(x, ref.x)
+
+
+def test_pipecg_init_matches_operators(cuda):
+    # reference tests/test_solvers.py:153-170
+    K = load_golden("kernels.npz")
+    dense = np.zeros((5, 5))
+    for i, cols in enumerate(((0, 1, 3), (0, 1, 4), (2, 3), (0, 2, 3, 4), (1, 3, 4))):
+        for j in cols:
+            dense[i, j] = 4.0 if i == j else -1.0
+    A = pb.csr_from_dense(dense)
+    rng = np.random.default_rng(31)
+    b = rng.standard_normal(5)
+    x0 = rng.standard_normal(5)
+    pc = pb.jacobi_setup(A)
+    st = pb.pipecg_init(A, b, x0, pc)
+    r = b - pb.spmv(A, x0)
+    u = pb.jacobi_apply(pc, r)
+    w = pb.spmv(A, u)
+    np.testing.assert_array_equal(st.r, r)
+    np.testing.assert_array_equal(st.u, u)
+    np.testing.assert_array_equal(st.w, w)
+    np.testing.assert_array_equal(st.m, pb.jacobi_apply(pc, w))
+    np.testing.assert_array_equal(st.n, pb.spmv(A, pb.jacobi_apply(pc, w)))
+    assert st.gamma == pb.dot(r, u)
+    assert st.delta == pb.dot(w, u)
+    assert st.norm == math.sqrt(pb.dot(u, u))
+    for nm in ("z", "q", "s", "p"):
+        np.testing.assert_array_equal(getattr(st, nm), np.zeros(5))
+    del K
