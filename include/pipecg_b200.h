@@ -37,7 +37,8 @@ enum {
   PCG_ENOMEM = 1002,    /* device allocation failed */
   PCG_ESTATE = 1003,    /* call out of order (e.g. iterate before init) */
   PCG_ERANGE = 1004,    /* index out of int32 range / out of bounds */
-  PCG_EDIAG = 1005      /* missing or zero diagonal (jacobi_setup) */
+  PCG_EDIAG = 1005,     /* missing or zero diagonal (jacobi_setup) */
+  PCG_ECOMM = 1006      /* distributed exchange timed out (peer stalled / died) */
 };
 
 /* dot-product modes */
@@ -151,6 +152,7 @@ typedef struct {
   int engine;          /* 0 auto, 1 fused single-kernel, 2 two-kernel */
   int chunk;           /* iterations per CUDA-graph chunk (0 = auto) */
   int use_graphs;      /* 1 (default) or 0 (plain launches, debugging) */
+  int max_sms;         /* size persistent grids for at most this many SMs (0 = all) */
 } pcg_options;
 
 typedef struct {
@@ -200,6 +202,30 @@ double* pipecg_b200_solver_x(pcg_solver* s);
  * x r u w m n z q s p (solvers.py:74-101).  m and n are materialised first
  * (the fused engine keeps them implicit).  ptrs: void*[10]. */
 int pipecg_b200_solver_state(pcg_solver* s, double** ptrs);
+
+/* ---------------------------------------------------------------------- */
+/* Multi-GPU row-block sharding; one process per GPU.    */
+/* Each rank creates a solver for its row block with local column indices */
+/* ([owned rows | halo], halo sorted by global index) and inv_diag over    */
+/* n_cols entries; the ranks exchange CUDA IPC handles of their vector     */
+/* block and comm block, then connect.  Per iteration the fused kernel is  */
+/* followed by an exchange kernel that stores the boundary rows of w into  */
+/* the neighbours' halo and this rank's dot partial into every rank's slot */
+/* over NVLink, then signals; the next iteration's prologue waits on that  */
+/* signal in-kernel.  No host synchronisation, no NCCL on the data path.   */
+/* ---------------------------------------------------------------------- */
+/* vector block base (vectors at base + k*ld, w0 = 7, w1 = 8), ld, comm block */
+int pipecg_b200_solver_comm_info(pcg_solver* s, void** vbuf, int64_t* ld, void** comm);
+/* cudaIpcMemHandle_t (64 bytes) of a device allocation, and its mapping */
+int pipecg_b200_ipc_get_handle(void* dev_ptr, void* handle_out);
+int pipecg_b200_ipc_open(const void* handle, void** dev_ptr_out);
+int pipecg_b200_ipc_close(void* dev_ptr);
+/* peer_*: world entries (this rank's own at [rank]); send_*: device arrays
+ * of n_send entries: local row, destination rank, destination local column */
+int pipecg_b200_solver_connect(pcg_solver* s, int rank, int world, void* const* peer_vbuf,
+                               const int64_t* peer_ld, void* const* peer_comm, int64_t n_send,
+                               const int32_t* send_row, const int32_t* send_peer,
+                               const int64_t* send_dst);
 
 /* ---------------------------------------------------------------------- */
 /* One-call host-buffer drop-in for pipecg_solve (solvers.py:324-387).     */

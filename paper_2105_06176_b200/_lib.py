@@ -18,7 +18,8 @@ LIB_PATH = _HERE / "_lib" / "libpipecg_b200.so"
 CSRC = _HERE / "csrc"
 
 PCG_OK = 0
-PCG_EINVAL, PCG_ENOMEM, PCG_ESTATE, PCG_ERANGE, PCG_EDIAG = 1001, 1002, 1003, 1004, 1005
+PCG_EINVAL, PCG_ENOMEM, PCG_ESTATE, PCG_ERANGE, PCG_EDIAG, PCG_ECOMM = (1001, 1002, 1003, 1004,
+                                                                    1005, 1006)
 PCG_DOT_TREE, PCG_DOT_SEQ = 0, 1
 PCG_RUNNING, PCG_STOPPED, PCG_BREAKDOWN = 0, 1, 2
 BREAKDOWN_QUANTITY = {1: "alpha denominator", 2: "gamma", 3: "delta"}
@@ -39,7 +40,8 @@ class PcgMatrix(ctypes.Structure):
 
 
 class PcgOptions(ctypes.Structure):
-    _fields_ = [("dot_mode", _int), ("engine", _int), ("chunk", _int), ("use_graphs", _int)]
+    _fields_ = [("dot_mode", _int), ("engine", _int), ("chunk", _int), ("use_graphs", _int),
+                ("max_sms", _int)]
 
 
 class PcgResult(ctypes.Structure):
@@ -90,6 +92,11 @@ _SIGS = {
     "pipecg_b200_solver_poll": ([_vp, ctypes.POINTER(PcgResult)], _int),
     "pipecg_b200_solver_x": ([_vp], _vp),
     "pipecg_b200_solver_state": ([_vp, ctypes.POINTER(_vp)], _int),
+    "pipecg_b200_solver_comm_info": ([_vp, ctypes.POINTER(_vp), _p_i64, ctypes.POINTER(_vp)], _int),
+    "pipecg_b200_ipc_get_handle": ([_vp, _vp], _int),
+    "pipecg_b200_ipc_open": ([_vp, ctypes.POINTER(_vp)], _int),
+    "pipecg_b200_ipc_close": ([_vp], _int),
+    "pipecg_b200_solver_connect": ([_vp, _int, _int, _vp, _vp, _vp, _i64, _vp, _vp, _vp], _int),
     "pipecg_b200_solve_host": ([_i64, _p_i64, _p_i64, _p_dbl, _p_dbl, _p_dbl, _p_dbl, _dbl, _i64,
                                 _i64, _int, _p_dbl, _p_dbl, _i64, _p_i64, _p_dbl, _i64,
                                 ctypes.POINTER(PcgResult)], _int),

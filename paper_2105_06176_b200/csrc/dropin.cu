@@ -94,6 +94,7 @@ extern "C" int pipecg_b200_solve_host(int64_t n, const int64_t* ro_h, const int6
     o.engine = 0;
     o.chunk = 0;
     o.use_graphs = 1;
+    o.max_sms = 0;
     rc = cuda_status(cudaStreamSynchronize(st), "solve_host upload");
     if (!rc) rc = pipecg_b200_solver_create(&A, &o, &S);
   }

@@ -24,6 +24,7 @@ inline unsigned elementwise_grid(int64_t n) {
 int spmv_any(int64_t n_rows, int rp64, const void* rowptr, const int* col, const double* val,
              const double* x, const double* b, double* y, const int* long_rows, int64_t n_long,
              int mode, cudaStream_t st);
+int preload_ops();
 int dots_any(int64_t n, int npairs, const double* const* a, const double* const* b, int mode,
              double* out, double* workspace, cudaStream_t st);
 

@@ -339,6 +339,29 @@ __global__ void long_rows_kernel(int64_t n, const RP* __restrict__ rp, int64_t t
   }
 }
 
+// Force-load every operator kernel.  Under CUDA lazy module loading the
+// first launch of a kernel loads it, and loading can wait for the device to
+// go idle; a kernel spinning on a peer's signal would then deadlock with a
+// peer whose first launch is stuck the same way.  Loading everything up front
+// removes that coupling (solver_create calls this once).
+int preload_ops() {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaSuccess;
+#define PCG_LOAD(k) if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void*)(k))
+  PCG_LOAD((spmv_rows_kernel<int, 0>)); PCG_LOAD((spmv_rows_kernel<int, 1>));
+  PCG_LOAD((spmv_rows_kernel<long long, 0>)); PCG_LOAD((spmv_rows_kernel<long long, 1>));
+  PCG_LOAD((spmv_long_kernel<int, 0>)); PCG_LOAD((spmv_long_kernel<int, 1>));
+  PCG_LOAD((spmv_long_kernel<long long, 0>)); PCG_LOAD((spmv_long_kernel<long long, 1>));
+  PCG_LOAD(jacobi_kernel); PCG_LOAD(fused_update_kernel); PCG_LOAD(fused_update_pc_dots_kernel);
+  PCG_LOAD(dots_partial_kernel<1>); PCG_LOAD(dots_partial_kernel<2>);
+  PCG_LOAD(dots_partial_kernel<3>); PCG_LOAD(dots_partial_kernel<4>);
+  PCG_LOAD(dots_finish_kernel);
+  PCG_LOAD(dots_seq_kernel<1>); PCG_LOAD(dots_seq_kernel<2>);
+  PCG_LOAD(dots_seq_kernel<3>); PCG_LOAD(dots_seq_kernel<4>);
+#undef PCG_LOAD
+  return cuda_status(e, "preload operator kernels");
+}
+
 }  // namespace pcg
 
 using namespace pcg;

@@ -35,6 +35,8 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <mutex>
+#include <set>
 #include <vector>
 
 #include "../../include/pipecg_b200.h"
@@ -43,7 +45,10 @@
 
 namespace pcg {
 
-constexpr int kHistRing = 1024;  // history / drift ring (power of two)
+constexpr int kHistRing = 1024;
+constexpr int kMaxRanks = 8;
+constexpr int kXchgBlocks = 16;    // exchange-kernel grid (identical on every rank)
+constexpr int PCG_ECOMM_STATUS = 3; // Ctrl.status: peer exchange timed out  // history / drift ring (power of two)
 constexpr int kMaxChunk = 256;   // 2*kMaxChunk <= kHistRing
 
 struct Slot {
@@ -66,7 +71,11 @@ struct Ctrl {
   long long final_it;
   double final_norm;
   Slot slot[2];
-  double pad_[4];
+  unsigned long long arrive_base;  // distributed: arrivals before this solve
+  int comm_error;                  // a setup exchange timed out
+  int diag_where;                  // 1 = iteration wait, 2 = setup wait timed out
+  unsigned long long diag_seen;    // counter value at the timeout
+  unsigned long long diag_target;  // value waited for
 };
 static_assert(sizeof(Ctrl) <= 256, "Ctrl must fit its 256-byte record slot");
 
@@ -95,6 +104,48 @@ struct Step {
   double alpha, beta;
 };
 
+// What the prologue of iteration `it` reduces: pin[(it-1)&1][0..n_pin)[0..2]
+// (block partials on one GPU; one partial per rank in distributed mode,
+// pushed by the peers' exchange kernels).  In distributed mode `arrive`
+// counts the peers' exchange-kernel arrivals (monotonic); iteration it may
+// start once arrive >= arrive_base + it * arrive_per_it.
+struct ReduceIn {
+  const double* pin;
+  int n_pin;
+  const unsigned long long* arrive;
+  unsigned long long arrive_per_it;
+};
+
+constexpr long long kSpinTimeoutNs = 10LL * 1000 * 1000 * 1000;  // 10 s
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// spin until *p >= target; false on timeout (a peer died or diverged)
+__device__ bool spin_until(const unsigned long long* p, unsigned long long target, Ctrl* C,
+                           int where) {
+  if (ld_acquire_sys(p) >= target) return true;
+  const unsigned long long t0 = globaltimer();
+  unsigned long long v;
+  while ((v = ld_acquire_sys(p)) < target) {
+    if (globaltimer() - t0 > (unsigned long long)kSpinTimeoutNs) {
+      C->diag_where = where;
+      C->diag_seen = v;
+      C->diag_target = target;
+      return false;
+    }
+    __nanosleep(64);
+  }
+  return true;
+}
+
 __device__ __forceinline__ int read_status(const Ctrl* C) {
   return *reinterpret_cast<const volatile int*>(&C->status);
 }
@@ -102,8 +153,8 @@ __device__ __forceinline__ int read_status(const Ctrl* C) {
 // The reference's loop head + tail, solvers.py:346-372, for iteration `it`.
 // NT threads (local id lt) participate; `leader` is one thread of block 0.
 template <int NT>
-__device__ Step prologue(Ctrl* C, double* hist, const double* partials, int n_partials,
-                         long long it, int lt, double* red, int bar_id, bool leader) {
+__device__ Step prologue(Ctrl* C, double* hist, const ReduceIn& R, long long it, int lt,
+                         double* red, int bar_id, bool leader) {
   Step st{0, 0.0, 0.0};
   double gamma, delta, norm, gamma_prev = 0.0, alpha_prev = 0.0;
   if (it == 0) {
@@ -111,7 +162,24 @@ __device__ Step prologue(Ctrl* C, double* hist, const double* partials, int n_pa
     delta = C->init.delta;
     norm = C->init.norm;
   } else {
-    const double* P = partials + (size_t)((it - 1) & 1) * (size_t)n_partials * 4;
+    if (R.arrive) {  // distributed: wait for every rank's exchange of it-1
+      if (lt == 0)
+        red[0] = spin_until(R.arrive, C->arrive_base + (unsigned long long)it * R.arrive_per_it,
+                            C, 1) ? 1.0 : -1.0;
+      bar_sync(bar_id, NT);
+      const bool ok = red[0] > 0.0;
+      bar_sync(bar_id, NT);
+      if (!ok) {
+        if (leader || lt == 0) {
+          C->bd_code = PCG_BD_NONE;
+          C->bd_it = it;
+          C->status = PCG_ECOMM_STATUS;
+        }
+        return st;
+      }
+    }
+    const double* P = R.pin + (size_t)((it - 1) & 1) * (size_t)R.n_pin * 4;
+    const int n_partials = R.n_pin;
     double v[3] = {0.0, 0.0, 0.0};
     for (int j = lt; j < n_partials; j += NT) {
       v[0] = add(v[0], P[j * 4 + 0]);
@@ -196,8 +264,8 @@ struct FusedParams {
   double* w[2];    // ping-pong: read w[it&1], write w[(it+1)&1]
   Ctrl* C;
   double* hist;
-  double* partials;  // [2][n_partials][4]
-  int n_partials;
+  ReduceIn rin;   // what the prologue reduces
+  double* pout;   // block partials [2][gridDim.x][4]
   int stages;
   int cap_val;  // doubles per stage
   int cap_col;  // ints per stage
@@ -280,7 +348,7 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel(FusedParams<RP> P
 
   // ---- prologue (consumers): entry scalars, guards, stop test ------------
   if (!producer) {
-    const Step stp = prologue<NT>(C, P.hist, P.partials, P.n_partials, it, tid - 32, red, 1,
+    const Step stp = prologue<NT>(C, P.hist, P.rin, it, tid - 32, red, 1,
                                   blockIdx.x == 0 && tid == 32);
     if (tid == 32) {
       sc[0] = stp.alpha;
@@ -379,7 +447,7 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel(FusedParams<RP> P
   }
   group_sum<3, NT>(acc, lt, red, 1);
   if (lt == 0) {
-    double* out = P.partials + (size_t)(it & 1) * (size_t)P.n_partials * 4 + (size_t)blockIdx.x * 4;
+    double* out = P.pout + (size_t)(it & 1) * (size_t)gridDim.x * 4 + (size_t)blockIdx.x * 4;
     out[0] = acc[0];
     out[1] = acc[1];
     out[2] = acc[2];
@@ -396,8 +464,8 @@ struct TwoParams {
   const double* dinv;
   Ctrl* C;
   double* hist;
-  double* partials;
-  int n_partials;
+  ReduceIn rin;
+  double* pout;
 };
 
 __global__ void __launch_bounds__(256) pipecg_k1_kernel(TwoParams P, int step) {
@@ -405,7 +473,7 @@ __global__ void __launch_bounds__(256) pipecg_k1_kernel(TwoParams P, int step) {
   Ctrl* C = P.C;
   if (read_status(C) != PCG_RUNNING) return;
   const long long it = C->base_it + step;
-  const Step stp = prologue<256>(C, P.hist, P.partials, P.n_partials, it, threadIdx.x, red, 1,
+  const Step stp = prologue<256>(C, P.hist, P.rin, it, threadIdx.x, red, 1,
                                  blockIdx.x == 0 && threadIdx.x == 0);
   if (!stp.go) return;
   const double alpha = stp.alpha, beta = stp.beta;
@@ -435,7 +503,7 @@ __global__ void __launch_bounds__(256) pipecg_k1_kernel(TwoParams P, int step) {
   }
   group_sum<3, 256>(acc, threadIdx.x, red, 1);
   if (threadIdx.x == 0) {
-    double* out = P.partials + (size_t)(it & 1) * (size_t)P.n_partials * 4 + (size_t)blockIdx.x * 4;
+    double* out = P.pout + (size_t)(it & 1) * (size_t)gridDim.x * 4 + (size_t)blockIdx.x * 4;
     out[0] = acc[0];
     out[1] = acc[1];
     out[2] = acc[2];
@@ -485,7 +553,7 @@ __global__ void __launch_bounds__(256) gated_spmv_long(const Ctrl* C, const int*
 __global__ void __launch_bounds__(32) seq_dots_kernel(const Ctrl* C, long long n, const double* r,
                                                        const double* u, const double* w0,
                                                        const double* w1, int pingpong,
-                                                       double* partials, int n_partials, int step) {
+                                                       double* seqbuf, int step) {
   constexpr int CH = 256;
   __shared__ double prod[3][CH];
   if (read_status(C) != PCG_RUNNING) return;
@@ -514,7 +582,7 @@ __global__ void __launch_bounds__(32) seq_dots_kernel(const Ctrl* C, long long n
     __syncwarp();
   }
   if (lane == 0) {
-    double* out = partials + (size_t)(it & 1) * (size_t)n_partials * 4;
+    double* out = seqbuf + (size_t)(it & 1) * 4;
     out[0] = acc[0];
     out[1] = acc[1];
     out[2] = acc[2];
@@ -568,15 +636,20 @@ __global__ void advance_kernel(Ctrl* C, int k) {
   if (threadIdx.x == 0) C->base_it += k;
 }
 
-// pipecg_init tail: read the four init dots, reset the control block
-__global__ void init_ctrl_kernel(Ctrl* C, const double* dots4, double tol, long long max_it,
-                                 long long drift_k, double* hist, long long* dit) {
+// pipecg_init tail: sum the per-rank init dots (r,u),(w,u),(u,u),(b,b) in
+// rank order (one rank on a single GPU), reset the control block.
+__global__ void init_ctrl_kernel(Ctrl* C, const double* dots, int nranks, double tol,
+                                 long long max_it, long long drift_k, double* hist, long long* dit,
+                                 const unsigned long long* arrive) {
   if (threadIdx.x == 0) {
+    double d4[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int q = 0; q < nranks; ++q)
+      for (int k = 0; k < 4; ++k) d4[k] = add(d4[k], dots[q * 4 + k]);
     C->tol = tol;
     C->max_it = max_it;
     C->drift_k = drift_k;
-    C->b_norm = sqrt(dots4[3]);
-    C->init = Slot{dots4[0], dots4[1], 0.0, sqrt(dots4[2])};
+    C->b_norm = sqrt(d4[3]);
+    C->init = Slot{d4[0], d4[1], 0.0, sqrt(d4[2])};
     C->base_it = 0;
     C->status = PCG_RUNNING;
     C->bd_code = PCG_BD_NONE;
@@ -586,9 +659,122 @@ __global__ void init_ctrl_kernel(Ctrl* C, const double* dots4, double tol, long 
     C->final_norm = 0.0;
     C->slot[0] = Slot{0, 0, 0, 0};
     C->slot[1] = Slot{0, 0, 0, 0};
+    if (!arrive) C->arrive_base = 0ull;  // distributed: snapshot taken at init start
+    if (C->comm_error) C->status = PCG_ECOMM_STATUS;
     hist[0] = C->init.norm;
   }
   for (int j = threadIdx.x; j < kHistRing; j += blockDim.x) dit[j] = -1;
+}
+
+// ===========================================================================
+// Distributed exchange over NVLink peer memory (CUDA IPC-mapped pointers).
+// Comm buffer layout (identical on every rank, cudaMalloc'd, IPC-exported):
+//   [0]   u64 arrive    (iteration exchanges received)
+//   [8]   u64 xarrive   (setup exchanges received)
+//   [256] double slots[2][kMaxRanks][4]   per-rank dot partials by parity
+//   [768] double islots[kMaxRanks][4]     per-rank init dots
+// ===========================================================================
+constexpr size_t kCommBytes = 1024;
+constexpr size_t kCommSlots = 256;
+constexpr size_t kCommISlots = 768;
+
+struct CommParams {
+  int rank, world;
+  char* peer_vbuf[kMaxRanks];  // base of each rank's vector block
+  long long peer_ld[kMaxRanks];
+  char* peer_comm[kMaxRanks];
+  long long n_send;
+  const int* send_row;        // local row to send
+  const int* send_peer;       // destination rank
+  const long long* send_dst;  // index in the destination's local column space
+};
+
+__device__ __forceinline__ unsigned long long* comm_arrive(char* c) {
+  return reinterpret_cast<unsigned long long*>(c);
+}
+__device__ __forceinline__ unsigned long long* comm_xarrive(char* c) {
+  return reinterpret_cast<unsigned long long*>(c + 8);
+}
+
+__device__ __forceinline__ void signal_peers(const CommParams& CP, bool iteration) {
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < CP.world; ++q)
+      atomicAdd_system(iteration ? comm_arrive(CP.peer_comm[q]) : comm_xarrive(CP.peer_comm[q]),
+                       1ull);
+  }
+}
+
+// After F(it): push the boundary rows of w_new into the neighbours' halo of
+// the same ping-pong buffer, push this rank's (r,u),(w,u),(u,u) partial to
+// every rank's slot[it&1][rank], then signal every rank.  Stream-ordered
+// after F(it), so every gather of F(it) on this rank is complete.
+__global__ void __launch_bounds__(256) iter_exchange_kernel(CommParams CP, const Ctrl* C, int step,
+                                                             const double* pout, int n_pout,
+                                                             const double* w0, const double* w1) {
+  __shared__ double red[3 * 8];
+  if (read_status(C) != PCG_RUNNING) return;
+  const long long it = C->base_it + step;
+  const int wi = (int)((it + 1) & 1);
+  const double* src = wi ? w1 : w0;
+  const int vec = 7 + wi;  // w0 / w1 are vectors 7 / 8 of the block
+  for (long long e = blockIdx.x * 256LL + threadIdx.x; e < CP.n_send; e += (long long)gridDim.x * 256) {
+    const int q = CP.send_peer[e];
+    double* dst = reinterpret_cast<double*>(CP.peer_vbuf[q]) + (size_t)vec * CP.peer_ld[q];
+    dst[CP.send_dst[e]] = src[CP.send_row[e]];
+  }
+  if (blockIdx.x == 0) {
+    const double* P = pout + (size_t)(it & 1) * (size_t)n_pout * 4;
+    double v[3] = {0.0, 0.0, 0.0};
+    for (int j = threadIdx.x; j < n_pout; j += 256) {
+      v[0] = add(v[0], P[j * 4 + 0]);
+      v[1] = add(v[1], P[j * 4 + 1]);
+      v[2] = add(v[2], P[j * 4 + 2]);
+    }
+    group_sum<3, 256>(v, threadIdx.x, red, 1);
+    if (threadIdx.x < CP.world) {
+      double* slot = reinterpret_cast<double*>(CP.peer_comm[threadIdx.x] + kCommSlots) +
+                     ((size_t)(it & 1) * kMaxRanks + CP.rank) * 4;
+      slot[0] = v[0];
+      slot[1] = v[1];
+      slot[2] = v[2];
+      slot[3] = 0.0;
+    }
+  }
+  signal_peers(CP, true);
+}
+
+// setup: push vector `vec` (index in the block) halo rows to the peers
+__global__ void __launch_bounds__(256) vec_exchange_kernel(CommParams CP, int vec, const double* src) {
+  for (long long e = blockIdx.x * 256LL + threadIdx.x; e < CP.n_send; e += (long long)gridDim.x * 256) {
+    const int q = CP.send_peer[e];
+    double* dst = reinterpret_cast<double*>(CP.peer_vbuf[q]) + (size_t)vec * CP.peer_ld[q];
+    dst[CP.send_dst[e]] = src[CP.send_row[e]];
+  }
+  signal_peers(CP, false);
+}
+
+// setup: push this rank's four init dots to every rank's islots[rank]
+__global__ void init_dots_exchange_kernel(CommParams CP, const double* dots4) {
+  if (threadIdx.x < CP.world) {
+    double* slot = reinterpret_cast<double*>(CP.peer_comm[threadIdx.x] + kCommISlots) + CP.rank * 4;
+    for (int k = 0; k < 4; ++k) slot[k] = dots4[k];
+  }
+  signal_peers(CP, false);
+}
+
+// init start (after the host barrier: no peer can produce iteration
+// arrivals for this solve until this rank's first setup push): snapshot the
+// iteration-arrival counter as this solve's base.
+__global__ void snapshot_arrive_kernel(Ctrl* C, const char* comm) {
+  if (threadIdx.x == 0)
+    C->arrive_base = *reinterpret_cast<const volatile unsigned long long*>(comm);
+}
+
+// setup: wait until xarrive >= target (sets an error status on timeout)
+__global__ void xwait_kernel(char* comm, unsigned long long target, Ctrl* C) {
+  if (threadIdx.x == 0 && !spin_until(comm_xarrive(comm), target, C, 2)) C->comm_error = 1;
 }
 
 // block-wide max (one atomic per block: a single-address atomic per row
@@ -665,15 +851,17 @@ struct pcg_solver {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_in = nullptr, ev_rec[2] = {nullptr, nullptr};
   double* vbuf = nullptr;
-  size_t ld = 0;  // padded vector length
+  size_t ld = 0;  // padded vector length (>= local columns incl. halo)
   double *z = nullptr, *q = nullptr, *s = nullptr, *p = nullptr, *x = nullptr, *r = nullptr,
          *u = nullptr, *w[2] = {nullptr, nullptr}, *m = nullptr, *nv = nullptr, *b = nullptr;
-  double* partials = nullptr;
+  double* partials = nullptr;  // block partials [2][grid][4]
+  double* seqbuf = nullptr;    // sequential-dot results [2][1][4]
   double* dpart = nullptr;
   double* dots_ws = nullptr;
   double* dots4 = nullptr;
   char* rec_dev = nullptr;
   char* rec_host[2] = {nullptr, nullptr};
+  char* comm = nullptr;        // distributed exchange block (IPC-exported)
   int* long_rows = nullptr;
   long long n_long = 0;
   std::map<int, cudaGraphExec_t> graphs[2];
@@ -684,6 +872,11 @@ struct pcg_solver {
   long long graph_launches = 0;
   int rec_parity = 0;
   bool mn_valid = false;
+  // distributed
+  int rank = 0, world = 1;
+  bool connected = false;
+  CommParams cp{};
+  unsigned long long xtarget = 0;  // cumulative setup arrivals expected
 };
 
 namespace {
@@ -735,10 +928,10 @@ int plan_tr(pcg_solver* S, FusedPlan* plan) {
 template <typename RP, int TR>
 int finish_plan(pcg_solver* S, const FusedPlan& p) {
   auto kfn = pipecg_fused_kernel<RP, TR>;
-  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-  if (e != cudaSuccess) return cuda_status(e, "fused smem attribute");
+  // the dynamic-smem limit was raised to the maximum once in preload_solver():
+  // it is per-function global state shared by every solver in the process
   int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, TR + 32, p.smem);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, TR + 32, p.smem);
   if (e != cudaSuccess) return cuda_status(e, "fused occupancy");
   if (occ < 1) return PCG_EINVAL;
   occ = std::min(occ, p.bps);
@@ -780,7 +973,7 @@ int fused_setup(pcg_solver* S) {
 }
 
 int alloc_state(pcg_solver* S) {
-  const long long n = S->A.n_rows;
+  const long long n = std::max(S->A.n_rows, S->A.n_cols);
   S->ld = (size_t)round_up(n + 32, 256);
   const int nvec = 13;  // z q s p x r u w0 w1 m n b + spare
   cudaError_t e = cudaMalloc(&S->vbuf, S->ld * nvec * sizeof(double));
@@ -799,20 +992,43 @@ int alloc_state(pcg_solver* S) {
   S->m = v + 9 * S->ld;
   S->nv = v + 10 * S->ld;
   S->b = v + 11 * S->ld;
-  const int maxp = std::max(S->n_partials, 1);
+  const int maxp = std::max(S->grid, 1);
   e = cudaMalloc(&S->partials, (size_t)2 * maxp * 4 * sizeof(double));
   if (e != cudaSuccess) return set_error(PCG_ENOMEM, "solver: partials allocation failed");
   cudaMemsetAsync(S->partials, 0, (size_t)2 * maxp * 4 * sizeof(double), S->stream);
-  if (cudaMalloc(&S->dpart, kDotGrid * sizeof(double)) != cudaSuccess ||
+  if (cudaMalloc(&S->seqbuf, 8 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&S->dpart, kDotGrid * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&S->dots_ws, (size_t)kDotGrid * 4 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&S->dots4, 4 * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&S->rec_dev, kRecBytes) != cudaSuccess)
+      cudaMalloc(&S->rec_dev, kRecBytes) != cudaSuccess ||
+      cudaMalloc(&S->comm, kCommBytes) != cudaSuccess)
     return set_error(PCG_ENOMEM, "solver: workspace allocation failed");
   cudaMemsetAsync(S->rec_dev, 0, kRecBytes, S->stream);
+  cudaMemsetAsync(S->comm, 0, kCommBytes, S->stream);
   for (int k = 0; k < 2; ++k)
     if (cudaMallocHost(&S->rec_host[k], kRecBytes) != cudaSuccess)
       return set_error(PCG_ENOMEM, "solver: pinned record allocation failed");
-  return PCG_OK;
+  return cuda_status(cudaStreamSynchronize(S->stream), "solver: workspace init");
+}
+
+// What the next prologue reduces, per mode
+ReduceIn reduce_in(pcg_solver* S) {
+  ReduceIn R;
+  R.arrive = nullptr;
+  R.arrive_per_it = 0;
+  if (S->connected) {
+    R.pin = reinterpret_cast<const double*>(S->comm + kCommSlots);
+    R.n_pin = kMaxRanks;  // slots are laid out [2][kMaxRanks][4]; unused ranks stay 0
+    R.arrive = reinterpret_cast<const unsigned long long*>(S->comm);
+    R.arrive_per_it = (unsigned long long)S->world * kXchgBlocks;
+  } else if (S->opt.dot_mode == PCG_DOT_SEQ) {
+    R.pin = S->seqbuf;
+    R.n_pin = 1;
+  } else {
+    R.pin = S->partials;
+    R.n_pin = S->grid;
+  }
+  return R;
 }
 
 template <typename RP>
@@ -836,8 +1052,8 @@ FusedParams<RP> fused_params(pcg_solver* S) {
   Record R = record_at(S->rec_dev);
   P.C = R.C;
   P.hist = R.hist;
-  P.partials = S->partials;
-  P.n_partials = S->opt.dot_mode == PCG_DOT_SEQ ? 1 : S->n_partials;
+  P.rin = reduce_in(S);
+  P.pout = S->partials;
   P.stages = S->stages;
   P.cap_val = S->cap_val;
   P.cap_col = S->cap_col;
@@ -854,7 +1070,7 @@ void launch_fused(pcg_solver* S, int k) {
   }
 }
 
-// enqueue graph step k (drift? -> iteration -> seq dots?)
+// enqueue graph step k (drift? -> iteration -> seq dots? -> exchange / SpMV)
 int enqueue_step(pcg_solver* S, int k) {
   Record R = record_at(S->rec_dev);
   cudaStream_t st = S->stream;
@@ -882,13 +1098,16 @@ int enqueue_step(pcg_solver* S, int k) {
     P.dinv = S->A.inv_diag;
     P.C = R.C;
     P.hist = R.hist;
-    P.partials = S->partials;
-    P.n_partials = S->opt.dot_mode == PCG_DOT_SEQ ? 1 : S->n_partials;
+    P.rin = reduce_in(S);
+    P.pout = S->partials;
     pipecg_k1_kernel<<<S->grid, 256, 0, st>>>(P, k);
   }
-  if (S->opt.dot_mode == PCG_DOT_SEQ)
+  if (S->opt.dot_mode == PCG_DOT_SEQ && !S->connected)
     seq_dots_kernel<<<1, 32, 0, st>>>(R.C, n, S->r, S->u, S->w[0], S->w[1], S->engine == 1,
-                                      S->partials, 1, k);
+                                      S->seqbuf, k);
+  if (S->connected)
+    iter_exchange_kernel<<<kXchgBlocks, 256, 0, st>>>(S->cp, R.C, k, S->partials, S->grid,
+                                                      S->w[0], S->w[1]);
   if (S->engine == 2) {
     const long long thr = S->n_long > 0 ? kLongRow : INT64_MAX;
     if (S->A.rp64) {
@@ -977,6 +1196,54 @@ void fill_result(pcg_solver* S, const Ctrl& c, pcg_result* res) {
   }
 }
 
+// Force-load every kernel the solver launches (see preload_ops in ops.cu:
+// lazy loading while a peer-waiting kernel spins can deadlock).
+int preload_solver() {
+  static std::mutex mu;
+  static std::set<int> done_devices;  // function attributes are per device
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (done_devices.count(dev)) return PCG_OK;
+  int rc = preload_ops();
+  if (rc) return rc;
+  cudaFuncAttributes a;
+  cudaError_t e = cudaSuccess;
+#define PCG_LOAD(k) if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void*)(k))
+  PCG_LOAD((pipecg_fused_kernel<int, 256>)); PCG_LOAD((pipecg_fused_kernel<int, 128>));
+  PCG_LOAD((pipecg_fused_kernel<int, 64>)); PCG_LOAD((pipecg_fused_kernel<long long, 256>));
+  PCG_LOAD((pipecg_fused_kernel<long long, 128>)); PCG_LOAD((pipecg_fused_kernel<long long, 64>));
+  PCG_LOAD(pipecg_k1_kernel); PCG_LOAD(gated_spmv_rows<int>); PCG_LOAD(gated_spmv_rows<long long>);
+  PCG_LOAD(gated_spmv_long<int>); PCG_LOAD(gated_spmv_long<long long>); PCG_LOAD(seq_dots_kernel);
+  PCG_LOAD(drift_partial_kernel<int>); PCG_LOAD(drift_partial_kernel<long long>);
+  PCG_LOAD(drift_finish_kernel); PCG_LOAD(advance_kernel); PCG_LOAD(init_ctrl_kernel);
+  PCG_LOAD(iter_exchange_kernel); PCG_LOAD(vec_exchange_kernel);
+  PCG_LOAD(init_dots_exchange_kernel); PCG_LOAD(snapshot_arrive_kernel); PCG_LOAD(xwait_kernel);
+  PCG_LOAD(tile_span_kernel<int>); PCG_LOAD(tile_span_kernel<long long>); PCG_LOAD(max_row_kernel);
+#undef PCG_LOAD
+#define PCG_SMEM(k) \
+  if (e == cudaSuccess)  \
+  e = cudaFuncSetAttribute((const void*)(k), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)
+  PCG_SMEM((pipecg_fused_kernel<int, 256>)); PCG_SMEM((pipecg_fused_kernel<int, 128>));
+  PCG_SMEM((pipecg_fused_kernel<int, 64>)); PCG_SMEM((pipecg_fused_kernel<long long, 256>));
+  PCG_SMEM((pipecg_fused_kernel<long long, 128>)); PCG_SMEM((pipecg_fused_kernel<long long, 64>));
+#undef PCG_SMEM
+  if (e != cudaSuccess) return cuda_status(e, "preload solver kernels");
+  done_devices.insert(dev);
+  return PCG_OK;
+}
+
+int comm_failed(const Ctrl& c) {
+  if (c.status != PCG_ECOMM_STATUS) return PCG_OK;
+  char buf[256];
+  snprintf(buf, sizeof(buf),
+           "distributed exchange timed out (a peer rank stalled): %s wait at iteration %lld saw "
+           "%llu of %llu arrivals (arrive_base %llu)",
+           c.diag_where == 1 ? "iteration" : "setup", c.bd_it, c.diag_seen, c.diag_target,
+           c.arrive_base);
+  return set_error(PCG_ECOMM, buf);
+}
+
 }  // namespace
 
 extern "C" {
@@ -988,6 +1255,8 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     return set_error(PCG_ERANGE, "solver_create: >= 2^31 rows per device; shard the matrix");
   if (!A->rp64 && A->nnz >= (1LL << 31))
     return set_error(PCG_ERANGE, "solver_create: nnz >= 2^31 needs int64 row pointers");
+  int prc = preload_solver();
+  if (prc) return prc;
   pcg_solver* S = new pcg_solver();
   S->A = *A;
   if (opts) S->opt = *opts;
@@ -996,10 +1265,12 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     S->opt.engine = 0;
     S->opt.chunk = 0;
     S->opt.use_graphs = 1;
+    S->opt.max_sms = 0;
   }
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&S->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (S->opt.max_sms > 0 && S->opt.max_sms < S->num_sms) S->num_sms = S->opt.max_sms;
   int rc = cuda_status(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking), "stream");
   if (!rc) rc = cuda_status(cudaEventCreateWithFlags(&S->ev_in, cudaEventDisableTiming), "event");
   for (int k = 0; k < 2 && !rc; ++k)
@@ -1033,11 +1304,10 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   }
   S->engine = engine;
   if (engine == 2) {
-    S->grid = kDotGrid;
-    S->n_partials = kDotGrid;
+    S->grid = std::min<int>(kDotGrid, 4 * S->num_sms);
+    S->n_partials = S->grid;
     if (max_row > (unsigned long long)kLongRow) {
       int64_t cnt = 0;
-      // count first, then fill
       rc = pipecg_b200_find_long_rows(A->n_rows, A->rp64, A->rowptr, kLongRow, nullptr, 0, &cnt,
                                       S->stream);
       if (!rc && cnt > 0) {
@@ -1073,10 +1343,12 @@ int pipecg_b200_solver_destroy(pcg_solver* S) {
   }
   cudaFree(S->vbuf);
   cudaFree(S->partials);
+  cudaFree(S->seqbuf);
   cudaFree(S->dpart);
   cudaFree(S->dots_ws);
   cudaFree(S->dots4);
   cudaFree(S->rec_dev);
+  cudaFree(S->comm);
   cudaFree(S->long_rows);
   if (S->ev_in) cudaEventDestroy(S->ev_in);
   if (S->stream) cudaStreamDestroy(S->stream);
@@ -1084,10 +1356,73 @@ int pipecg_b200_solver_destroy(pcg_solver* S) {
   return PCG_OK;
 }
 
+int pipecg_b200_solver_comm_info(pcg_solver* S, void** vbuf, int64_t* ld, void** comm) {
+  if (!S) return set_error(PCG_EINVAL, "solver_comm_info: null solver");
+  if (vbuf) *vbuf = S->vbuf;
+  if (ld) *ld = (int64_t)S->ld;
+  if (comm) *comm = S->comm;
+  return PCG_OK;
+}
+
+int pipecg_b200_ipc_get_handle(void* dev_ptr, void* handle_out) {
+  if (!dev_ptr || !handle_out) return set_error(PCG_EINVAL, "ipc_get_handle: null");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, dev_ptr);
+  if (e != cudaSuccess) return cuda_status(e, "cudaIpcGetMemHandle");
+  memcpy(handle_out, &h, sizeof(h));
+  return PCG_OK;
+}
+
+int pipecg_b200_ipc_open(const void* handle, void** dev_ptr_out) {
+  if (!handle || !dev_ptr_out) return set_error(PCG_EINVAL, "ipc_open: null");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  return cuda_status(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess),
+                     "cudaIpcOpenMemHandle");
+}
+
+int pipecg_b200_ipc_close(void* dev_ptr) {
+  return cuda_status(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
+}
+
+int pipecg_b200_solver_connect(pcg_solver* S, int rank, int world, void* const* peer_vbuf,
+                               const int64_t* peer_ld, void* const* peer_comm, int64_t n_send,
+                               const int32_t* send_row, const int32_t* send_peer,
+                               const int64_t* send_dst) {
+  if (!S || world < 1 || world > kMaxRanks || rank < 0 || rank >= world || !peer_vbuf ||
+      !peer_ld || !peer_comm || (n_send > 0 && (!send_row || !send_peer || !send_dst)))
+    return set_error(PCG_EINVAL, "solver_connect: bad arguments");
+  if (S->engine != 1)
+    return set_error(PCG_EINVAL, "solver_connect: distributed mode needs the fused engine");
+  S->rank = rank;
+  S->world = world;
+  CommParams cp{};
+  cp.rank = rank;
+  cp.world = world;
+  for (int q = 0; q < world; ++q) {
+    cp.peer_vbuf[q] = static_cast<char*>(peer_vbuf[q]);
+    cp.peer_ld[q] = peer_ld[q];
+    cp.peer_comm[q] = static_cast<char*>(peer_comm[q]);
+  }
+  cp.n_send = n_send;
+  cp.send_row = send_row;
+  cp.send_peer = send_peer;
+  cp.send_dst = reinterpret_cast<const long long*>(send_dst);
+  S->cp = cp;
+  S->connected = true;
+  for (int k = 0; k < 2; ++k) {  // graphs captured without the exchange are stale
+    for (auto& kv : S->graphs[k]) cudaGraphExecDestroy(kv.second);
+    S->graphs[k].clear();
+  }
+  return PCG_OK;
+}
+
 int pipecg_b200_solver_init(pcg_solver* S, const double* b, const double* x0, double tolerance,
                             int64_t max_iterations, int64_t drift_check_interval, void* stream) {
   if (!S || !b || !x0) return set_error(PCG_EINVAL, "solver_init: bad arguments");
   if (max_iterations < 1) return set_error(PCG_EINVAL, "solver_init: max_iterations < 1");
+  if (S->connected && drift_check_interval > 0)
+    return set_error(PCG_EINVAL, "solver_init: drift samples are single-GPU only");
   cudaStream_t st = S->stream;
   cudaEventRecord(S->ev_in, (cudaStream_t)stream);
   cudaStreamWaitEvent(st, S->ev_in, 0);
@@ -1096,17 +1431,35 @@ int pipecg_b200_solver_init(pcg_solver* S, const double* b, const double* x0, do
   S->tol = tolerance;
   S->max_it = max_iterations;
   S->drift_k = drift_check_interval;
+  Record R = record_at(S->rec_dev);
+  cudaMemsetAsync(&R.C->comm_error, 0, sizeof(int), st);
   // solvers.py:305-321
   cudaMemcpyAsync(S->b, b, bytes, cudaMemcpyDeviceToDevice, st);
   cudaMemcpyAsync(S->x, x0, bytes, cudaMemcpyDeviceToDevice, st);
+  if (S->connected) {  // x halo (r = b - A x reads it)
+    snapshot_arrive_kernel<<<1, 32, 0, st>>>(R.C, S->comm);
+    vec_exchange_kernel<<<kXchgBlocks, 256, 0, st>>>(S->cp, 4, S->x);
+    S->xtarget += (unsigned long long)S->world * kXchgBlocks;
+    xwait_kernel<<<1, 32, 0, st>>>(S->comm, S->xtarget, R.C);
+  }
   int rc = spmv_any(n, S->A.rp64, S->A.rowptr, S->A.col, S->A.val, S->x, S->b, S->r,
                     S->long_rows, S->n_long, 1, st);  // r = b - A x
   if (rc) return rc;
   rc = pipecg_b200_jacobi_apply(n, S->A.inv_diag, S->r, S->u, st);  // u = M^-1 r
   if (rc) return rc;
+  if (S->connected) {  // u halo (w = A u reads it)
+    vec_exchange_kernel<<<kXchgBlocks, 256, 0, st>>>(S->cp, 6, S->u);
+    S->xtarget += (unsigned long long)S->world * kXchgBlocks;
+    xwait_kernel<<<1, 32, 0, st>>>(S->comm, S->xtarget, R.C);
+  }
   rc = spmv_any(n, S->A.rp64, S->A.rowptr, S->A.col, S->A.val, S->u, nullptr, S->w[0],
                 S->long_rows, S->n_long, 0, st);  // w = A u
   if (rc) return rc;
+  if (S->connected) {  // w halo (F(0) computes n = A M^-1 w on the fly)
+    vec_exchange_kernel<<<kXchgBlocks, 256, 0, st>>>(S->cp, 7, S->w[0]);
+    S->xtarget += (unsigned long long)S->world * kXchgBlocks;
+    xwait_kernel<<<1, 32, 0, st>>>(S->comm, S->xtarget, R.C);
+  }
   if (S->engine == 2) {
     rc = pipecg_b200_jacobi_apply(n, S->A.inv_diag, S->w[0], S->m, st);  // m = M^-1 w
     if (rc) return rc;
@@ -1114,7 +1467,7 @@ int pipecg_b200_solver_init(pcg_solver* S, const double* b, const double* x0, do
                   S->long_rows, S->n_long, 0, st);  // n = A m
     if (rc) return rc;
   }
-  S->mn_valid = S->engine == 2;
+  S->mn_valid = S->engine == 2 && !S->connected;
   cudaMemsetAsync(S->z, 0, bytes, st);
   cudaMemsetAsync(S->q, 0, bytes, st);
   cudaMemsetAsync(S->s, 0, bytes, st);
@@ -1123,9 +1476,18 @@ int pipecg_b200_solver_init(pcg_solver* S, const double* b, const double* x0, do
   const double* db[4] = {S->u, S->u, S->u, S->b};
   rc = dots_any(n, 4, da, db, S->opt.dot_mode, S->dots4, S->dots_ws, st);
   if (rc) return rc;
-  Record R = record_at(S->rec_dev);
-  init_ctrl_kernel<<<1, 256, 0, st>>>(R.C, S->dots4, tolerance, max_iterations,
-                                      drift_check_interval, R.hist, R.dit);
+  if (S->connected) {
+    init_dots_exchange_kernel<<<1, 32, 0, st>>>(S->cp, S->dots4);
+    S->xtarget += (unsigned long long)S->world;
+    xwait_kernel<<<1, 32, 0, st>>>(S->comm, S->xtarget, R.C);
+    init_ctrl_kernel<<<1, 256, 0, st>>>(
+        R.C, reinterpret_cast<const double*>(S->comm + kCommISlots), S->world, tolerance,
+        max_iterations, drift_check_interval, R.hist, R.dit,
+        reinterpret_cast<const unsigned long long*>(S->comm));
+  } else {
+    init_ctrl_kernel<<<1, 256, 0, st>>>(R.C, S->dots4, 1, tolerance, max_iterations,
+                                        drift_check_interval, R.hist, R.dit, nullptr);
+  }
   S->host_base = 0;
   S->initialized = true;
   return cuda_status(cudaGetLastError(), "solver_init");
@@ -1148,7 +1510,7 @@ int pipecg_b200_solver_run(pcg_solver* S, pcg_result* res, double* history_host,
   bool first = true;
   while (true) {
     const int nxt = cur ^ 1;
-    const bool more = S->host_base < S->max_it + 1;  // F(max_it) must run to stop
+    const bool more = S->host_base <= S->max_it;  // F(max_it) must run to stop
     if (more) {
       chunk_lo[nxt] = S->host_base;
       rc = launch_chunk(S, K, nxt);
@@ -1166,6 +1528,7 @@ int pipecg_b200_solver_run(pcg_solver* S, pcg_result* res, double* history_host,
     long long hi = chunk_lo[cur] + K - 1;  // last iteration whose entry this chunk ran
     if (c.status == PCG_STOPPED) hi = std::min(hi, c.final_it);
     if (c.status == PCG_BREAKDOWN) hi = std::min(hi, c.bd_it);
+    if (c.status == PCG_ECOMM_STATUS) hi = -1;
     for (long long itx = next_hist; itx <= hi; ++itx) {
       if (history_host && hist_n < hist_cap) history_host[hist_n] = R.hist[itx & (kHistRing - 1)];
       hist_n++;
@@ -1195,7 +1558,7 @@ int pipecg_b200_solver_run(pcg_solver* S, pcg_result* res, double* history_host,
   res->n_history = hist_n;
   res->n_drift = drift_n;
   S->mn_valid = false;
-  return PCG_OK;
+  return comm_failed(c);
 }
 
 int pipecg_b200_solver_enqueue(pcg_solver* S, int64_t count) {
@@ -1225,11 +1588,12 @@ int pipecg_b200_solver_poll(pcg_solver* S, pcg_result* res) {
   if (e != cudaSuccess) return cuda_status(e, "poll copy");
   memset(res, 0, sizeof(*res));
   fill_result(S, c, res);
-  return PCG_OK;
+  return comm_failed(c);
 }
 
 int pipecg_b200_solver_state(pcg_solver* S, double** ptrs) {
   if (!S || !ptrs) return set_error(PCG_EINVAL, "solver_state: bad arguments");
+  if (S->connected) return set_error(PCG_EINVAL, "solver_state: single-GPU only");
   Ctrl c{};
   cudaError_t e = cudaStreamSynchronize(S->stream);
   if (e == cudaSuccess) e = cudaMemcpy(&c, S->rec_dev, sizeof(Ctrl), cudaMemcpyDeviceToHost);

@@ -170,20 +170,25 @@ class DeviceOptions:
       kernel + SpMV kernel; general matrices with very long rows).
     chunk: iterations per CUDA-graph chunk (0 = sized from the problem).
     use_graphs: capture chunks as CUDA graphs.
+    max_sms: size persistent grids for this many SMs (0 = all; used when
+      several solvers must be co-resident on one GPU).
     """
 
     dot_mode: str = "tree"
     engine: str = "auto"
     chunk: int = 0
     use_graphs: bool = True
+    max_sms: int = 0
 
     def native(self) -> _lib.PcgOptions:
         eng = {"auto": 0, "fused": 1, "two": 2}[self.engine]
         dm = {"tree": _lib.PCG_DOT_TREE, "seq": _lib.PCG_DOT_SEQ}[self.dot_mode]
-        return _lib.PcgOptions(dm, eng, int(self.chunk), 1 if self.use_graphs else 0)
+        return _lib.PcgOptions(dm, eng, int(self.chunk), 1 if self.use_graphs else 0,
+                               int(self.max_sms))
 
     def key(self) -> tuple:
-        return (self.dot_mode, self.engine, int(self.chunk), bool(self.use_graphs))
+        return (self.dot_mode, self.engine, int(self.chunk), bool(self.use_graphs),
+                int(self.max_sms))
 
 
 def _check_system(A, b, x0):

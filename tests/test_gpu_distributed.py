@@ -1,0 +1,143 @@
+"""The multi-GPU device protocol on ONE B200: P "virtual ranks" in one
+process (one thread + one stream + one solver each, grids sized so all
+ranks are co-resident), exchanging halo rows and dot partials through the
+same peer-memory exchange kernel and in-kernel waits that the multi-process
+NVLink path uses (only the pointer source differs: direct vs CUDA IPC).
+
+Parity: the sharded solve must match the single-GPU solve within the
+oracle's reorder envelope (only the dot reduction order differs; every row
+of the sharded SpMV is bitwise the global one)."""
+
+from __future__ import annotations
+
+import math
+import threading
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+pb = pytest.importorskip("paper_2105_06176_b200")
+torch = pytest.importorskip("torch")
+from paper_2105_06176_b200 import distributed as D  # noqa: E402
+
+
+def run_virtual(world, make_problem, cfg, chunk=0):
+    G = D.LocalGroup(world)
+    out = [None] * world
+    errs = []
+    opts = pb.DeviceOptions(max_sms=max(8, 148 // world - 10), chunk=chunk)
+
+    def work(r):
+        try:
+            torch.cuda.set_device(0)
+            g = G.view(r)
+            prob = make_problem(g)
+            xt, b = D.manufactured_local(prob)
+            x, rep = D.pipecg_solve_distributed(prob, b, torch.zeros_like(b), cfg, g, opts)
+            out[r] = (x.cpu().numpy(), rep, prob.plan)
+        except BaseException as e:  # noqa: BLE001
+            errs.append((r, repr(e)))
+            G._barrier.abort()
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    assert not errs, errs
+    return out
+
+
+@pytest.mark.parametrize("world,kind,n", [(2, "3d7", 40), (3, "3d7", 33), (2, "2d5", 200),
+                                          (4, "3d27", 24)])
+def test_virtual_ranks_match_single_gpu(cuda, world, kind, n):
+    A = oracle.stencil(kind, n)
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=20000, record_history=True)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=20000)
+    out = run_virtual(world, lambda g: D.shard_stencil(kind, n, g), cfg)
+    x = np.concatenate([o[0] for o in out])
+    reps = [o[1] for o in out]
+    assert len({r.iterations for r in reps}) == 1          # ranks agree
+    assert all(r.history == reps[0].history for r in reps)  # identical scalars on every rank
+    rep = reps[0]
+    assert rep.converged
+    assert abs(rep.iterations - ref.iterations) <= 1
+    assert oracle.history_gap(rep.history, ref.history) <= 1e-10
+    assert np.max(np.abs(x - ref.x)) / np.max(np.abs(ref.x)) <= 1e-8
+    assert np.max(np.abs(x - x_true)) < 1e-6
+
+
+def test_virtual_ranks_host_csr_irregular(cuda):
+    """shard_csr on a non-stencil SPD matrix (irregular halo sets)."""
+    import scipy.sparse as sp
+
+    n = 3000
+    M = sp.random(n, n, density=0.003, random_state=11, format="csr")
+    M = (M + M.T).tocsr()
+    M.data[:] = -np.abs(M.data)
+    M = M + sp.diags(np.asarray(np.abs(M).sum(axis=1)).ravel() + 1.0)
+    M = M.tocsr()
+    M.sort_indices()
+    A = pb.CsrMatrix(n, n, M.indptr, M.indices, M.data)
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=5000, record_history=True)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=5000)
+    out = run_virtual(3, lambda g: D.shard_csr(A, g), cfg)
+    x = np.concatenate([o[0] for o in out])
+    rep = out[0][1]
+    assert abs(rep.iterations - ref.iterations) <= 1
+    assert oracle.history_gap(rep.history, ref.history) <= 1e-10
+    assert np.max(np.abs(x - ref.x)) / np.max(np.abs(ref.x)) <= 1e-8
+
+
+def test_virtual_ranks_repeat_and_max_iterations(cuda):
+    """Two solves on the same connected solvers (counters carry over) and an
+    iteration cap that ends mid-chunk."""
+    kind, n, world = "3d7", 24, 2
+    G = D.LocalGroup(world)
+    res = [None] * world
+    errs = []
+
+    def work(r):
+        try:
+            torch.cuda.set_device(0)
+            g = G.view(r)
+            prob = D.shard_stencil(kind, n, g)
+            solver = D.DistributedSolver(prob, g, pb.DeviceOptions(max_sms=60, chunk=8))
+            xt, b = D.manufactured_local(prob)
+            reps = []
+            for maxit in (5, 13, 2000):
+                cfg = pb.SolverConfig(tolerance=1e-10, max_iterations=maxit, record_history=True)
+                x, rep = D.pipecg_solve_distributed(prob, b, torch.zeros_like(b), cfg, g,
+                                                    solver=solver)
+                reps.append((rep, x.cpu().numpy()))
+            solver.close()
+            res[r] = reps
+        except BaseException as e:  # noqa: BLE001
+            errs.append((r, repr(e)))
+            G._barrier.abort()
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    assert not errs, errs
+    A = oracle.stencil(kind, n)
+    x_true, b, x0, d = oracle.manufactured(A)
+    for k, maxit in enumerate((5, 13, 2000)):
+        ref = oracle.pipecg_solve(A, b, x0, d, tol=1e-10, max_iterations=maxit)
+        rep = res[0][k][0]
+        assert abs(rep.iterations - ref.iterations) <= 1
+        assert oracle.history_gap(rep.history, ref.history) <= 1e-10
+        x = np.concatenate([res[r][k][1] for r in range(world)])
+        assert np.max(np.abs(x - ref.x)) / max(np.max(np.abs(ref.x)), 1e-300) <= 1e-8
+        if maxit < 100:
+            assert rep.iterations == maxit and not rep.converged

@@ -1,0 +1,168 @@
+"""CPU-only tests: the C-ABI library loads and exports what include/*.h
+declares, the host-side API mirrors the reference's types and errors, and
+the product path refuses to run without a GPU (no CPU fallback)."""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+pb = pytest.importorskip("paper_2105_06176_b200")
+from paper_2105_06176_b200 import _lib  # noqa: E402
+
+HEADER = ROOT / "include" / "pipecg_b200.h"
+
+
+def header_functions():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"\b(pipecg_b200_\w+)\s*\(", text)))
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    L = _lib.load()
+    for name in header_functions():
+        assert hasattr(L, name), name
+    assert L.pipecg_b200_version().startswith(b"pipecg_b200")
+
+
+def test_binding_table_matches_header():
+    assert sorted(_lib.EXPORTED) == header_functions()
+
+
+def test_dynamic_symbol_table():
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    exported = set(re.findall(r"\b(pipecg_b200_\w+)\b", out))
+    assert set(header_functions()) <= exported
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_fused_kernel_uses_bulk_copy_engine():
+    sass = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], capture_output=True,
+                          text=True).stdout
+    assert "UBLKCP" in sass  # cp.async.bulk (TMA engine)
+    assert "SYNCS" in sass   # mbarrier
+
+
+def test_host_abi_rejects_bad_arguments_without_gpu():
+    L = _lib.load()
+    assert L.pipecg_b200_stencil_shape(3, 10, None, None) == _lib.PCG_EINVAL
+    N, nnz = ctypes.c_int64(), ctypes.c_int64()
+    assert L.pipecg_b200_stencil_shape(7, 256, ctypes.byref(N), ctypes.byref(nnz)) == 0
+    assert (N.value, nnz.value) == (16_777_216, 117_047_296)
+    assert L.pipecg_b200_stencil_shape(27, 400, ctypes.byref(N), ctypes.byref(nnz)) == 0
+    assert (N.value, nnz.value) == (64_000_000, 1_719_374_392)
+    assert L.pipecg_b200_stencil_shape(7, 1145, ctypes.byref(N), ctypes.byref(nnz)) == 0
+    assert (N.value, nnz.value) == (1_501_123_625, 10_499_999_225)
+    assert L.pipecg_b200_solver_create(None, None, None) == _lib.PCG_EINVAL
+    assert b"bad matrix" in L.pipecg_b200_last_error()
+
+
+@pytest.mark.parametrize("kind,n", [("2d5", 9), ("3d7", 6), ("3d27", 5), ("p125", 6)])
+def test_stencil_prefix_closed_form_matches_oracle(kind, n):
+    import oracle
+
+    A = oracle.stencil(kind, n)
+    k = {"2d5": 5, "3d7": 7, "3d27": 27, "p125": 125}[kind]
+    out = ctypes.c_int64()
+    for r in range(A.n_rows + 1):
+        _lib.call("pipecg_b200_stencil_prefix", k, n, r, ctypes.byref(out))
+        assert out.value == A.row_offsets[r]
+
+
+def test_no_cpu_fallback():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    A = pb.csr_from_dense(np.eye(3))
+    with pytest.raises(RuntimeError, match="CUDA"):
+        pb.spmv(A, np.ones(3))
+    with pytest.raises(RuntimeError, match="CUDA"):
+        pb.pipecg_solve(A, np.ones(3), np.zeros(3), pb.JacobiPreconditioner(np.ones(3)))
+
+
+def test_product_never_imports_oracle():
+    for path in (ROOT / "paper_2105_06176_b200").rglob("*.py"):
+        src = path.read_text()
+        assert not re.search(r"^\s*(import|from)\s+oracle", src, re.M), path
+        assert "oracle/" not in src.replace("oracle/ is", ""), path
+
+
+# --- host-side mirror of the reference types (solvers.py, sparse.py) --------
+
+def test_solver_config_defaults_and_validation():
+    cfg = pb.SolverConfig()
+    assert (cfg.tolerance, cfg.max_iterations, cfg.record_history, cfg.drift_check_interval) == \
+        (1e-5, 10000, False, 0)
+    for kw in ({"tolerance": 0.0}, {"tolerance": -1.0}, {"max_iterations": 0},
+               {"drift_check_interval": -1}):
+        with pytest.raises(ValueError):
+            pb.SolverConfig(**kw)
+
+
+def test_pipecg_scalars_known_answers():
+    assert pb.pipecg_scalars(0.5, 123.0, 0.25, 456.0, 0) == (2.0, 0.0)
+    assert pb.pipecg_scalars(1.0, 2.0, 3.0, 0.5, 1) == (0.5, 0.5)
+    with pytest.raises(pb.SolverBreakdown) as e:
+        pb.pipecg_scalars(1.0, 1.0, 0.0, 1.0, 0)
+    assert e.value.quantity == "alpha denominator" and e.value.iteration == 0
+    with pytest.raises(pb.SolverBreakdown):
+        pb.pipecg_scalars(1.0, 1.0, 1.0, 1.0, 3)
+    with pytest.raises(pb.SolverBreakdown):
+        pb.pipecg_scalars(1.0, 1.0, math.inf, 1.0, 0)
+
+
+def test_breakdown_fields():
+    err = pb.SolverBreakdown("delta", 7, -2.5)
+    assert (err.quantity, err.iteration, err.value) == ("delta", 7, -2.5)
+    assert "delta" in str(err) and isinstance(err, RuntimeError)
+
+
+def test_report_round_trip():
+    rep = pb.SolveReport(converged=True, iterations=3, final_norm=1e-9, strategy="pipecg",
+                         history=[1.0, 0.1, 0.01, 1e-9], phase_times={"setup": 0.1, "iterations": 0.2},
+                         drift_history=[[2, 1e-12]])
+    back = pb.SolveReport.from_dict(rep.to_dict())
+    assert back == rep
+
+
+def test_csr_validation_mirrors_reference():
+    with pytest.raises(ValueError, match="n_rows \\+ 1"):
+        pb.CsrMatrix(2, 2, [0, 1], [0], [1.0])
+    with pytest.raises(ValueError, match="start at 0"):
+        pb.CsrMatrix(1, 1, [1, 1], [], [])
+    with pytest.raises(ValueError, match="nondecreasing"):
+        pb.CsrMatrix(2, 2, [0, 2, 1], [0, 1], [1.0, 1.0])
+    with pytest.raises(ValueError, match="out of range"):
+        pb.CsrMatrix(1, 1, [0, 1], [3], [1.0])
+    with pytest.raises(ValueError, match="strictly increasing"):
+        pb.CsrMatrix(1, 3, [0, 2], [1, 1], [1.0, 1.0])
+    A = pb.csr_from_dense(np.array([[1.0, 0.0], [2.0, 3.0]]))
+    assert A.nnz == 3 and A.shape == (2, 2)
+    np.testing.assert_array_equal(A.to_dense(), [[1.0, 0.0], [2.0, 3.0]])
+    assert A.take_rows(1).nnz == 1
+
+
+def test_poisson125_shape_and_capacity():
+    assert pb.poisson125_shape(5) == (125, 19 ** 3)
+    with pytest.raises(ValueError):
+        pb.poisson125_shape(4)
+    with pytest.raises(pb.CapacityError):
+        pb.generate_poisson125(200)
+
+
+def test_device_options():
+    o = pb.DeviceOptions(dot_mode="seq", engine="two", chunk=8, use_graphs=False).native()
+    assert (o.dot_mode, o.engine, o.chunk, o.use_graphs) == (_lib.PCG_DOT_SEQ, 2, 8, 0)
