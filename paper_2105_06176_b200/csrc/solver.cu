@@ -34,6 +34,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <set>
@@ -269,6 +270,7 @@ struct FusedParams {
   int stages;
   int cap_val;  // doubles per stage
   int cap_col;  // ints per stage
+  int flags;    // experiment switches (PIPECG_B200_FLAGS): 1 = gathers read the row itself
 };
 
 template <typename RP, int TR>
@@ -304,8 +306,15 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel(FusedParams<RP> P
 
   const int tid = threadIdx.x;
   const bool producer = tid < 32;
-  const long long my_tiles =
-      blockIdx.x < P.n_tiles ? (P.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // tile ownership: round-robin (tile t -> CTA t % grid) keeps the whole GPU
+  // sweeping one narrow window of rows, so the far (+-n^2) gathers of every
+  // CTA hit the same L2-resident planes; contiguous ranges per CTA (flag 2)
+  // measured 28% slower at 256^3 (far gathers re-read from HBM).
+  const bool contiguous = (P.flags & 2) != 0;
+  const long long t_lo = contiguous ? (long long)blockIdx.x * P.n_tiles / gridDim.x : blockIdx.x;
+  const long long t_hi = contiguous ? (long long)(blockIdx.x + 1) * P.n_tiles / gridDim.x : P.n_tiles;
+  const long long t_step = contiguous ? 1 : gridDim.x;
+  const long long my_tiles = t_hi > t_lo ? (t_hi - t_lo + t_step - 1) / t_step : 0;
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
@@ -320,7 +329,7 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel(FusedParams<RP> P
   uint64_t pol = 0;
   auto issue = [&](long long j) {
     const int s = (int)(j % S);
-    const long long t = blockIdx.x + j * gridDim.x;
+    const long long t = t_lo + j * t_step;
     const long long t0 = t * TR;
     const long long rows = min((long long)TR, P.n - t0);
     const long long e0 = P.rp[t0], e1 = P.rp[t0 + rows];
@@ -382,7 +391,7 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel(FusedParams<RP> P
   double acc[3] = {0.0, 0.0, 0.0};
   for (long long j = 0; j < my_tiles; ++j) {
     const int s = (int)(j % S);
-    const long long t = blockIdx.x + j * gridDim.x;
+    const long long t = t_lo + j * t_step;
     const long long t0 = t * TR;
     const long long rows = min((long long)TR, P.n - t0);
     unsigned char* sb = stage0 + (size_t)s * SB;
@@ -411,7 +420,7 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel(FusedParams<RP> P
         for (int t = 0; t < 8; ++t) {
           const long long k = k0 + t;
           if (k < hi) {
-            const int c = col_s[k - cb];
+            const int c = (P.flags & 1) ? (int)i : col_s[k - cb];
             av[t] = val_s[k - vb];
             mv[t] = mul(ldg_nc(P.dinv + c), ldg_nc(w_old + c));  // m = M^-1 w
           }
@@ -877,6 +886,7 @@ struct pcg_solver {
   bool connected = false;
   CommParams cp{};
   unsigned long long xtarget = 0;  // cumulative setup arrivals expected
+  int flags = 0;                   // experiment switches (env PIPECG_B200_FLAGS)
 };
 
 namespace {
@@ -910,8 +920,11 @@ int plan_tr(pcg_solver* S, FusedPlan* plan) {
   p.cap_val = (int)((std::max<unsigned long long>(h[1], 2) + 1) & ~1ULL);
   const size_t sb = (size_t)L::stage_bytes(p.cap_val, p.cap_col);
   const size_t sm_budget = 228 * 1024, cta_max = 227 * 1024;
+  // 2 CTAs/SM (register-bound at ~90 regs), then as FEW stages as possible:
+  // shared memory not taken by stages is L1 for the gathers (S=2 measured
+  // 3-5% faster than S=3 at 256^3 and 400^3).
   for (int bps = 2; bps >= 1 && !p.stages; --bps) {
-    for (int st = 4; st >= 2; --st) {
+    for (int st = 2; st <= 4; ++st) {
       const size_t need = L::kHeader + st * sb;
       if (need <= cta_max && (need + 1024) * bps <= sm_budget) {
         p.stages = st;
@@ -959,6 +972,22 @@ int fused_setup(pcg_solver* S) {
   if (rc) return rc;
   const FusedPlan* best = nullptr;
   int best_score = 0;
+  // experiment overrides: PIPECG_B200_TR / _STAGES / _BPS
+  const char* e_tr = getenv("PIPECG_B200_TR");
+  const char* e_st = getenv("PIPECG_B200_STAGES");
+  const char* e_bps = getenv("PIPECG_B200_BPS");
+  for (FusedPlan* p : {&p256, &p128, &p64}) {
+    if (e_tr && atoi(e_tr) != p->tr) p->stages = 0;
+    if (p->stages && e_st) {
+      using L256 = FusedLayout<RP, 256>;
+      (void)sizeof(L256);
+      const int want = atoi(e_st);
+      const size_t per = (p->smem - 1024) / p->stages;
+      p->stages = want;
+      p->smem = 1024 + per * want;
+    }
+    if (p->stages && e_bps) p->bps = atoi(e_bps);
+  }
   for (const FusedPlan* p : {&p256, &p128, &p64}) {
     const int score = p->stages ? p->tr * p->bps : 0;
     if (score > best_score) {
@@ -1057,6 +1086,7 @@ FusedParams<RP> fused_params(pcg_solver* S) {
   P.stages = S->stages;
   P.cap_val = S->cap_val;
   P.cap_col = S->cap_col;
+  P.flags = S->flags;
   return P;
 }
 
@@ -1259,6 +1289,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   if (prc) return prc;
   pcg_solver* S = new pcg_solver();
   S->A = *A;
+  if (const char* f = getenv("PIPECG_B200_FLAGS")) S->flags = atoi(f);
   if (opts) S->opt = *opts;
   else {
     S->opt.dot_mode = PCG_DOT_TREE;
