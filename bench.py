@@ -250,7 +250,8 @@ def time_iterations(pb, torch, A, pc_d, warmup: int, steps: int, options=None):
     res = solver.poll()
     ok = res.status == 0 and res.iterations == warmup + steps
     info = {"engine": res.engine, "graph_launches": res.graph_launches, "ok": bool(ok),
-            "status": res.status, "iterations_run": res.iterations}
+            "status": res.status, "iterations_run": res.iterations,
+            "tune_ms": [round(v, 4) for v in res.tune_ms]}
     solver.close()
     del b, x0, x_true
     return ms, info
@@ -357,7 +358,11 @@ def run_b200(args):
                                "(BASELINE.json configs[1])",
                    "N": N, "nnz": nnz, "parallelism": "single GPU",
                    "l2": "inputs (4.4 GB/iteration) >> 126 MB L2; no flush needed",
-                   "engine": {1: "fused", 2: "two-kernel"}.get(info["engine"], "?")},
+                   "engine": {2: "two-kernel", 3: "fused-A (consumer gathers)",
+                              4: "fused-B (gather warps)"}.get(info["engine"], "?"),
+                   "autotune_ms_per_iter": {"fused_A": info["tune_ms"][0],
+                                            "fused_B": info["tune_ms"][1],
+                                            "two_kernel": info["tune_ms"][2]}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None,
                      "bytes_per_iteration": B,

@@ -48,6 +48,7 @@ namespace pcg {
 
 constexpr int kHistRing = 1024;
 constexpr int kMaxRanks = 8;
+constexpr long long kTuneRows = 1LL << 16;  // autotune engines for >= 64K rows
 constexpr int kXchgBlocks = 16;    // exchange-kernel grid (identical on every rank)
 constexpr int PCG_ECOMM_STATUS = 3; // Ctrl.status: peer exchange timed out  // history / drift ring (power of two)
 constexpr int kMaxChunk = 256;   // 2*kMaxChunk <= kHistRing
@@ -263,6 +264,7 @@ struct FusedParams {
   const double* dinv;
   double* vec[7];  // z q s p x r u (in place)
   double* w[2];    // ping-pong: read w[it&1], write w[(it+1)&1]
+  double* m[2];    // variant C: stored m = M^-1 w, ping-pong like w
   Ctrl* C;
   double* hist;
   ReduceIn rin;   // what the prologue reduces
@@ -275,6 +277,241 @@ struct FusedParams {
 
 template <typename RP, int TR>
 struct FusedLayout {
+  static constexpr int kGatherWarps = TR / 64;  // 4 / 2 / 1 for TR = 256 / 128 / 64
+  static constexpr int kThreads = 32 + 32 * kGatherWarps + TR;
+  static constexpr int kRpBytes = (int)(((TR + 1) * sizeof(RP) + 15) / 16 * 16);
+  static constexpr int kVecBytes = TR * 8;
+  static constexpr int kVecs = 9;  // z q s p x r u (streams) + w_old + dinv (own rows)
+  // stage: row pointers | 9 vectors | values | columns | m per nonzero
+  __host__ __device__ static int stage_bytes(int cap_val, int cap_col) {
+    return kRpBytes + kVecs * kVecBytes + cap_val * 8 + (cap_col * 4 + 15) / 16 * 16 +
+           cap_val * 8;
+  }
+  // barriers + reduction scratch + decision, in front of the stages
+  static constexpr int kHeader = 1024;
+};
+
+// Warp-specialised CTA:
+//   warp 0            producer: bulk-copies (TMA engine) each tile's row
+//                     pointers, the 7 streamed vectors, w_old and dinv of the
+//                     tile rows, CSR values and columns into an S-stage ring;
+//   warps 1..GW       gather: m_k = dinv[c_k] * w_old[c_k] for every nonzero
+//                     of the tile into shared memory (the only scattered
+//                     global loads, issued in batches, running ahead of the
+//                     consumers by up to S-1 tiles);
+//   warps GW+1..      consumers: one row per thread, everything from shared
+//                     memory: n_i = sum a_k m_k in CSR order, m_i, the eight
+//                     recurrences, streaming stores, dot partials.
+// Barriers per stage: full (TMA bytes landed), gdone (m written by all
+// gather threads), empty (all consumer warps done with the stage).
+template <typename RP, int TR>
+__global__ void __launch_bounds__(FusedLayout<RP, TR>::kThreads) pipecg_fused_kernel(FusedParams<RP> P,
+                                                                                     int step) {
+  using L = FusedLayout<RP, TR>;
+  constexpr int NT = TR;                          // consumer threads
+  constexpr int NG = 32 * L::kGatherWarps;        // gather threads
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [stages]
+  uint64_t* gdone = full + 8;                          // [stages]
+  uint64_t* empty = full + 16;                         // [stages]
+  double* red = reinterpret_cast<double*>(smem + 256);  // 3*8 (+)
+  volatile int* decision = reinterpret_cast<volatile int*>(smem + 512);
+  double* sc = reinterpret_cast<double*>(smem + 768);  // alpha, beta
+  unsigned char* stage0 = smem + L::kHeader;
+  const int SB = L::stage_bytes(P.cap_val, P.cap_col);
+  const int S = P.stages;
+
+  Ctrl* C = P.C;
+  if (read_status(C) != PCG_RUNNING) return;
+  const long long it = C->base_it + step;
+  const double* w_old = P.w[it & 1];
+  double* w_new = P.w[(it + 1) & 1];
+
+  const int tid = threadIdx.x;
+  const int role = tid < 32 ? 0 : (tid < 32 + NG ? 1 : 2);  // producer / gather / consumer
+  // tile ownership: round-robin (tile t -> CTA t % grid) keeps the whole GPU
+  // sweeping one narrow window of rows, so the far (+-n^2) gathers of every
+  // CTA hit the same L2-resident planes; contiguous ranges per CTA (flag 2)
+  // measured 28% slower at 256^3 (far gathers re-read from HBM).
+  const bool contiguous = (P.flags & 2) != 0;
+  const long long t_lo = contiguous ? (long long)blockIdx.x * P.n_tiles / gridDim.x : blockIdx.x;
+  const long long t_hi = contiguous ? (long long)(blockIdx.x + 1) * P.n_tiles / gridDim.x : P.n_tiles;
+  const long long t_step = contiguous ? 1 : gridDim.x;
+  const long long my_tiles = t_hi > t_lo ? (t_hi - t_lo + t_step - 1) / t_step : 0;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&gdone[s], NG);
+      mbar_init(&empty[s], NT / 32);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  // ---- producer: stage tile j of this block into stage j % S -------------
+  uint64_t pol = 0;
+  auto issue = [&](long long j) {
+    const int s = (int)(j % S);
+    const long long t = t_lo + j * t_step;
+    const long long t0 = t * TR;
+    const long long rows = min((long long)TR, P.n - t0);
+    const long long e0 = P.rp[t0], e1 = P.rp[t0 + rows];
+    const long long cb = e0 & ~3LL, ce = (e1 + 3) & ~3LL;
+    const long long vb = e0 & ~1LL, ve = (e1 + 1) & ~1LL;
+    const uint32_t b_rp = (uint32_t)((((rows + 1) * sizeof(RP)) + 15) / 16 * 16);
+    const uint32_t b_vec = (uint32_t)((rows * 8 + 15) / 16 * 16);
+    const uint32_t b_val = (uint32_t)((ve - vb) * 8);
+    const uint32_t b_col = (uint32_t)((ce - cb) * 4);
+    unsigned char* sb = stage0 + (size_t)s * SB;
+    mbar_arrive_expect_tx(&full[s], b_rp + L::kVecs * b_vec + b_val + b_col);
+    bulk_g2s(sb, P.rp + t0, b_rp, &full[s], pol);
+#pragma unroll
+    for (int k = 0; k < 7; ++k)
+      bulk_g2s(sb + L::kRpBytes + k * L::kVecBytes, P.vec[k] + t0, b_vec, &full[s], pol);
+    // w_old and dinv of the tile rows: default L2 policy (neighbours gather them)
+    bulk_g2s_nohint(sb + L::kRpBytes + 7 * L::kVecBytes, w_old + t0, b_vec, &full[s]);
+    bulk_g2s_nohint(sb + L::kRpBytes + 8 * L::kVecBytes, P.dinv + t0, b_vec, &full[s]);
+    unsigned char* sval = sb + L::kRpBytes + L::kVecs * L::kVecBytes;
+    if (b_val) bulk_g2s(sval, P.val + vb, b_val, &full[s], pol);
+    if (b_col) bulk_g2s(sval + (size_t)P.cap_val * 8, P.col + cb, b_col, &full[s], pol);
+  };
+
+  if (tid == 0) {
+    pol = policy_evict_first();
+    for (long long j = 0; j < my_tiles && j < S; ++j) issue(j);
+  }
+
+  // ---- prologue (consumers): entry scalars, guards, stop test ------------
+  if (role == 2) {
+    const int lt = tid - 32 - NG;
+    const Step stp = prologue<NT>(C, P.hist, P.rin, it, lt, red, 1, blockIdx.x == 0 && lt == 0);
+    if (lt == 0) {
+      sc[0] = stp.alpha;
+      sc[1] = stp.beta;
+      *decision = stp.go;
+    }
+  }
+  __syncthreads();
+  const int go = *decision;
+  if (!go) {
+    // drain the copies already in flight before the CTA retires
+    if (tid == 0)
+      for (long long j = 0; j < my_tiles && j < S; ++j) mbar_wait(&full[j], 0);
+    return;
+  }
+
+  if (role == 0) {
+    if (tid == 0) {
+      for (long long j = S; j < my_tiles; ++j) {
+        const int s = (int)(j % S);
+        mbar_wait(&empty[s], (uint32_t)((j / S - 1) & 1));
+        issue(j);
+      }
+    }
+    return;
+  }
+
+  if (role == 1) {
+    // ---- gather warps: m_k = dinv[c_k] * w_old[c_k] for the whole tile ----
+    const int gt = tid - 32;
+    constexpr int U = 8;
+    for (long long j = 0; j < my_tiles; ++j) {
+      const int s = (int)(j % S);
+      const long long t = t_lo + j * t_step;
+      const long long rows = min((long long)TR, P.n - t * TR);
+      unsigned char* sb = stage0 + (size_t)s * SB;
+      const RP* rp_s = reinterpret_cast<const RP*>(sb);
+      const double* val_s = reinterpret_cast<const double*>(sb + L::kRpBytes + L::kVecs * L::kVecBytes);
+      const int* col_s = reinterpret_cast<const int*>(val_s + P.cap_val);
+      double* m_s = const_cast<double*>(val_s) + P.cap_val + (P.cap_col * 4 + 15) / 16 * 2;
+      mbar_wait(&full[s], (uint32_t)((j / S) & 1));
+      const long long e0 = rp_s[0], e1 = rp_s[rows];
+      const long long cb = e0 & ~3LL, vb = e0 & ~1LL;
+      for (long long k0 = e0 + gt; k0 < e1; k0 += (long long)NG * U) {
+        double dv[U], wv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const long long k = k0 + (long long)u * NG;
+          if (k < e1) {
+            const int c = col_s[k - cb];
+            dv[u] = ldg_nc(P.dinv + c);
+            wv[u] = ldg_nc(w_old + c);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const long long k = k0 + (long long)u * NG;
+          if (k < e1) m_s[k - vb] = mul(dv[u], wv[u]);  // m = M^-1 w (jacobi_apply)
+        }
+      }
+      mbar_arrive(&gdone[s]);
+    }
+    return;
+  }
+
+  // ---- consumers ----------------------------------------------------------
+  const int lt = tid - 32 - NG;
+  const double alpha = sc[0], beta = sc[1];
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (long long j = 0; j < my_tiles; ++j) {
+    const int s = (int)(j % S);
+    const long long t = t_lo + j * t_step;
+    const long long t0 = t * TR;
+    const long long rows = min((long long)TR, P.n - t0);
+    unsigned char* sb = stage0 + (size_t)s * SB;
+    const RP* rp_s = reinterpret_cast<const RP*>(sb);
+    const double* v_s = reinterpret_cast<const double*>(sb + L::kRpBytes);
+    const double* val_s = reinterpret_cast<const double*>(sb + L::kRpBytes + L::kVecs * L::kVecBytes);
+    const double* m_s = val_s + P.cap_val + (P.cap_col * 4 + 15) / 16 * 2;
+    const long long i = t0 + lt;
+    mbar_wait(&full[s], (uint32_t)((j / S) & 1));
+    mbar_wait(&gdone[s], (uint32_t)((j / S) & 1));
+    if (lt < rows) {
+      const long long e0 = rp_s[0];
+      const long long vb = e0 & ~1LL;
+      const long long lo = rp_s[lt] - vb, hi = rp_s[lt + 1] - vb;
+      // n_i = sum_k a_ik * m_ck in CSR order (kernels.py:64-70 on m)
+      double nacc = 0.0;
+      for (long long k = lo; k < hi; ++k) nacc = add(nacc, mul(val_s[k], m_s[k]));
+      const double wi = v_s[7 * TR + lt], di = v_s[8 * TR + lt];
+      const double mi = mul(di, wi);
+      const double zi = add(nacc, mul(beta, v_s[0 * TR + lt]));
+      const double qi = add(mi, mul(beta, v_s[1 * TR + lt]));
+      const double si = add(wi, mul(beta, v_s[2 * TR + lt]));
+      const double ui = v_s[6 * TR + lt];
+      const double pi = add(ui, mul(beta, v_s[3 * TR + lt]));
+      const double xi = add(v_s[4 * TR + lt], mul(alpha, pi));
+      const double ri = sub(v_s[5 * TR + lt], mul(alpha, si));
+      const double un = sub(ui, mul(alpha, qi));
+      const double wn = sub(wi, mul(alpha, zi));
+      st_stream(P.vec[0] + i, zi);
+      st_stream(P.vec[1] + i, qi);
+      st_stream(P.vec[2] + i, si);
+      st_stream(P.vec[3] + i, pi);
+      st_stream(P.vec[4] + i, xi);
+      st_stream(P.vec[5] + i, ri);
+      st_stream(P.vec[6] + i, un);
+      w_new[i] = wn;  // default policy: the next iteration gathers it
+      acc[0] = add(acc[0], mul(ri, un));
+      acc[1] = add(acc[1], mul(wn, un));
+      acc[2] = add(acc[2], mul(un, un));
+    }
+    __syncwarp();
+    if ((lt & 31) == 0) mbar_arrive(&empty[s]);
+  }
+  group_sum<3, NT>(acc, lt, red, 1);
+  if (lt == 0) {
+    double* out = P.pout + (size_t)(it & 1) * (size_t)gridDim.x * 4 + (size_t)blockIdx.x * 4;
+    out[0] = acc[0];
+    out[1] = acc[1];
+    out[2] = acc[2];
+    out[3] = 0.0;
+  }
+}
+
+template <typename RP, int TR>
+struct FusedLayoutA {
   static constexpr int kRpBytes = (int)(((TR + 1) * sizeof(RP) + 15) / 16 * 16);
   static constexpr int kVecBytes = TR * 8;
   __host__ __device__ static int stage_bytes(int cap_val, int cap_col) {
@@ -284,9 +521,18 @@ struct FusedLayout {
   static constexpr int kHeader = 1024;
 };
 
-template <typename RP, int TR>
-__global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel(FusedParams<RP> P, int step) {
-  using L = FusedLayout<RP, TR>;
+// Variants A and C (consumer warps gather themselves; no gather warps, 7
+// staged vectors, L1 serves part of the gathers).
+//   A (MG = false): gathers dinv[c] and w_old[c] and forms m_c on the fly
+//                   (17 vector streams, 2 gather loads per nonzero);
+//   C (MG = true):  gathers a stored m_old[c] and writes m_new = dinv*w_new
+//                   beside w_new (19 vector streams, 1 gather load per
+//                   nonzero -- better for wide rows).
+// Both round exactly like the reference (m is the same rounded product).
+// Selected per matrix by the setup-time autotuner.
+template <typename RP, int TR, bool MG>
+__global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_a(FusedParams<RP> P, int step) {
+  using L = FusedLayoutA<RP, TR>;
   constexpr int NT = TR;  // consumer threads
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);       // [stages]
@@ -422,7 +668,8 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel(FusedParams<RP> P
           if (k < hi) {
             const int c = (P.flags & 1) ? (int)i : col_s[k - cb];
             av[t] = val_s[k - vb];
-            mv[t] = mul(ldg_nc(P.dinv + c), ldg_nc(w_old + c));  // m = M^-1 w
+            mv[t] = MG ? ldg_nc(P.m[it & 1] + c)                      // stored m
+                       : mul(ldg_nc(P.dinv + c), ldg_nc(w_old + c));  // m = M^-1 w
           }
         }
 #pragma unroll
@@ -447,6 +694,7 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel(FusedParams<RP> P
       st_stream(P.vec[5] + i, ri);
       st_stream(P.vec[6] + i, un);
       st_stream(w_new + i, wn);
+      if (MG) P.m[(it + 1) & 1][i] = mul(di, wn);  // solvers.py:358 (gathered next iteration)
       acc[0] = add(acc[0], mul(ri, un));
       acc[1] = add(acc[1], mul(wn, un));
       acc[2] = add(acc[2], mul(un, un));
@@ -719,15 +967,18 @@ __device__ __forceinline__ void signal_peers(const CommParams& CP, bool iteratio
 // the same ping-pong buffer, push this rank's (r,u),(w,u),(u,u) partial to
 // every rank's slot[it&1][rank], then signal every rank.  Stream-ordered
 // after F(it), so every gather of F(it) on this rank is complete.
+// The pushed vector is the one the next iteration gathers: w (vectors 7/8 of
+// the block) for variants A/B, the stored m (vectors 9/12) for variant C.
 __global__ void __launch_bounds__(256) iter_exchange_kernel(CommParams CP, const Ctrl* C, int step,
                                                              const double* pout, int n_pout,
-                                                             const double* w0, const double* w1) {
+                                                             const double* g0, const double* g1,
+                                                             int vec0, int vec1) {
   __shared__ double red[3 * 8];
   if (read_status(C) != PCG_RUNNING) return;
   const long long it = C->base_it + step;
   const int wi = (int)((it + 1) & 1);
-  const double* src = wi ? w1 : w0;
-  const int vec = 7 + wi;  // w0 / w1 are vectors 7 / 8 of the block
+  const double* src = wi ? g1 : g0;
+  const int vec = wi ? vec1 : vec0;
   for (long long e = blockIdx.x * 256LL + threadIdx.x; e < CP.n_send; e += (long long)gridDim.x * 256) {
     const int q = CP.send_peer[e];
     double* dst = reinterpret_cast<double*>(CP.peer_vbuf[q]) + (size_t)vec * CP.peer_ld[q];
@@ -845,6 +1096,12 @@ using namespace pcg;
 // ===========================================================================
 // host runtime
 // ===========================================================================
+struct FusedPlan {
+  int variant = 0;  // 0: consumer gathers dinv,w (A); 1: gather warps (B); 2: stored m (C)
+  int tr = 0, stages = 0, bps = 0, cap_val = 0, cap_col = 0, grid = 0, score = 0;
+  size_t smem = 0;
+};
+
 struct pcg_solver {
   pcg_matrix A{};
   pcg_options opt{};
@@ -862,7 +1119,8 @@ struct pcg_solver {
   double* vbuf = nullptr;
   size_t ld = 0;  // padded vector length (>= local columns incl. halo)
   double *z = nullptr, *q = nullptr, *s = nullptr, *p = nullptr, *x = nullptr, *r = nullptr,
-         *u = nullptr, *w[2] = {nullptr, nullptr}, *m = nullptr, *nv = nullptr, *b = nullptr;
+         *u = nullptr, *w[2] = {nullptr, nullptr}, *m = nullptr, *nv = nullptr, *b = nullptr,
+         *m2 = nullptr;  // m ping-pong partner (fused variant C)
   double* partials = nullptr;  // block partials [2][grid][4]
   double* seqbuf = nullptr;    // sequential-dot results [2][1][4]
   double* dpart = nullptr;
@@ -887,45 +1145,54 @@ struct pcg_solver {
   CommParams cp{};
   unsigned long long xtarget = 0;  // cumulative setup arrivals expected
   int flags = 0;                   // experiment switches (env PIPECG_B200_FLAGS)
+  int variant = 1;                 // fused kernel variant in use
+  FusedPlan plans[3];              // per fused variant (stages == 0: does not fit)
+  double tune_ms[4] = {0, 0, 0, 0};  // autotune ms/iteration: fused A, B, C, engine 2
 };
 
 namespace {
 
-struct FusedPlan {
-  int tr = 0, stages = 0, bps = 0, cap_val = 0, cap_col = 0;
-  size_t smem = 0;
-};
-
-// Staged span of the widest tile of `tr` rows -> the shared-memory plan
-// (stages, CTAs/SM) for that tile height, or an empty plan if it cannot fit.
-template <typename RP, int TR>
-int plan_tr(pcg_solver* S, FusedPlan* plan) {
-  using L = FusedLayout<RP, TR>;
+// Tile spans: widest staged column / value span of any tile of `tr` rows.
+template <typename RP>
+int tile_spans(pcg_solver* S, int tr, int* cap_col, int* cap_val) {
   const long long n = S->A.n_rows;
-  const long long n_tiles = (n + TR - 1) / TR;
+  const long long n_tiles = (n + tr - 1) / tr;
   unsigned long long* mx = nullptr;
   cudaError_t e = cudaMallocAsync(&mx, 2 * sizeof(unsigned long long), S->stream);
   if (e != cudaSuccess) return cuda_status(e, "tile span alloc");
   cudaMemsetAsync(mx, 0, 2 * sizeof(unsigned long long), S->stream);
   tile_span_kernel<RP><<<elementwise_grid(n_tiles), 256, 0, S->stream>>>(
-      n, n_tiles, TR, static_cast<const RP*>(S->A.rowptr), mx, mx + 1);
+      n, n_tiles, tr, static_cast<const RP*>(S->A.rowptr), mx, mx + 1);
   unsigned long long h[2] = {0, 0};
   cudaMemcpyAsync(h, mx, sizeof(h), cudaMemcpyDeviceToHost, S->stream);
   cudaFreeAsync(mx, S->stream);
   e = cudaStreamSynchronize(S->stream);
   if (e != cudaSuccess) return cuda_status(e, "tile span");
+  *cap_col = (int)std::max<unsigned long long>(h[0], 4);
+  *cap_val = (int)((std::max<unsigned long long>(h[1], 2) + 1) & ~1ULL);
+  return PCG_OK;
+}
+
+// Shared-memory plan for one (variant, tile height): as many CTAs/SM as
+// fit (<= 2), then as FEW stages as possible (shared memory not taken by
+// stages is L1 for the gathers: S=2 measured 3-5% faster than S=3 for
+// variant A at 256^3 and 400^3), then the occupancy the kernel really gets.
+template <typename RP, int TR, int V>
+int plan_one(pcg_solver* S, int cap_col, int cap_val, FusedPlan* out) {
   FusedPlan p;
+  p.variant = V;
   p.tr = TR;
-  p.cap_col = (int)std::max<unsigned long long>(h[0], 4);
-  p.cap_val = (int)((std::max<unsigned long long>(h[1], 2) + 1) & ~1ULL);
-  const size_t sb = (size_t)L::stage_bytes(p.cap_val, p.cap_col);
+  p.cap_col = cap_col;
+  p.cap_val = cap_val;
+  const size_t sb = V == 1 ? (size_t)FusedLayout<RP, TR>::stage_bytes(cap_val, cap_col)
+                           : (size_t)FusedLayoutA<RP, TR>::stage_bytes(cap_val, cap_col);
+  const size_t hdr = 1024;
   const size_t sm_budget = 228 * 1024, cta_max = 227 * 1024;
-  // 2 CTAs/SM (register-bound at ~90 regs), then as FEW stages as possible:
-  // shared memory not taken by stages is L1 for the gathers (S=2 measured
-  // 3-5% faster than S=3 at 256^3 and 400^3).
+  const char* e_st = getenv("PIPECG_B200_STAGES");  // experiment override
   for (int bps = 2; bps >= 1 && !p.stages; --bps) {
     for (int st = 2; st <= 4; ++st) {
-      const size_t need = L::kHeader + st * sb;
+      if (e_st && atoi(e_st) != st) continue;
+      const size_t need = hdr + st * sb;
       if (need <= cta_max && (need + 1024) * bps <= sm_budget) {
         p.stages = st;
         p.bps = bps;
@@ -934,71 +1201,77 @@ int plan_tr(pcg_solver* S, FusedPlan* plan) {
       }
     }
   }
-  *plan = p;
+  if (!p.stages) {
+    *out = p;
+    return PCG_OK;
+  }
+  int occ = 0;
+  cudaError_t e =
+      V == 1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pipecg_fused_kernel<RP, TR>,
+                                                             FusedLayout<RP, TR>::kThreads, p.smem)
+      : V == 2 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                     &occ, pipecg_fused_kernel_a<RP, TR, true>, TR + 32, p.smem)
+               : cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                     &occ, pipecg_fused_kernel_a<RP, TR, false>, TR + 32, p.smem);
+  if (e != cudaSuccess) return cuda_status(e, "fused occupancy");
+  occ = std::min(occ, p.bps);
+  if (occ < 1) {
+    p.stages = 0;
+    *out = p;
+    return PCG_OK;
+  }
+  const long long n_tiles = (S->A.n_rows + TR - 1) / TR;
+  p.grid = (int)std::max<long long>(std::min<long long>((long long)occ * S->num_sms, n_tiles), 1);
+  p.score = occ * TR;  // resident consumer rows per SM
+  *out = p;
   return PCG_OK;
 }
 
-template <typename RP, int TR>
-int finish_plan(pcg_solver* S, const FusedPlan& p) {
-  auto kfn = pipecg_fused_kernel<RP, TR>;
-  // the dynamic-smem limit was raised to the maximum once in preload_solver():
-  // it is per-function global state shared by every solver in the process
-  int occ = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, TR + 32, p.smem);
-  if (e != cudaSuccess) return cuda_status(e, "fused occupancy");
-  if (occ < 1) return PCG_EINVAL;
-  occ = std::min(occ, p.bps);
-  S->tr = TR;
-  S->n_tiles = (S->A.n_rows + TR - 1) / TR;
+// Best tile height for a variant: most resident consumer rows per SM; ties
+// -> taller tiles.
+template <typename RP, int V>
+int plan_variant(pcg_solver* S, const int* cc, const int* cv, FusedPlan* best) {
+  FusedPlan p[3];
+  int rc = plan_one<RP, 256, V>(S, cc[0], cv[0], &p[0]);
+  if (!rc) rc = plan_one<RP, 128, V>(S, cc[1], cv[1], &p[1]);
+  if (!rc) rc = plan_one<RP, 64, V>(S, cc[2], cv[2], &p[2]);
+  if (rc) return rc;
+  const char* e_tr = getenv("PIPECG_B200_TR");  // experiment override
+  *best = FusedPlan();
+  for (int k = 0; k < 3; ++k) {
+    if (!p[k].stages || (e_tr && atoi(e_tr) != p[k].tr)) continue;
+    if (p[k].score > best->score) *best = p[k];
+  }
+  return PCG_OK;
+}
+
+template <typename RP>
+int fused_setup(pcg_solver* S) {
+  int cc[3], cv[3];
+  const int trs[3] = {256, 128, 64};
+  for (int k = 0; k < 3; ++k) {
+    int rc = tile_spans<RP>(S, trs[k], &cc[k], &cv[k]);
+    if (rc) return rc;
+  }
+  int rc = plan_variant<RP, 0>(S, cc, cv, &S->plans[0]);
+  if (!rc) rc = plan_variant<RP, 1>(S, cc, cv, &S->plans[1]);
+  if (!rc) rc = plan_variant<RP, 2>(S, cc, cv, &S->plans[2]);
+  if (rc) return rc;
+  if (!S->plans[0].stages && !S->plans[1].stages && !S->plans[2].stages)
+    return PCG_EINVAL;  // -> engine 2
+  return PCG_OK;
+}
+
+void apply_plan(pcg_solver* S, const FusedPlan& p) {
+  S->variant = p.variant;
+  S->tr = p.tr;
+  S->n_tiles = (S->A.n_rows + p.tr - 1) / p.tr;
   S->stages = p.stages;
   S->cap_val = p.cap_val;
   S->cap_col = p.cap_col;
   S->smem = p.smem;
-  long long g = (long long)occ * S->num_sms;
-  if (g > S->n_tiles) g = S->n_tiles;
-  S->grid = (int)std::max<long long>(g, 1);
-  S->n_partials = S->grid;
-  return PCG_OK;
-}
-
-// Pick the tile height (256/128/64 rows) that keeps the most consumer
-// threads resident per SM with >= 2 bulk-copy stages; ties -> taller tiles.
-template <typename RP>
-int fused_setup(pcg_solver* S) {
-  FusedPlan p256, p128, p64;
-  int rc = plan_tr<RP, 256>(S, &p256);
-  if (!rc) rc = plan_tr<RP, 128>(S, &p128);
-  if (!rc) rc = plan_tr<RP, 64>(S, &p64);
-  if (rc) return rc;
-  const FusedPlan* best = nullptr;
-  int best_score = 0;
-  // experiment overrides: PIPECG_B200_TR / _STAGES / _BPS
-  const char* e_tr = getenv("PIPECG_B200_TR");
-  const char* e_st = getenv("PIPECG_B200_STAGES");
-  const char* e_bps = getenv("PIPECG_B200_BPS");
-  for (FusedPlan* p : {&p256, &p128, &p64}) {
-    if (e_tr && atoi(e_tr) != p->tr) p->stages = 0;
-    if (p->stages && e_st) {
-      using L256 = FusedLayout<RP, 256>;
-      (void)sizeof(L256);
-      const int want = atoi(e_st);
-      const size_t per = (p->smem - 1024) / p->stages;
-      p->stages = want;
-      p->smem = 1024 + per * want;
-    }
-    if (p->stages && e_bps) p->bps = atoi(e_bps);
-  }
-  for (const FusedPlan* p : {&p256, &p128, &p64}) {
-    const int score = p->stages ? p->tr * p->bps : 0;
-    if (score > best_score) {
-      best = p;
-      best_score = score;
-    }
-  }
-  if (!best) return PCG_EINVAL;  // rows too wide for shared memory -> engine 2
-  if (best->tr == 256) return finish_plan<RP, 256>(S, *best);
-  if (best->tr == 128) return finish_plan<RP, 128>(S, *best);
-  return finish_plan<RP, 64>(S, *best);
+  S->grid = p.grid;
+  S->n_partials = p.grid;
 }
 
 int alloc_state(pcg_solver* S) {
@@ -1021,6 +1294,7 @@ int alloc_state(pcg_solver* S) {
   S->m = v + 9 * S->ld;
   S->nv = v + 10 * S->ld;
   S->b = v + 11 * S->ld;
+  S->m2 = v + 12 * S->ld;
   const int maxp = std::max(S->grid, 1);
   e = cudaMalloc(&S->partials, (size_t)2 * maxp * 4 * sizeof(double));
   if (e != cudaSuccess) return set_error(PCG_ENOMEM, "solver: partials allocation failed");
@@ -1078,6 +1352,8 @@ FusedParams<RP> fused_params(pcg_solver* S) {
   P.vec[6] = S->u;
   P.w[0] = S->w[0];
   P.w[1] = S->w[1];
+  P.m[0] = S->m;
+  P.m[1] = S->m2;
   Record R = record_at(S->rec_dev);
   P.C = R.C;
   P.hist = R.hist;
@@ -1093,10 +1369,25 @@ FusedParams<RP> fused_params(pcg_solver* S) {
 template <typename RP>
 void launch_fused(pcg_solver* S, int k) {
   const FusedParams<RP> P = fused_params<RP>(S);
-  switch (S->tr) {
-    case 256: pipecg_fused_kernel<RP, 256><<<S->grid, 256 + 32, S->smem, S->stream>>>(P, k); break;
-    case 128: pipecg_fused_kernel<RP, 128><<<S->grid, 128 + 32, S->smem, S->stream>>>(P, k); break;
-    default: pipecg_fused_kernel<RP, 64><<<S->grid, 64 + 32, S->smem, S->stream>>>(P, k); break;
+  cudaStream_t st = S->stream;
+  if (S->variant == 1) {
+    switch (S->tr) {
+      case 256: pipecg_fused_kernel<RP, 256><<<S->grid, FusedLayout<RP, 256>::kThreads, S->smem, st>>>(P, k); break;
+      case 128: pipecg_fused_kernel<RP, 128><<<S->grid, FusedLayout<RP, 128>::kThreads, S->smem, st>>>(P, k); break;
+      default: pipecg_fused_kernel<RP, 64><<<S->grid, FusedLayout<RP, 64>::kThreads, S->smem, st>>>(P, k); break;
+    }
+  } else if (S->variant == 2) {
+    switch (S->tr) {
+      case 256: pipecg_fused_kernel_a<RP, 256, true><<<S->grid, 256 + 32, S->smem, st>>>(P, k); break;
+      case 128: pipecg_fused_kernel_a<RP, 128, true><<<S->grid, 128 + 32, S->smem, st>>>(P, k); break;
+      default: pipecg_fused_kernel_a<RP, 64, true><<<S->grid, 64 + 32, S->smem, st>>>(P, k); break;
+    }
+  } else {
+    switch (S->tr) {
+      case 256: pipecg_fused_kernel_a<RP, 256, false><<<S->grid, 256 + 32, S->smem, st>>>(P, k); break;
+      case 128: pipecg_fused_kernel_a<RP, 128, false><<<S->grid, 128 + 32, S->smem, st>>>(P, k); break;
+      default: pipecg_fused_kernel_a<RP, 64, false><<<S->grid, 64 + 32, S->smem, st>>>(P, k); break;
+    }
   }
 }
 
@@ -1136,8 +1427,9 @@ int enqueue_step(pcg_solver* S, int k) {
     seq_dots_kernel<<<1, 32, 0, st>>>(R.C, n, S->r, S->u, S->w[0], S->w[1], S->engine == 1,
                                       S->seqbuf, k);
   if (S->connected)
-    iter_exchange_kernel<<<kXchgBlocks, 256, 0, st>>>(S->cp, R.C, k, S->partials, S->grid,
-                                                      S->w[0], S->w[1]);
+    iter_exchange_kernel<<<kXchgBlocks, 256, 0, st>>>(
+        S->cp, R.C, k, S->partials, S->grid, S->variant == 2 ? S->m : S->w[0],
+        S->variant == 2 ? S->m2 : S->w[1], S->variant == 2 ? 9 : 7, S->variant == 2 ? 12 : 8);
   if (S->engine == 2) {
     const long long thr = S->n_long > 0 ? kLongRow : INT64_MAX;
     if (S->A.rp64) {
@@ -1209,7 +1501,8 @@ int auto_chunk(pcg_solver* S) {
 
 void fill_result(pcg_solver* S, const Ctrl& c, pcg_result* res) {
   res->status = c.status;
-  res->engine = S->engine;
+  res->engine = S->engine == 1 ? 3 + S->variant : 2;
+  for (int k = 0; k < 4; ++k) res->tune_ms[k] = S->tune_ms[k];
   res->graph_launches = S->graph_launches;
   res->norm0 = c.init.norm;
   res->breakdown_quantity = c.bd_code;
@@ -1243,6 +1536,13 @@ int preload_solver() {
   PCG_LOAD((pipecg_fused_kernel<int, 256>)); PCG_LOAD((pipecg_fused_kernel<int, 128>));
   PCG_LOAD((pipecg_fused_kernel<int, 64>)); PCG_LOAD((pipecg_fused_kernel<long long, 256>));
   PCG_LOAD((pipecg_fused_kernel<long long, 128>)); PCG_LOAD((pipecg_fused_kernel<long long, 64>));
+#define PCG_LOAD_A(MG) \
+  PCG_LOAD((pipecg_fused_kernel_a<int, 256, MG>)); PCG_LOAD((pipecg_fused_kernel_a<int, 128, MG>)); \
+  PCG_LOAD((pipecg_fused_kernel_a<int, 64, MG>)); PCG_LOAD((pipecg_fused_kernel_a<long long, 256, MG>)); \
+  PCG_LOAD((pipecg_fused_kernel_a<long long, 128, MG>)); PCG_LOAD((pipecg_fused_kernel_a<long long, 64, MG>))
+  PCG_LOAD_A(false);
+  PCG_LOAD_A(true);
+#undef PCG_LOAD_A
   PCG_LOAD(pipecg_k1_kernel); PCG_LOAD(gated_spmv_rows<int>); PCG_LOAD(gated_spmv_rows<long long>);
   PCG_LOAD(gated_spmv_long<int>); PCG_LOAD(gated_spmv_long<long long>); PCG_LOAD(seq_dots_kernel);
   PCG_LOAD(drift_partial_kernel<int>); PCG_LOAD(drift_partial_kernel<long long>);
@@ -1257,6 +1557,13 @@ int preload_solver() {
   PCG_SMEM((pipecg_fused_kernel<int, 256>)); PCG_SMEM((pipecg_fused_kernel<int, 128>));
   PCG_SMEM((pipecg_fused_kernel<int, 64>)); PCG_SMEM((pipecg_fused_kernel<long long, 256>));
   PCG_SMEM((pipecg_fused_kernel<long long, 128>)); PCG_SMEM((pipecg_fused_kernel<long long, 64>));
+#define PCG_SMEM_A(MG) \
+  PCG_SMEM((pipecg_fused_kernel_a<int, 256, MG>)); PCG_SMEM((pipecg_fused_kernel_a<int, 128, MG>)); \
+  PCG_SMEM((pipecg_fused_kernel_a<int, 64, MG>)); PCG_SMEM((pipecg_fused_kernel_a<long long, 256, MG>)); \
+  PCG_SMEM((pipecg_fused_kernel_a<long long, 128, MG>)); PCG_SMEM((pipecg_fused_kernel_a<long long, 64, MG>))
+  PCG_SMEM_A(false);
+  PCG_SMEM_A(true);
+#undef PCG_SMEM_A
 #undef PCG_SMEM
   if (e != cudaSuccess) return cuda_status(e, "preload solver kernels");
   done_devices.insert(dev);
@@ -1272,6 +1579,70 @@ int comm_failed(const Ctrl& c) {
            c.diag_where == 1 ? "iteration" : "setup", c.bd_it, c.diag_seen, c.diag_target,
            c.arrive_base);
   return set_error(PCG_ECOMM, buf);
+}
+
+__global__ void fill_kernel(double* p, long long n, double v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+// Setup-time autotuner: time a few real iterations (b = 1, x0 = 0, no stop
+// test) of every engine/variant that fits this matrix on this GPU and keep
+// the fastest.  Costs ~10 iterations once per solver; the state is
+// re-initialised by the caller's solver_init.
+int autotune(pcg_solver* S, int grid2, bool with_engine2) {
+  const long long n = S->A.n_rows;
+  cudaStream_t st = S->stream;
+  fill_kernel<<<elementwise_grid(n), 256, 0, st>>>(S->nv, n, 1.0);
+  fill_kernel<<<elementwise_grid(n), 256, 0, st>>>(S->z, n, 0.0);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int saved_graphs = S->opt.use_graphs;
+  S->opt.use_graphs = 0;
+  int best = -1;
+  float best_ms = 0.f;
+  int rc = PCG_OK;
+  for (int cand = 0; cand < (with_engine2 ? 4 : 3) && !rc; ++cand) {
+    if (cand < 3) {
+      if (!S->plans[cand].stages) continue;
+      S->engine = 1;
+      apply_plan(S, S->plans[cand]);
+    } else {
+      S->engine = 2;
+      S->grid = S->n_partials = grid2;
+    }
+    // b := n (ones), x0 := z (zeros); init copies them before overwriting
+    rc = pipecg_b200_solver_init(S, S->nv, S->z, 0.0, 1LL << 40, 0, st);
+    if (!rc) rc = launch_chunk(S, 1, 0);
+    cudaEventRecord(e0, st);
+    if (!rc) rc = launch_chunk(S, 3, 1);
+    cudaEventRecord(e1, st);
+    if (!rc) rc = cuda_status(cudaEventSynchronize(e1), "autotune");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms /= 3.f;
+    S->tune_ms[cand] = ms;
+    if (!rc && (best < 0 || ms < best_ms)) {
+      best = cand;
+      best_ms = ms;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  S->opt.use_graphs = saved_graphs;
+  S->initialized = false;
+  S->host_base = 0;
+  if (rc) return rc;
+  if (best < 3) {
+    S->engine = 1;
+    apply_plan(S, S->plans[best]);
+  } else {
+    S->engine = 2;
+    S->grid = S->n_partials = grid2;
+  }
+  return PCG_OK;
 }
 
 }  // namespace
@@ -1323,21 +1694,26 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     pipecg_b200_solver_destroy(S);
     return rc;
   }
-  int engine = S->opt.engine;
-  if (engine == 0) engine = max_row > (unsigned long long)kLongRow ? 2 : 1;
-  if (engine == 1) {
+  // engine: 0 auto (autotuned), 1 fused (heuristic variant), 2 two-kernel,
+  // 3 fused variant A, 4 fused variant B
+  const int req = S->opt.engine;
+  const bool has_long = max_row > (unsigned long long)kLongRow;
+  bool fused_ok = false;
+  if (req != 2 && !(req == 0 && has_long)) {
     rc = A->rp64 ? fused_setup<long long>(S) : fused_setup<int>(S);
-    if (rc == PCG_EINVAL && S->opt.engine == 0) engine = 2;  // too wide -> general engine
-    else if (rc) {
+    if (rc && rc != PCG_EINVAL) {
       pipecg_b200_solver_destroy(S);
-      return rc == PCG_EINVAL ? set_error(rc, "fused engine: tiles exceed shared memory") : rc;
+      return rc;
+    }
+    fused_ok = rc == PCG_OK;
+    if (req >= 3 && !S->plans[req - 3].stages) fused_ok = false;
+    if (!fused_ok && req != 0) {
+      pipecg_b200_solver_destroy(S);
+      return set_error(PCG_EINVAL, "fused engine: tiles exceed shared memory");
     }
   }
-  S->engine = engine;
-  if (engine == 2) {
-    S->grid = std::min<int>(kDotGrid, 4 * S->num_sms);
-    S->n_partials = S->grid;
-    if (max_row > (unsigned long long)kLongRow) {
+  if (!fused_ok || req == 0 || req == 2) {  // engine-2 resources (also an autotune candidate)
+    if (has_long) {
       int64_t cnt = 0;
       rc = pipecg_b200_find_long_rows(A->n_rows, A->rp64, A->rowptr, kLongRow, nullptr, 0, &cnt,
                                       S->stream);
@@ -1355,10 +1731,35 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
       }
     }
   }
+  const int grid2 = std::min<int>(kDotGrid, 4 * S->num_sms);
+  S->grid = std::max({grid2, S->plans[0].grid, S->plans[1].grid, S->plans[2].grid});
   rc = alloc_state(S);
   if (rc) {
     pipecg_b200_solver_destroy(S);
     return rc;
+  }
+  if (!fused_ok) {
+    S->engine = 2;
+    S->grid = S->n_partials = grid2;
+  } else if (req >= 3) {
+    S->engine = 1;
+    apply_plan(S, S->plans[req - 3]);
+  } else if (A->n_rows < kTuneRows) {
+    // small: no autotune; wide rows (> 12 nnz/row) gather the stored m (C)
+    const bool wide = A->nnz > 12 * A->n_rows;
+    const int order[3] = {wide ? 2 : 0, wide ? 0 : 2, 1};
+    S->engine = 1;
+    for (int k = 0; k < 3; ++k)
+      if (S->plans[order[k]].stages) {
+        apply_plan(S, S->plans[order[k]]);
+        break;
+      }
+  } else {
+    rc = autotune(S, grid2, req == 0);
+    if (rc) {
+      pipecg_b200_solver_destroy(S);
+      return rc;
+    }
   }
   *out = S;
   return PCG_OK;
@@ -1486,8 +1887,14 @@ int pipecg_b200_solver_init(pcg_solver* S, const double* b, const double* x0, do
   rc = spmv_any(n, S->A.rp64, S->A.rowptr, S->A.col, S->A.val, S->u, nullptr, S->w[0],
                 S->long_rows, S->n_long, 0, st);  // w = A u
   if (rc) return rc;
-  if (S->connected) {  // w halo (F(0) computes n = A M^-1 w on the fly)
-    vec_exchange_kernel<<<kXchgBlocks, 256, 0, st>>>(S->cp, 7, S->w[0]);
+  const bool stored_m = S->engine == 2 || S->variant == 2;
+  if (S->engine == 1 && S->variant == 2) {
+    rc = pipecg_b200_jacobi_apply(n, S->A.inv_diag, S->w[0], S->m, st);  // m = M^-1 w
+    if (rc) return rc;
+  }
+  if (S->connected) {  // halo of what F(0) gathers: w (A/B) or the stored m (C)
+    vec_exchange_kernel<<<kXchgBlocks, 256, 0, st>>>(S->cp, stored_m ? 9 : 7,
+                                                     stored_m ? S->m : S->w[0]);
     S->xtarget += (unsigned long long)S->world * kXchgBlocks;
     xwait_kernel<<<1, 32, 0, st>>>(S->comm, S->xtarget, R.C);
   }

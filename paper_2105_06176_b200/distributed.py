@@ -350,7 +350,8 @@ class DistributedSolver:
         opts = options or DeviceOptions()
         if opts.engine == "two":
             raise ValueError("the distributed path runs the fused engine")
-        opts = DeviceOptions(dot_mode=opts.dot_mode, engine="fused", chunk=opts.chunk,
+        engine = opts.engine if opts.engine.startswith("fused") else "fused"
+        opts = DeviceOptions(dot_mode=opts.dot_mode, engine=engine, chunk=opts.chunk,
                              use_graphs=opts.use_graphs, max_sms=opts.max_sms)
         self.solver = PipecgSolver(problem.A, problem.inv_diag, opts)
         vbuf, ld, comm = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_void_p()

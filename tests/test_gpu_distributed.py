@@ -25,11 +25,11 @@ torch = pytest.importorskip("torch")
 from paper_2105_06176_b200 import distributed as D  # noqa: E402
 
 
-def run_virtual(world, make_problem, cfg, chunk=0):
+def run_virtual(world, make_problem, cfg, chunk=0, engine="fused"):
     G = D.LocalGroup(world)
     out = [None] * world
     errs = []
-    opts = pb.DeviceOptions(max_sms=max(8, 148 // world - 10), chunk=chunk)
+    opts = pb.DeviceOptions(max_sms=max(8, 148 // world - 10), chunk=chunk, engine=engine)
 
     def work(r):
         try:
@@ -52,15 +52,16 @@ def run_virtual(world, make_problem, cfg, chunk=0):
     return out
 
 
-@pytest.mark.parametrize("world,kind,n", [(2, "3d7", 40), (3, "3d7", 33), (2, "2d5", 200),
-                                          (4, "3d27", 24)])
-def test_virtual_ranks_match_single_gpu(cuda, world, kind, n):
+@pytest.mark.parametrize("world,kind,n,engine", [(2, "3d7", 40, "fused-a"), (3, "3d7", 33, "fused-b"),
+                                                 (2, "2d5", 200, "fused-c"), (4, "3d27", 24, "fused"),
+                                                 (3, "3d27", 20, "fused-c")])
+def test_virtual_ranks_match_single_gpu(cuda, world, kind, n, engine):
     A = oracle.stencil(kind, n)
     x_true, b, x0, d = oracle.manufactured(A)
     tol = oracle.recipe_tolerance(A, b, d)
     cfg = pb.SolverConfig(tolerance=tol, max_iterations=20000, record_history=True)
     ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=20000)
-    out = run_virtual(world, lambda g: D.shard_stencil(kind, n, g), cfg)
+    out = run_virtual(world, lambda g: D.shard_stencil(kind, n, g), cfg, engine=engine)
     x = np.concatenate([o[0] for o in out])
     reps = [o[1] for o in out]
     assert len({r.iterations for r in reps}) == 1          # ranks agree
