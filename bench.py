@@ -55,13 +55,42 @@ def parse():
     ap.add_argument("--no-north-star", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-tts", action="store_true", help="skip the time-to-solution leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--engine", default="auto",
+                    help="DeviceOptions.engine (auto | fused | fused-a | fused-b | fused-c | two)")
     return ap.parse_args()
 
 
 def parse_config(cfg: str):
+    """'3d7-256' (stencil kind, order n) or 'powerlaw-22' (N = 2^22)."""
     kind, n = cfg.split("-")
     return kind, int(n)
+
+
+_HOST_CACHE = {}
+
+
+def workload_name(kind: str, n: int, N: int, nnz: int) -> str:
+    if kind == "powerlaw":
+        return (f"power-law SPD N=2^{n} (N={N}, nnz={nnz}; SURVEY.md §8(d) recipe, seed 20261017), "
+                "Jacobi PIPECG fp64")
+    return f"{kind} Poisson n={n} (N={N}, nnz={nnz}), Jacobi PIPECG fp64"
+
+
+def host_problem(kind: str, n: int):
+    """Host CSR (reference layout, int64 indices) of a bench workload."""
+    if (kind, n) not in _HOST_CACHE:
+        if kind == "powerlaw":
+            from paper_2105_06176_b200.sparse import generate_powerlaw
+
+            _HOST_CACHE[(kind, n)] = generate_powerlaw(2**n)
+        else:
+            sys.path.insert(0, str(ROOT / "oracle"))
+            import oracle
+
+            _HOST_CACHE[(kind, n)] = oracle.stencil(kind, n)
+    return _HOST_CACHE[(kind, n)]
 
 
 def canonical_bytes(N: int, nnz: int) -> int:
@@ -152,7 +181,7 @@ def cpu_baseline(kind: str, n: int, seconds: float, warmup: int = 1, steps: int 
     oracle.build()
     threads = os.cpu_count() or 1
     oracle.set_threads(threads)
-    A = oracle.stencil(kind, n)
+    A = oracle.as_csr(host_problem(kind, n))
     x_true, b, x0, d = oracle.manufactured(A)
     st = oracle.Stepper(A, b, d)
     st.steps(max(warmup, 1))
@@ -193,7 +222,7 @@ def run_reference(args):
     oracle.build()
     threads = os.cpu_count() or 1
     oracle.set_threads(threads)
-    A = oracle.stencil(kind, n)
+    A = oracle.as_csr(host_problem(kind, n))
     x_true, b, x0, d = oracle.manufactured(A)
     st = oracle.Stepper(A, b, d)
     st.steps(args.warmup)
@@ -208,7 +237,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (manufactured solution x=1/sqrt(N))",
-        "config": {"workload": f"{kind} Poisson n={n} (N={N}, nnz={nnz}), Jacobi PIPECG fp64",
+        "config": {"workload": workload_name(kind, n, N, nnz),
                    "N": N, "nnz": nnz},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{args.steps} full PIPECG iterations of {kind} n={n} after "
@@ -224,8 +253,33 @@ def run_reference(args):
 # B200 arm
 # ---------------------------------------------------------------------------
 def problem_device(pb, torch, kind, n, row_begin=0, row_end=None):
-    A = pb.stencil_device(kind, n, row_begin, row_end)
-    return A
+    if kind == "powerlaw":  # host recipe (numpy), uploaded once
+        return pb.as_device_csr(host_problem(kind, n))
+    return pb.stencil_device(kind, n, row_begin, row_end)
+
+
+ENGINES = {2: "two-kernel", 3: "fused-A (consumer gathers dinv*w)",
+           4: "fused-B (gather warps)", 5: "fused-C (stored m, one gather per nonzero)",
+           6: "fused-D (nnz-balanced tiles, cooperative gathers of the stored m)"}
+KERNELS = {2: "gated_spmv_rows + pipecg_k1_kernel", 3: "pipecg_fused_kernel_a<int,TR,0>",
+           4: "pipecg_fused_kernel<int,TR>", 5: "pipecg_fused_kernel_a<int,TR,1>",
+           6: "pipecg_fused_kernel_d<int,TR>"}
+CONFIG_NAMES = {"3d7-256": "BASELINE.json configs[1]", "2d5-512": "BASELINE.json configs[0]",
+                "3d27-400": "BASELINE.json configs[2], single-GPU leg",
+                "3d7-400": "north_star headline (>= 64M rows)",
+                "powerlaw-22": "BASELINE.json configs[3]"}
+
+
+def committed_traffic(config: str, engine: int):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    --set full capture (profiles/traffic.json, written by tools/ncu_summary.py)."""
+    p = ROOT / "profiles" / "traffic.json"
+    if not p.exists():
+        return None, None
+    d = json.loads(p.read_text()).get(f"{config}/{engine}")
+    if not d:
+        return None, None
+    return d["dram_bytes_per_launch"], d["source"]
 
 
 def time_iterations(pb, torch, A, pc_d, warmup: int, steps: int, options=None):
@@ -239,6 +293,7 @@ def time_iterations(pb, torch, A, pc_d, warmup: int, steps: int, options=None):
     solver.init(b, x0, 0.0, warmup + steps + 1, 0)
     solver.enqueue(warmup)
     torch.cuda.synchronize()
+    g0 = solver.poll().graph_launches
     stream = torch.cuda.ExternalStream(solver.stream)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -249,7 +304,11 @@ def time_iterations(pb, torch, A, pc_d, warmup: int, steps: int, options=None):
     ms = e0.elapsed_time(e1)
     res = solver.poll()
     ok = res.status == 0 and res.iterations == warmup + steps
+    # kernels launched in the timed region: one iteration kernel per step
+    # (+ the SpMV kernel(s) for engine 2) and one advance kernel per chunk
+    per_step = 1 if res.engine != 2 else 2
     info = {"engine": res.engine, "graph_launches": res.graph_launches, "ok": bool(ok),
+            "kernel_launches": steps * per_step + (res.graph_launches - g0),
             "status": res.status, "iterations_run": res.iterations,
             "tune_ms": [round(v, 4) for v in res.tune_ms]}
     solver.close()
@@ -279,11 +338,14 @@ def e2e_host(pb, torch, kind, n, reps: int = 1):
     """The reference-facing drop-in call with host numpy buffers."""
     import numpy as np
 
-    Ad = pb.stencil_device(kind, n)
-    Ah = Ad.to_host()  # host int64/float64 arrays (reference layout)
+    if kind == "powerlaw":
+        Ah = host_problem(kind, n)
+    else:
+        Ad = pb.stencil_device(kind, n)
+        Ah = Ad.to_host()  # host int64/float64 arrays (reference layout)
+        del Ad
     N, nnz = Ah.n_rows, Ah.nnz
     ro, ci, va = Ah.row_offsets, Ah.col_indices, Ah.values
-    del Ad
     torch.cuda.empty_cache()
     x_true = np.full(N, 1.0 / math.sqrt(N))
     b = pb.spmv(Ah, x_true)
@@ -344,41 +406,46 @@ def run_b200(args):
 
     # timed region: exactly K iterations
     with ClockSampler(local) as clk:
-        ms, info = time_iterations(pb, torch, A, pc_d, args.warmup, args.steps)
+        ms, info = time_iterations(pb, torch, A, pc_d, args.warmup, args.steps,
+                                   pb.DeviceOptions(engine=args.engine))
     t_iter = ms / 1e3 / args.steps
     value = args.steps / (ms / 1e3)
     achieved = B / t_iter / 1e9
-    chunk = 16
+    traffic, traffic_src = committed_traffic(args.config, info["engine"])
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: stencil matrix generated in HBM, manufactured solution x=1/sqrt(N)",
-        "config": {"workload": f"{kind} Poisson n={n} (N={N}, nnz={nnz}), Jacobi PIPECG fp64 "
-                               "(BASELINE.json configs[1])",
+        "data": ("synthetic: power-law SPD matrix generated on the host (numpy recipe) and uploaded"
+                 if kind == "powerlaw" else "synthetic: stencil matrix generated in HBM") +
+                ", manufactured solution x=1/sqrt(N)",
+        "config": {"workload": workload_name(kind, n, N, nnz) +
+                               f" ({CONFIG_NAMES.get(args.config, 'custom')})",
                    "N": N, "nnz": nnz, "parallelism": "single GPU",
-                   "l2": "inputs (4.4 GB/iteration) >> 126 MB L2; no flush needed",
-                   "engine": {2: "two-kernel", 3: "fused-A (consumer gathers)",
-                              4: "fused-B (gather warps)"}.get(info["engine"], "?"),
+                   "l2": f"inputs ({B / 1e9:.1f} GB/iteration) >> 126 MB L2; no flush needed",
+                   "engine": ENGINES.get(info["engine"], "?"),
                    "autotune_ms_per_iter": {"fused_A": info["tune_ms"][0],
                                             "fused_B": info["tune_ms"][1],
-                                            "two_kernel": info["tune_ms"][2]}},
+                                            "fused_C": info["tune_ms"][2],
+                                            "fused_D": info["tune_ms"][3],
+                                            "two_kernel": info["tune_ms"][4]}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "bytes_per_iteration": B,
                      "bytes_formula": "176N + 12nnz + 4(N+1) (canonical, SURVEY.md §8(d))",
                      "peak_source": peak_src,
                      "frac_of_8TBs_spec": achieved / 8000.0,
-                     "kernel": "pipecg_fused_kernel (one launch per iteration)"},
-        "gpu_launches": args.steps + math.ceil(args.steps / chunk),
+                     "kernel": KERNELS.get(info["engine"], "?") + " (one launch per iteration)"},
+        "gpu_launches": info["kernel_launches"],
         "timing_ok": info["ok"],
         "clocks": clk.summary(),
     }
-    del A
-    torch.cuda.empty_cache()
-    A = problem_device(pb, torch, kind, n)
-    tts = time_to_solution(pb, torch, A, pc_d)
-    line["time_to_solution"] = tts
+    if not args.no_tts:
+        del A
+        torch.cuda.empty_cache()
+        A = problem_device(pb, torch, kind, n)
+        line["time_to_solution"] = time_to_solution(pb, torch, A, pc_d)
     del A
     torch.cuda.empty_cache()
     if not args.no_north_star:

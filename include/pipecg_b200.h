@@ -150,7 +150,7 @@ typedef struct {
 typedef struct {
   int dot_mode;        /* PCG_DOT_TREE (default) or PCG_DOT_SEQ */
   int engine;          /* 0 auto (autotuned for >= 64K rows), 1 fused (variant autotuned),
-                          2 two-kernel, 3/4/5 fused variant A/B/C */
+                          2 two-kernel, 3/4/5/6 fused variant A/B/C/D */
   int chunk;           /* iterations per CUDA-graph chunk (0 = auto) */
   int use_graphs;      /* 1 (default) or 0 (plain launches, debugging) */
   int max_sms;         /* size persistent grids for at most this many SMs (0 = all) */
@@ -167,9 +167,9 @@ typedef struct {
   double breakdown_value;
   int64_t n_history;   /* entries written to history_host */
   int64_t n_drift;     /* samples written to drift_*_host */
-  int engine;          /* engine used: 2 two-kernel, 3/4/5 fused variant A/B/C */
+  int engine;          /* engine used: 2 two-kernel, 3/4/5/6 fused variant A/B/C/D */
   int64_t graph_launches;
-  double tune_ms[4];   /* autotune ms/iteration: fused A, B, C, two-kernel (0 = not run) */
+  double tune_ms[5];   /* autotune ms/iteration: fused A, B, C, D, two-kernel (0 = not run) */
 } pcg_result;
 
 int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_solver** out);

@@ -18,6 +18,7 @@ from .sparse import (
     as_device_csr,
     csr_from_dense,
     generate_poisson125,
+    generate_powerlaw,
     poisson125_shape,
     stencil_device,
     stencil_host,
@@ -58,6 +59,7 @@ __all__ = [
     "as_device_csr",
     "csr_from_dense",
     "generate_poisson125",
+    "generate_powerlaw",
     "poisson125_shape",
     "stencil_device",
     "stencil_host",

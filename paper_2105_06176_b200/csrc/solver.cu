@@ -30,6 +30,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cub/device/device_scan.cuh>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -273,6 +275,10 @@ struct FusedParams {
   int cap_val;  // doubles per stage
   int cap_col;  // ints per stage
   int flags;    // experiment switches (PIPECG_B200_FLAGS): 1 = gathers read the row itself
+  // variant D (nnz-balanced tiles)
+  const int* tile_row;        // [n_tiles + 1] first row of each tile
+  const long long* tile_e;    // [n_tiles + 1] first nonzero of each tile
+  long long hub_len;          // rows longer than this are single-row hub tiles
 };
 
 template <typename RP, int TR>
@@ -712,6 +718,248 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_a(FusedParams<RP>
   }
 }
 
+// ---------------------------------------------------------------------------
+// Variant D: nnz-balanced tiles for irregular rows (power-law graphs,
+// SuiteSparse-like matrices).  Tiles are row ranges [tile_row[t],
+// tile_row[t+1]) of at most TR rows and at most `cap` staged nonzeros,
+// built once per matrix (tile_build_kernel); a row longer than `hub_len`
+// is a tile of its own ("hub") whose nonzeros are not staged.
+//   normal tile: the 9 own-row vectors (z q s p x r u w_old dinv) and the
+//     tile's CSR are bulk-copied to shared memory; the consumers then form
+//     every product a_k * m_old[c_k] cooperatively (thread k mod TR: the
+//     scattered gathers are spread evenly over the CTA whatever the row
+//     lengths), in place over the staged values, and after one named
+//     barrier each thread sums its own row's products strictly in CSR
+//     order -- the same roundings as kernels.py:64-70, so every non-hub row
+//     is bitwise the reference's;
+//   hub tile: all TR consumers stride the row's nonzeros straight from
+//     global memory and combine with a fixed tree (deterministic; not the
+//     reference's order -- tolerance-graded like any parallel dot).
+// Everything after n_i is variant C: stored m_new = dinv * w_new is the
+// next iteration's gather source (one gather per nonzero).
+template <typename RP, int TR>
+struct FusedLayoutD {
+  static constexpr int kRpBytes = (int)(((TR + 1 + 4) * sizeof(RP) + 15) / 16 * 16);
+  static constexpr int kVecStride = TR + 2;  // doubles per staged vector (start aligned down)
+  static constexpr int kVecs = 9;
+  __host__ __device__ static int stage_bytes(int cap_val, int cap_col) {
+    return kRpBytes + kVecs * kVecStride * 8 + cap_val * 8 + (cap_col * 4 + 15) / 16 * 16;
+  }
+  static constexpr int kHeader = 2048;  // barriers, reduction scratch, per-stage tile meta
+};
+
+struct TileMeta {
+  long long t0, e0;
+  int rows, hub;
+  long long pad;
+};
+
+// Consumer threads per CTA (all TR tile heights): the gather phase of a
+// tile is spread over every consumer, the row phase uses the first `rows`.
+constexpr int kDThreads = 256;
+constexpr int kDBatch = 8;  // gathers in flight per consumer thread
+
+template <typename RP, int TR>
+__global__ void __launch_bounds__(kDThreads + 32) pipecg_fused_kernel_d(FusedParams<RP> P, int step) {
+  using L = FusedLayoutD<RP, TR>;
+  constexpr int NT = kDThreads;  // consumer threads
+  constexpr int RPA = 16 / (int)sizeof(RP);
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);       // [stages]
+  uint64_t* empty = full + 8;                                // [stages]
+  double* red = reinterpret_cast<double*>(smem + 256);       // 3*NT/32 doubles
+  volatile int* decision = reinterpret_cast<volatile int*>(smem + 640);
+  double* sc = reinterpret_cast<double*>(smem + 704);        // alpha, beta
+  TileMeta* meta = reinterpret_cast<TileMeta*>(smem + 768);  // [stages]
+  unsigned char* stage0 = smem + L::kHeader;
+  const int SB = L::stage_bytes(P.cap_val, P.cap_col);
+  const int S = P.stages;
+
+  Ctrl* C = P.C;
+  if (read_status(C) != PCG_RUNNING) return;
+  const long long it = C->base_it + step;
+  const double* w_old = P.w[it & 1];
+  double* w_new = P.w[(it + 1) & 1];
+  const double* m_old = P.m[it & 1];
+  double* m_new = P.m[(it + 1) & 1];
+
+  const int tid = threadIdx.x;
+  const bool producer = tid < 32;
+  const long long my_tiles =
+      P.n_tiles > (long long)blockIdx.x ? (P.n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NT / 32);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  uint64_t pol = 0;
+  auto issue = [&](long long j) {
+    const int s = (int)(j % S);
+    const long long t = blockIdx.x + j * (long long)gridDim.x;
+    const long long t0 = P.tile_row[t], t1 = P.tile_row[t + 1];
+    const long long e0 = P.tile_e[t], e1 = P.tile_e[t + 1];
+    const int rows = (int)(t1 - t0);
+    const int hub = rows == 1 && e1 - e0 > P.hub_len;
+    meta[s] = TileMeta{t0, e0, rows, hub, 0};
+    const long long ra = t0 & ~(long long)(RPA - 1), va = t0 & ~1LL;
+    const uint32_t b_rp = (uint32_t)(((t1 + 1 - ra) * (long long)sizeof(RP) + 15) / 16 * 16);
+    const uint32_t b_vec = (uint32_t)(((t1 - va) * 8 + 15) / 16 * 16);
+    const long long cb = e0 & ~3LL, ce = (e1 + 3) & ~3LL;
+    const long long vb = e0 & ~1LL, ve = (e1 + 1) & ~1LL;
+    const uint32_t b_val = hub ? 0u : (uint32_t)((ve - vb) * 8);
+    const uint32_t b_col = hub ? 0u : (uint32_t)((ce - cb) * 4);
+    unsigned char* sb = stage0 + (size_t)s * SB;
+    mbar_arrive_expect_tx(&full[s], b_rp + L::kVecs * b_vec + b_val + b_col);
+    bulk_g2s(sb, P.rp + ra, b_rp, &full[s], pol);
+    double* vs = reinterpret_cast<double*>(sb + L::kRpBytes);
+#pragma unroll
+    for (int k = 0; k < 7; ++k) bulk_g2s(vs + k * L::kVecStride, P.vec[k] + va, b_vec, &full[s], pol);
+    bulk_g2s(vs + 7 * L::kVecStride, w_old + va, b_vec, &full[s], pol);
+    bulk_g2s(vs + 8 * L::kVecStride, P.dinv + va, b_vec, &full[s], pol);
+    unsigned char* sval = sb + L::kRpBytes + L::kVecs * L::kVecStride * 8;
+    if (b_val) bulk_g2s(sval, P.val + vb, b_val, &full[s], pol);
+    if (b_col) bulk_g2s(sval + (size_t)P.cap_val * 8, P.col + cb, b_col, &full[s], pol);
+  };
+
+  if (producer && tid == 0) {
+    pol = policy_evict_first();
+    for (long long j = 0; j < my_tiles && j < S; ++j) issue(j);
+  }
+
+  if (!producer) {
+    const Step stp = prologue<NT>(C, P.hist, P.rin, it, tid - 32, red, 1,
+                                  blockIdx.x == 0 && tid == 32);
+    if (tid == 32) {
+      sc[0] = stp.alpha;
+      sc[1] = stp.beta;
+      *decision = stp.go;
+    }
+  }
+  __syncthreads();
+  const int go = *decision;
+  if (!go) {
+    if (tid == 0)
+      for (long long j = 0; j < my_tiles && j < S; ++j) mbar_wait(&full[j], 0);
+    return;
+  }
+  const double alpha = sc[0], beta = sc[1];
+
+  if (producer) {
+    if (tid == 0) {
+      for (long long j = S; j < my_tiles; ++j) {
+        const int s = (int)(j % S);
+        mbar_wait(&empty[s], (uint32_t)((j / S - 1) & 1));
+        issue(j);
+      }
+    }
+    return;
+  }
+
+  // ---- consumers ----------------------------------------------------------
+  const int lt = tid - 32;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (long long j = 0; j < my_tiles; ++j) {
+    const int s = (int)(j % S);
+    mbar_wait(&full[s], (uint32_t)((j / S) & 1));
+    const TileMeta tm = meta[s];
+    unsigned char* sb = stage0 + (size_t)s * SB;
+    const long long ra = tm.t0 & ~(long long)(RPA - 1), va = tm.t0 & ~1LL;
+    const RP* rp_s = reinterpret_cast<const RP*>(sb) + (tm.t0 - ra);
+    const double* v_s = reinterpret_cast<const double*>(sb + L::kRpBytes) + (tm.t0 - va);
+    double* val_s = reinterpret_cast<double*>(sb + L::kRpBytes + L::kVecs * L::kVecStride * 8);
+    const int* col_s = reinterpret_cast<const int*>(val_s + P.cap_val);
+    double nacc = 0.0;
+    if (tm.hub) {
+      // one long row, all consumers, straight from global memory
+      const long long lo = rp_s[0], hi = rp_s[1];
+      double part[1] = {0.0};
+      for (long long k0 = lo + lt; k0 < hi; k0 += (long long)kDBatch * NT) {
+        double a[kDBatch], mv[kDBatch];
+#pragma unroll
+        for (int u = 0; u < kDBatch; ++u) {
+          const long long k = k0 + (long long)u * NT;
+          a[u] = 0.0;
+          mv[u] = 0.0;
+          if (k < hi) {
+            a[u] = ldg_nc(P.val + k);
+            mv[u] = ldg_nc(m_old + ldg_nc(P.col + k));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kDBatch; ++u)
+          if (k0 + (long long)u * NT < hi) part[0] = add(part[0], mul(a[u], mv[u]));
+      }
+      group_sum<1, NT>(part, lt, red, 1);
+      nacc = part[0];
+    } else {
+      // products a_k * m_old[c_k] for every staged nonzero, in place
+      const int vo = (int)(tm.e0 & 1LL), co = (int)(tm.e0 & 3LL);
+      const int span = (int)(rp_s[tm.rows] - tm.e0);
+      for (int k0 = lt; k0 < span; k0 += kDBatch * NT) {
+        double mv[kDBatch];
+#pragma unroll
+        for (int u = 0; u < kDBatch; ++u) {
+          const int k = k0 + u * NT;
+          mv[u] = k < span ? ldg_nc(m_old + col_s[co + k]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kDBatch; ++u) {
+          const int k = k0 + u * NT;
+          if (k < span) val_s[vo + k] = mul(val_s[vo + k], mv[u]);
+        }
+      }
+      bar_sync(1, NT);
+      if (lt < tm.rows) {
+        const int lo = (int)(rp_s[lt] - tm.e0), hi = (int)(rp_s[lt + 1] - tm.e0);
+        for (int k = lo; k < hi; ++k) nacc = add(nacc, val_s[vo + k]);  // n = A m, CSR order
+      }
+    }
+    const int row_thread = tm.hub ? 0 : lt;
+    if (lt == row_thread && lt < tm.rows) {
+      const long long i = tm.t0 + lt;
+      const double wi = v_s[7 * L::kVecStride + lt];
+      const double di = v_s[8 * L::kVecStride + lt];
+      const double mi = mul(di, wi);
+      const double zi = add(nacc, mul(beta, v_s[0 * L::kVecStride + lt]));
+      const double qi = add(mi, mul(beta, v_s[1 * L::kVecStride + lt]));
+      const double si = add(wi, mul(beta, v_s[2 * L::kVecStride + lt]));
+      const double ui = v_s[6 * L::kVecStride + lt];
+      const double pi = add(ui, mul(beta, v_s[3 * L::kVecStride + lt]));
+      const double xi = add(v_s[4 * L::kVecStride + lt], mul(alpha, pi));
+      const double ri = sub(v_s[5 * L::kVecStride + lt], mul(alpha, si));
+      const double un = sub(ui, mul(alpha, qi));
+      const double wn = sub(wi, mul(alpha, zi));
+      st_stream(P.vec[0] + i, zi);
+      st_stream(P.vec[1] + i, qi);
+      st_stream(P.vec[2] + i, si);
+      st_stream(P.vec[3] + i, pi);
+      st_stream(P.vec[4] + i, xi);
+      st_stream(P.vec[5] + i, ri);
+      st_stream(P.vec[6] + i, un);
+      st_stream(w_new + i, wn);
+      m_new[i] = mul(di, wn);  // solvers.py:358 (gathered next iteration)
+      acc[0] = add(acc[0], mul(ri, un));
+      acc[1] = add(acc[1], mul(wn, un));
+      acc[2] = add(acc[2], mul(un, un));
+    }
+    __syncwarp();
+    if ((lt & 31) == 0) mbar_arrive(&empty[s]);
+  }
+  group_sum<3, NT>(acc, lt, red, 1);
+  if (lt == 0) {
+    double* out = P.pout + (size_t)(it & 1) * (size_t)gridDim.x * 4 + (size_t)blockIdx.x * 4;
+    out[0] = acc[0];
+    out[1] = acc[1];
+    out[2] = acc[2];
+    out[3] = 0.0;
+  }
+}
+
 // ===========================================================================
 // Engine 2: K1 (update + Jacobi + dot partials) and K2 (gated SpMV)
 // ===========================================================================
@@ -1089,6 +1337,57 @@ __global__ void __launch_bounds__(256) max_row_kernel(long long n, const void* r
   block_max_atomic(m, out);
 }
 
+// Variant D tiling: greedy inside each block of `tr` rows -- a tile grows
+// until adding the next row would exceed `cap` nonzeros; a row longer than
+// `hub_len` becomes a tile of its own.  Pass 1 (write = 0) counts tiles per
+// block, pass 2 writes each tile's first row and first nonzero at offs[b].
+template <typename RP>
+__global__ void __launch_bounds__(256) tile_build_kernel(long long n, int tr, long long cap,
+                                                          long long hub_len, const RP* rp,
+                                                          int write, int* counts,
+                                                          const long long* offs, int* tile_row,
+                                                          long long* tile_e) {
+  const long long n_blocks = (n + tr - 1) / tr;
+  for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < n_blocks;
+       b += (long long)gridDim.x * blockDim.x) {
+    const long long r0 = b * tr, r1 = min(n, r0 + tr);
+    long long out = write ? offs[b] : 0;
+    int cnt = 0;
+    bool open = false;
+    long long cur = 0;
+    for (long long i = r0; i < r1; ++i) {
+      const long long e = rp[i], len = (long long)rp[i + 1] - e;
+      bool start;
+      if (len > hub_len) {
+        start = true;
+        open = false;
+      } else {
+        start = !open || cur + len > cap;
+        if (start) {
+          open = true;
+          cur = 0;
+        }
+        cur += len;
+      }
+      if (start) {
+        if (write) {
+          tile_row[out] = (int)i;
+          tile_e[out] = e;
+          ++out;
+        }
+        ++cnt;
+      }
+    }
+    if (!write) counts[b] = cnt;
+  }
+}
+
+__global__ void tile_close_kernel(long long n, long long n_tiles, long long nnz, int* tile_row,
+                                  long long* tile_e) {
+  tile_row[n_tiles] = (int)n;
+  tile_e[n_tiles] = nnz;
+}
+
 }  // namespace pcg
 
 using namespace pcg;
@@ -1097,10 +1396,15 @@ using namespace pcg;
 // host runtime
 // ===========================================================================
 struct FusedPlan {
-  int variant = 0;  // 0: consumer gathers dinv,w (A); 1: gather warps (B); 2: stored m (C)
+  int variant = 0;  // 0: consumer gathers dinv,w (A); 1: gather warps (B); 2: stored m (C);
+                    // 3: nnz-balanced tiles + cooperative gathers of the stored m (D)
   int tr = 0, stages = 0, bps = 0, cap_val = 0, cap_col = 0, grid = 0, score = 0;
   size_t smem = 0;
+  long long n_tiles = 0;  // variant D: tiles built for this plan
+  long long cap = 0, hub_len = 0;
 };
+
+constexpr int kVariants = 4;
 
 struct pcg_solver {
   pcg_matrix A{};
@@ -1146,8 +1450,11 @@ struct pcg_solver {
   unsigned long long xtarget = 0;  // cumulative setup arrivals expected
   int flags = 0;                   // experiment switches (env PIPECG_B200_FLAGS)
   int variant = 1;                 // fused kernel variant in use
-  FusedPlan plans[3];              // per fused variant (stages == 0: does not fit)
-  double tune_ms[4] = {0, 0, 0, 0};  // autotune ms/iteration: fused A, B, C, engine 2
+  FusedPlan plans[kVariants];      // per fused variant (stages == 0: does not fit)
+  double tune_ms[5] = {0, 0, 0, 0, 0};  // autotune ms/iteration: fused A, B, C, D, engine 2
+  int* tile_row = nullptr;         // variant D tiles (first row, first nonzero)
+  long long* tile_e = nullptr;
+  long long hub_len = 0;
 };
 
 namespace {
@@ -1184,14 +1491,17 @@ int plan_one(pcg_solver* S, int cap_col, int cap_val, FusedPlan* out) {
   p.tr = TR;
   p.cap_col = cap_col;
   p.cap_val = cap_val;
-  const size_t sb = V == 1 ? (size_t)FusedLayout<RP, TR>::stage_bytes(cap_val, cap_col)
-                           : (size_t)FusedLayoutA<RP, TR>::stage_bytes(cap_val, cap_col);
-  const size_t hdr = 1024;
+  const size_t sb = V == 1   ? (size_t)FusedLayout<RP, TR>::stage_bytes(cap_val, cap_col)
+                    : V == 3 ? (size_t)FusedLayoutD<RP, TR>::stage_bytes(cap_val, cap_col)
+                             : (size_t)FusedLayoutA<RP, TR>::stage_bytes(cap_val, cap_col);
+  const size_t hdr = V == 3 ? (size_t)FusedLayoutD<RP, TR>::kHeader : 1024;
   const size_t sm_budget = 228 * 1024, cta_max = 227 * 1024;
-  const char* e_st = getenv("PIPECG_B200_STAGES");  // experiment override
-  for (int bps = 2; bps >= 1 && !p.stages; --bps) {
-    for (int st = 2; st <= 4; ++st) {
-      if (e_st && atoi(e_st) != st) continue;
+  const char* e_st = getenv("PIPECG_B200_STAGES");  // experiment overrides
+  const char* e_bps = getenv("PIPECG_B200_BPS");
+  for (int bps = e_bps ? atoi(e_bps) : 2; bps >= 1 && !p.stages; --bps) {
+    if (e_bps && bps != atoi(e_bps)) break;
+    for (int st = 2; st <= 8; ++st) {
+      if (e_st ? atoi(e_st) != st : st > 4) continue;
       const size_t need = hdr + st * sb;
       if (need <= cta_max && (need + 1024) * bps <= sm_budget) {
         p.stages = st;
@@ -1209,6 +1519,8 @@ int plan_one(pcg_solver* S, int cap_col, int cap_val, FusedPlan* out) {
   cudaError_t e =
       V == 1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pipecg_fused_kernel<RP, TR>,
                                                              FusedLayout<RP, TR>::kThreads, p.smem)
+      : V == 3 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                     &occ, pipecg_fused_kernel_d<RP, TR>, kDThreads + 32, p.smem)
       : V == 2 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                      &occ, pipecg_fused_kernel_a<RP, TR, true>, TR + 32, p.smem)
                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(
@@ -1245,6 +1557,104 @@ int plan_variant(pcg_solver* S, const int* cc, const int* cv, FusedPlan* best) {
   return PCG_OK;
 }
 
+// Variant D tile geometry for tile height TR: when every TR-row block's
+// nonzeros fit twice the average tile (cap_target) the blocks are the tiles
+// (no hubs); otherwise tiles are capped at cap_target nonzeros and rows
+// longer than cap_target / 2 become single-row hub tiles.
+template <int TR>
+void d_geometry(const pcg_solver* S, int cv_block, long long* cap, long long* hub_len) {
+  const long long n = S->A.n_rows, nnz = S->A.nnz;
+  const long long avg = std::max<long long>(4, (nnz + n - 1) / std::max<long long>(n, 1));
+  long long target = 2LL * TR * avg;
+  if (const char* e = getenv("PIPECG_B200_DCAP")) target = std::max(atoll(e), 8LL);  // experiment / test override
+  if (cv_block <= target) {
+    *cap = cv_block;
+    *hub_len = INT64_MAX / 2;
+  } else {
+    *cap = target;
+    *hub_len = target / 2;
+  }
+}
+
+template <typename RP>
+int build_tiles_d(pcg_solver* S, FusedPlan* p) {
+  const long long n = S->A.n_rows;
+  const long long n_blocks = (n + p->tr - 1) / p->tr;
+  cudaStream_t st = S->stream;
+  int* counts = nullptr;
+  long long* offs = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, offs, n_blocks, st);
+  if (cudaMalloc(&counts, n_blocks * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&offs, (n_blocks + 1) * sizeof(long long)) != cudaSuccess ||
+      cudaMalloc(&tmp, tmp_bytes) != cudaSuccess) {
+    cudaFree(counts);
+    cudaFree(offs);
+    return set_error(PCG_ENOMEM, "variant D tiles: workspace");
+  }
+  const RP* rp = static_cast<const RP*>(S->A.rowptr);
+  const unsigned g = elementwise_grid(n_blocks);
+  tile_build_kernel<RP><<<g, 256, 0, st>>>(n, p->tr, p->cap, p->hub_len, rp, 0, counts, nullptr,
+                                           nullptr, nullptr);
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, offs, n_blocks, st);
+  long long last_off = 0;
+  int last_cnt = 0;
+  cudaMemcpyAsync(&last_off, offs + n_blocks - 1, sizeof(long long), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&last_cnt, counts + n_blocks - 1, sizeof(int), cudaMemcpyDeviceToHost, st);
+  int rc = cuda_status(cudaStreamSynchronize(st), "variant D tile count");
+  const long long n_tiles = last_off + last_cnt;
+  if (!rc) {
+    cudaFree(S->tile_row);
+    cudaFree(S->tile_e);
+    S->tile_row = nullptr;
+    S->tile_e = nullptr;
+    if (cudaMalloc(&S->tile_row, (n_tiles + 1) * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&S->tile_e, (n_tiles + 1) * sizeof(long long)) != cudaSuccess)
+      rc = set_error(PCG_ENOMEM, "variant D tiles");
+  }
+  if (!rc) {
+    tile_build_kernel<RP><<<g, 256, 0, st>>>(n, p->tr, p->cap, p->hub_len, rp, 1, counts, offs,
+                                             S->tile_row, S->tile_e);
+    tile_close_kernel<<<1, 1, 0, st>>>(n, n_tiles, S->A.nnz, S->tile_row, S->tile_e);
+    rc = cuda_status(cudaStreamSynchronize(st), "variant D tile build");
+  }
+  cudaFree(counts);
+  cudaFree(offs);
+  cudaFree(tmp);
+  if (rc) return rc;
+  p->n_tiles = n_tiles;
+  p->grid = (int)std::max<long long>(std::min<long long>(p->grid, n_tiles), 1);
+  S->hub_len = p->hub_len;
+  return PCG_OK;
+}
+
+template <typename RP>
+int plan_d(pcg_solver* S, const int* cv, FusedPlan* best) {
+  FusedPlan p[3];
+  long long caps[3], hubs[3];
+  d_geometry<256>(S, cv[0], &caps[0], &hubs[0]);
+  d_geometry<128>(S, cv[1], &caps[1], &hubs[1]);
+  d_geometry<64>(S, cv[2], &caps[2], &hubs[2]);
+  // staged spans: values rounded to 2 (start aligned down by <= 1), columns to 4
+  auto cv_of = [](long long cap) { return (int)round_up(cap + 2, 2); };
+  auto cc_of = [](long long cap) { return (int)round_up(cap + 6, 4); };
+  int rc = plan_one<RP, 256, 3>(S, cc_of(caps[0]), cv_of(caps[0]), &p[0]);
+  if (!rc) rc = plan_one<RP, 128, 3>(S, cc_of(caps[1]), cv_of(caps[1]), &p[1]);
+  if (!rc) rc = plan_one<RP, 64, 3>(S, cc_of(caps[2]), cv_of(caps[2]), &p[2]);
+  if (rc) return rc;
+  const char* e_tr = getenv("PIPECG_B200_TR");
+  *best = FusedPlan();
+  for (int k = 0; k < 3; ++k) {
+    p[k].cap = caps[k];
+    p[k].hub_len = hubs[k];
+    if (!p[k].stages || (e_tr && atoi(e_tr) != p[k].tr)) continue;
+    if (p[k].score > best->score) *best = p[k];
+  }
+  if (!best->stages) return PCG_OK;
+  return build_tiles_d<RP>(S, best);
+}
+
 template <typename RP>
 int fused_setup(pcg_solver* S) {
   int cc[3], cv[3];
@@ -1256,16 +1666,17 @@ int fused_setup(pcg_solver* S) {
   int rc = plan_variant<RP, 0>(S, cc, cv, &S->plans[0]);
   if (!rc) rc = plan_variant<RP, 1>(S, cc, cv, &S->plans[1]);
   if (!rc) rc = plan_variant<RP, 2>(S, cc, cv, &S->plans[2]);
+  if (!rc) rc = plan_d<RP>(S, cv, &S->plans[3]);
   if (rc) return rc;
-  if (!S->plans[0].stages && !S->plans[1].stages && !S->plans[2].stages)
-    return PCG_EINVAL;  // -> engine 2
-  return PCG_OK;
+  bool any = false;
+  for (int v = 0; v < kVariants; ++v) any = any || S->plans[v].stages > 0;
+  return any ? PCG_OK : PCG_EINVAL;  // none fits -> engine 2
 }
 
 void apply_plan(pcg_solver* S, const FusedPlan& p) {
   S->variant = p.variant;
   S->tr = p.tr;
-  S->n_tiles = (S->A.n_rows + p.tr - 1) / p.tr;
+  S->n_tiles = p.variant == 3 ? p.n_tiles : (S->A.n_rows + p.tr - 1) / p.tr;
   S->stages = p.stages;
   S->cap_val = p.cap_val;
   S->cap_col = p.cap_col;
@@ -1363,6 +1774,9 @@ FusedParams<RP> fused_params(pcg_solver* S) {
   P.cap_val = S->cap_val;
   P.cap_col = S->cap_col;
   P.flags = S->flags;
+  P.tile_row = S->tile_row;
+  P.tile_e = S->tile_e;
+  P.hub_len = S->hub_len;
   return P;
 }
 
@@ -1375,6 +1789,12 @@ void launch_fused(pcg_solver* S, int k) {
       case 256: pipecg_fused_kernel<RP, 256><<<S->grid, FusedLayout<RP, 256>::kThreads, S->smem, st>>>(P, k); break;
       case 128: pipecg_fused_kernel<RP, 128><<<S->grid, FusedLayout<RP, 128>::kThreads, S->smem, st>>>(P, k); break;
       default: pipecg_fused_kernel<RP, 64><<<S->grid, FusedLayout<RP, 64>::kThreads, S->smem, st>>>(P, k); break;
+    }
+  } else if (S->variant == 3) {
+    switch (S->tr) {
+      case 256: pipecg_fused_kernel_d<RP, 256><<<S->grid, kDThreads + 32, S->smem, st>>>(P, k); break;
+      case 128: pipecg_fused_kernel_d<RP, 128><<<S->grid, kDThreads + 32, S->smem, st>>>(P, k); break;
+      default: pipecg_fused_kernel_d<RP, 64><<<S->grid, kDThreads + 32, S->smem, st>>>(P, k); break;
     }
   } else if (S->variant == 2) {
     switch (S->tr) {
@@ -1390,6 +1810,9 @@ void launch_fused(pcg_solver* S, int k) {
     }
   }
 }
+
+// fused variants C and D gather a stored m (ping-pong m / m2) instead of w
+inline bool stored_m_fused(const pcg_solver* S) { return S->engine == 1 && S->variant >= 2; }
 
 // enqueue graph step k (drift? -> iteration -> seq dots? -> exchange / SpMV)
 int enqueue_step(pcg_solver* S, int k) {
@@ -1428,8 +1851,8 @@ int enqueue_step(pcg_solver* S, int k) {
                                       S->seqbuf, k);
   if (S->connected)
     iter_exchange_kernel<<<kXchgBlocks, 256, 0, st>>>(
-        S->cp, R.C, k, S->partials, S->grid, S->variant == 2 ? S->m : S->w[0],
-        S->variant == 2 ? S->m2 : S->w[1], S->variant == 2 ? 9 : 7, S->variant == 2 ? 12 : 8);
+        S->cp, R.C, k, S->partials, S->grid, stored_m_fused(S) ? S->m : S->w[0],
+        stored_m_fused(S) ? S->m2 : S->w[1], stored_m_fused(S) ? 9 : 7, stored_m_fused(S) ? 12 : 8);
   if (S->engine == 2) {
     const long long thr = S->n_long > 0 ? kLongRow : INT64_MAX;
     if (S->A.rp64) {
@@ -1502,7 +1925,7 @@ int auto_chunk(pcg_solver* S) {
 void fill_result(pcg_solver* S, const Ctrl& c, pcg_result* res) {
   res->status = c.status;
   res->engine = S->engine == 1 ? 3 + S->variant : 2;
-  for (int k = 0; k < 4; ++k) res->tune_ms[k] = S->tune_ms[k];
+  for (int k = 0; k < 5; ++k) res->tune_ms[k] = S->tune_ms[k];
   res->graph_launches = S->graph_launches;
   res->norm0 = c.init.norm;
   res->breakdown_quantity = c.bd_code;
@@ -1543,6 +1966,10 @@ int preload_solver() {
   PCG_LOAD_A(false);
   PCG_LOAD_A(true);
 #undef PCG_LOAD_A
+  PCG_LOAD((pipecg_fused_kernel_d<int, 256>)); PCG_LOAD((pipecg_fused_kernel_d<int, 128>));
+  PCG_LOAD((pipecg_fused_kernel_d<int, 64>)); PCG_LOAD((pipecg_fused_kernel_d<long long, 256>));
+  PCG_LOAD((pipecg_fused_kernel_d<long long, 128>)); PCG_LOAD((pipecg_fused_kernel_d<long long, 64>));
+  PCG_LOAD(tile_build_kernel<int>); PCG_LOAD(tile_build_kernel<long long>); PCG_LOAD(tile_close_kernel);
   PCG_LOAD(pipecg_k1_kernel); PCG_LOAD(gated_spmv_rows<int>); PCG_LOAD(gated_spmv_rows<long long>);
   PCG_LOAD(gated_spmv_long<int>); PCG_LOAD(gated_spmv_long<long long>); PCG_LOAD(seq_dots_kernel);
   PCG_LOAD(drift_partial_kernel<int>); PCG_LOAD(drift_partial_kernel<long long>);
@@ -1564,6 +1991,9 @@ int preload_solver() {
   PCG_SMEM_A(false);
   PCG_SMEM_A(true);
 #undef PCG_SMEM_A
+  PCG_SMEM((pipecg_fused_kernel_d<int, 256>)); PCG_SMEM((pipecg_fused_kernel_d<int, 128>));
+  PCG_SMEM((pipecg_fused_kernel_d<int, 64>)); PCG_SMEM((pipecg_fused_kernel_d<long long, 256>));
+  PCG_SMEM((pipecg_fused_kernel_d<long long, 128>)); PCG_SMEM((pipecg_fused_kernel_d<long long, 64>));
 #undef PCG_SMEM
   if (e != cudaSuccess) return cuda_status(e, "preload solver kernels");
   done_devices.insert(dev);
@@ -1604,8 +2034,8 @@ int autotune(pcg_solver* S, int grid2, bool with_engine2) {
   int best = -1;
   float best_ms = 0.f;
   int rc = PCG_OK;
-  for (int cand = 0; cand < (with_engine2 ? 4 : 3) && !rc; ++cand) {
-    if (cand < 3) {
+  for (int cand = 0; cand < (with_engine2 ? kVariants + 1 : kVariants) && !rc; ++cand) {
+    if (cand < kVariants) {
       if (!S->plans[cand].stages) continue;
       S->engine = 1;
       apply_plan(S, S->plans[cand]);
@@ -1635,7 +2065,7 @@ int autotune(pcg_solver* S, int grid2, bool with_engine2) {
   S->initialized = false;
   S->host_base = 0;
   if (rc) return rc;
-  if (best < 3) {
+  if (best < kVariants) {
     S->engine = 1;
     apply_plan(S, S->plans[best]);
   } else {
@@ -1695,11 +2125,15 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     return rc;
   }
   // engine: 0 auto (autotuned), 1 fused (heuristic variant), 2 two-kernel,
-  // 3 fused variant A, 4 fused variant B
+  // 3/4/5/6 fused variant A/B/C/D
   const int req = S->opt.engine;
+  if (req < 0 || req > 3 + kVariants - 1) {
+    pipecg_b200_solver_destroy(S);
+    return set_error(PCG_EINVAL, "solver_create: unknown engine");
+  }
   const bool has_long = max_row > (unsigned long long)kLongRow;
   bool fused_ok = false;
-  if (req != 2 && !(req == 0 && has_long)) {
+  if (req != 2) {
     rc = A->rp64 ? fused_setup<long long>(S) : fused_setup<int>(S);
     if (rc && rc != PCG_EINVAL) {
       pipecg_b200_solver_destroy(S);
@@ -1712,7 +2146,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
       return set_error(PCG_EINVAL, "fused engine: tiles exceed shared memory");
     }
   }
-  if (!fused_ok || req == 0 || req == 2) {  // engine-2 resources (also an autotune candidate)
+  {  // block-per-row list of long rows: engine 2 (also an autotune candidate) and the init SpMVs
     if (has_long) {
       int64_t cnt = 0;
       rc = pipecg_b200_find_long_rows(A->n_rows, A->rp64, A->rowptr, kLongRow, nullptr, 0, &cnt,
@@ -1732,7 +2166,8 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     }
   }
   const int grid2 = std::min<int>(kDotGrid, 4 * S->num_sms);
-  S->grid = std::max({grid2, S->plans[0].grid, S->plans[1].grid, S->plans[2].grid});
+  S->grid = grid2;
+  for (int v = 0; v < kVariants; ++v) S->grid = std::max(S->grid, S->plans[v].grid);
   rc = alloc_state(S);
   if (rc) {
     pipecg_b200_solver_destroy(S);
@@ -1745,11 +2180,14 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     S->engine = 1;
     apply_plan(S, S->plans[req - 3]);
   } else if (A->n_rows < kTuneRows) {
-    // small: no autotune; wide rows (> 12 nnz/row) gather the stored m (C)
+    // small: no autotune.  Irregular rows -> D (balanced tiles); wide rows
+    // (> 12 nnz/row) gather the stored m (C); else A
     const bool wide = A->nnz > 12 * A->n_rows;
-    const int order[3] = {wide ? 2 : 0, wide ? 0 : 2, 1};
+    int order[kVariants] = {0, 2, 3, 1};
+    if (has_long) order[0] = 3, order[1] = 2, order[2] = 0;
+    else if (wide) order[0] = 2, order[1] = 0;
     S->engine = 1;
-    for (int k = 0; k < 3; ++k)
+    for (int k = 0; k < kVariants; ++k)
       if (S->plans[order[k]].stages) {
         apply_plan(S, S->plans[order[k]]);
         break;
@@ -1782,6 +2220,8 @@ int pipecg_b200_solver_destroy(pcg_solver* S) {
   cudaFree(S->rec_dev);
   cudaFree(S->comm);
   cudaFree(S->long_rows);
+  cudaFree(S->tile_row);
+  cudaFree(S->tile_e);
   if (S->ev_in) cudaEventDestroy(S->ev_in);
   if (S->stream) cudaStreamDestroy(S->stream);
   delete S;
@@ -1887,8 +2327,8 @@ int pipecg_b200_solver_init(pcg_solver* S, const double* b, const double* x0, do
   rc = spmv_any(n, S->A.rp64, S->A.rowptr, S->A.col, S->A.val, S->u, nullptr, S->w[0],
                 S->long_rows, S->n_long, 0, st);  // w = A u
   if (rc) return rc;
-  const bool stored_m = S->engine == 2 || S->variant == 2;
-  if (S->engine == 1 && S->variant == 2) {
+  const bool stored_m = S->engine == 2 || stored_m_fused(S);
+  if (stored_m_fused(S)) {
     rc = pipecg_b200_jacobi_apply(n, S->A.inv_diag, S->w[0], S->m, st);  // m = M^-1 w
     if (rc) return rc;
   }

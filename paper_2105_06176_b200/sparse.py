@@ -31,6 +31,7 @@ __all__ = [
     "stencil_host",
     "poisson125_shape",
     "generate_poisson125",
+    "generate_powerlaw",
 ]
 
 PAD = 16  # trailing elements the staged (bulk-copy) reads may touch
@@ -301,3 +302,63 @@ def generate_poisson125(n: int, max_bytes: int = 2**31) -> CsrMatrix:
             f"n={n} needs about {need / 2**30:.2f} GiB (budget {max_bytes / 2**30:.2f} GiB)"
         )
     return stencil_host("p125", n)
+
+
+def generate_powerlaw(n_rows: int = 2**22, seed: int = 20261017, tau: float = 2.2,
+                      avg_degree: float = 11.92) -> CsrMatrix:
+    """BASELINE.json configs[3]: irregular SPD CSR with power-law row lengths.
+
+    The recipe of SURVEY.md §8(d) config 4 (host numpy; it is defined by
+    numpy's PCG64 stream): weights w_i = (i+10)^(-1/(tau-1)); M =
+    (avg_degree*N - N)/2 edges, one endpoint drawn with probability
+    proportional to w, the other uniform; self-loops dropped; values
+    -U(0.1, 1.0), duplicates summed per unordered pair then mirrored
+    (exactly symmetric); diagonal =
+    sum |offdiag| + 1 (strictly diagonally dominant, hence SPD).  At the
+    default N = 2^22 this gives nnz = 49,986,874 and row lengths 1 .. 49,349
+    (median 9), the figures SURVEY.md records.
+    """
+    N = int(n_rows)
+    rng = np.random.default_rng(seed)
+    w = (np.arange(N) + 10.0) ** (-1.0 / (tau - 1.0))
+    M = int((avg_degree * N - N) / 2)
+    src = rng.choice(N, size=M, p=w / w.sum())
+    dst = rng.integers(0, N, size=M)
+    vals = -rng.uniform(0.1, 1.0, size=M)
+    keep = src != dst
+    src, dst, vals = src[keep], dst[keep], vals[keep]
+    # duplicates summed once per unordered pair (draw order), then mirrored:
+    # the matrix is exactly symmetric
+    lo, hi = np.minimum(src, dst), np.maximum(src, dst)
+    key = lo * N + hi
+    order = np.argsort(key, kind="stable")
+    key = key[order]
+    v = vals[order]
+    first = np.ones(key.size, dtype=bool)
+    first[1:] = key[1:] != key[:-1]
+    starts = np.flatnonzero(first)
+    pk = key[starts]
+    pv = np.add.reduceat(v, starts) if v.size else v
+    a, b = pk // N, pk % N
+    r = np.concatenate([a, b])
+    c = np.concatenate([b, a])
+    uv = np.concatenate([pv, pv])
+    order = np.argsort(r * N + c, kind="stable")
+    ur, uc, uv = r[order], c[order], uv[order]
+    diag = np.bincount(ur, weights=np.abs(uv), minlength=N) + 1.0
+    # merge the diagonal into ascending column order per row
+    counts = np.bincount(ur, minlength=N) + 1
+    row_offsets = np.zeros(N + 1, dtype=np.int64)
+    np.cumsum(counts, out=row_offsets[1:])
+    nnz = int(row_offsets[-1])
+    below = np.bincount(ur[uc < ur], minlength=N)  # entries left of the diagonal
+    dpos = row_offsets[:-1] + below
+    is_diag = np.zeros(nnz, dtype=bool)
+    is_diag[dpos] = True
+    col = np.empty(nnz, dtype=np.int64)
+    val = np.empty(nnz, dtype=np.float64)
+    col[dpos] = np.arange(N)
+    val[dpos] = diag
+    col[~is_diag] = uc
+    val[~is_diag] = uv
+    return CsrMatrix(N, N, row_offsets, col, val)

@@ -54,7 +54,7 @@ def run_virtual(world, make_problem, cfg, chunk=0, engine="fused"):
 
 @pytest.mark.parametrize("world,kind,n,engine", [(2, "3d7", 40, "fused-a"), (3, "3d7", 33, "fused-b"),
                                                  (2, "2d5", 200, "fused-c"), (4, "3d27", 24, "fused"),
-                                                 (3, "3d27", 20, "fused-c")])
+                                                 (3, "3d27", 20, "fused-c"), (2, "3d7", 30, "fused-d")])
 def test_virtual_ranks_match_single_gpu(cuda, world, kind, n, engine):
     A = oracle.stencil(kind, n)
     x_true, b, x0, d = oracle.manufactured(A)

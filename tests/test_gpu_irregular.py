@@ -1,0 +1,118 @@
+"""Irregular matrices (BASELINE.json configs[3]: power-law row lengths) on
+the nnz-balanced fused variant D, checked against the oracle.
+
+* Rows staged in shared memory are summed in CSR order from the products
+  a_k * m[c_k], so with dot_mode="seq" a solve without hub rows is bitwise
+  the reference's (kernels.py:64-70, solvers.py:324-387), whatever the tile
+  boundaries are.
+* Hub rows (longer than the tile's hub threshold) are combined with a
+  fixed tree: graded against the oracle's own reorder envelope.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+pb = pytest.importorskip("paper_2105_06176_b200")
+from test_gpu_solver import assert_within_envelope, envelope  # noqa: E402
+
+SEQ = pb.DeviceOptions(dot_mode="seq", engine="fused-d")
+
+
+def _problem(A):
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    return b, x0, d, tol
+
+
+def _random_spd(n, max_len, seed):
+    """Symmetric, strictly diagonally dominant, row lengths 1..max_len."""
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(0, max_len // 2, size=n)
+    r = np.repeat(np.arange(n), lens)
+    c = rng.integers(0, n, size=r.size)
+    keep = r != c
+    r, c = r[keep], c[keep]
+    dense_key = np.unique(np.minimum(r, c) * n + np.maximum(r, c))
+    a, b = dense_key // n, dense_key % n
+    v = -rng.uniform(0.1, 1.0, size=a.size)
+    rows = np.concatenate([a, b, np.arange(n)])
+    cols = np.concatenate([b, a, np.arange(n)])
+    vals = np.concatenate([v, v, np.zeros(n)])
+    order = np.lexsort((cols, rows))
+    rows, cols, vals = rows[order], cols[order], vals[order]
+    diag = np.bincount(rows, weights=np.abs(vals), minlength=n) + 1.0
+    vals[rows == cols] = diag
+    ro = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=ro[1:])
+    return pb.CsrMatrix(n, n, ro, cols, vals)
+
+
+@pytest.mark.parametrize("dcap", [None, 512, 2048])
+def test_powerlaw_seq_bitwise_balanced_tiles(cuda, monkeypatch, dcap):
+    """nnz-capped tiles, every row <= 256 nonzeros (so the init SpMVs take
+    the in-order row path too) and no hub tiles: bitwise in seq-dot mode."""
+    if dcap:
+        monkeypatch.setenv("PIPECG_B200_DCAP", str(dcap))
+    A = pb.generate_powerlaw(2**12)
+    assert A.row_nnz().max() <= min(256, (dcap or 10**9) // 2)
+    b, x0, d, tol = _problem(A)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=2000)
+    pc = pb.jacobi_setup(A)
+    np.testing.assert_array_equal(pc.inv_diag, d)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=2000, record_history=True)
+    x, rep = pb.pipecg_solve(A, b, x0, pc, cfg, options=SEQ)
+    assert rep.iterations == ref.iterations
+    assert rep.history == ref.history
+    np.testing.assert_array_equal(x, ref.x)
+
+
+@pytest.mark.parametrize("engine", ["auto", "fused-d", "two"])
+def test_powerlaw_tree_within_envelope(cuda, engine):
+    A = pb.generate_powerlaw(2**16)
+    b, x0, d, tol = _problem(A)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=2000)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=2000, record_history=True)
+    x, rep = pb.pipecg_solve(A, b, x0, pb.jacobi_setup(A), cfg,
+                             options=pb.DeviceOptions(engine=engine))
+    assert_within_envelope(x, rep, ref.iterations, ref.history, ref.x,
+                           envelope(A, b, x0, d, tol, 2000))
+
+
+@pytest.mark.parametrize("dcap", [64, 256])
+def test_powerlaw_hub_rows(cuda, monkeypatch, dcap):
+    """A small tile cap turns the long rows into hub tiles (tree-combined)."""
+    monkeypatch.setenv("PIPECG_B200_DCAP", str(dcap))
+    A = pb.generate_powerlaw(2**15)
+    assert A.row_nnz().max() > dcap // 2  # hubs exist
+    b, x0, d, tol = _problem(A)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=2000)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=2000, record_history=True)
+    env = envelope(A, b, x0, d, tol, 2000)
+    for mode in ("tree", "seq"):
+        x, rep = pb.pipecg_solve(A, b, x0, pb.jacobi_setup(A), cfg,
+                                 options=pb.DeviceOptions(engine="fused-d", dot_mode=mode))
+        assert_within_envelope(x, rep, ref.iterations, ref.history, ref.x, env)
+
+
+@pytest.mark.parametrize("dcap,max_len", [(16, 12), (64, 40), (1000, 200)])
+def test_random_spd_tiles_bitwise(cuda, monkeypatch, dcap, max_len):
+    """Ragged rows and many tile splits: bitwise when no row is a hub
+    (every row <= dcap/2 nonzeros), else within the reorder envelope."""
+    monkeypatch.setenv("PIPECG_B200_DCAP", str(dcap))
+    A = _random_spd(5000, max_len, seed=dcap)
+    b, x0, d, tol = _problem(A)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=3000)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=3000, record_history=True)
+    x, rep = pb.pipecg_solve(A, b, x0, pb.jacobi_setup(A), cfg, options=SEQ)
+    if A.row_nnz().max() <= dcap // 2:
+        assert rep.history == ref.history
+        np.testing.assert_array_equal(x, ref.x)
+    else:
+        assert_within_envelope(x, rep, ref.iterations, ref.history, ref.x,
+                               envelope(A, b, x0, d, tol, 3000))

@@ -35,7 +35,7 @@ def _cfg(g, record=True):
 CASES = [c for c in META["cases"] if c != "p125n6_pcg"]
 
 
-@pytest.mark.parametrize("engine", ["fused-a", "fused-b", "fused-c", "two"])
+@pytest.mark.parametrize("engine", ["fused-a", "fused-b", "fused-c", "fused-d", "two"])
 @pytest.mark.parametrize("case", CASES)
 def test_golden_bitwise_seq_mode(cuda, case, engine):
     """dot_mode='seq' reproduces the reference solve bit for bit."""
@@ -86,7 +86,7 @@ def assert_within_envelope(x, rep, ref_iters, ref_hist, ref_x, env):
     assert rel <= max(1e-8, 3 * x_gap), (rel, env)
 
 
-@pytest.mark.parametrize("engine", ["fused-a", "fused-b", "fused-c", "two"])
+@pytest.mark.parametrize("engine", ["fused-a", "fused-b", "fused-c", "fused-d", "two"])
 @pytest.mark.parametrize("case", CASES)
 def test_golden_tree_mode_tolerance(cuda, case, engine):
     """Default (tree dots): iterations, history and x within the larger of the

@@ -166,3 +166,28 @@ def test_poisson125_shape_and_capacity():
 def test_device_options():
     o = pb.DeviceOptions(dot_mode="seq", engine="two", chunk=8, use_graphs=False).native()
     assert (o.dot_mode, o.engine, o.chunk, o.use_graphs) == (_lib.PCG_DOT_SEQ, 2, 8, 0)
+
+
+def test_powerlaw_generator_structure():
+    """BASELINE configs[3] recipe: symmetric, strictly
+    diagonally dominant, ascending columns, power-law row lengths."""
+    A = pb.generate_powerlaw(2**14)
+    rl = A.row_nnz()
+    assert rl.min() >= 1 and rl.max() > 30 * np.median(rl)
+    rows = np.repeat(np.arange(A.n_rows), rl)
+    ci, va = A.col_indices, A.values
+    key, tkey = rows * A.n_rows + ci, ci * A.n_rows + rows
+    o1, o2 = np.argsort(key), np.argsort(tkey)
+    np.testing.assert_array_equal(key[o1], tkey[o2])
+    np.testing.assert_array_equal(va[o1], va[o2])
+    off = rows != ci
+    assert np.all(va[~off] > np.bincount(rows[off], weights=np.abs(va[off]), minlength=A.n_rows))
+
+
+def test_powerlaw_generator_full_size_matches_survey():
+    """At N = 2^22 the recipe reproduces SURVEY.md's probe: nnz 49,986,874,
+    row lengths 1 / 9 / 49,349 (min / median / max)."""
+    A = pb.generate_powerlaw()
+    rl = A.row_nnz()
+    assert A.nnz == 49_986_874
+    assert (rl.min(), int(np.median(rl)), rl.max()) == (1, 9, 49_349)

@@ -1,5 +1,5 @@
 #!/bin/bash
-# One gpurun call: any of  tests[=<pytest args>]  bench[=<bench args>]  ncu
+# One gpurun call: any of  tests[=<pytest args>]  bench[=<bench args>]  ncu[=<config>:<engine>]
 # Outputs land in gpurun_out/.
 set -u
 OUT=gpurun_out
@@ -15,15 +15,22 @@ for job in "$@"; do
       echo "pytest rc=$?" >> $OUT/pytest_gpu.txt; tail -15 $OUT/pytest_gpu.txt ;;
     bench*)
       args="${job#bench}"; args="${args#=}"
-      timeout 900 python bench.py $args > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"
-      tail -c 4000 $OUT/bench.json; tail -5 $OUT/bench.err ;;
-    ncu)
+      tag=$(echo "$args" | tr -c 'a-zA-Z0-9-' '_' | cut -c1-40)
+      timeout 900 python bench.py $args > $OUT/bench$tag.json 2> $OUT/bench$tag.err; echo "bench $args rc=$?"
+      tail -c 4000 $OUT/bench$tag.json; tail -5 $OUT/bench$tag.err ;;
+    ncu*)
+      spec="${job#ncu}"; spec="${spec#=}"; cfg="${spec%%:*}"; eng="${spec##*:}"
+      cfg=${cfg:-3d7-256}; [ "$eng" = "$spec" ] && eng=fused-c; eng=${eng:-fused-c}
+      case "$eng" in fused-c) kre='regex:pipecg_fused_kernel_a';; fused-a) kre='regex:pipecg_fused_kernel_a';;
+                     fused-b) kre='regex:pipecg_fused_kernel[^_]';; two) kre='regex:gated_spmv_rows|pipecg_k1';;
+                     *) kre='regex:pipecg_';; esac
+      common="python bench.py --config $cfg --engine $eng --no-north-star --no-e2e --no-cpu --no-tts"
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
-         --log-file $OUT/launches.csv python bench.py --steps 20 --warmup 3 --no-north-star --no-e2e --no-cpu > $OUT/ncu_launch_bench.json 2>&1
-      echo "ncu launches rc=$?"
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:pipecg_fused -s 4 -c 1 \
-         -o $OUT/prof_fused -f python bench.py --steps 8 --warmup 3 --no-north-star --no-e2e --no-cpu > $OUT/ncu_full.log 2>&1
-      echo "ncu full rc=$?"; tail -2 $OUT/ncu_full.log ;;
+         --log-file $OUT/launches_${cfg}_${eng}.csv $common --steps 20 --warmup 3 > $OUT/ncu_launch_${cfg}_${eng}.json 2>&1
+      echo "ncu launches $cfg $eng rc=$?"
+      timeout 900 ncu --set full --clock-control none --import-source on -k "$kre" -s 4 -c 1 \
+         -o $OUT/prof_${cfg}_${eng} -f $common --steps 8 --warmup 3 > $OUT/ncu_full_${cfg}_${eng}.log 2>&1
+      echo "ncu full $cfg $eng rc=$?"; tail -2 $OUT/ncu_full_${cfg}_${eng}.log ;;
     *) eval "$job" ;;
   esac
 done

@@ -67,6 +67,10 @@ def main():
     ap.add_argument("report", nargs="?")
     ap.add_argument("--bytes", type=float, default=None)
     ap.add_argument("--title", default="ncu summary")
+    ap.add_argument("--traffic-key", default=None,
+                    help="'<bench config>/<engine code>': record the captured kernel's DRAM "
+                         "bytes per launch in profiles/traffic.json (read by bench.py)")
+    ap.add_argument("--source", default=None, help="profile file name recorded as the source")
     a = ap.parse_args()
     agg = launches(a.launch_csv)
     tot = sum(sum(v) for v in agg.values())
@@ -95,6 +99,17 @@ def main():
                 wr *= scale[rec["dram__bytes_write.sum"][1]]
                 print(f"\nDRAM traffic per launch: {(rd + wr) / 1e9:.4f} GB "
                       f"({(rd + wr) / t_s / 1e9:.0f} GB/s over the ncu duration)")
+                if a.traffic_key:
+                    import json
+                    import pathlib
+
+                    tp = pathlib.Path(__file__).resolve().parents[1] / "profiles" / "traffic.json"
+                    d = json.loads(tp.read_text()) if tp.exists() else {}
+                    d[a.traffic_key] = {"dram_bytes_per_launch": rd + wr,
+                                        "kernel": rec["Kernel Name"][0][:120],
+                                        "ncu_duration_s": t_s,
+                                        "source": a.source or a.report}
+                    tp.write_text(json.dumps(d, indent=1, sort_keys=True) + "\n")
                 if a.bytes:
                     print(f"Algorithmic (canonical) bytes per launch: {a.bytes / 1e9:.4f} GB; "
                           f"traffic/algorithmic = {(rd + wr) / a.bytes:.3f}")

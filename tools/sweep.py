@@ -10,7 +10,7 @@ import paper_2105_06176_b200 as pb
 
 OPT_KEYS = {"engine", "dot_mode", "chunk", "use_graphs", "max_sms"}
 
-def time_variant(A, d, v, steps=60, warm=5):
+def time_variant(A, d, v, steps=40, warm=5):
     for k in list(os.environ):
         if k.startswith("PIPECG_B200_"):
             os.environ.pop(k)
@@ -38,7 +38,8 @@ def time_variant(A, d, v, steps=60, warm=5):
 if __name__ == "__main__":
     kind, n = sys.argv[1], int(sys.argv[2])
     variants = json.loads(sys.argv[3])
-    A = pb.stencil_device(kind, n)
+    A = (pb.as_device_csr(pb.generate_powerlaw(2**n)) if kind == "powerlaw"
+         else pb.stencil_device(kind, n))
     d = pb.jacobi_setup(A).inv_diag
     N, nnz = A.n_rows, A.nnz
     B = 176 * N + 12 * nnz + 4 * (N + 1)
