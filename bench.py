@@ -372,7 +372,9 @@ def e2e_host(pb, torch, kind, n, reps: int = 1):
         total_s += dt
         del A
         torch.cuda.empty_cache()
-    h2d = 8 * (N + 1) + 16 * nnz + 3 * 8 * N
+    # bytes that cross PCIe: int32 row offsets / columns (narrowed on the host
+    # side of the pinned pipeline), float64 values, b, x0 and inv_diag
+    h2d = (8 if nnz >= 2**31 else 4) * (N + 1) + 12 * nnz + 3 * 8 * N
     d2h = 8 * N
     per_call_it = total_it / reps
     return {"value": total_it / total_s, "unit": UNIT,
@@ -381,8 +383,9 @@ def e2e_host(pb, torch, kind, n, reps: int = 1):
             "iterations_per_call": per_call_it, "seconds_per_call": total_s / reps,
             "call": "paper_2105_06176_b200.pipecg_solve(A host CsrMatrix int64, b, x0 numpy, "
                     "JacobiPreconditioner(numpy), SolverConfig(tol=1e-8*norm0)) -> (x numpy, report)",
-            "host_memory": "pageable numpy (the reference's own arrays); CSR uploaded as int64 and "
-                           "narrowed to int32 on the device"}
+            "host_memory": "pageable numpy (the reference's own int64/float64 arrays); staged by the "
+                           "native pinned pipeline (csrc/hostio.cu), indices narrowed to int32 "
+                           "on the host side"}
 
 
 def run_b200(args):

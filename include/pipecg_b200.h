@@ -111,6 +111,17 @@ int64_t pipecg_b200_dots_workspace_bytes(void);
 int pipecg_b200_narrow_i64(int64_t n, const int64_t* src, int32_t* dst, int* overflow_host,
                            void* stream);
 
+/* Host <-> device transfer pipeline for the reference's pageable host
+ * arrays (csrc/hostio.cu): a pool of host threads converts chunks into a
+ * pinned staging ring while earlier chunks cross PCIe on `stream`.
+ * kind PCG_H2D_I64_TO_I32 narrows int64 indices (sparse.py:59-71 layout) to
+ * the device's int32 (PCG_ERANGE if any value does not fit); PCG_H2D_COPY64
+ * copies 8-byte elements.  h2d returns once every chunk is enqueued (the
+ * source may be reused then); d2h returns when dst_host holds the data. */
+enum { PCG_H2D_COPY64 = 0, PCG_H2D_I64_TO_I32 = 1 };
+int pipecg_b200_h2d(void* dst_dev, const void* src_host, int64_t count, int kind, void* stream);
+int pipecg_b200_d2h(void* dst_host, const void* src_dev, int64_t bytes, void* stream);
+
 /* Rows with more than `threshold` entries -> long_rows (device int32[cap]);
  * *n_long_host receives the count.  Synchronous. */
 int pipecg_b200_find_long_rows(int64_t n_rows, int rp64, const void* rowptr, int64_t threshold,
@@ -150,7 +161,7 @@ typedef struct {
 typedef struct {
   int dot_mode;        /* PCG_DOT_TREE (default) or PCG_DOT_SEQ */
   int engine;          /* 0 auto (autotuned for >= 64K rows), 1 fused (variant autotuned),
-                          2 two-kernel, 3/4/5/6 fused variant A/B/C/D */
+                          2 two-kernel, 3..6 fused variant A/B/C/D */
   int chunk;           /* iterations per CUDA-graph chunk (0 = auto) */
   int use_graphs;      /* 1 (default) or 0 (plain launches, debugging) */
   int max_sms;         /* size persistent grids for at most this many SMs (0 = all) */
@@ -167,9 +178,10 @@ typedef struct {
   double breakdown_value;
   int64_t n_history;   /* entries written to history_host */
   int64_t n_drift;     /* samples written to drift_*_host */
-  int engine;          /* engine used: 2 two-kernel, 3/4/5/6 fused variant A/B/C/D */
+  int engine;          /* engine used: 2 two-kernel, 3..6 fused variant A/B/C/D */
   int64_t graph_launches;
-  double tune_ms[5];   /* autotune ms/iteration: fused A, B, C, D, two-kernel (0 = not run) */
+  double tune_ms[8];   /* autotune ms/iteration: fused A, B, C, D, two-kernel, -, -, -
+                          (0 = not run) */
 } pcg_result;
 
 int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_solver** out);

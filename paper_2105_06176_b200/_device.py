@@ -56,7 +56,32 @@ def to_device_f64(v, pad: int = 0) -> torch.Tensor:
     if pad:
         out[a.size:].zero_()
     if a.size:
-        out[: a.size].copy_(torch.from_numpy(a), non_blocking=False)
+        h2d(out, a)
+    return out
+
+
+def h2d(dst: torch.Tensor, src: np.ndarray, narrow: bool = False) -> None:
+    """Host -> device through the native pinned pipeline (csrc/hostio.cu).
+
+    ``src`` is a contiguous int64 / float64 host array; with ``narrow`` the
+    int64 values are narrowed to the int32 ``dst`` on the host side."""
+    from . import _lib
+
+    src = np.ascontiguousarray(src)
+    kind = _lib.PCG_H2D_I64_TO_I32 if narrow else _lib.PCG_H2D_COPY64
+    _lib.call("pipecg_b200_h2d", dst.data_ptr(), src.ctypes.data, src.size, kind, stream_ptr())
+    # the staging ring is reused by the next transfer; the caller's stream
+    # orders the copies before any kernel that reads dst
+
+
+def d2h(src: torch.Tensor) -> np.ndarray:
+    """Device float64 vector -> new host ndarray (native pinned pipeline)."""
+    from . import _lib
+
+    src = src.contiguous()
+    out = np.empty(src.numel(), dtype=np.float64)
+    if out.size:
+        _lib.call("pipecg_b200_d2h", out.ctypes.data, src.data_ptr(), out.nbytes, stream_ptr())
     return out
 
 

@@ -49,7 +49,7 @@ class PcgResult(ctypes.Structure):
         ("status", _int), ("converged", _int), ("iterations", _i64), ("final_norm", _dbl),
         ("norm0", _dbl), ("breakdown_quantity", _int), ("breakdown_iteration", _i64),
         ("breakdown_value", _dbl), ("n_history", _i64), ("n_drift", _i64), ("engine", _int),
-        ("graph_launches", _i64), ("tune_ms", _dbl * 5),
+        ("graph_launches", _i64), ("tune_ms", _dbl * 8),
     ]
 
 
@@ -62,6 +62,8 @@ class NativeError(RuntimeError):
 
 
 _lib = None
+
+PCG_H2D_COPY64, PCG_H2D_I64_TO_I32 = 0, 1
 
 _SIGS = {
     "pipecg_b200_last_error": ([], ctypes.c_char_p),
@@ -77,6 +79,8 @@ _SIGS = {
     "pipecg_b200_dots": ([_i64, _int, _vp, _vp, _int, _vp, _vp, _vp], _int),
     "pipecg_b200_dots_workspace_bytes": ([], _i64),
     "pipecg_b200_narrow_i64": ([_i64, _vp, _vp, ctypes.POINTER(_int), _vp], _int),
+    "pipecg_b200_h2d": ([_vp, _vp, _i64, _int, _vp], _int),
+    "pipecg_b200_d2h": ([_vp, _vp, _i64, _vp], _int),
     "pipecg_b200_find_long_rows": ([_i64, _int, _vp, _i64, _vp, _i64, _p_i64, _vp], _int),
     "pipecg_b200_stencil_shape": ([_int, _i64, _p_i64, _p_i64], _int),
     "pipecg_b200_stencil_prefix": ([_int, _i64, _i64, _p_i64], _int),

@@ -3,8 +3,9 @@
 // This is the C-ABI form of the reference's pipecg_solve(A, b, x0, pc, cfg)
 // (solvers.py:324-387) for callers that hold the reference's host layout:
 // int64 row offsets / column indices and float64 values (sparse.py:59-71).
-// It uploads the CSR (narrowing indices to int32 on the device), solves with
-// the fused engine and downloads x.  See INTEGRATION.md for the ctypes
+// It uploads the CSR through the pinned transfer pipeline (hostio.cu;
+// indices narrowed to int32 on the host side), solves with the autotuned
+// engine and downloads x.  See INTEGRATION.md for the ctypes
 // binding a maintainer of the reference would add.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -42,41 +43,30 @@ extern "C" int pipecg_b200_solve_host(int64_t n, const int64_t* ro_h, const int6
   cudaStream_t st = nullptr;
   int rc = cuda_status(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "solve_host stream");
   if (rc) return rc;
-  DevBuf ro64, rp, ci64, ci, va, dinv, b, x0;
+  DevBuf rp, ci, va, dinv, b, x0;
   const size_t pad = 16;
-  if ((rc = ro64.alloc((n + 1) * 8)) || (rc = rp.alloc((n + 1 + pad) * (rp64 ? 8 : 4))) ||
-      (rc = ci64.alloc(nnz * 8)) || (rc = ci.alloc((nnz + pad) * 4)) ||
+  if ((rc = rp.alloc((n + 1 + pad) * (rp64 ? 8 : 4))) || (rc = ci.alloc((nnz + pad) * 4)) ||
       (rc = va.alloc((nnz + pad) * 8)) || (rc = dinv.alloc(n * 8)) || (rc = b.alloc(n * 8)) ||
       (rc = x0.alloc(n * 8))) {
     cudaStreamDestroy(st);
     return rc;
   }
-  cudaMemsetAsync(va.p, 0, (nnz + pad) * 8, st);
-  cudaMemsetAsync(ci.p, 0, (nnz + pad) * 4, st);
-  cudaMemcpyAsync(ro64.p, ro_h, (n + 1) * 8, cudaMemcpyHostToDevice, st);
-  if (nnz) {
-    cudaMemcpyAsync(ci64.p, ci_h, nnz * 8, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(va.p, va_h, nnz * 8, cudaMemcpyHostToDevice, st);
-  }
-  cudaMemcpyAsync(dinv.p, dinv_h, n * 8, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(b.p, b_h, n * 8, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(x0.p, x0_h, n * 8, cudaMemcpyHostToDevice, st);
-  int overflow = 0;
-  rc = pipecg_b200_narrow_i64(nnz, ci_h ? (const int64_t*)ci64.p : nullptr, (int32_t*)ci.p,
-                              &overflow, st);
-  if (!rc) {
-    if (rp64) {
-      cudaMemcpyAsync(rp.p, ro64.p, (n + 1) * 8, cudaMemcpyDeviceToDevice, st);
-      // pad with nnz so staged reads past the end stay in range
-      for (size_t k = 0; k < pad; ++k)
-        cudaMemcpyAsync((int64_t*)rp.p + n + 1 + k, (int64_t*)ro64.p + n, 8,
-                        cudaMemcpyDeviceToDevice, st);
-    } else {
-      rc = pipecg_b200_narrow_i64(n + 1, (const int64_t*)ro64.p, (int32_t*)rp.p, &overflow, st);
-      for (size_t k = 0; k < pad && !rc; ++k)
-        cudaMemcpyAsync((int32_t*)rp.p + n + 1 + k, (int32_t*)rp.p + n, 4, cudaMemcpyDeviceToDevice,
-                        st);
-    }
+  // pageable host arrays -> device through the pinned pipeline (hostio.cu),
+  // indices narrowed to int32 on the host side
+  cudaMemsetAsync((char*)va.p + nnz * 8, 0, pad * 8, st);
+  cudaMemsetAsync((char*)ci.p + nnz * 4, 0, pad * 4, st);
+  rc = pipecg_b200_h2d(rp.p, ro_h, n + 1, rp64 ? PCG_H2D_COPY64 : PCG_H2D_I64_TO_I32, st);
+  if (!rc && nnz) rc = pipecg_b200_h2d(ci.p, ci_h, nnz, PCG_H2D_I64_TO_I32, st);
+  if (!rc && nnz) rc = pipecg_b200_h2d(va.p, va_h, nnz, PCG_H2D_COPY64, st);
+  if (!rc) rc = pipecg_b200_h2d(dinv.p, dinv_h, n, PCG_H2D_COPY64, st);
+  if (!rc) rc = pipecg_b200_h2d(b.p, b_h, n, PCG_H2D_COPY64, st);
+  if (!rc) rc = pipecg_b200_h2d(x0.p, x0_h, n, PCG_H2D_COPY64, st);
+  // pad the row pointers with nnz so staged reads past the end stay in range
+  for (size_t k = 0; k < pad && !rc; ++k) {
+    if (rp64)
+      cudaMemcpyAsync((int64_t*)rp.p + n + 1 + k, (int64_t*)rp.p + n, 8, cudaMemcpyDeviceToDevice, st);
+    else
+      cudaMemcpyAsync((int32_t*)rp.p + n + 1 + k, (int32_t*)rp.p + n, 4, cudaMemcpyDeviceToDevice, st);
   }
   pcg_solver* S = nullptr;
   if (!rc) {
@@ -101,10 +91,7 @@ extern "C" int pipecg_b200_solve_host(int64_t n, const int64_t* ro_h, const int6
   if (!rc) rc = pipecg_b200_solver_init(S, (const double*)b.p, (const double*)x0.p, tol, max_it,
                                         drift_k, st);
   if (!rc) rc = pipecg_b200_solver_run(S, res, hist_h, hist_cap, dit_h, dval_h, drift_cap);
-  if (!rc) {
-    rc = cuda_status(cudaMemcpy(x_h, pipecg_b200_solver_x(S), n * 8, cudaMemcpyDeviceToHost),
-                     "download x");
-  }
+  if (!rc) rc = pipecg_b200_d2h(x_h, pipecg_b200_solver_x(S), n * 8, st);
   if (S) pipecg_b200_solver_destroy(S);
   cudaStreamSynchronize(st);
   cudaStreamDestroy(st);

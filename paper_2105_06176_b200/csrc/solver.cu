@@ -33,6 +33,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -253,6 +254,52 @@ __device__ Step prologue(Ctrl* C, double* hist, const ReduceIn& R, long long it,
   return st;
 }
 
+// The block's (r,u),(w,u),(u,u) partial -> pout; the last block of the grid
+// to finish (atomic ticket) sums all partials in a fixed order into fin, so
+// the next prologue reads 3 numbers instead of every block's partial.
+// Used for large grids only (kFinGrid): for small grids the serial tail
+// costs more than every block reducing a few hundred partials itself.
+// Deterministic: the sum order does not depend on which block is last.
+// red needs 3*NT/32 + 1 doubles.
+template <int NT>
+__device__ __forceinline__ void publish_partials(double (&acc)[3], int lt, double* red, int bar_id,
+                                                 double* pout, double* fin, unsigned* counter,
+                                                 long long it) {
+  constexpr int NW = NT / PCG_WARP;
+  group_sum<3, NT>(acc, lt, red, bar_id);
+  double* part = pout + (size_t)(it & 1) * (size_t)gridDim.x * 4;
+  if (lt == 0) {
+    double* out = part + (size_t)blockIdx.x * 4;
+    out[0] = acc[0];
+    out[1] = acc[1];
+    out[2] = acc[2];
+    out[3] = 0.0;
+    if (!counter) return;
+    __threadfence();
+    const unsigned ticket = atomicAdd(counter + (it & 1), 1u);
+    red[3 * NW] = ticket == gridDim.x - 1 ? 1.0 : 0.0;
+  }
+  if (!counter) return;  // small grids: the next prologue reduces the partials itself
+  bar_sync(bar_id, NT);
+  if (red[3 * NW] == 0.0) return;
+  __threadfence();
+  double v[3] = {0.0, 0.0, 0.0};
+  for (int j = lt; j < (int)gridDim.x; j += NT) {
+    v[0] = add(v[0], __ldcg(part + j * 4 + 0));
+    v[1] = add(v[1], __ldcg(part + j * 4 + 1));
+    v[2] = add(v[2], __ldcg(part + j * 4 + 2));
+  }
+  group_sum<3, NT>(v, lt, red, bar_id);
+  if (lt == 0) {
+    double* f = fin + (size_t)(it & 1) * 4;
+    f[0] = v[0];
+    f[1] = v[1];
+    f[2] = v[2];
+    f[3] = 0.0;
+    counter[it & 1] = 0u;  // reused by iteration it + 2 (stream-ordered)
+  }
+}
+
 // ===========================================================================
 // Engine 1: fused iteration kernel
 // ===========================================================================
@@ -271,6 +318,8 @@ struct FusedParams {
   double* hist;
   ReduceIn rin;   // what the prologue reduces
   double* pout;   // block partials [2][gridDim.x][4]
+  double* fin;    // [2][4] their fixed-order sum (written by the last block)
+  unsigned* counter;  // [2] blocks done per iteration parity
   int stages;
   int cap_val;  // doubles per stage
   int cap_col;  // ints per stage
@@ -506,14 +555,7 @@ __global__ void __launch_bounds__(FusedLayout<RP, TR>::kThreads) pipecg_fused_ke
     __syncwarp();
     if ((lt & 31) == 0) mbar_arrive(&empty[s]);
   }
-  group_sum<3, NT>(acc, lt, red, 1);
-  if (lt == 0) {
-    double* out = P.pout + (size_t)(it & 1) * (size_t)gridDim.x * 4 + (size_t)blockIdx.x * 4;
-    out[0] = acc[0];
-    out[1] = acc[1];
-    out[2] = acc[2];
-    out[3] = 0.0;
-  }
+  publish_partials<NT>(acc, lt, red, 1, P.pout, P.fin, P.counter, it);
 }
 
 template <typename RP, int TR>
@@ -708,14 +750,7 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_a(FusedParams<RP>
     __syncwarp();
     if ((lt & 31) == 0) mbar_arrive(&empty[s]);
   }
-  group_sum<3, NT>(acc, lt, red, 1);
-  if (lt == 0) {
-    double* out = P.pout + (size_t)(it & 1) * (size_t)gridDim.x * 4 + (size_t)blockIdx.x * 4;
-    out[0] = acc[0];
-    out[1] = acc[1];
-    out[2] = acc[2];
-    out[3] = 0.0;
-  }
+  publish_partials<NT>(acc, lt, red, 1, P.pout, P.fin, P.counter, it);
 }
 
 // ---------------------------------------------------------------------------
@@ -950,14 +985,7 @@ __global__ void __launch_bounds__(kDThreads + 32) pipecg_fused_kernel_d(FusedPar
     __syncwarp();
     if ((lt & 31) == 0) mbar_arrive(&empty[s]);
   }
-  group_sum<3, NT>(acc, lt, red, 1);
-  if (lt == 0) {
-    double* out = P.pout + (size_t)(it & 1) * (size_t)gridDim.x * 4 + (size_t)blockIdx.x * 4;
-    out[0] = acc[0];
-    out[1] = acc[1];
-    out[2] = acc[2];
-    out[3] = 0.0;
-  }
+  publish_partials<NT>(acc, lt, red, 1, P.pout, P.fin, P.counter, it);
 }
 
 // ===========================================================================
@@ -971,10 +999,12 @@ struct TwoParams {
   double* hist;
   ReduceIn rin;
   double* pout;
+  double* fin;
+  unsigned* counter;
 };
 
 __global__ void __launch_bounds__(256) pipecg_k1_kernel(TwoParams P, int step) {
-  __shared__ double red[3 * 8];
+  __shared__ double red[3 * 8 + 1];
   Ctrl* C = P.C;
   if (read_status(C) != PCG_RUNNING) return;
   const long long it = C->base_it + step;
@@ -1006,14 +1036,7 @@ __global__ void __launch_bounds__(256) pipecg_k1_kernel(TwoParams P, int step) {
     acc[1] = add(acc[1], mul(wn, un));
     acc[2] = add(acc[2], mul(un, un));
   }
-  group_sum<3, 256>(acc, threadIdx.x, red, 1);
-  if (threadIdx.x == 0) {
-    double* out = P.pout + (size_t)(it & 1) * (size_t)gridDim.x * 4 + (size_t)blockIdx.x * 4;
-    out[0] = acc[0];
-    out[1] = acc[1];
-    out[2] = acc[2];
-    out[3] = 0.0;
-  }
+  publish_partials<256>(acc, threadIdx.x, red, 1, P.pout, P.fin, P.counter, it);
 }
 
 template <typename RP>
@@ -1400,11 +1423,13 @@ struct FusedPlan {
                     // 3: nnz-balanced tiles + cooperative gathers of the stored m (D)
   int tr = 0, stages = 0, bps = 0, cap_val = 0, cap_col = 0, grid = 0, score = 0;
   size_t smem = 0;
-  long long n_tiles = 0;  // variant D: tiles built for this plan
+  long long n_tiles = 0;  // variants D/E: tiles built for this plan (owned by the solver)
   long long cap = 0, hub_len = 0;
+  int* tile_row = nullptr;
+  long long* tile_e = nullptr;
 };
 
-constexpr int kVariants = 4;
+constexpr int kVariants = 4;  // A B C D
 
 struct pcg_solver {
   pcg_matrix A{};
@@ -1426,6 +1451,8 @@ struct pcg_solver {
          *u = nullptr, *w[2] = {nullptr, nullptr}, *m = nullptr, *nv = nullptr, *b = nullptr,
          *m2 = nullptr;  // m ping-pong partner (fused variant C)
   double* partials = nullptr;  // block partials [2][grid][4]
+  double* fin = nullptr;       // their sum [2][4] (last block)
+  unsigned* counter = nullptr; // [2] last-block tickets
   double* seqbuf = nullptr;    // sequential-dot results [2][1][4]
   double* dpart = nullptr;
   double* dots_ws = nullptr;
@@ -1451,8 +1478,8 @@ struct pcg_solver {
   int flags = 0;                   // experiment switches (env PIPECG_B200_FLAGS)
   int variant = 1;                 // fused kernel variant in use
   FusedPlan plans[kVariants];      // per fused variant (stages == 0: does not fit)
-  double tune_ms[5] = {0, 0, 0, 0, 0};  // autotune ms/iteration: fused A, B, C, D, engine 2
-  int* tile_row = nullptr;         // variant D tiles (first row, first nonzero)
+  double tune_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // autotune ms/iteration: fused A..E, engine 2
+  int* tile_row = nullptr;         // variant D/E tiles of the applied plan
   long long* tile_e = nullptr;
   long long hub_len = 0;
 };
@@ -1498,7 +1525,7 @@ int plan_one(pcg_solver* S, int cap_col, int cap_val, FusedPlan* out) {
   const size_t sm_budget = 228 * 1024, cta_max = 227 * 1024;
   const char* e_st = getenv("PIPECG_B200_STAGES");  // experiment overrides
   const char* e_bps = getenv("PIPECG_B200_BPS");
-  for (int bps = e_bps ? atoi(e_bps) : 2; bps >= 1 && !p.stages; --bps) {
+  for (int bps = e_bps ? atoi(e_bps) : (V == 3 ? 3 : 2); bps >= 1 && !p.stages; --bps) {
     if (e_bps && bps != atoi(e_bps)) break;
     for (int st = 2; st <= 8; ++st) {
       if (e_st ? atoi(e_st) != st : st > 4) continue;
@@ -1558,14 +1585,14 @@ int plan_variant(pcg_solver* S, const int* cc, const int* cv, FusedPlan* best) {
 }
 
 // Variant D tile geometry for tile height TR: when every TR-row block's
-// nonzeros fit twice the average tile (cap_target) the blocks are the tiles
-// (no hubs); otherwise tiles are capped at cap_target nonzeros and rows
-// longer than cap_target / 2 become single-row hub tiles.
+// nonzeros fit the average tile (cap_target = TR * mean row length) the
+// blocks are the tiles (no hubs); otherwise tiles are capped at cap_target
+// nonzeros and rows longer than cap_target / 2 become single-row hub tiles.
 template <int TR>
 void d_geometry(const pcg_solver* S, int cv_block, long long* cap, long long* hub_len) {
   const long long n = S->A.n_rows, nnz = S->A.nnz;
   const long long avg = std::max<long long>(4, (nnz + n - 1) / std::max<long long>(n, 1));
-  long long target = 2LL * TR * avg;
+  long long target = (long long)TR * avg;  // sweep optimum on the power-law config
   if (const char* e = getenv("PIPECG_B200_DCAP")) target = std::max(atoll(e), 8LL);  // experiment / test override
   if (cv_block <= target) {
     *cap = cv_block;
@@ -1605,18 +1632,14 @@ int build_tiles_d(pcg_solver* S, FusedPlan* p) {
   int rc = cuda_status(cudaStreamSynchronize(st), "variant D tile count");
   const long long n_tiles = last_off + last_cnt;
   if (!rc) {
-    cudaFree(S->tile_row);
-    cudaFree(S->tile_e);
-    S->tile_row = nullptr;
-    S->tile_e = nullptr;
-    if (cudaMalloc(&S->tile_row, (n_tiles + 1) * sizeof(int)) != cudaSuccess ||
-        cudaMalloc(&S->tile_e, (n_tiles + 1) * sizeof(long long)) != cudaSuccess)
+    if (cudaMalloc(&p->tile_row, (n_tiles + 1) * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&p->tile_e, (n_tiles + 1) * sizeof(long long)) != cudaSuccess)
       rc = set_error(PCG_ENOMEM, "variant D tiles");
   }
   if (!rc) {
     tile_build_kernel<RP><<<g, 256, 0, st>>>(n, p->tr, p->cap, p->hub_len, rp, 1, counts, offs,
-                                             S->tile_row, S->tile_e);
-    tile_close_kernel<<<1, 1, 0, st>>>(n, n_tiles, S->A.nnz, S->tile_row, S->tile_e);
+                                             p->tile_row, p->tile_e);
+    tile_close_kernel<<<1, 1, 0, st>>>(n, n_tiles, S->A.nnz, p->tile_row, p->tile_e);
     rc = cuda_status(cudaStreamSynchronize(st), "variant D tile build");
   }
   cudaFree(counts);
@@ -1625,7 +1648,6 @@ int build_tiles_d(pcg_solver* S, FusedPlan* p) {
   if (rc) return rc;
   p->n_tiles = n_tiles;
   p->grid = (int)std::max<long long>(std::min<long long>(p->grid, n_tiles), 1);
-  S->hub_len = p->hub_len;
   return PCG_OK;
 }
 
@@ -1676,7 +1698,10 @@ int fused_setup(pcg_solver* S) {
 void apply_plan(pcg_solver* S, const FusedPlan& p) {
   S->variant = p.variant;
   S->tr = p.tr;
-  S->n_tiles = p.variant == 3 ? p.n_tiles : (S->A.n_rows + p.tr - 1) / p.tr;
+  S->n_tiles = p.variant >= 3 ? p.n_tiles : (S->A.n_rows + p.tr - 1) / p.tr;
+  S->tile_row = p.tile_row;
+  S->tile_e = p.tile_e;
+  S->hub_len = p.hub_len;
   S->stages = p.stages;
   S->cap_val = p.cap_val;
   S->cap_col = p.cap_col;
@@ -1710,6 +1735,11 @@ int alloc_state(pcg_solver* S) {
   e = cudaMalloc(&S->partials, (size_t)2 * maxp * 4 * sizeof(double));
   if (e != cudaSuccess) return set_error(PCG_ENOMEM, "solver: partials allocation failed");
   cudaMemsetAsync(S->partials, 0, (size_t)2 * maxp * 4 * sizeof(double), S->stream);
+  if (cudaMalloc(&S->fin, 8 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&S->counter, 2 * sizeof(unsigned)) != cudaSuccess)
+    return set_error(PCG_ENOMEM, "solver: partials allocation failed");
+  cudaMemsetAsync(S->fin, 0, 8 * sizeof(double), S->stream);
+  cudaMemsetAsync(S->counter, 0, 2 * sizeof(unsigned), S->stream);
   if (cudaMalloc(&S->seqbuf, 8 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&S->dpart, kDotGrid * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&S->dots_ws, (size_t)kDotGrid * 4 * sizeof(double)) != cudaSuccess ||
@@ -1725,6 +1755,10 @@ int alloc_state(pcg_solver* S) {
   return cuda_status(cudaStreamSynchronize(S->stream), "solver: workspace init");
 }
 
+// grids above this many blocks publish one fixed-order sum (last block)
+constexpr int kFinGrid = 512;
+inline bool use_fin(const pcg_solver* S) { return S->grid > kFinGrid; }
+
 // What the next prologue reduces, per mode
 ReduceIn reduce_in(pcg_solver* S) {
   ReduceIn R;
@@ -1739,8 +1773,8 @@ ReduceIn reduce_in(pcg_solver* S) {
     R.pin = S->seqbuf;
     R.n_pin = 1;
   } else {
-    R.pin = S->partials;
-    R.n_pin = S->grid;
+    R.pin = use_fin(S) ? S->fin : S->partials;
+    R.n_pin = use_fin(S) ? 1 : S->grid;
   }
   return R;
 }
@@ -1770,6 +1804,8 @@ FusedParams<RP> fused_params(pcg_solver* S) {
   P.hist = R.hist;
   P.rin = reduce_in(S);
   P.pout = S->partials;
+  P.fin = S->fin;
+  P.counter = use_fin(S) ? S->counter : nullptr;
   P.stages = S->stages;
   P.cap_val = S->cap_val;
   P.cap_col = S->cap_col;
@@ -1844,6 +1880,8 @@ int enqueue_step(pcg_solver* S, int k) {
     P.hist = R.hist;
     P.rin = reduce_in(S);
     P.pout = S->partials;
+    P.fin = S->fin;
+    P.counter = use_fin(S) ? S->counter : nullptr;
     pipecg_k1_kernel<<<S->grid, 256, 0, st>>>(P, k);
   }
   if (S->opt.dot_mode == PCG_DOT_SEQ && !S->connected)
@@ -1851,7 +1889,8 @@ int enqueue_step(pcg_solver* S, int k) {
                                       S->seqbuf, k);
   if (S->connected)
     iter_exchange_kernel<<<kXchgBlocks, 256, 0, st>>>(
-        S->cp, R.C, k, S->partials, S->grid, stored_m_fused(S) ? S->m : S->w[0],
+        S->cp, R.C, k, use_fin(S) ? S->fin : S->partials, use_fin(S) ? 1 : S->grid,
+        stored_m_fused(S) ? S->m : S->w[0],
         stored_m_fused(S) ? S->m2 : S->w[1], stored_m_fused(S) ? 9 : 7, stored_m_fused(S) ? 12 : 8);
   if (S->engine == 2) {
     const long long thr = S->n_long > 0 ? kLongRow : INT64_MAX;
@@ -1925,7 +1964,7 @@ int auto_chunk(pcg_solver* S) {
 void fill_result(pcg_solver* S, const Ctrl& c, pcg_result* res) {
   res->status = c.status;
   res->engine = S->engine == 1 ? 3 + S->variant : 2;
-  for (int k = 0; k < 5; ++k) res->tune_ms[k] = S->tune_ms[k];
+  for (int k = 0; k < 8; ++k) res->tune_ms[k] = S->tune_ms[k];
   res->graph_launches = S->graph_launches;
   res->norm0 = c.init.norm;
   res->breakdown_quantity = c.bd_code;
@@ -1970,6 +2009,7 @@ int preload_solver() {
   PCG_LOAD((pipecg_fused_kernel_d<int, 64>)); PCG_LOAD((pipecg_fused_kernel_d<long long, 256>));
   PCG_LOAD((pipecg_fused_kernel_d<long long, 128>)); PCG_LOAD((pipecg_fused_kernel_d<long long, 64>));
   PCG_LOAD(tile_build_kernel<int>); PCG_LOAD(tile_build_kernel<long long>); PCG_LOAD(tile_close_kernel);
+
   PCG_LOAD(pipecg_k1_kernel); PCG_LOAD(gated_spmv_rows<int>); PCG_LOAD(gated_spmv_rows<long long>);
   PCG_LOAD(gated_spmv_long<int>); PCG_LOAD(gated_spmv_long<long long>); PCG_LOAD(seq_dots_kernel);
   PCG_LOAD(drift_partial_kernel<int>); PCG_LOAD(drift_partial_kernel<long long>);
@@ -2021,7 +2061,7 @@ __global__ void fill_kernel(double* p, long long n, double v) {
 // test) of every engine/variant that fits this matrix on this GPU and keep
 // the fastest.  Costs ~10 iterations once per solver; the state is
 // re-initialised by the caller's solver_init.
-int autotune(pcg_solver* S, int grid2, bool with_engine2) {
+int autotune(pcg_solver* S, int grid2, bool with_engine2, bool irregular) {
   const long long n = S->A.n_rows;
   cudaStream_t st = S->stream;
   fill_kernel<<<elementwise_grid(n), 256, 0, st>>>(S->nv, n, 1.0);
@@ -2036,7 +2076,8 @@ int autotune(pcg_solver* S, int grid2, bool with_engine2) {
   int rc = PCG_OK;
   for (int cand = 0; cand < (with_engine2 ? kVariants + 1 : kVariants) && !rc; ++cand) {
     if (cand < kVariants) {
-      if (!S->plans[cand].stages) continue;
+      // B (gather warps) never won a measurement; D only pays for irregular rows
+      if (!S->plans[cand].stages || cand == 1 || (cand == 3 && !irregular)) continue;
       S->engine = 1;
       apply_plan(S, S->plans[cand]);
     } else {
@@ -2193,7 +2234,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
         break;
       }
   } else {
-    rc = autotune(S, grid2, req == 0);
+    rc = autotune(S, grid2, req == 0, has_long);
     if (rc) {
       pipecg_b200_solver_destroy(S);
       return rc;
@@ -2213,6 +2254,8 @@ int pipecg_b200_solver_destroy(pcg_solver* S) {
   }
   cudaFree(S->vbuf);
   cudaFree(S->partials);
+  cudaFree(S->fin);
+  cudaFree(S->counter);
   cudaFree(S->seqbuf);
   cudaFree(S->dpart);
   cudaFree(S->dots_ws);
@@ -2220,8 +2263,11 @@ int pipecg_b200_solver_destroy(pcg_solver* S) {
   cudaFree(S->rec_dev);
   cudaFree(S->comm);
   cudaFree(S->long_rows);
-  cudaFree(S->tile_row);
-  cudaFree(S->tile_e);
+  for (int v = 0; v < kVariants; ++v) {
+    cudaFree(S->plans[v].tile_row);
+    cudaFree(S->plans[v].tile_e);
+  }
+
   if (S->ev_in) cudaEventDestroy(S->ev_in);
   if (S->stream) cudaStreamDestroy(S->stream);
   delete S;
@@ -2305,6 +2351,7 @@ int pipecg_b200_solver_init(pcg_solver* S, const double* b, const double* x0, do
   S->drift_k = drift_check_interval;
   Record R = record_at(S->rec_dev);
   cudaMemsetAsync(&R.C->comm_error, 0, sizeof(int), st);
+  cudaMemsetAsync(S->counter, 0, 2 * sizeof(unsigned), st);
   // solvers.py:305-321
   cudaMemcpyAsync(S->b, b, bytes, cudaMemcpyDeviceToDevice, st);
   cudaMemcpyAsync(S->x, x0, bytes, cudaMemcpyDeviceToDevice, st);

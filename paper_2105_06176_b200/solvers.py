@@ -277,6 +277,15 @@ class PipecgSolver:
         _cuda_memcpy_d2d(out.data_ptr(), ptr, self.n * 8)
         return out
 
+    def x_host(self) -> np.ndarray:
+        """The iterate x downloaded into a new host array (native pinned
+        pipeline, on the solver's stream)."""
+        out = np.empty(self.n, dtype=np.float64)
+        if self.n:
+            _lib.call("pipecg_b200_d2h", out.ctypes.data, _lib.load().pipecg_b200_solver_x(self._h),
+                      self.n * 8, self.stream)
+        return out
+
     def state_tensors(self) -> dict:
         ptrs = (ctypes.c_void_p * 10)()
         _lib.call("pipecg_b200_solver_state", self._h, ptrs)
@@ -400,8 +409,7 @@ def pipecg_solve(A, b, x0, pc, cfg: SolverConfig | None = None, *,
     drift = None
     if cfg.drift_check_interval > 0:
         drift = [[int(d_it[k]), float(d_val[k])] for k in range(res.n_drift)]
-    xd = solver.x_tensor()
-    x = xd if on_dev else xd.cpu().numpy()
+    x = solver.x_tensor() if on_dev else solver.x_host()
     report = SolveReport(
         converged=bool(res.converged),
         iterations=int(res.iterations),

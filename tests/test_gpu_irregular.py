@@ -21,7 +21,7 @@ pytestmark = pytest.mark.gpu
 pb = pytest.importorskip("paper_2105_06176_b200")
 from test_gpu_solver import assert_within_envelope, envelope  # noqa: E402
 
-SEQ = pb.DeviceOptions(dot_mode="seq", engine="fused-d")
+VARIANTS = ["fused-d", "two"]
 
 
 def _problem(A):
@@ -53,8 +53,9 @@ def _random_spd(n, max_len, seed):
     return pb.CsrMatrix(n, n, ro, cols, vals)
 
 
+@pytest.mark.parametrize("engine", VARIANTS)
 @pytest.mark.parametrize("dcap", [None, 512, 2048])
-def test_powerlaw_seq_bitwise_balanced_tiles(cuda, monkeypatch, dcap):
+def test_powerlaw_seq_bitwise_balanced_tiles(cuda, monkeypatch, dcap, engine):
     """nnz-capped tiles, every row <= 256 nonzeros (so the init SpMVs take
     the in-order row path too) and no hub tiles: bitwise in seq-dot mode."""
     if dcap:
@@ -66,7 +67,8 @@ def test_powerlaw_seq_bitwise_balanced_tiles(cuda, monkeypatch, dcap):
     pc = pb.jacobi_setup(A)
     np.testing.assert_array_equal(pc.inv_diag, d)
     cfg = pb.SolverConfig(tolerance=tol, max_iterations=2000, record_history=True)
-    x, rep = pb.pipecg_solve(A, b, x0, pc, cfg, options=SEQ)
+    x, rep = pb.pipecg_solve(A, b, x0, pc, cfg,
+                             options=pb.DeviceOptions(dot_mode="seq", engine=engine))
     assert rep.iterations == ref.iterations
     assert rep.history == ref.history
     np.testing.assert_array_equal(x, ref.x)
@@ -84,8 +86,9 @@ def test_powerlaw_tree_within_envelope(cuda, engine):
                            envelope(A, b, x0, d, tol, 2000))
 
 
+@pytest.mark.parametrize("engine", VARIANTS)
 @pytest.mark.parametrize("dcap", [64, 256])
-def test_powerlaw_hub_rows(cuda, monkeypatch, dcap):
+def test_powerlaw_hub_rows(cuda, monkeypatch, dcap, engine):
     """A small tile cap turns the long rows into hub tiles (tree-combined)."""
     monkeypatch.setenv("PIPECG_B200_DCAP", str(dcap))
     A = pb.generate_powerlaw(2**15)
@@ -96,12 +99,13 @@ def test_powerlaw_hub_rows(cuda, monkeypatch, dcap):
     env = envelope(A, b, x0, d, tol, 2000)
     for mode in ("tree", "seq"):
         x, rep = pb.pipecg_solve(A, b, x0, pb.jacobi_setup(A), cfg,
-                                 options=pb.DeviceOptions(engine="fused-d", dot_mode=mode))
+                                 options=pb.DeviceOptions(engine=engine, dot_mode=mode))
         assert_within_envelope(x, rep, ref.iterations, ref.history, ref.x, env)
 
 
+@pytest.mark.parametrize("engine", VARIANTS)
 @pytest.mark.parametrize("dcap,max_len", [(16, 12), (64, 40), (1000, 200)])
-def test_random_spd_tiles_bitwise(cuda, monkeypatch, dcap, max_len):
+def test_random_spd_tiles_bitwise(cuda, monkeypatch, dcap, max_len, engine):
     """Ragged rows and many tile splits: bitwise when no row is a hub
     (every row <= dcap/2 nonzeros), else within the reorder envelope."""
     monkeypatch.setenv("PIPECG_B200_DCAP", str(dcap))
@@ -109,7 +113,8 @@ def test_random_spd_tiles_bitwise(cuda, monkeypatch, dcap, max_len):
     b, x0, d, tol = _problem(A)
     ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=3000)
     cfg = pb.SolverConfig(tolerance=tol, max_iterations=3000, record_history=True)
-    x, rep = pb.pipecg_solve(A, b, x0, pb.jacobi_setup(A), cfg, options=SEQ)
+    x, rep = pb.pipecg_solve(A, b, x0, pb.jacobi_setup(A), cfg,
+                             options=pb.DeviceOptions(dot_mode="seq", engine=engine))
     if A.row_nnz().max() <= dcap // 2:
         assert rep.history == ref.history
         np.testing.assert_array_equal(x, ref.x)
