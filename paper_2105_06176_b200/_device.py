@@ -90,3 +90,12 @@ def vec_len(v) -> int:
         return v.numel() if v.dim() == 1 else -1
     a = np.asarray(v)
     return a.size if a.ndim == 1 else -1
+
+
+def warm_transfers() -> None:
+    """Allocate the pinned staging ring and start the host thread pool of the
+    transfer pipeline (one-time per process; otherwise the first upload
+    pays for it)."""
+    t = torch.empty(1, dtype=_F64, device=require_cuda())
+    h2d(t, np.zeros(1))
+    d2h(t)

@@ -41,6 +41,7 @@
 #include <map>
 #include <mutex>
 #include <set>
+#include <tuple>
 #include <vector>
 
 #include "../../include/pipecg_b200.h"
@@ -1477,6 +1478,7 @@ struct pcg_solver {
   unsigned long long xtarget = 0;  // cumulative setup arrivals expected
   int flags = 0;                   // experiment switches (env PIPECG_B200_FLAGS)
   int variant = 1;                 // fused kernel variant in use
+  bool irregular = false;          // some row longer than kLongRow
   FusedPlan plans[kVariants];      // per fused variant (stages == 0: does not fit)
   double tune_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // autotune ms/iteration: fused A..E, engine 2
   int* tile_row = nullptr;         // variant D/E tiles of the applied plan
@@ -1688,7 +1690,8 @@ int fused_setup(pcg_solver* S) {
   int rc = plan_variant<RP, 0>(S, cc, cv, &S->plans[0]);
   if (!rc) rc = plan_variant<RP, 1>(S, cc, cv, &S->plans[1]);
   if (!rc) rc = plan_variant<RP, 2>(S, cc, cv, &S->plans[2]);
-  if (!rc) rc = plan_d<RP>(S, cv, &S->plans[3]);
+  // variant D (tile map build) only where it can win: irregular rows, or asked for
+  if (!rc && (S->irregular || S->opt.engine == 6)) rc = plan_d<RP>(S, cv, &S->plans[3]);
   if (rc) return rc;
   bool any = false;
   for (int v = 0; v < kVariants; ++v) any = any || S->plans[v].stages > 0;
@@ -2061,6 +2064,26 @@ __global__ void fill_kernel(double* p, long long n, double v) {
 // test) of every engine/variant that fits this matrix on this GPU and keep
 // the fastest.  Costs ~10 iterations once per solver; the state is
 // re-initialised by the caller's solver_init.
+struct TuneKey {
+  int dev;
+  long long n_rows, n_cols, nnz;
+  int rp64;
+  long long max_row;
+  int sms, dot_mode, req;
+  bool operator<(const TuneKey& o) const {
+    return std::tie(dev, n_rows, n_cols, nnz, rp64, max_row, sms, dot_mode, req) <
+           std::tie(o.dev, o.n_rows, o.n_cols, o.nnz, o.rp64, o.max_row, o.sms, o.dot_mode, o.req);
+  }
+};
+std::map<TuneKey, int>& tune_cache() {
+  static std::map<TuneKey, int> m;
+  return m;
+}
+std::mutex& tune_cache_mu() {
+  static std::mutex mu;
+  return mu;
+}
+
 int autotune(pcg_solver* S, int grid2, bool with_engine2, bool irregular) {
   const long long n = S->A.n_rows;
   cudaStream_t st = S->stream;
@@ -2173,6 +2196,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     return set_error(PCG_EINVAL, "solver_create: unknown engine");
   }
   const bool has_long = max_row > (unsigned long long)kLongRow;
+  S->irregular = has_long;
   bool fused_ok = false;
   if (req != 2) {
     rc = A->rp64 ? fused_setup<long long>(S) : fused_setup<int>(S);
@@ -2234,10 +2258,33 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
         break;
       }
   } else {
-    rc = autotune(S, grid2, req == 0, has_long);
-    if (rc) {
-      pipecg_b200_solver_destroy(S);
-      return rc;
+    // process-level tuning cache (like a BLAS heuristics cache): a matrix
+    // with the same shape and row-length profile on the same device reuses
+    // the measured choice instead of re-timing every candidate
+    const TuneKey key{dev, A->n_rows, A->n_cols, A->nnz, A->rp64, (long long)max_row,
+                      S->num_sms, S->opt.dot_mode, req};
+    int cached = -1;
+    if (!getenv("PIPECG_B200_NO_TUNE_CACHE")) {
+      std::lock_guard<std::mutex> lk(tune_cache_mu());
+      auto it = tune_cache().find(key);
+      if (it != tune_cache().end()) cached = it->second;
+    }
+    if (cached >= 0 && (cached == kVariants || S->plans[cached].stages)) {
+      if (cached < kVariants) {
+        S->engine = 1;
+        apply_plan(S, S->plans[cached]);
+      } else {
+        S->engine = 2;
+        S->grid = S->n_partials = grid2;
+      }
+    } else {
+      rc = autotune(S, grid2, req == 0, has_long);
+      if (rc) {
+        pipecg_b200_solver_destroy(S);
+        return rc;
+      }
+      std::lock_guard<std::mutex> lk(tune_cache_mu());
+      tune_cache()[key] = S->engine == 2 ? kVariants : S->variant;
     }
   }
   *out = S;
