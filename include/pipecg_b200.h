@@ -38,7 +38,9 @@ enum {
   PCG_ESTATE = 1003,    /* call out of order (e.g. iterate before init) */
   PCG_ERANGE = 1004,    /* index out of int32 range / out of bounds */
   PCG_EDIAG = 1005,     /* missing or zero diagonal (jacobi_setup) */
-  PCG_ECOMM = 1006      /* distributed exchange timed out (peer stalled / died) */
+  PCG_ECOMM = 1006,     /* distributed exchange timed out (peer stalled / died) */
+  PCG_EPARSE = 1007,    /* malformed Matrix Market input (see pipecg_b200_mm_error_line) */
+  PCG_EIO = 1008        /* file cannot be opened / read */
 };
 
 /* dot-product modes */
@@ -121,6 +123,23 @@ int pipecg_b200_narrow_i64(int64_t n, const int64_t* src, int32_t* dst, int* ove
 enum { PCG_H2D_COPY64 = 0, PCG_H2D_I64_TO_I32 = 1 };
 int pipecg_b200_h2d(void* dst_dev, const void* src_host, int64_t count, int kind, void* stream);
 int pipecg_b200_d2h(void* dst_host, const void* src_dev, int64_t bytes, void* stream);
+
+/* Matrix Market ingestion (replaces sparse.py:195-326
+ * parse_matrix_market / load_matrix_market).  Same accepted subset
+ * (`matrix coordinate real general|symmetric`), checks, messages and
+ * 1-based line numbers; PCG_EPARSE + pipecg_b200_mm_error_line() on bad
+ * input.  Parsing is multi-threaded host code; mm_to_csr builds the CSR on
+ * the device (stable key sort, duplicates summed in document order):
+ * rowptr has n_rows+1 entries (int32, or int64 if rp64), col/val need
+ * n_coo entries of capacity, *nnz_out receives the distinct count. */
+typedef struct pcg_mm pcg_mm;
+int pipecg_b200_mm_parse(const char* data, int64_t len, int universal_newlines, pcg_mm** out);
+int pipecg_b200_mm_read(const char* path, pcg_mm** out);
+int64_t pipecg_b200_mm_error_line(void);
+int pipecg_b200_mm_info(const pcg_mm* m, int64_t* n_rows, int64_t* n_cols, int64_t* n_coo);
+int pipecg_b200_mm_to_csr(const pcg_mm* m, int rp64, void* rowptr, int32_t* col, double* val,
+                          int64_t* nnz_out, void* stream);
+void pipecg_b200_mm_free(pcg_mm* m);
 
 /* Rows with more than `threshold` entries -> long_rows (device int32[cap]);
  * *n_long_host receives the count.  Synchronous. */

@@ -349,3 +349,133 @@ class Stepper:
 
 def lib_path() -> str:
     return os.fspath(_LIB_PATH)
+
+
+# --- sparse.py:183-326 (Matrix Market) -------------------------------------
+
+class MMError(ValueError):
+    """Oracle form of MatrixMarketError (sparse.py:29-36): message + line."""
+
+    def __init__(self, message, line):
+        self.line_number = line
+        super().__init__(f"line {line}: {message}")
+
+
+def _mm_float(tok, line):
+    # sparse.py:183-192: Python float(), then the Fortran 'd' exponent retry
+    try:
+        return float(tok)
+    except ValueError:
+        try:
+            return float(tok.replace("d", "e").replace("D", "E"))
+        except ValueError:
+            raise MMError(f"bad value {tok!r}", line) from None
+
+
+def _np_pairwise(a):
+    """numpy's pairwise_sum for float64 (what np.add.reduceat applies to a
+    segment after its first element): < 8 terms sequential from 0.0,
+    <= 128 eight interleaved accumulators, else halves (multiple of 8)."""
+    n = len(a)
+    if n < 8:
+        r = 0.0
+        for x in a:
+            r = r + x
+        return r
+    if n <= 128:
+        r = list(a[:8])
+        i = 8
+        while i < n - n % 8:
+            for j in range(8):
+                r[j] = r[j] + a[i + j]
+            i += 8
+        res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+        for x in a[i:]:
+            res = res + x
+        return res
+    n2 = n // 2
+    n2 -= n2 % 8
+    return _np_pairwise(a[:n2]) + _np_pairwise(a[n2:])
+
+
+def parse_matrix_market(text: str) -> Csr:
+    """Restatement of parse_matrix_market (sparse.py:195-320): header and
+    size checks in the reference's order, 1-based line numbers, symmetric
+    mirroring, (row, col) stable sort, duplicates summed like the
+    reference's np.add.reduceat (numpy 2.x pairwise order)."""
+    if not text:
+        raise MMError("empty document", 1)
+    lines = text.split("\n")
+    if text.endswith("\n"):
+        lines = lines[:-1]
+    tok = lines[0].strip().lower().split()
+    if len(tok) < 5 or tok[0] != "%%matrixmarket":
+        raise MMError("missing %%MatrixMarket header", 1)
+    checks = (("matrix", "object"), ("coordinate", "format"), ("real", "field"))
+    for k, (want, what) in enumerate(checks, start=1):
+        if tok[k] != want:
+            raise MMError(f"unsupported {what} {tok[k]!r}", 1)
+    if tok[4] not in ("general", "symmetric"):
+        raise MMError(f"unsupported symmetry {tok[4]!r}", 1)
+    sym = tok[4] == "symmetric"
+    k = 1
+    while k < len(lines) and (not lines[k].strip() or lines[k].strip().startswith("%")):
+        k += 1
+    if k >= len(lines):
+        raise MMError("missing size line", 2)
+    size_no = k + 1
+    parts = lines[k].split()
+    if len(parts) != 3:
+        raise MMError("size line must hold rows cols entries", size_no)
+    try:
+        nr, nc, ne = (int(p) for p in parts)
+    except ValueError:
+        raise MMError("size line must hold three integers", size_no) from None
+    if nr <= 0 or nc <= 0 or ne <= 0:
+        raise MMError("empty matrix", size_no)
+    if sym and nr != nc:
+        raise MMError("symmetric matrix must be square", size_no)
+    rows, cols, vals = [], [], []
+    last = size_no
+    for ln in range(k + 1, len(lines)):
+        t = lines[ln].strip()
+        if not t or t.startswith("%"):
+            continue
+        no = ln + 1
+        if len(rows) >= ne:
+            raise MMError(f"more than the declared {ne} entries", no)
+        p = t.split()
+        if len(p) != 3:
+            raise MMError("entry must hold row col value", no)
+        try:
+            i, j = int(p[0]), int(p[1])
+        except ValueError:
+            raise MMError("bad coordinate", no) from None
+        if not 1 <= i <= nr:
+            raise MMError(f"row index {i} out of range", no)
+        if not 1 <= j <= nc:
+            raise MMError(f"column index {j} out of range", no)
+        vals.append(_mm_float(p[2], no))
+        rows.append(i - 1)
+        cols.append(j - 1)
+        last = no
+    if len(rows) != ne:
+        raise MMError(f"expected {ne} entries, found {len(rows)}", last + 1)
+    r = np.array(rows, dtype=np.int64)
+    c = np.array(cols, dtype=np.int64)
+    v = np.array(vals, dtype=np.float64)
+    if sym:
+        off = r != c
+        r, c, v = np.concatenate([r, c[off]]), np.concatenate([c, r[off]]), np.concatenate([v, v[off]])
+    key = r * nc + c
+    order = np.argsort(key, kind="stable")
+    key, v = key[order], v[order]
+    heads = np.flatnonzero(np.r_[True, key[1:] != key[:-1]])
+    bounds = np.r_[heads, key.size]
+    sums = np.empty(heads.size)
+    for s in range(heads.size):  # np.add.reduceat order: first + pairwise(rest)
+        seg = [float(x) for x in v[bounds[s]:bounds[s + 1]]]
+        sums[s] = seg[0] + _np_pairwise(seg[1:])
+    ro = np.zeros(nr + 1, dtype=np.int64)
+    np.cumsum(np.bincount(key[heads] // nc, minlength=nr), out=ro[1:])
+    return Csr(nr, nc, ro, key[heads] % nc, sums)

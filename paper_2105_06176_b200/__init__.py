@@ -15,10 +15,13 @@ from .sparse import (
     CapacityError,
     CsrMatrix,
     DeviceCsr,
+    MatrixMarketError,
     as_device_csr,
     csr_from_dense,
     generate_poisson125,
     generate_powerlaw,
+    load_matrix_market,
+    parse_matrix_market,
     poisson125_shape,
     stencil_device,
     stencil_host,
@@ -60,6 +63,9 @@ __all__ = [
     "csr_from_dense",
     "generate_poisson125",
     "generate_powerlaw",
+    "MatrixMarketError",
+    "load_matrix_market",
+    "parse_matrix_market",
     "poisson125_shape",
     "stencil_device",
     "stencil_host",

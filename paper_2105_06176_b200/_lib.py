@@ -18,6 +18,7 @@ LIB_PATH = _HERE / "_lib" / "libpipecg_b200.so"
 CSRC = _HERE / "csrc"
 
 PCG_OK = 0
+PCG_EPARSE, PCG_EIO = 1007, 1008
 PCG_EINVAL, PCG_ENOMEM, PCG_ESTATE, PCG_ERANGE, PCG_EDIAG, PCG_ECOMM = (1001, 1002, 1003, 1004,
                                                                     1005, 1006)
 PCG_DOT_TREE, PCG_DOT_SEQ = 0, 1
@@ -81,6 +82,12 @@ _SIGS = {
     "pipecg_b200_narrow_i64": ([_i64, _vp, _vp, ctypes.POINTER(_int), _vp], _int),
     "pipecg_b200_h2d": ([_vp, _vp, _i64, _int, _vp], _int),
     "pipecg_b200_d2h": ([_vp, _vp, _i64, _vp], _int),
+    "pipecg_b200_mm_parse": ([ctypes.c_char_p, _i64, _int, ctypes.POINTER(_vp)], _int),
+    "pipecg_b200_mm_read": ([ctypes.c_char_p, ctypes.POINTER(_vp)], _int),
+    "pipecg_b200_mm_error_line": ([], _i64),
+    "pipecg_b200_mm_info": ([_vp, _p_i64, _p_i64, _p_i64], _int),
+    "pipecg_b200_mm_to_csr": ([_vp, _int, _vp, _vp, _vp, _p_i64, _vp], _int),
+    "pipecg_b200_mm_free": ([_vp], None),
     "pipecg_b200_find_long_rows": ([_i64, _int, _vp, _i64, _vp, _i64, _p_i64, _vp], _int),
     "pipecg_b200_stencil_shape": ([_int, _i64, _p_i64, _p_i64], _int),
     "pipecg_b200_stencil_prefix": ([_int, _i64, _i64, _p_i64], _int),

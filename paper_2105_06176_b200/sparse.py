@@ -32,9 +32,23 @@ __all__ = [
     "poisson125_shape",
     "generate_poisson125",
     "generate_powerlaw",
+    "MatrixMarketError",
+    "parse_matrix_market",
+    "load_matrix_market",
 ]
 
 PAD = 16  # trailing elements the staged (bulk-copy) reads may touch
+
+
+class MatrixMarketError(ValueError):
+    """Malformed Matrix Market input.  Carries the 1-based offending line
+    (sparse.py:29-36: same message form ``line N: ...``)."""
+
+    def __init__(self, message: str, line_number: int | None = None):
+        self.line_number = line_number
+        if line_number is not None:
+            message = f"line {line_number}: {message}"
+        super().__init__(message)
 
 
 class CapacityError(RuntimeError):
@@ -359,3 +373,77 @@ def generate_powerlaw(n_rows: int = 2**22, seed: int = 20261017, tau: float = 2.
     col[~is_diag] = uc
     val[~is_diag] = uv
     return CsrMatrix(N, N, row_offsets, col, val)
+
+
+# --- Matrix Market ingestion ---------------------------
+
+def _mm_raise(rc: int) -> None:
+    msg = _lib.last_error()
+    suffix = f" (code {rc})"
+    if msg.endswith(suffix):
+        msg = msg[: -len(suffix)]
+    if rc == _lib.PCG_EPARSE:
+        line = int(_lib.load().pipecg_b200_mm_error_line())
+        prefix = f"line {line}: "
+        raise MatrixMarketError(msg[len(prefix):] if msg.startswith(prefix) else msg, line)
+    if rc == _lib.PCG_EIO:
+        raise OSError(msg)
+    raise _lib.NativeError("Matrix Market ingestion", rc, msg)
+
+
+def _mm_csr(handle) -> CsrMatrix:
+    """COO handle -> CSR built on the device; returns the host CsrMatrix (the
+    reference's return type) with the device copy cached on it."""
+    L = _lib.load()
+    try:
+        n_rows, n_cols, n_coo = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _lib.call("pipecg_b200_mm_info", handle, ctypes.byref(n_rows), ctypes.byref(n_cols),
+                  ctypes.byref(n_coo))
+        n, m, cap = int(n_rows.value), int(n_cols.value), int(n_coo.value)
+        dev = require_cuda()
+        rp64 = cap >= 2**31
+        rowptr = torch.empty(n + 1 + PAD, dtype=torch.int64 if rp64 else torch.int32, device=dev)
+        col = torch.zeros(cap + PAD, dtype=torch.int32, device=dev)
+        val = torch.zeros(cap + PAD, dtype=torch.float64, device=dev)
+        nnz = ctypes.c_int64()
+        rc = L.pipecg_b200_mm_to_csr(handle, int(rp64), rowptr.data_ptr(), col.data_ptr(),
+                                     val.data_ptr(), ctypes.byref(nnz), stream_ptr())
+        if rc:
+            _mm_raise(rc)
+    finally:
+        L.pipecg_b200_mm_free(handle)
+    rowptr[n + 1:].fill_(int(nnz.value))
+    d = DeviceCsr(n, m, int(nnz.value), rowptr, col, val)
+    A = d.to_host()
+    object.__setattr__(A, "_b200_device", d)
+    return A
+
+
+def parse_matrix_market(source) -> CsrMatrix:
+    """Parse a Matrix Market coordinate document (sparse.py:195-320).
+
+    ``source`` is the document text or an open text stream.  Only
+    ``matrix coordinate real general|symmetric`` is accepted; symmetric
+    storage is mirrored, duplicate coordinates are summed (document order);
+    malformed input raises :class:`MatrixMarketError` naming the 1-based
+    line, exactly as the reference does.  Tokenising runs in the native
+    multi-threaded parser (csrc/mmio.cu); the CSR is assembled on the GPU."""
+    text = source if isinstance(source, str) else source.read()
+    data = text.encode("utf-8", errors="replace")
+    h = ctypes.c_void_p()
+    rc = _lib.load().pipecg_b200_mm_parse(data, len(data), 0, ctypes.byref(h))
+    if rc:
+        _mm_raise(rc)
+    return _mm_csr(h)
+
+
+def load_matrix_market(path) -> CsrMatrix:
+    """Read and parse a Matrix Market file (sparse.py:323-326; universal
+    newlines like the reference's text-mode read)."""
+    import os
+
+    h = ctypes.c_void_p()
+    rc = _lib.load().pipecg_b200_mm_read(os.fsencode(path), ctypes.byref(h))
+    if rc:
+        _mm_raise(rc)
+    return _mm_csr(h)
