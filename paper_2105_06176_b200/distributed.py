@@ -42,6 +42,9 @@ __all__ = [
     "ShardedProblem",
     "shard_stencil",
     "shard_csr",
+    "shard_block",
+    "stencil_block_host",
+    "e2e_distributed",
     "DistributedSolver",
     "pipecg_solve_distributed",
     "LocalGroup",
@@ -313,8 +316,6 @@ def shard_stencil(kind, n: int, group) -> ShardedProblem:
 def shard_csr(A, group) -> ShardedProblem:
     """This rank's nnz-balanced row block of a host CSR matrix (duck-typed
     CsrMatrix), uploaded and localized."""
-    from .sparse import DeviceCsr, upload_csr
-
     ro = np.asarray(A.row_offsets, dtype=np.int64)
     cuts = nnz_balanced_cuts(ro, group.world)
     r0, r1 = cuts[group.rank], cuts[group.rank + 1]
@@ -327,11 +328,75 @@ def shard_csr(A, group) -> ShardedProblem:
         col_indices = np.asarray(A.col_indices)[lo:hi]
         values = np.asarray(A.values)[lo:hi]
 
-    dA = upload_csr(_Block)
+    return shard_block(_Block, cuts, group, int(A.n_rows), int(ro[-1]))
+
+
+def shard_block(block, cuts, group, global_rows: int, global_nnz: int, meta=None) -> ShardedProblem:
+    """This rank's rows [cuts[rank], cuts[rank+1]) given as host CSR arrays
+    with GLOBAL column indices (the caller's own block: nothing global is
+    materialised anywhere), uploaded through the pinned pipeline and
+    localized to [owned | halo]."""
+    from .sparse import DeviceCsr, upload_csr
+
+    r0, r1 = cuts[group.rank], cuts[group.rank + 1]
+    dA = upload_csr(block)
     assert isinstance(dA, DeviceCsr)
     halo = _localize(dA, r0, r1)
     plan = build_plan(group.rank, group.world, cuts, halo, group)
-    return _finish(dA, plan, group, int(A.n_rows), int(ro[-1]))
+    return _finish(dA, plan, group, global_rows, global_nnz, meta)
+
+
+def stencil_block_host(kind, n: int, group):
+    """(block, cuts, N, nnz): this rank's stencil row block as host arrays
+    with global columns -- the input of the host-buffer (e2e) path."""
+    from . import sparse
+
+    k = sparse._KINDS[kind]
+    N, nnz = sparse.stencil_shape(k, n)
+    cuts = stencil_cuts(lambda r: sparse._prefix_count(k, n, r), N, group.world)
+    r0, r1 = cuts[group.rank], cuts[group.rank + 1]
+    d = sparse.stencil_device(k, n, r0, r1)
+    block = d.to_host()
+    del d
+    return block, cuts, N, nnz
+
+
+def e2e_distributed(kind, n: int, group, tolerance: float, max_iterations: int = 20000,
+                    block=None, options=None):
+    """The multi-GPU public call with host buffers: this rank's host block
+    -> upload + localize + halo plan + connect + solve + x download.
+    Returns (iterations, seconds (max over ranks), h2d bytes of this rank,
+    d2h bytes of this rank, max |x - x_true| over ranks)."""
+    import torch
+
+    from .solvers import SolverConfig
+
+    from ._device import d2h, to_device_f64
+
+    block, cuts, N, nnz = block or stencil_block_host(kind, n, group)
+    r0, r1 = cuts[group.rank], cuts[group.rank + 1]
+    x_true = np.full(r1 - r0, 1.0 / math.sqrt(N))
+    # the caller's right-hand side b = A x_true as a host array (not timed)
+    prob0 = shard_block(block, cuts, group, N, nnz)
+    b_host = d2h(manufactured_local(prob0)[1])
+    del prob0
+    torch.cuda.empty_cache()
+    x0_host = np.zeros(r1 - r0)
+    group.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    prob = shard_block(block, cuts, group, N, nnz)
+    b = to_device_f64(b_host)
+    x, rep = pipecg_solve_distributed(prob, b, to_device_f64(x0_host),
+                                      SolverConfig(tolerance=tolerance,
+                                                   max_iterations=max_iterations), group,
+                                      options=options)
+    x_host = d2h(x)
+    dt = time.perf_counter() - t0
+    err = float(np.max(np.abs(x_host - x_true))) if x_host.size else 0.0
+    rp = 8 if block.nnz >= 2**31 else 4
+    h2d = rp * (block.n_rows + 1) + 12 * block.nnz + 16 * (r1 - r0)
+    return rep.iterations, group.max(dt), h2d, 8 * x_host.size, group.max(err)
 
 
 # ---------------------------------------------------------------------------
@@ -354,6 +419,18 @@ class DistributedSolver:
         opts = DeviceOptions(dot_mode=opts.dot_mode, engine=engine, chunk=opts.chunk,
                              use_graphs=opts.use_graphs, max_sms=opts.max_sms)
         self.solver = PipecgSolver(problem.A, problem.inv_diag, opts)
+        # every rank must run the same fused variant: the exchange pushes the
+        # vector the variant gathers (w for A/B, the stored m for C/D), and
+        # per-rank autotuning could pick differently on differently shaped
+        # blocks -> adopt rank 0's choice
+        names = {3: "fused-a", 4: "fused-b", 5: "fused-c", 6: "fused-d"}
+        mine = int(self.solver.poll().engine)
+        chosen = group.all_gather_object(mine)[0]
+        if mine != chosen:
+            self.solver.close()
+            opts = DeviceOptions(dot_mode=opts.dot_mode, engine=names[chosen], chunk=opts.chunk,
+                                 use_graphs=opts.use_graphs, max_sms=opts.max_sms)
+            self.solver = PipecgSolver(problem.A, problem.inv_diag, opts)
         vbuf, ld, comm = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_void_p()
         _lib.call("pipecg_b200_solver_comm_info", self.solver._h, ctypes.byref(vbuf),
                   ctypes.byref(ld), ctypes.byref(comm))
@@ -471,89 +548,3 @@ def pipecg_solve_distributed(problem: ShardedProblem, b_local, x0_local, cfg, gr
         partition=problem.plan.summary(),
     )
     return x, rep
-
-
-# ---------------------------------------------------------------------------
-# bench.py --gpus N (torchrun): strong scaling of the headline workload
-# ---------------------------------------------------------------------------
-def bench_main(args, metric: str, unit: str) -> int:
-    import json
-    import os
-
-    import torch
-    import torch.distributed as dist
-
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    group = TorchGroup()
-    kind, n = args.config.split("-")
-    n = int(n)
-    from .solvers import DeviceOptions
-
-    prob = shard_stencil(kind, n, group)
-    solver = DistributedSolver(prob, group, DeviceOptions())
-    xt, b = manufactured_local(prob)
-    x0 = torch.zeros_like(b)
-    steps, warm = args.steps, args.warmup
-    solver.init(b, x0, 0.0, warm + steps + 1)
-    solver.solver.enqueue(warm)
-    torch.cuda.synchronize()
-    group.barrier()
-    stream = torch.cuda.ExternalStream(solver.stream)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    solver.solver.enqueue(steps)
-    e1.record(stream)
-    e1.synchronize()
-    ms = group.max(e0.elapsed_time(e1))
-    res = solver.solver.poll()
-    ok = res.status == 0 and res.iterations == warm + steps
-    # time to solution at the recipe tolerance (same connected solver)
-    from .kernels import dots, jacobi_apply
-    from .kernels import JacobiPreconditioner
-
-    u0 = jacobi_apply(JacobiPreconditioner(prob.inv_diag[: prob.plan.n_local]), b)
-    uu = group.all_gather_object(dots([(u0, u0)], mode="tree")[0])
-    tol = 1e-8 * math.sqrt(sum(uu))
-    from .solvers import SolverConfig
-
-    group.barrier()
-    t0 = time.perf_counter()
-    x, rep = pipecg_solve_distributed(prob, b, torch.zeros_like(b),
-                                      SolverConfig(tolerance=tol, max_iterations=20000), group,
-                                      solver=solver)
-    tts = group.max(time.perf_counter() - t0)
-    err = group.max(float((x - xt).abs().max()))
-    solver.close()
-    if group.rank == 0:
-        N, nnz = prob.global_rows, prob.global_nnz
-        B = 176 * N + 12 * nnz + 4 * (N + group.world)
-        t_iter = ms / 1e3 / steps
-        from pathlib import Path
-
-        peak = 6554.2
-        p = Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json"
-        if p.exists():
-            peak = float(json.loads(p.read_text())["hbm_gbs"])
-        achieved = B / t_iter / 1e9
-        line = {
-            "metric": metric, "value": steps / (ms / 1e3), "unit": unit, "n_gpus": group.world,
-            "steps": steps, "warmup": warm, "ms_per_step": ms / steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: each rank generates its row block in HBM; x=1/sqrt(N)",
-            "config": {"workload": f"{kind} Poisson n={n} (N={N}, nnz={nnz}) row-sharded",
-                       "N": N, "nnz": nnz, "parallelism": f"row-block x{group.world}, NVLink P2P "
-                       "halo + dot-partial exchange fused after each iteration kernel"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * group.world,
-                         "unit": "GB/s", "frac": achieved / (peak * group.world), "traffic": None,
-                         "note": "aggregate over ranks"},
-            "gpu_launches": 2 * steps,
-            "timing_ok": bool(ok),
-            "time_to_solution": {"iterations": rep.iterations, "seconds": tts,
-                                 "verify_inf_err": err},
-            "partition": prob.plan.summary(),
-        }
-        print(json.dumps(line), flush=True)
-    dist.destroy_process_group()
-    return 0

@@ -142,3 +142,38 @@ def test_virtual_ranks_repeat_and_max_iterations(cuda):
         assert np.max(np.abs(x - ref.x)) / max(np.max(np.abs(ref.x)), 1e-300) <= 1e-8
         if maxit < 100:
             assert rep.iterations == maxit and not rep.converged
+
+
+def test_virtual_ranks_e2e_host_blocks_and_autotune_agreement(cuda):
+    """The host-buffer multi-GPU call (bench e2e leg at N > 1): each rank
+    uploads its own host row block; blocks >= 64K rows autotune per rank and
+    must agree on one fused variant (the exchange pushes that variant's
+    gathered vector)."""
+    kind, n, world = "3d7", 64, 2
+    A = oracle.stencil(kind, n)
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=20000)
+    G = D.LocalGroup(world)
+    out, errs = [None] * world, []
+
+    def work(r):
+        try:
+            torch.cuda.set_device(0)
+            g = G.view(r)
+            out[r] = D.e2e_distributed(kind, n, g, tol,
+                                       options=pb.DeviceOptions(max_sms=148 // world - 10))
+        except BaseException as e:  # noqa: BLE001
+            errs.append((r, repr(e)))
+            G._barrier.abort()
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    assert not errs, errs
+    it, secs, h2d, d2h, err = out[0]
+    assert abs(it - ref.iterations) <= 1 and secs > 0
+    assert err < 1e-6
+    assert sum(o[3] for o in out) == 8 * A.n_rows
