@@ -16,6 +16,7 @@ pytestmark = pytest.mark.gpu
 
 pb = pytest.importorskip("paper_2105_06176_b200")
 torch = pytest.importorskip("torch")
+from paper_2105_06176_b200 import _lib  # noqa: E402
 
 NAMES = ("z", "q", "s", "p", "x", "r", "u", "w", "m", "n")
 
@@ -177,3 +178,25 @@ def test_fused_update_pc_dots(cuda):
     for got, (a, b) in zip((g, dl, uu), ((exp["r"], exp["u"]), (exp["w"], exp["u"]),
                                           (exp["u"], exp["u"]))):
         assert abs(got - oracle.dot(a, b)) <= 1e-12 * np.sum(np.abs(a * b))
+
+
+def test_host_transfer_pipeline(cuda):
+    """csrc/hostio.cu: chunked pinned-ring uploads (with int64 -> int32
+    narrowing) and downloads, across several 32 MB slots."""
+    from paper_2105_06176_b200._device import d2h, h2d
+
+    n = (32 << 20) // 4 * 3 + 12345  # > 2 ring slots of narrowed data
+    rng = np.random.default_rng(5)
+    idx = rng.integers(-2**31, 2**31, size=n, dtype=np.int64)
+    dst = torch.empty(n, dtype=torch.int32, device="cuda")
+    h2d(dst, idx, narrow=True)
+    np.testing.assert_array_equal(dst.cpu().numpy(), idx.astype(np.int32))
+    vals = rng.standard_normal(n // 2 + 7)
+    dv = torch.empty(vals.size, dtype=torch.float64, device="cuda")
+    h2d(dv, vals)
+    np.testing.assert_array_equal(d2h(dv), vals)
+    bad = idx.copy()
+    bad[n - 3] = 2**31  # outside int32
+    with pytest.raises(_lib.NativeError) as e:
+        h2d(dst, bad, narrow=True)
+    assert e.value.code == _lib.PCG_ERANGE
