@@ -156,6 +156,22 @@ __device__ __forceinline__ int read_status(const Ctrl* C) {
   return *reinterpret_cast<const volatile int*>(&C->status);
 }
 
+// CTA-uniform "is the solve still running?" plus the iteration index: ONE
+// thread reads the control block and the whole CTA acts on that value (a
+// per-thread read could straddle block 0's status write and split a CTA
+// across a later bar.sync).  Returns -1 when the CTA must exit.
+// `slot` is a shared-memory word (kernels with a dynamic-smem header pass a
+// header slot: static __shared__ would eat into their 227 KB dynamic budget).
+__device__ __forceinline__ long long cta_iteration(const Ctrl* C, int step, long long* slot) {
+  if (threadIdx.x == 0) *slot = read_status(C) == PCG_RUNNING ? C->base_it + step : -1;
+  __syncthreads();
+  return *reinterpret_cast<volatile long long*>(slot);
+}
+__device__ __forceinline__ long long cta_iteration(const Ctrl* C, int step) {
+  __shared__ long long s_it;
+  return cta_iteration(C, step, &s_it);
+}
+
 // The reference's loop head + tail, solvers.py:346-372, for iteration `it`.
 // NT threads (local id lt) participate; `leader` is one thread of block 0.
 template <int NT>
@@ -378,8 +394,8 @@ __global__ void __launch_bounds__(FusedLayout<RP, TR>::kThreads) pipecg_fused_ke
   const int S = P.stages;
 
   Ctrl* C = P.C;
-  if (read_status(C) != PCG_RUNNING) return;
-  const long long it = C->base_it + step;
+  const long long it = cta_iteration(C, step, reinterpret_cast<long long*>(smem + 896));
+  if (it < 0) return;
   const double* w_old = P.w[it & 1];
   double* w_new = P.w[(it + 1) & 1];
 
@@ -594,11 +610,6 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_a(FusedParams<RP>
   const int S = P.stages;
 
   Ctrl* C = P.C;
-  if (read_status(C) != PCG_RUNNING) return;
-  const long long it = C->base_it + step;
-  const double* w_old = P.w[it & 1];
-  double* w_new = P.w[(it + 1) & 1];
-
   const int tid = threadIdx.x;
   const bool producer = tid < 32;
   // tile ownership: round-robin (tile t -> CTA t % grid) keeps the whole GPU
@@ -618,7 +629,6 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_a(FusedParams<RP>
     }
     fence_barrier_init();
   }
-  __syncthreads();
 
   // ---- producer: stage tile j of this block into stage j % S -------------
   uint64_t pol = 0;
@@ -645,10 +655,25 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_a(FusedParams<RP>
     if (b_col) bulk_g2s(sval + (size_t)P.cap_val * 8, P.col + cb, b_col, &full[s], pol);
   };
 
+  // The first S tiles are requested before the control block is even read
+  // (tile addresses do not depend on the iteration): the status load of
+  // thread 32 and the CTA barrier overlap the first bulk copies.  One
+  // thread reads the status, so the whole CTA takes the same exit.
+  long long* s_it = reinterpret_cast<long long*>(smem + 896);
   if (producer && tid == 0) {
     pol = policy_evict_first();
     for (long long j = 0; j < my_tiles && j < S; ++j) issue(j);
   }
+  if (tid == 32) *s_it = read_status(C) == PCG_RUNNING ? C->base_it + step : -1;
+  __syncthreads();
+  const long long it = *reinterpret_cast<volatile long long*>(s_it);
+  if (it < 0) {
+    if (tid == 0)  // drain the copies in flight before the CTA retires
+      for (long long j = 0; j < my_tiles && j < S; ++j) mbar_wait(&full[j], 0);
+    return;
+  }
+  const double* w_old = P.w[it & 1];
+  double* w_new = P.w[(it + 1) & 1];
 
   // ---- prologue (consumers): entry scalars, guards, stop test ------------
   if (!producer) {
@@ -812,8 +837,8 @@ __global__ void __launch_bounds__(kDThreads + 32) pipecg_fused_kernel_d(FusedPar
   const int S = P.stages;
 
   Ctrl* C = P.C;
-  if (read_status(C) != PCG_RUNNING) return;
-  const long long it = C->base_it + step;
+  const long long it = cta_iteration(C, step, reinterpret_cast<long long*>(smem + 1024));
+  if (it < 0) return;
   const double* w_old = P.w[it & 1];
   double* w_new = P.w[(it + 1) & 1];
   const double* m_old = P.m[it & 1];
@@ -1007,8 +1032,8 @@ struct TwoParams {
 __global__ void __launch_bounds__(256) pipecg_k1_kernel(TwoParams P, int step) {
   __shared__ double red[3 * 8 + 1];
   Ctrl* C = P.C;
-  if (read_status(C) != PCG_RUNNING) return;
-  const long long it = C->base_it + step;
+  const long long it = cta_iteration(C, step);
+  if (it < 0) return;
   const Step stp = prologue<256>(C, P.hist, P.rin, it, threadIdx.x, red, 1,
                                  blockIdx.x == 0 && threadIdx.x == 0);
   if (!stp.go) return;
@@ -1064,7 +1089,7 @@ __global__ void __launch_bounds__(256) gated_spmv_long(const Ctrl* C, const int*
                                                         const double* __restrict__ x,
                                                         double* __restrict__ y) {
   __shared__ double red[8];
-  if (read_status(C) != PCG_RUNNING) return;
+  if (cta_iteration(C, 0) < 0) return;
   const long long i = rows[blockIdx.x];
   const long long lo = rp[i], hi = rp[i + 1];
   double v[1] = {0.0};
@@ -1085,8 +1110,8 @@ __global__ void __launch_bounds__(32) seq_dots_kernel(const Ctrl* C, long long n
                                                        double* seqbuf, int step) {
   constexpr int CH = 256;
   __shared__ double prod[3][CH];
-  if (read_status(C) != PCG_RUNNING) return;
-  const long long it = C->base_it + step;
+  const long long it = cta_iteration(C, step);
+  if (it < 0) return;
   const double* w = pingpong ? (((it + 1) & 1) ? w1 : w0) : w0;
   double acc[3] = {0.0, 0.0, 0.0};
   const int lane = threadIdx.x;
@@ -1130,8 +1155,8 @@ __global__ void __launch_bounds__(256) drift_partial_kernel(const Ctrl* C, int s
                                                              const double* __restrict__ r,
                                                              double* __restrict__ dpart) {
   __shared__ double red[8];
-  if (read_status(C) != PCG_RUNNING) return;
-  const long long it = C->base_it + step;
+  const long long it = cta_iteration(C, step);
+  if (it < 0) return;
   if (it < 1 || C->drift_k <= 0 || it % C->drift_k != 0) return;
   double v[1] = {0.0};
   for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
@@ -1147,8 +1172,8 @@ __global__ void __launch_bounds__(256) drift_partial_kernel(const Ctrl* C, int s
 __global__ void __launch_bounds__(256) drift_finish_kernel(const Ctrl* C, int step, const double* dpart,
                                                             int count, double* dval, long long* dit) {
   __shared__ double red[8];
-  if (read_status(C) != PCG_RUNNING) return;
-  const long long it = C->base_it + step;
+  const long long it = cta_iteration(C, step);
+  if (it < 0) return;
   if (it < 1 || C->drift_k <= 0 || it % C->drift_k != 0) return;
   double v[1] = {0.0};
   for (int j = threadIdx.x; j < count; j += 256) v[0] = add(v[0], dpart[j]);
@@ -1246,8 +1271,8 @@ __global__ void __launch_bounds__(256) iter_exchange_kernel(CommParams CP, const
                                                              const double* g0, const double* g1,
                                                              int vec0, int vec1) {
   __shared__ double red[3 * 8];
-  if (read_status(C) != PCG_RUNNING) return;
-  const long long it = C->base_it + step;
+  const long long it = cta_iteration(C, step);
+  if (it < 0) return;
   const int wi = (int)((it + 1) & 1);
   const double* src = wi ? g1 : g0;
   const int vec = wi ? vec1 : vec0;
@@ -1529,7 +1554,7 @@ int plan_one(pcg_solver* S, int cap_col, int cap_val, FusedPlan* out) {
   const char* e_bps = getenv("PIPECG_B200_BPS");
   for (int bps = e_bps ? atoi(e_bps) : (V == 3 ? 3 : 2); bps >= 1 && !p.stages; --bps) {
     if (e_bps && bps != atoi(e_bps)) break;
-    for (int st = 2; st <= 8; ++st) {
+    for (int st = e_st ? 1 : 2; st <= 8; ++st) {
       if (e_st ? atoi(e_st) != st : st > 4) continue;
       const size_t need = hdr + st * sb;
       if (need <= cta_max && (need + 1024) * bps <= sm_budget) {
