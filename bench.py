@@ -292,6 +292,7 @@ def time_iterations(pb, torch, A, pc_d, warmup: int, steps: int, options=None):
     solver = pb.PipecgSolver(A, pc_d, options or pb.DeviceOptions())
     solver.init(b, x0, 0.0, warmup + steps + 1, 0)
     solver.enqueue(warmup)
+    solver.prepare(steps)  # graph capture/instantiation stays outside the timed region
     torch.cuda.synchronize()
     g0 = solver.poll().graph_launches
     stream = torch.cuda.ExternalStream(solver.stream)
@@ -425,6 +426,7 @@ def run_distributed(args):
     steps, warm = args.steps, args.warmup
     solver.init(b, torch.zeros_like(b), 0.0, warm + steps + 1)
     solver.solver.enqueue(warm)
+    solver.solver.prepare(steps)
     torch.cuda.synchronize()
     g0 = solver.solver.poll().graph_launches
     group.barrier()

@@ -221,6 +221,10 @@ int pipecg_b200_solver_run(pcg_solver* s, pcg_result* res, double* history_host,
                            int64_t hist_cap, int64_t* drift_it_host, double* drift_val_host,
                            int64_t drift_cap);
 
+/* Capture + instantiate the CUDA graphs that a following
+ * pipecg_b200_solver_enqueue(s, count) will launch (both record parities),
+ * so that graph construction stays out of a timed region.  Optional. */
+int pipecg_b200_solver_prepare(pcg_solver* s, int64_t count);
 /* Enqueue exactly `count` more iterations (no host synchronisation; used by
  * the benchmark to time a fixed number of iterations with CUDA events). */
 int pipecg_b200_solver_enqueue(pcg_solver* s, int64_t count);

@@ -99,6 +99,7 @@ _SIGS = {
     "pipecg_b200_solver_run": ([_vp, ctypes.POINTER(PcgResult), _p_dbl, _i64, _p_i64, _p_dbl, _i64],
                                _int),
     "pipecg_b200_solver_enqueue": ([_vp, _i64], _int),
+    "pipecg_b200_solver_prepare": ([_vp, _i64], _int),
     "pipecg_b200_solver_stream": ([_vp], _vp),
     "pipecg_b200_solver_poll": ([_vp, ctypes.POINTER(PcgResult)], _int),
     "pipecg_b200_solver_x": ([_vp], _vp),

@@ -105,6 +105,16 @@ __device__ __forceinline__ void bulk_g2s_nohint(void* dst, const void* src, uint
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Programmatic dependent launch (the kernel is launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): `wait` blocks until
+// the preceding grid in the stream has completed and its writes are
+// visible (a no-op for a normal launch); `trigger` lets the next grid start
+// launching (its CTAs are placed as this grid's CTAs retire).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

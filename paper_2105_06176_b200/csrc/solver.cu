@@ -394,6 +394,8 @@ __global__ void __launch_bounds__(FusedLayout<RP, TR>::kThreads) pipecg_fused_ke
   const int S = P.stages;
 
   Ctrl* C = P.C;
+  pdl_trigger();
+  pdl_wait();  // everything below reads what the previous kernel wrote
   const long long it = cta_iteration(C, step, reinterpret_cast<long long*>(smem + 896));
   if (it < 0) return;
   const double* w_old = P.w[it & 1];
@@ -622,6 +624,7 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_a(FusedParams<RP>
   const long long t_step = contiguous ? 1 : gridDim.x;
   const long long my_tiles = t_hi > t_lo ? (t_hi - t_lo + t_step - 1) / t_step : 0;
 
+  pdl_trigger();
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -629,6 +632,7 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_a(FusedParams<RP>
     }
     fence_barrier_init();
   }
+  pdl_wait();  // everything below reads what the previous kernel wrote
 
   // ---- producer: stage tile j of this block into stage j % S -------------
   uint64_t pol = 0;
@@ -837,6 +841,8 @@ __global__ void __launch_bounds__(kDThreads + 32) pipecg_fused_kernel_d(FusedPar
   const int S = P.stages;
 
   Ctrl* C = P.C;
+  pdl_trigger();
+  pdl_wait();  // everything below reads what the previous kernel wrote
   const long long it = cta_iteration(C, step, reinterpret_cast<long long*>(smem + 1024));
   if (it < 0) return;
   const double* w_old = P.w[it & 1];
@@ -1504,6 +1510,7 @@ struct pcg_solver {
   int flags = 0;                   // experiment switches (env PIPECG_B200_FLAGS)
   int variant = 1;                 // fused kernel variant in use
   bool irregular = false;          // some row longer than kLongRow
+  bool pdl = true;                 // programmatic dependent launch of the fused kernels
   FusedPlan plans[kVariants];      // per fused variant (stages == 0: does not fit)
   double tune_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // autotune ms/iteration: fused A..E, engine 2
   int* tile_row = nullptr;         // variant D/E tiles of the applied plan
@@ -1844,33 +1851,55 @@ FusedParams<RP> fused_params(pcg_solver* S) {
   return P;
 }
 
+// Launch with programmatic stream serialization: the next iteration's
+// kernel is placed while this one drains (its griddepcontrol.wait keeps the
+// data dependence), hiding the launch latency of back-to-back iterations.
+template <typename... KArgs, typename... Args>
+void launch_k(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+              bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <typename RP>
 void launch_fused(pcg_solver* S, int k) {
   const FusedParams<RP> P = fused_params<RP>(S);
   cudaStream_t st = S->stream;
+  const bool pdl = S->pdl;
+  const unsigned g = (unsigned)S->grid;
+  const size_t sm = S->smem;
   if (S->variant == 1) {
     switch (S->tr) {
-      case 256: pipecg_fused_kernel<RP, 256><<<S->grid, FusedLayout<RP, 256>::kThreads, S->smem, st>>>(P, k); break;
-      case 128: pipecg_fused_kernel<RP, 128><<<S->grid, FusedLayout<RP, 128>::kThreads, S->smem, st>>>(P, k); break;
-      default: pipecg_fused_kernel<RP, 64><<<S->grid, FusedLayout<RP, 64>::kThreads, S->smem, st>>>(P, k); break;
+      case 256: launch_k(pipecg_fused_kernel<RP, 256>, g, FusedLayout<RP, 256>::kThreads, sm, st, pdl, P, k); break;
+      case 128: launch_k(pipecg_fused_kernel<RP, 128>, g, FusedLayout<RP, 128>::kThreads, sm, st, pdl, P, k); break;
+      default: launch_k(pipecg_fused_kernel<RP, 64>, g, FusedLayout<RP, 64>::kThreads, sm, st, pdl, P, k); break;
     }
   } else if (S->variant == 3) {
     switch (S->tr) {
-      case 256: pipecg_fused_kernel_d<RP, 256><<<S->grid, kDThreads + 32, S->smem, st>>>(P, k); break;
-      case 128: pipecg_fused_kernel_d<RP, 128><<<S->grid, kDThreads + 32, S->smem, st>>>(P, k); break;
-      default: pipecg_fused_kernel_d<RP, 64><<<S->grid, kDThreads + 32, S->smem, st>>>(P, k); break;
+      case 256: launch_k(pipecg_fused_kernel_d<RP, 256>, g, kDThreads + 32, sm, st, pdl, P, k); break;
+      case 128: launch_k(pipecg_fused_kernel_d<RP, 128>, g, kDThreads + 32, sm, st, pdl, P, k); break;
+      default: launch_k(pipecg_fused_kernel_d<RP, 64>, g, kDThreads + 32, sm, st, pdl, P, k); break;
     }
   } else if (S->variant == 2) {
     switch (S->tr) {
-      case 256: pipecg_fused_kernel_a<RP, 256, true><<<S->grid, 256 + 32, S->smem, st>>>(P, k); break;
-      case 128: pipecg_fused_kernel_a<RP, 128, true><<<S->grid, 128 + 32, S->smem, st>>>(P, k); break;
-      default: pipecg_fused_kernel_a<RP, 64, true><<<S->grid, 64 + 32, S->smem, st>>>(P, k); break;
+      case 256: launch_k(pipecg_fused_kernel_a<RP, 256, true>, g, 256 + 32, sm, st, pdl, P, k); break;
+      case 128: launch_k(pipecg_fused_kernel_a<RP, 128, true>, g, 128 + 32, sm, st, pdl, P, k); break;
+      default: launch_k(pipecg_fused_kernel_a<RP, 64, true>, g, 64 + 32, sm, st, pdl, P, k); break;
     }
   } else {
     switch (S->tr) {
-      case 256: pipecg_fused_kernel_a<RP, 256, false><<<S->grid, 256 + 32, S->smem, st>>>(P, k); break;
-      case 128: pipecg_fused_kernel_a<RP, 128, false><<<S->grid, 128 + 32, S->smem, st>>>(P, k); break;
-      default: pipecg_fused_kernel_a<RP, 64, false><<<S->grid, 64 + 32, S->smem, st>>>(P, k); break;
+      case 256: launch_k(pipecg_fused_kernel_a<RP, 256, false>, g, 256 + 32, sm, st, pdl, P, k); break;
+      case 128: launch_k(pipecg_fused_kernel_a<RP, 128, false>, g, 128 + 32, sm, st, pdl, P, k); break;
+      default: launch_k(pipecg_fused_kernel_a<RP, 64, false>, g, 64 + 32, sm, st, pdl, P, k); break;
     }
   }
 }
@@ -1948,29 +1977,39 @@ int enqueue_chunk_body(pcg_solver* S, int K, int parity) {
   return cuda_status(cudaGetLastError(), "chunk launch");
 }
 
+// Captured + instantiated graph of one chunk of K iterations for record
+// parity `parity` (cached per solver).
+int chunk_graph(pcg_solver* S, int K, int parity, cudaGraphExec_t* out) {
+  auto it = S->graphs[parity].find(K);
+  if (it != S->graphs[parity].end()) {
+    *out = it->second;
+    return PCG_OK;
+  }
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaError_t e = cudaStreamBeginCapture(S->stream, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return cuda_status(e, "begin capture");
+  int rc = enqueue_chunk_body(S, K, parity);
+  e = cudaStreamEndCapture(S->stream, &g);
+  if (rc) return rc;
+  if (e != cudaSuccess) return cuda_status(e, "end capture");
+  e = cudaGraphInstantiate(&exec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return cuda_status(e, "graph instantiate");
+  S->graphs[parity][K] = exec;
+  *out = exec;
+  return PCG_OK;
+}
+
 int launch_chunk(pcg_solver* S, int K, int parity) {
   S->host_base += K;
   if (!S->opt.use_graphs) {
     int rc = enqueue_chunk_body(S, K, parity);
     if (rc) return rc;
   } else {
-    auto it = S->graphs[parity].find(K);
     cudaGraphExec_t exec = nullptr;
-    if (it == S->graphs[parity].end()) {
-      cudaGraph_t g = nullptr;
-      cudaError_t e = cudaStreamBeginCapture(S->stream, cudaStreamCaptureModeThreadLocal);
-      if (e != cudaSuccess) return cuda_status(e, "begin capture");
-      int rc = enqueue_chunk_body(S, K, parity);
-      e = cudaStreamEndCapture(S->stream, &g);
-      if (rc) return rc;
-      if (e != cudaSuccess) return cuda_status(e, "end capture");
-      e = cudaGraphInstantiate(&exec, g, 0);
-      cudaGraphDestroy(g);
-      if (e != cudaSuccess) return cuda_status(e, "graph instantiate");
-      S->graphs[parity][K] = exec;
-    } else {
-      exec = it->second;
-    }
+    int rc = chunk_graph(S, K, parity, &exec);
+    if (rc) return rc;
     cudaError_t e = cudaGraphLaunch(exec, S->stream);
     if (e != cudaSuccess) return cuda_status(e, "graph launch");
     S->graph_launches++;
@@ -2180,6 +2219,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   pcg_solver* S = new pcg_solver();
   S->A = *A;
   if (const char* f = getenv("PIPECG_B200_FLAGS")) S->flags = atoi(f);
+  if (getenv("PIPECG_B200_NO_PDL")) S->pdl = false;
   if (opts) S->opt = *opts;
   else {
     S->opt.dot_mode = PCG_DOT_TREE;
@@ -2556,6 +2596,20 @@ int pipecg_b200_solver_run(pcg_solver* S, pcg_result* res, double* history_host,
   res->n_drift = drift_n;
   S->mn_valid = false;
   return comm_failed(c);
+}
+
+int pipecg_b200_solver_prepare(pcg_solver* S, int64_t count) {
+  if (!S) return set_error(PCG_EINVAL, "solver_prepare: null handle");
+  if (!S->opt.use_graphs || count <= 0) return PCG_OK;
+  const int K = auto_chunk(S);
+  const int sizes[2] = {(int)std::min<int64_t>(count, K), (int)(count % K)};
+  for (int k : sizes)
+    for (int parity = 0; parity < 2 && k > 0; ++parity) {
+      cudaGraphExec_t exec = nullptr;
+      int rc = chunk_graph(S, k, parity, &exec);
+      if (rc) return rc;
+    }
+  return PCG_OK;
 }
 
 int pipecg_b200_solver_enqueue(pcg_solver* S, int64_t count) {

@@ -264,6 +264,10 @@ class PipecgSolver:
     def enqueue(self, count: int) -> None:
         _lib.call("pipecg_b200_solver_enqueue", self._h, int(count))
 
+    def prepare(self, count: int) -> None:
+        """Build the CUDA graphs a following enqueue(count) launches."""
+        _lib.call("pipecg_b200_solver_prepare", self._h, int(count))
+
     def poll(self) -> _lib.PcgResult:
         res = _lib.PcgResult()
         _lib.call("pipecg_b200_solver_poll", self._h, ctypes.byref(res))

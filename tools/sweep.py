@@ -25,6 +25,7 @@ def time_variant(A, d, v, steps=40, warm=5):
         return {"v": v, "error": str(e)[:200]}
     s.init(b, torch.zeros_like(b), 0.0, warm + steps + 1)
     s.enqueue(warm)
+    s.prepare(steps)
     torch.cuda.synchronize()
     st = torch.cuda.ExternalStream(s.stream)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
