@@ -271,6 +271,30 @@ __device__ Step prologue(Ctrl* C, double* hist, const ReduceIn& R, long long it,
   return st;
 }
 
+// Distributed comm buffer layout (identical on every rank, IPC-exported):
+//   [0] u64 arrive, [8] u64 xarrive, [256] slots[2][kMaxRanks][4],
+//   [768] islots[kMaxRanks][4]  (see the exchange section below)
+constexpr size_t kCommBytes = 1024;
+constexpr size_t kCommSlots = 256;
+constexpr size_t kCommISlots = 768;
+
+// Peer-memory exchange fused into the iteration kernel (distributed mode,
+// fused variants A/C/D): after a tile's rows are final the CTA stores the
+// tile's halo rows of the gathered vector (w for A, the stored m for C/D)
+// straight into the neighbours' HBM over NVLink; the grid's last block then
+// pushes this rank's dot partial into every rank's slot and signals every
+// rank's arrival counter.  ptr == nullptr: not connected / separate kernel.
+struct FusedXchg {
+  const int* ptr;        // [n_tiles + 1] send entries of each tile (sorted by row)
+  const int* row;        // local row to send
+  const int* peer;       // destination rank
+  const long long* dst;  // index in the destination's local column space
+  char* peer_vbuf[kMaxRanks];
+  long long peer_ld[kMaxRanks];
+  char* peer_comm[kMaxRanks];
+  int rank, world;
+};
+
 // The block's (r,u),(w,u),(u,u) partial -> pout; the last block of the grid
 // to finish (atomic ticket) sums all partials in a fixed order into fin, so
 // the next prologue reads 3 numbers instead of every block's partial.
@@ -281,7 +305,7 @@ __device__ Step prologue(Ctrl* C, double* hist, const ReduceIn& R, long long it,
 template <int NT>
 __device__ __forceinline__ void publish_partials(double (&acc)[3], int lt, double* red, int bar_id,
                                                  double* pout, double* fin, unsigned* counter,
-                                                 long long it) {
+                                                 long long it, const FusedXchg* X = nullptr) {
   constexpr int NW = NT / PCG_WARP;
   group_sum<3, NT>(acc, lt, red, bar_id);
   double* part = pout + (size_t)(it & 1) * (size_t)gridDim.x * 4;
@@ -292,7 +316,11 @@ __device__ __forceinline__ void publish_partials(double (&acc)[3], int lt, doubl
     out[2] = acc[2];
     out[3] = 0.0;
     if (!counter) return;
-    __threadfence();
+    // fused exchange: this CTA's halo stores (all consumer threads, ordered
+    // before this point by group_sum's barrier) reach the peers before the
+    // ticket, hence before the last block's signal
+    if (X) __threadfence_system();
+    else __threadfence();
     const unsigned ticket = atomicAdd(counter + (it & 1), 1u);
     red[3 * NW] = ticket == gridDim.x - 1 ? 1.0 : 0.0;
   }
@@ -315,6 +343,40 @@ __device__ __forceinline__ void publish_partials(double (&acc)[3], int lt, doubl
     f[3] = 0.0;
     counter[it & 1] = 0u;  // reused by iteration it + 2 (stream-ordered)
   }
+  if (X && lt < X->world) {  // this rank's partial into every rank's slot
+    double* slot = reinterpret_cast<double*>(X->peer_comm[lt] + kCommSlots) +
+                   ((size_t)(it & 1) * kMaxRanks + X->rank) * 4;
+    slot[0] = v[0];
+    slot[1] = v[1];
+    slot[2] = v[2];
+    slot[3] = 0.0;
+  }
+  if (X) {
+    bar_sync(bar_id, NT);
+    if (lt == 0) {
+      __threadfence_system();
+      for (int q = 0; q < X->world; ++q)
+        atomicAdd_system(reinterpret_cast<unsigned long long*>(X->peer_comm[q]), 1ull);
+    }
+  }
+}
+
+// Halo rows of tile t -> the peers (see FusedXchg); consumers only (named
+// barrier `bar_id` makes the tile's new values visible CTA-wide first).
+template <int NT>
+__device__ __forceinline__ void tile_exchange(const FusedXchg& X, long long t, int lt,
+                                              const double* src, int vec, int bar_id) {
+  const int e0 = X.ptr[t], e1 = X.ptr[t + 1];
+  if (e1 <= e0) return;  // uniform across the CTA
+  bar_sync(bar_id, NT);
+  bool sent = false;
+  for (int e = e0 + lt; e < e1; e += NT) {
+    const int q = X.peer[e];
+    double* dst = reinterpret_cast<double*>(X.peer_vbuf[q]) + (size_t)vec * X.peer_ld[q] + X.dst[e];
+    *dst = __ldcg(src + X.row[e]);  // written by this CTA (L2-coherent read)
+    sent = true;
+  }
+  if (sent) __threadfence_system();  // before this CTA's ticket (publish_partials)
 }
 
 // ===========================================================================
@@ -341,6 +403,7 @@ struct FusedParams {
   int cap_val;  // doubles per stage
   int cap_col;  // ints per stage
   int flags;    // experiment switches (PIPECG_B200_FLAGS): 1 = gathers read the row itself
+  FusedXchg X;                // fused peer exchange (X.ptr == nullptr: off)
   // variant D (nnz-balanced tiles)
   const int* tile_row;        // [n_tiles + 1] first row of each tile
   const long long* tile_e;    // [n_tiles + 1] first nonzero of each tile
@@ -779,8 +842,11 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_a(FusedParams<RP>
     }
     __syncwarp();
     if ((lt & 31) == 0) mbar_arrive(&empty[s]);
+    if (P.X.ptr)  // the tile's halo rows of the vector the peers gather next
+      tile_exchange<NT>(P.X, t, lt, MG ? P.m[(it + 1) & 1] : w_new,
+                        MG ? (((it + 1) & 1) ? 12 : 9) : 7 + (int)((it + 1) & 1), 1);
   }
-  publish_partials<NT>(acc, lt, red, 1, P.pout, P.fin, P.counter, it);
+  publish_partials<NT>(acc, lt, red, 1, P.pout, P.fin, P.counter, it, P.X.ptr ? &P.X : nullptr);
 }
 
 // ---------------------------------------------------------------------------
@@ -1016,8 +1082,11 @@ __global__ void __launch_bounds__(kDThreads + 32) pipecg_fused_kernel_d(FusedPar
     }
     __syncwarp();
     if ((lt & 31) == 0) mbar_arrive(&empty[s]);
+    if (P.X.ptr)  // the tile's halo rows of the stored m (gathered next iteration)
+      tile_exchange<NT>(P.X, blockIdx.x + j * (long long)gridDim.x, lt, m_new,
+                        ((it + 1) & 1) ? 12 : 9, 1);
   }
-  publish_partials<NT>(acc, lt, red, 1, P.pout, P.fin, P.counter, it);
+  publish_partials<NT>(acc, lt, red, 1, P.pout, P.fin, P.counter, it, P.X.ptr ? &P.X : nullptr);
 }
 
 // ===========================================================================
@@ -1234,9 +1303,6 @@ __global__ void init_ctrl_kernel(Ctrl* C, const double* dots, int nranks, double
 //   [256] double slots[2][kMaxRanks][4]   per-rank dot partials by parity
 //   [768] double islots[kMaxRanks][4]     per-rank init dots
 // ===========================================================================
-constexpr size_t kCommBytes = 1024;
-constexpr size_t kCommSlots = 256;
-constexpr size_t kCommISlots = 768;
 
 struct CommParams {
   int rank, world;
@@ -1511,6 +1577,11 @@ struct pcg_solver {
   int variant = 1;                 // fused kernel variant in use
   bool irregular = false;          // some row longer than kLongRow
   bool pdl = true;                 // programmatic dependent launch of the fused kernels
+  bool fused_xchg = false;         // distributed: halo + partial push inside the fused kernel
+  int* x_ptr = nullptr;            // its per-tile send lists (sorted by row)
+  int* x_row = nullptr;
+  int* x_peer = nullptr;
+  long long* x_dst = nullptr;
   FusedPlan plans[kVariants];      // per fused variant (stages == 0: does not fit)
   double tune_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // autotune ms/iteration: fused A..E, engine 2
   int* tile_row = nullptr;         // variant D/E tiles of the applied plan
@@ -1803,7 +1874,7 @@ ReduceIn reduce_in(pcg_solver* S) {
     R.pin = reinterpret_cast<const double*>(S->comm + kCommSlots);
     R.n_pin = kMaxRanks;  // slots are laid out [2][kMaxRanks][4]; unused ranks stay 0
     R.arrive = reinterpret_cast<const unsigned long long*>(S->comm);
-    R.arrive_per_it = (unsigned long long)S->world * kXchgBlocks;
+    R.arrive_per_it = (unsigned long long)S->world * (S->fused_xchg ? 1 : kXchgBlocks);
   } else if (S->opt.dot_mode == PCG_DOT_SEQ) {
     R.pin = S->seqbuf;
     R.n_pin = 1;
@@ -1848,6 +1919,21 @@ FusedParams<RP> fused_params(pcg_solver* S) {
   P.tile_row = S->tile_row;
   P.tile_e = S->tile_e;
   P.hub_len = S->hub_len;
+  P.X = FusedXchg{};
+  if (S->fused_xchg) {
+    P.X.ptr = S->x_ptr;
+    P.X.row = S->x_row;
+    P.X.peer = S->x_peer;
+    P.X.dst = S->x_dst;
+    for (int q = 0; q < S->world; ++q) {
+      P.X.peer_vbuf[q] = S->cp.peer_vbuf[q];
+      P.X.peer_ld[q] = S->cp.peer_ld[q];
+      P.X.peer_comm[q] = S->cp.peer_comm[q];
+    }
+    P.X.rank = S->rank;
+    P.X.world = S->world;
+    P.counter = S->counter;  // the last block pushes the partial and signals
+  }
   return P;
 }
 
@@ -1944,7 +2030,7 @@ int enqueue_step(pcg_solver* S, int k) {
   if (S->opt.dot_mode == PCG_DOT_SEQ && !S->connected)
     seq_dots_kernel<<<1, 32, 0, st>>>(R.C, n, S->r, S->u, S->w[0], S->w[1], S->engine == 1,
                                       S->seqbuf, k);
-  if (S->connected)
+  if (S->connected && !S->fused_xchg)
     iter_exchange_kernel<<<kXchgBlocks, 256, 0, st>>>(
         S->cp, R.C, k, use_fin(S) ? S->fin : S->partials, use_fin(S) ? 1 : S->grid,
         stored_m_fused(S) ? S->m : S->w[0],
@@ -2232,6 +2318,10 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&S->num_sms, cudaDevAttrMultiProcessorCount, dev);
   if (S->opt.max_sms > 0 && S->opt.max_sms < S->num_sms) S->num_sms = S->opt.max_sms;
+  // Early (programmatic) launch assumes the grid owns the GPU: with several
+  // solvers co-resident on one GPU (max_sms), a next-iteration grid parked on
+  // SMs could starve a peer rank's grid that this one waits for.
+  if (S->opt.max_sms > 0) S->pdl = false;
   int rc = cuda_status(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking), "stream");
   if (!rc) rc = cuda_status(cudaEventCreateWithFlags(&S->ev_in, cudaEventDisableTiming), "event");
   for (int k = 0; k < 2 && !rc; ++k)
@@ -2375,6 +2465,10 @@ int pipecg_b200_solver_destroy(pcg_solver* S) {
   cudaFree(S->rec_dev);
   cudaFree(S->comm);
   cudaFree(S->long_rows);
+  cudaFree(S->x_ptr);
+  cudaFree(S->x_row);
+  cudaFree(S->x_peer);
+  cudaFree(S->x_dst);
   for (int v = 0; v < kVariants; ++v) {
     cudaFree(S->plans[v].tile_row);
     cudaFree(S->plans[v].tile_e);
@@ -2415,6 +2509,59 @@ int pipecg_b200_ipc_close(void* dev_ptr) {
   return cuda_status(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
 }
 
+// Per-tile send lists for the fused exchange: the plan's send entries sorted
+// by local row, and for every tile of the applied plan the range of entries
+// whose row it owns.
+int build_tile_sends(pcg_solver* S) {
+  const long long ns = S->cp.n_send, nt = S->n_tiles, n = S->A.n_rows;
+  std::vector<int> row(ns), peer(ns);
+  std::vector<long long> dst(ns);
+  cudaStream_t st = S->stream;
+  if (ns) {
+    cudaMemcpyAsync(row.data(), S->cp.send_row, ns * sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(peer.data(), S->cp.send_peer, ns * sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(dst.data(), S->cp.send_dst, ns * sizeof(long long), cudaMemcpyDeviceToHost, st);
+  }
+  std::vector<int> tstart(nt + 1);
+  if (S->variant == 3) {
+    cudaMemcpyAsync(tstart.data(), S->tile_row, (nt + 1) * sizeof(int), cudaMemcpyDeviceToHost, st);
+  } else {
+    for (long long t = 0; t <= nt; ++t) tstart[t] = (int)std::min<long long>(t * S->tr, n);
+  }
+  int rc = cuda_status(cudaStreamSynchronize(st), "fused exchange plan");
+  if (rc) return rc;
+  std::vector<long long> ord(ns);
+  for (long long e = 0; e < ns; ++e) ord[e] = e;
+  std::stable_sort(ord.begin(), ord.end(), [&](long long a, long long b) { return row[a] < row[b]; });
+  std::vector<int> srow(ns), speer(ns), ptr(nt + 1);
+  std::vector<long long> sdst(ns);
+  for (long long e = 0; e < ns; ++e) {
+    srow[e] = row[ord[e]];
+    speer[e] = peer[ord[e]];
+    sdst[e] = dst[ord[e]];
+  }
+  for (long long t = 0; t <= nt; ++t)
+    ptr[t] = (int)(std::lower_bound(srow.begin(), srow.end(), tstart[t]) - srow.begin());
+  cudaFree(S->x_ptr);
+  cudaFree(S->x_row);
+  cudaFree(S->x_peer);
+  cudaFree(S->x_dst);
+  S->x_ptr = S->x_row = S->x_peer = nullptr;
+  S->x_dst = nullptr;
+  if (cudaMalloc(&S->x_ptr, (nt + 1) * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&S->x_row, std::max<long long>(ns, 1) * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&S->x_peer, std::max<long long>(ns, 1) * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&S->x_dst, std::max<long long>(ns, 1) * sizeof(long long)) != cudaSuccess)
+    return set_error(PCG_ENOMEM, "fused exchange lists");
+  cudaMemcpyAsync(S->x_ptr, ptr.data(), (nt + 1) * sizeof(int), cudaMemcpyHostToDevice, st);
+  if (ns) {
+    cudaMemcpyAsync(S->x_row, srow.data(), ns * sizeof(int), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(S->x_peer, speer.data(), ns * sizeof(int), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(S->x_dst, sdst.data(), ns * sizeof(long long), cudaMemcpyHostToDevice, st);
+  }
+  return cuda_status(cudaStreamSynchronize(st), "fused exchange lists");
+}
+
 int pipecg_b200_solver_connect(pcg_solver* S, int rank, int world, void* const* peer_vbuf,
                                const int64_t* peer_ld, void* const* peer_comm, int64_t n_send,
                                const int32_t* send_row, const int32_t* send_peer,
@@ -2440,6 +2587,12 @@ int pipecg_b200_solver_connect(pcg_solver* S, int rank, int world, void* const* 
   cp.send_dst = reinterpret_cast<const long long*>(send_dst);
   S->cp = cp;
   S->connected = true;
+  // fused exchange for variants A, C, D (B keeps the separate exchange kernel)
+  S->fused_xchg = S->variant != 1 && !getenv("PIPECG_B200_SEPARATE_XCHG");
+  if (S->fused_xchg) {
+    int rc = build_tile_sends(S);
+    if (rc) return rc;
+  }
   for (int k = 0; k < 2; ++k) {  // graphs captured without the exchange are stale
     for (auto& kv : S->graphs[k]) cudaGraphExecDestroy(kv.second);
     S->graphs[k].clear();
