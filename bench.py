@@ -440,7 +440,10 @@ def run_distributed(args):
     ms = group.max(e0.elapsed_time(e1))
     res = solver.solver.poll()
     ok = group.max(0.0 if (res.status == 0 and res.iterations == warm + steps) else 1.0) == 0.0
-    launches = 2 * steps + (res.graph_launches - g0)  # fused + exchange per step, advance per chunk
+    # one fused kernel per step (halo + partial exchange inside it; variant B
+    # keeps a separate exchange kernel) and one advance kernel per chunk
+    per_step = 2 if (res.engine == 4 or os.environ.get("PIPECG_B200_SEPARATE_XCHG")) else 1
+    launches = per_step * steps + (res.graph_launches - g0)
     # time to solution at the recipe tolerance (same connected solver)
     u0 = pb.jacobi_apply(pb.JacobiPreconditioner(prob.inv_diag[: prob.plan.n_local]), b)
     tol = 1e-8 * math.sqrt(sum(group.all_gather_object(pb.dots([(u0, u0)], mode="tree")[0])))
@@ -483,7 +486,7 @@ def run_distributed(args):
                                    f"({CONFIG_NAMES.get(args.config, 'custom')})",
                        "N": N, "nnz": nnz,
                        "parallelism": f"row-block x{ws}, NVLink peer-memory halo + dot-partial "
-                                      "exchange fused after each iteration kernel",
+                                      "exchange fused into each iteration kernel",
                        "l2": "inputs >> L2; no flush needed"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * ws, "unit": "GB/s",
                          "frac": achieved / (peak * ws), "traffic": None,
