@@ -180,7 +180,7 @@ typedef struct {
 typedef struct {
   int dot_mode;        /* PCG_DOT_TREE (default) or PCG_DOT_SEQ */
   int engine;          /* 0 auto (autotuned for >= 64K rows), 1 fused (variant autotuned),
-                          2 two-kernel, 3..6 fused variant A/B/C/D */
+                          2 two-kernel, 3..7 fused variant A/B/C/D/P */
   int chunk;           /* iterations per CUDA-graph chunk (0 = auto) */
   int use_graphs;      /* 1 (default) or 0 (plain launches, debugging) */
   int max_sms;         /* size persistent grids for at most this many SMs (0 = all) */
@@ -197,9 +197,9 @@ typedef struct {
   double breakdown_value;
   int64_t n_history;   /* entries written to history_host */
   int64_t n_drift;     /* samples written to drift_*_host */
-  int engine;          /* engine used: 2 two-kernel, 3..6 fused variant A/B/C/D */
+  int engine;          /* engine used: 2 two-kernel, 3..7 fused variant A/B/C/D/P */
   int64_t graph_launches;
-  double tune_ms[8];   /* autotune ms/iteration: fused A, B, C, D, two-kernel, -, -, -
+  double tune_ms[8];   /* autotune ms/iteration: fused A, B, C, D, P, two-kernel, -, -
                           (0 = not run) */
 } pcg_result;
 

@@ -14,7 +14,7 @@ import subprocess
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "_lib" / "libpipecg_b200.so"
+LIB_PATH = Path(os.environ["PIPECG_B200_LIB"]) if os.environ.get("PIPECG_B200_LIB") else _HERE / "_lib" / "libpipecg_b200.so"  # env: experiments only
 CSRC = _HERE / "csrc"
 
 PCG_OK = 0

@@ -204,17 +204,19 @@ __device__ Step prologue(Ctrl* C, double* hist, const ReduceIn& R, long long it,
     const int n_partials = R.n_pin;
     double v[3] = {0.0, 0.0, 0.0};
     for (int j = lt; j < n_partials; j += NT) {
-      v[0] = add(v[0], P[j * 4 + 0]);
-      v[1] = add(v[1], P[j * 4 + 1]);
-      v[2] = add(v[2], P[j * 4 + 2]);
+      // L2-coherent loads: in the persistent kernel these were written by
+      // other CTAs of the same launch (an L1 line could be stale)
+      v[0] = add(v[0], __ldcg(P + j * 4 + 0));
+      v[1] = add(v[1], __ldcg(P + j * 4 + 1));
+      v[2] = add(v[2], __ldcg(P + j * 4 + 2));
     }
     group_sum<3, NT>(v, lt, red, bar_id);
     gamma = v[0];
     delta = v[1];
     norm = sqrt(v[2]);
-    const Slot prev = C->slot[(it - 1) & 1];
-    gamma_prev = prev.gamma;
-    alpha_prev = prev.alpha;
+    const Slot* prev = &C->slot[(it - 1) & 1];
+    gamma_prev = __ldcg(&prev->gamma);
+    alpha_prev = __ldcg(&prev->alpha);
     // solvers.py:354-357 (iteration it-1's guards)
     if (gamma < 0.0 || !isfinite(gamma)) {
       if (leader) {
@@ -660,7 +662,10 @@ struct FusedLayoutA {
 //                   nonzero -- better for wide rows).
 // Both round exactly like the reference (m is the same rounded product).
 // Selected per matrix by the setup-time autotuner.
-template <typename RP, int TR, bool MG>
+// XG: the distributed fused exchange is compiled in (a separate
+// instantiation: its presence in the tile loop costs ~30% at 256^3 even
+// when not taken, measured).
+template <typename RP, int TR, bool MG, bool XG = false>
 __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_a(FusedParams<RP> P, int step) {
   using L = FusedLayoutA<RP, TR>;
   constexpr int NT = TR;  // consumer threads
@@ -842,11 +847,11 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_a(FusedParams<RP>
     }
     __syncwarp();
     if ((lt & 31) == 0) mbar_arrive(&empty[s]);
-    if (P.X.ptr)  // the tile's halo rows of the vector the peers gather next
+    if (XG)  // the tile's halo rows of the vector the peers gather next
       tile_exchange<NT>(P.X, t, lt, MG ? P.m[(it + 1) & 1] : w_new,
                         MG ? (((it + 1) & 1) ? 12 : 9) : 7 + (int)((it + 1) & 1), 1);
   }
-  publish_partials<NT>(acc, lt, red, 1, P.pout, P.fin, P.counter, it, P.X.ptr ? &P.X : nullptr);
+  publish_partials<NT>(acc, lt, red, 1, P.pout, P.fin, P.counter, it, XG ? &P.X : nullptr);
 }
 
 // ---------------------------------------------------------------------------
@@ -890,7 +895,7 @@ struct TileMeta {
 constexpr int kDThreads = 256;
 constexpr int kDBatch = 8;  // gathers in flight per consumer thread
 
-template <typename RP, int TR>
+template <typename RP, int TR, bool XG = false>
 __global__ void __launch_bounds__(kDThreads + 32) pipecg_fused_kernel_d(FusedParams<RP> P, int step) {
   using L = FusedLayoutD<RP, TR>;
   constexpr int NT = kDThreads;  // consumer threads
@@ -1082,11 +1087,219 @@ __global__ void __launch_bounds__(kDThreads + 32) pipecg_fused_kernel_d(FusedPar
     }
     __syncwarp();
     if ((lt & 31) == 0) mbar_arrive(&empty[s]);
-    if (P.X.ptr)  // the tile's halo rows of the stored m (gathered next iteration)
+    if (XG)  // the tile's halo rows of the stored m (gathered next iteration)
       tile_exchange<NT>(P.X, blockIdx.x + j * (long long)gridDim.x, lt, m_new,
                         ((it + 1) & 1) ? 12 : 9, 1);
   }
-  publish_partials<NT>(acc, lt, red, 1, P.pout, P.fin, P.counter, it, P.X.ptr ? &P.X : nullptr);
+  publish_partials<NT>(acc, lt, red, 1, P.pout, P.fin, P.counter, it, XG ? &P.X : nullptr);
+}
+
+
+// ---------------------------------------------------------------------------
+// Persistent variant of A/C for latency-bound (small) problems: ONE launch
+// runs a whole chunk of K iterations, CTAs meeting at a grid-wide barrier
+// (monotonic counter, reset by the chunk graph) between iterations instead
+// of a kernel boundary.  The producer keeps streaming: the first tiles of
+// iteration it+1 are bulk-copied while the grid is still finishing it (they
+// only read this CTA's own rows, ordered by a proxy fence + the stage's
+// empty barrier); only the gathers of neighbour rows and the dot partials
+// wait for the grid barrier.  Cross-CTA data written inside the launch is
+// read with L2-coherent loads.  Same arithmetic as A/C (bitwise).
+template <typename RP, int TR, bool MG>
+__global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_p(FusedParams<RP> P, int K,
+                                                                  unsigned long long* gbar) {
+  using L = FusedLayoutA<RP, TR>;
+  constexpr int NT = TR;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + 8;
+  double* red = reinterpret_cast<double*>(smem + 256);
+  volatile int* stop = reinterpret_cast<volatile int*>(smem + 512);           // consumers stopped
+  volatile int* producer_done = reinterpret_cast<volatile int*>(smem + 516);
+  volatile long long* issued = reinterpret_cast<volatile long long*>(smem + 768);
+  long long* s_base = reinterpret_cast<long long*>(smem + 896);
+  unsigned char* stage0 = smem + L::kHeader;
+  const int SB = L::stage_bytes(P.cap_val, P.cap_col);
+  Ctrl* C = P.C;
+  const int tid = threadIdx.x;
+  const bool producer = tid < 32;
+  const long long my_tiles =
+      P.n_tiles > (long long)blockIdx.x ? (P.n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  // never more stages than own tiles: a stage is then only refilled after
+  // the consumers finished the SAME tile of the previous iteration
+  const int S = (int)max(1LL, min((long long)P.stages, my_tiles));
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NT / 32);
+    }
+    fence_barrier_init();
+    *s_base = read_status(C) == PCG_RUNNING ? *reinterpret_cast<volatile long long*>(&C->base_it) : -1;
+    *stop = 0;
+    *producer_done = 0;
+    *issued = 0;
+  }
+  __syncthreads();
+  const long long base = *reinterpret_cast<volatile long long*>(s_base);
+  if (base < 0) return;
+
+  uint64_t pol = 0;
+  auto issue = [&](long long g) {  // g = running tile counter over the launch
+    const int s = (int)(g % S);
+    const long long t = blockIdx.x + (g % my_tiles) * (long long)gridDim.x;
+    const long long t0 = t * TR;
+    const long long rows = min((long long)TR, P.n - t0);
+    const long long e0 = P.rp[t0], e1 = P.rp[t0 + rows];
+    const long long cb = e0 & ~3LL, ce = (e1 + 3) & ~3LL;
+    const long long vb = e0 & ~1LL, ve = (e1 + 1) & ~1LL;
+    const uint32_t b_rp = (uint32_t)((((rows + 1) * sizeof(RP)) + 15) / 16 * 16);
+    const uint32_t b_vec = (uint32_t)((rows * 8 + 15) / 16 * 16);
+    const uint32_t b_val = (uint32_t)((ve - vb) * 8);
+    const uint32_t b_col = (uint32_t)((ce - cb) * 4);
+    unsigned char* sb = stage0 + (size_t)s * SB;
+    mbar_arrive_expect_tx(&full[s], b_rp + 7 * b_vec + b_val + b_col);
+    bulk_g2s(sb, P.rp + t0, b_rp, &full[s], pol);
+#pragma unroll
+    for (int k = 0; k < 7; ++k)
+      bulk_g2s(sb + L::kRpBytes + k * L::kVecBytes, P.vec[k] + t0, b_vec, &full[s], pol);
+    unsigned char* sval = sb + L::kRpBytes + 7 * L::kVecBytes;
+    if (b_val) bulk_g2s(sval, P.val + vb, b_val, &full[s], pol);
+    if (b_col) bulk_g2s(sval + (size_t)P.cap_val * 8, P.col + cb, b_col, &full[s], pol);
+  };
+  const long long total = (long long)K * my_tiles;
+
+  if (producer) {
+    // streams every tile of every iteration of the chunk, up to S ahead of
+    // the consumers; after a stop (breakdown / convergence / max_iterations
+    // mid-chunk) it issues nothing new, and the consumers drain what it did
+    // issue before the CTA retires
+    if (tid == 0) {
+      pol = policy_evict_first();
+      for (long long g = 0; g < total; ++g) {
+        const int s = (int)(g % S);
+        if (g >= S) mbar_wait(&empty[s], (uint32_t)((g / S - 1) & 1));
+        if (*stop) break;
+        issue(g);
+        *issued = g + 1;
+      }
+      __threadfence_block();
+      *producer_done = 1;
+    }
+    return;
+  }
+  const int lt = tid - 32;
+  long long g = 0;
+  bool stopped = false;
+  for (int step = 0; step < K; ++step) {
+    const long long it = base + step;
+    if (step > 0) {  // grid barrier: every CTA finished iteration it - 1
+      if (lt == 0) {
+        const unsigned long long target = (unsigned long long)step * gridDim.x;
+        while (ld_acquire_sys(gbar) < target) __nanosleep(32);
+      }
+      bar_sync(1, NT);
+    }
+    const Step stp = prologue<NT>(C, P.hist, P.rin, it, lt, red, 1, blockIdx.x == 0 && lt == 0);
+    if (!stp.go) {  // identical decision in every CTA: nobody waits at a later barrier
+      if (lt == 0) *stop = 1;
+      stopped = true;
+      break;
+    }
+    const double alpha = stp.alpha, beta = stp.beta;
+    const double* w_old = P.w[it & 1];
+    double* w_new = P.w[(it + 1) & 1];
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (long long j = 0; j < my_tiles; ++j, ++g) {
+      const int s = (int)(g % S);
+      const long long t = blockIdx.x + j * (long long)gridDim.x;
+      const long long t0 = t * TR;
+      const long long rows = min((long long)TR, P.n - t0);
+      unsigned char* sb = stage0 + (size_t)s * SB;
+      const RP* rp_s = reinterpret_cast<const RP*>(sb);
+      const double* v_s = reinterpret_cast<const double*>(sb + L::kRpBytes);
+      const double* val_s = reinterpret_cast<const double*>(sb + L::kRpBytes + 7 * L::kVecBytes);
+      const int* col_s = reinterpret_cast<const int*>(val_s + P.cap_val);
+      const long long i = t0 + lt;
+      double wi = 0.0, di = 0.0;
+      if (lt < rows) {
+        wi = __ldcg(w_old + i);
+        di = ldg_nc(P.dinv + i);
+      }
+      mbar_wait(&full[s], (uint32_t)((g / S) & 1));
+      if (lt < rows) {
+        const long long e0 = rp_s[0];
+        const long long cb = e0 & ~3LL, vb = e0 & ~1LL;
+        const long long lo = rp_s[lt], hi = rp_s[lt + 1];
+        double nacc = 0.0;
+        for (long long k0 = lo; k0 < hi; k0 += 8) {
+          double av[8], mv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const long long k = k0 + u;
+            if (k < hi) {
+              const int c = col_s[k - cb];
+              av[u] = val_s[k - vb];
+              mv[u] = MG ? __ldcg(P.m[it & 1] + c) : mul(ldg_nc(P.dinv + c), __ldcg(w_old + c));
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (k0 + u < hi) nacc = add(nacc, mul(av[u], mv[u]));
+        }
+        const double mi = mul(di, wi);
+        const double zi = add(nacc, mul(beta, v_s[0 * TR + lt]));
+        const double qi = add(mi, mul(beta, v_s[1 * TR + lt]));
+        const double si = add(wi, mul(beta, v_s[2 * TR + lt]));
+        const double ui = v_s[6 * TR + lt];
+        const double pi = add(ui, mul(beta, v_s[3 * TR + lt]));
+        const double xi = add(v_s[4 * TR + lt], mul(alpha, pi));
+        const double ri = sub(v_s[5 * TR + lt], mul(alpha, si));
+        const double un = sub(ui, mul(alpha, qi));
+        const double wn = sub(wi, mul(alpha, zi));
+        P.vec[0][i] = zi;
+        P.vec[1][i] = qi;
+        P.vec[2][i] = si;
+        P.vec[3][i] = pi;
+        P.vec[4][i] = xi;
+        P.vec[5][i] = ri;
+        P.vec[6][i] = un;
+        w_new[i] = wn;
+        if (MG) P.m[(it + 1) & 1][i] = mul(di, wn);
+        acc[0] = add(acc[0], mul(ri, un));
+        acc[1] = add(acc[1], mul(wn, un));
+        acc[2] = add(acc[2], mul(un, un));
+      }
+      // the producer re-reads these rows with the bulk-copy (async) proxy
+      // next iteration: order the generic-proxy stores before the release
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __syncwarp();
+      if ((lt & 31) == 0) mbar_arrive(&empty[s]);
+    }
+    publish_partials<NT>(acc, lt, red, 1, P.pout, P.fin, nullptr, it);
+    // arrive at the grid barrier (all of this CTA's stores before the count)
+    bar_sync(1, NT);
+    if (lt == 0) {
+      __threadfence();
+      atomicAdd(gbar, 1ull);
+    }
+  }
+  // stopped mid-chunk: consume (without computing) every tile the producer
+  // still issued, releasing its stages, until it has quit -- no bulk copy may
+  // be in flight when the CTA retires, and the producer never blocks
+  if (stopped) {
+    for (;;) {
+      if (g < *issued) {
+        const int s = (int)(g % S);
+        mbar_wait(&full[s], (uint32_t)((g / S) & 1));
+        __syncwarp();
+        if ((lt & 31) == 0) mbar_arrive(&empty[s]);
+        ++g;
+        continue;
+      }
+      if (*producer_done && g >= *issued) break;
+      __nanosleep(64);
+    }
+  }
 }
 
 // ===========================================================================
@@ -1527,7 +1740,8 @@ struct FusedPlan {
   long long* tile_e = nullptr;
 };
 
-constexpr int kVariants = 4;  // A B C D
+constexpr int kVariants = 5;  // A B C D P (= C in one persistent launch per chunk)
+constexpr long long kPersistMaxRows = 8LL << 20;  // P is a candidate up to this size
 
 struct pcg_solver {
   pcg_matrix A{};
@@ -1578,6 +1792,7 @@ struct pcg_solver {
   bool irregular = false;          // some row longer than kLongRow
   bool pdl = true;                 // programmatic dependent launch of the fused kernels
   bool fused_xchg = false;         // distributed: halo + partial push inside the fused kernel
+  unsigned long long* gbar = nullptr;  // variant P grid-barrier counter
   int* x_ptr = nullptr;            // its per-tile send lists (sorted by row)
   int* x_row = nullptr;
   int* x_peer = nullptr;
@@ -1795,6 +2010,18 @@ int fused_setup(pcg_solver* S) {
   if (!rc) rc = plan_variant<RP, 2>(S, cc, cv, &S->plans[2]);
   // variant D (tile map build) only where it can win: irregular rows, or asked for
   if (!rc && (S->irregular || S->opt.engine == 6)) rc = plan_d<RP>(S, cv, &S->plans[3]);
+  if (!rc && S->plans[2].stages && (S->A.n_rows <= kPersistMaxRows || S->opt.engine == 7)) {
+    FusedPlan p = S->plans[2];  // same tiles and shared memory as C
+    p.variant = 4;
+    // the cooperative launch needs the whole grid co-resident
+    int occ = 0;
+    cudaError_t e =
+        p.tr == 256   ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pipecg_fused_kernel_p<RP, 256, true>, 288, p.smem)
+        : p.tr == 128 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pipecg_fused_kernel_p<RP, 128, true>, 160, p.smem)
+                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pipecg_fused_kernel_p<RP, 64, true>, 96, p.smem);
+    if (e != cudaSuccess) return cuda_status(e, "persistent occupancy");
+    if ((long long)occ * S->num_sms >= p.grid) S->plans[4] = p;
+  }
   if (rc) return rc;
   bool any = false;
   for (int v = 0; v < kVariants; ++v) any = any || S->plans[v].stages > 0;
@@ -1804,7 +2031,7 @@ int fused_setup(pcg_solver* S) {
 void apply_plan(pcg_solver* S, const FusedPlan& p) {
   S->variant = p.variant;
   S->tr = p.tr;
-  S->n_tiles = p.variant >= 3 ? p.n_tiles : (S->A.n_rows + p.tr - 1) / p.tr;
+  S->n_tiles = p.variant == 3 ? p.n_tiles : (S->A.n_rows + p.tr - 1) / p.tr;
   S->tile_row = p.tile_row;
   S->tile_e = p.tile_e;
   S->hub_len = p.hub_len;
@@ -1841,7 +2068,8 @@ int alloc_state(pcg_solver* S) {
   e = cudaMalloc(&S->partials, (size_t)2 * maxp * 4 * sizeof(double));
   if (e != cudaSuccess) return set_error(PCG_ENOMEM, "solver: partials allocation failed");
   cudaMemsetAsync(S->partials, 0, (size_t)2 * maxp * 4 * sizeof(double), S->stream);
-  if (cudaMalloc(&S->fin, 8 * sizeof(double)) != cudaSuccess ||
+  if (cudaMalloc(&S->gbar, sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMalloc(&S->fin, 8 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&S->counter, 2 * sizeof(unsigned)) != cudaSuccess)
     return set_error(PCG_ENOMEM, "solver: partials allocation failed");
   cudaMemsetAsync(S->fin, 0, 8 * sizeof(double), S->stream);
@@ -1865,6 +2093,13 @@ int alloc_state(pcg_solver* S) {
 constexpr int kFinGrid = 512;
 inline bool use_fin(const pcg_solver* S) { return S->grid > kFinGrid; }
 
+// Variant P: the whole chunk in one cooperative (co-resident) launch.
+// Only single-GPU, tree dots, no drift samples; otherwise P runs as C.
+inline bool persistent_chunk(const pcg_solver* S) {
+  return S->engine == 1 && S->variant == 4 && !S->connected && S->opt.dot_mode == PCG_DOT_TREE &&
+         S->drift_k == 0;
+}
+
 // What the next prologue reduces, per mode
 ReduceIn reduce_in(pcg_solver* S) {
   ReduceIn R;
@@ -1879,8 +2114,9 @@ ReduceIn reduce_in(pcg_solver* S) {
     R.pin = S->seqbuf;
     R.n_pin = 1;
   } else {
-    R.pin = use_fin(S) ? S->fin : S->partials;
-    R.n_pin = use_fin(S) ? 1 : S->grid;
+    const bool fin = use_fin(S) && !persistent_chunk(S);
+    R.pin = fin ? S->fin : S->partials;
+    R.n_pin = fin ? 1 : S->grid;
   }
   return R;
 }
@@ -1963,30 +2199,36 @@ void launch_fused(pcg_solver* S, int k) {
   const bool pdl = S->pdl;
   const unsigned g = (unsigned)S->grid;
   const size_t sm = S->smem;
-  if (S->variant == 1) {
+  const int variant = S->variant == 4 ? 2 : S->variant;  // P, launched per iteration, is C
+  if (variant == 1) {
     switch (S->tr) {
       case 256: launch_k(pipecg_fused_kernel<RP, 256>, g, FusedLayout<RP, 256>::kThreads, sm, st, pdl, P, k); break;
       case 128: launch_k(pipecg_fused_kernel<RP, 128>, g, FusedLayout<RP, 128>::kThreads, sm, st, pdl, P, k); break;
       default: launch_k(pipecg_fused_kernel<RP, 64>, g, FusedLayout<RP, 64>::kThreads, sm, st, pdl, P, k); break;
     }
-  } else if (S->variant == 3) {
-    switch (S->tr) {
-      case 256: launch_k(pipecg_fused_kernel_d<RP, 256>, g, kDThreads + 32, sm, st, pdl, P, k); break;
-      case 128: launch_k(pipecg_fused_kernel_d<RP, 128>, g, kDThreads + 32, sm, st, pdl, P, k); break;
-      default: launch_k(pipecg_fused_kernel_d<RP, 64>, g, kDThreads + 32, sm, st, pdl, P, k); break;
-    }
-  } else if (S->variant == 2) {
-    switch (S->tr) {
-      case 256: launch_k(pipecg_fused_kernel_a<RP, 256, true>, g, 256 + 32, sm, st, pdl, P, k); break;
-      case 128: launch_k(pipecg_fused_kernel_a<RP, 128, true>, g, 128 + 32, sm, st, pdl, P, k); break;
-      default: launch_k(pipecg_fused_kernel_a<RP, 64, true>, g, 64 + 32, sm, st, pdl, P, k); break;
-    }
+  } else if (variant == 3) {
+#define PCG_LD(XGV)                                                                                    \
+  switch (S->tr) {                                                                                     \
+    case 256: launch_k(pipecg_fused_kernel_d<RP, 256, XGV>, g, kDThreads + 32, sm, st, pdl, P, k); break; \
+    case 128: launch_k(pipecg_fused_kernel_d<RP, 128, XGV>, g, kDThreads + 32, sm, st, pdl, P, k); break; \
+    default: launch_k(pipecg_fused_kernel_d<RP, 64, XGV>, g, kDThreads + 32, sm, st, pdl, P, k); break;   \
+  }
+    if (S->fused_xchg) { PCG_LD(true) } else { PCG_LD(false) }
+#undef PCG_LD
   } else {
-    switch (S->tr) {
-      case 256: launch_k(pipecg_fused_kernel_a<RP, 256, false>, g, 256 + 32, sm, st, pdl, P, k); break;
-      case 128: launch_k(pipecg_fused_kernel_a<RP, 128, false>, g, 128 + 32, sm, st, pdl, P, k); break;
-      default: launch_k(pipecg_fused_kernel_a<RP, 64, false>, g, 64 + 32, sm, st, pdl, P, k); break;
-    }
+    // A (MG = false) / C (MG = true), with or without the fused exchange
+#define PCG_LA(MGV, XGV)                                                                             \
+  switch (S->tr) {                                                                                   \
+    case 256: launch_k(pipecg_fused_kernel_a<RP, 256, MGV, XGV>, g, 256 + 32, sm, st, pdl, P, k); break; \
+    case 128: launch_k(pipecg_fused_kernel_a<RP, 128, MGV, XGV>, g, 128 + 32, sm, st, pdl, P, k); break; \
+    default: launch_k(pipecg_fused_kernel_a<RP, 64, MGV, XGV>, g, 64 + 32, sm, st, pdl, P, k); break;    \
+  }
+    const bool mg = variant == 2;
+    if (mg && S->fused_xchg) { PCG_LA(true, true) }
+    else if (mg) { PCG_LA(true, false) }
+    else if (S->fused_xchg) { PCG_LA(false, true) }
+    else { PCG_LA(false, false) }
+#undef PCG_LA
   }
 }
 
@@ -2056,8 +2298,39 @@ int enqueue_step(pcg_solver* S, int k) {
   return PCG_OK;
 }
 
+template <typename RP>
+int launch_persistent(pcg_solver* S, int K) {
+  FusedParams<RP> P = fused_params<RP>(S);
+  P.counter = nullptr;
+  cudaStream_t st = S->stream;
+  cudaMemsetAsync(S->gbar, 0, sizeof(unsigned long long), st);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)S->grid);
+  cfg.blockDim = dim3((unsigned)S->tr + 32);
+  cfg.dynamicSmemBytes = S->smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (grid barrier)
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  unsigned long long* gbar = S->gbar;
+  cudaError_t e;
+  switch (S->tr) {
+    case 256: e = cudaLaunchKernelEx(&cfg, pipecg_fused_kernel_p<RP, 256, true>, P, K, gbar); break;
+    case 128: e = cudaLaunchKernelEx(&cfg, pipecg_fused_kernel_p<RP, 128, true>, P, K, gbar); break;
+    default: e = cudaLaunchKernelEx(&cfg, pipecg_fused_kernel_p<RP, 64, true>, P, K, gbar); break;
+  }
+  return cuda_status(e, "persistent launch");
+}
+
 int enqueue_chunk_body(pcg_solver* S, int K, int parity) {
-  for (int k = 0; k < K; ++k) enqueue_step(S, k);
+  if (persistent_chunk(S)) {
+    int rc = S->A.rp64 ? launch_persistent<long long>(S, K) : launch_persistent<int>(S, K);
+    if (rc) return rc;
+  } else {
+    for (int k = 0; k < K; ++k) enqueue_step(S, k);
+  }
   advance_kernel<<<1, 32, 0, S->stream>>>(record_at(S->rec_dev).C, K);
   cudaMemcpyAsync(S->rec_host[parity], S->rec_dev, kRecBytes, cudaMemcpyDeviceToHost, S->stream);
   return cuda_status(cudaGetLastError(), "chunk launch");
@@ -2158,6 +2431,15 @@ int preload_solver() {
   PCG_LOAD_A(false);
   PCG_LOAD_A(true);
 #undef PCG_LOAD_A
+#define PCG_LOAD_X(RPT, TRV) \
+  PCG_LOAD((pipecg_fused_kernel_a<RPT, TRV, false, true>)); PCG_LOAD((pipecg_fused_kernel_a<RPT, TRV, true, true>)); \
+  PCG_LOAD((pipecg_fused_kernel_d<RPT, TRV, true>))
+  PCG_LOAD_X(int, 256); PCG_LOAD_X(int, 128); PCG_LOAD_X(int, 64);
+  PCG_LOAD_X(long long, 256); PCG_LOAD_X(long long, 128); PCG_LOAD_X(long long, 64);
+#undef PCG_LOAD_X
+  PCG_LOAD((pipecg_fused_kernel_p<int, 256, true>)); PCG_LOAD((pipecg_fused_kernel_p<int, 128, true>));
+  PCG_LOAD((pipecg_fused_kernel_p<int, 64, true>)); PCG_LOAD((pipecg_fused_kernel_p<long long, 256, true>));
+  PCG_LOAD((pipecg_fused_kernel_p<long long, 128, true>)); PCG_LOAD((pipecg_fused_kernel_p<long long, 64, true>));
   PCG_LOAD((pipecg_fused_kernel_d<int, 256>)); PCG_LOAD((pipecg_fused_kernel_d<int, 128>));
   PCG_LOAD((pipecg_fused_kernel_d<int, 64>)); PCG_LOAD((pipecg_fused_kernel_d<long long, 256>));
   PCG_LOAD((pipecg_fused_kernel_d<long long, 128>)); PCG_LOAD((pipecg_fused_kernel_d<long long, 64>));
@@ -2184,6 +2466,15 @@ int preload_solver() {
   PCG_SMEM_A(false);
   PCG_SMEM_A(true);
 #undef PCG_SMEM_A
+#define PCG_SMEM_X(RPT, TRV) \
+  PCG_SMEM((pipecg_fused_kernel_a<RPT, TRV, false, true>)); PCG_SMEM((pipecg_fused_kernel_a<RPT, TRV, true, true>)); \
+  PCG_SMEM((pipecg_fused_kernel_d<RPT, TRV, true>))
+  PCG_SMEM_X(int, 256); PCG_SMEM_X(int, 128); PCG_SMEM_X(int, 64);
+  PCG_SMEM_X(long long, 256); PCG_SMEM_X(long long, 128); PCG_SMEM_X(long long, 64);
+#undef PCG_SMEM_X
+  PCG_SMEM((pipecg_fused_kernel_p<int, 256, true>)); PCG_SMEM((pipecg_fused_kernel_p<int, 128, true>));
+  PCG_SMEM((pipecg_fused_kernel_p<int, 64, true>)); PCG_SMEM((pipecg_fused_kernel_p<long long, 256, true>));
+  PCG_SMEM((pipecg_fused_kernel_p<long long, 128, true>)); PCG_SMEM((pipecg_fused_kernel_p<long long, 64, true>));
   PCG_SMEM((pipecg_fused_kernel_d<int, 256>)); PCG_SMEM((pipecg_fused_kernel_d<int, 128>));
   PCG_SMEM((pipecg_fused_kernel_d<int, 64>)); PCG_SMEM((pipecg_fused_kernel_d<long long, 256>));
   PCG_SMEM((pipecg_fused_kernel_d<long long, 128>)); PCG_SMEM((pipecg_fused_kernel_d<long long, 64>));
@@ -2242,8 +2533,9 @@ int autotune(pcg_solver* S, int grid2, bool with_engine2, bool irregular) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  const int saved_graphs = S->opt.use_graphs;
-  S->opt.use_graphs = 0;
+  // timed as the solve runs: graph chunks (built before the timed chunk),
+  // kTuneIters iterations after a 2-iteration warm-up
+  constexpr int kTuneIters = 8;
   int best = -1;
   float best_ms = 0.f;
   int rc = PCG_OK;
@@ -2259,15 +2551,21 @@ int autotune(pcg_solver* S, int grid2, bool with_engine2, bool irregular) {
     }
     // b := n (ones), x0 := z (zeros); init copies them before overwriting
     rc = pipecg_b200_solver_init(S, S->nv, S->z, 0.0, 1LL << 40, 0, st);
-    if (!rc) rc = launch_chunk(S, 1, 0);
+    cudaGraphExec_t ge = nullptr;
+    if (!rc && S->opt.use_graphs) rc = chunk_graph(S, kTuneIters, 1, &ge);
+    if (!rc) rc = launch_chunk(S, 2, 0);
     cudaEventRecord(e0, st);
-    if (!rc) rc = launch_chunk(S, 3, 1);
+    if (!rc) rc = launch_chunk(S, kTuneIters, 1);
     cudaEventRecord(e1, st);
     if (!rc) rc = cuda_status(cudaEventSynchronize(e1), "autotune");
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
-    ms /= 3.f;
+    ms /= (float)kTuneIters;
     S->tune_ms[cand] = ms;
+    for (int k = 0; k < 2; ++k) {  // graphs bake in this candidate's launch parameters
+      for (auto& kv : S->graphs[k]) cudaGraphExecDestroy(kv.second);
+      S->graphs[k].clear();
+    }
     if (!rc && (best < 0 || ms < best_ms)) {
       best = cand;
       best_ms = ms;
@@ -2275,7 +2573,6 @@ int autotune(pcg_solver* S, int grid2, bool with_engine2, bool irregular) {
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  S->opt.use_graphs = saved_graphs;
   S->initialized = false;
   S->host_base = 0;
   if (rc) return rc;
@@ -2400,12 +2697,13 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     S->engine = 1;
     apply_plan(S, S->plans[req - 3]);
   } else if (A->n_rows < kTuneRows) {
-    // small: no autotune.  Irregular rows -> D (balanced tiles); wide rows
-    // (> 12 nnz/row) gather the stored m (C); else A
+    // small: no autotune.  Irregular rows -> D (balanced tiles); else P, then
+    // C for wide rows (> 12 nnz/row, one gather per nonzero) or A
     const bool wide = A->nnz > 12 * A->n_rows;
-    int order[kVariants] = {0, 2, 3, 1};
-    if (has_long) order[0] = 3, order[1] = 2, order[2] = 0;
-    else if (wide) order[0] = 2, order[1] = 0;
+    // small problems are launch-latency bound: P (one launch per chunk) first
+    int order[kVariants] = {4, 0, 2, 3, 1};
+    if (has_long) order[0] = 3, order[1] = 4, order[2] = 2, order[3] = 0;
+    else if (wide) order[1] = 2, order[2] = 0;
     S->engine = 1;
     for (int k = 0; k < kVariants; ++k)
       if (S->plans[order[k]].stages) {
@@ -2457,6 +2755,7 @@ int pipecg_b200_solver_destroy(pcg_solver* S) {
   cudaFree(S->vbuf);
   cudaFree(S->partials);
   cudaFree(S->fin);
+  cudaFree(S->gbar);
   cudaFree(S->counter);
   cudaFree(S->seqbuf);
   cudaFree(S->dpart);
@@ -2587,6 +2886,7 @@ int pipecg_b200_solver_connect(pcg_solver* S, int rank, int world, void* const* 
   cp.send_dst = reinterpret_cast<const long long*>(send_dst);
   S->cp = cp;
   S->connected = true;
+  if (S->variant == 4) S->variant = 2;  // per-iteration launches (the exchange needs them)
   // fused exchange for variants A, C, D (B keeps the separate exchange kernel)
   S->fused_xchg = S->variant != 1 && !getenv("PIPECG_B200_SEPARATE_XCHG");
   if (S->fused_xchg) {

@@ -168,8 +168,10 @@ class DeviceOptions:
       reference's left-to-right order: bitwise-identical histories).
     engine: "auto" (autotuned at solver creation for >= 1M rows), "fused"
       (one kernel per iteration; variant autotuned), "fused-a" / "fused-b" /
-      "fused-c" / "fused-d" (consumer gathers dinv*w / gather warps / stored m /
-      nnz-balanced tiles with cooperative gathers, for irregular rows) or "two" (update kernel +
+      "fused-c" / "fused-d" / "fused-p" (consumer gathers dinv*w / gather warps /
+      stored m / nnz-balanced tiles with cooperative gathers, for irregular rows /
+      C with a whole chunk of iterations in one persistent launch, for small
+      latency-bound problems) or "two" (update kernel +
       SpMV kernel; general matrices, very long rows).
     chunk: iterations per CUDA-graph chunk (0 = sized from the problem).
     use_graphs: capture chunks as CUDA graphs.
@@ -185,7 +187,7 @@ class DeviceOptions:
 
     def native(self) -> _lib.PcgOptions:
         eng = {"auto": 0, "fused": 1, "two": 2, "fused-a": 3, "fused-b": 4,
-               "fused-c": 5, "fused-d": 6}[self.engine]
+               "fused-c": 5, "fused-d": 6, "fused-p": 7}[self.engine]
         dm = {"tree": _lib.PCG_DOT_TREE, "seq": _lib.PCG_DOT_SEQ}[self.dot_mode]
         return _lib.PcgOptions(dm, eng, int(self.chunk), 1 if self.use_graphs else 0,
                                int(self.max_sms))

@@ -247,3 +247,38 @@ def test_pipecg_init_matches_operators(cuda):
     for nm in ("z", "q", "s", "p"):
         np.testing.assert_array_equal(getattr(st, nm), np.zeros(5))
     del K
+
+
+@pytest.mark.parametrize("kind,n,maxit,tol", [("2d5", 64, 20000, None), ("3d7", 24, 37, None),
+                                              ("3d7", 24, 20000, 1e-300), ("2d5", 300, 20000, None)])
+def test_persistent_chunks_bitwise_equal_per_iteration_launches(cuda, kind, n, maxit, tol):
+    """Variant P (a whole chunk of iterations in one cooperative launch,
+    grid barrier between iterations) computes exactly what C computes with
+    one launch per iteration: identical history and x, including stops in
+    the middle of a chunk (convergence, max_iterations)."""
+    A = pb.stencil_host(kind, n)
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = tol or oracle.recipe_tolerance(A, b, d)
+    pc = pb.JacobiPreconditioner(d)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=maxit, record_history=True)
+    runs = {}
+    for eng, chunk in (("fused-c", 8), ("fused-p", 16), ("fused-p", 7), ("fused-p", 0)):
+        runs[(eng, chunk)] = pb.pipecg_solve(A, b, x0, pc, cfg,
+                                             options=pb.DeviceOptions(engine=eng, chunk=chunk))
+    xc, rc = runs[("fused-c", 8)]
+    for key, (x, rep) in runs.items():
+        assert rep.iterations == rc.iterations, key
+        assert rep.history == rc.history, key
+        np.testing.assert_array_equal(x, xc)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=maxit)
+    assert abs(rc.iterations - ref.iterations) <= 1
+
+
+def test_persistent_chunks_breakdown_mid_chunk(cuda):
+    g = load_golden("solve_indefinite.npz")
+    A = golden_matrix(g)
+    opts = pb.DeviceOptions(engine="fused-p", chunk=16)
+    with pytest.raises(pb.SolverBreakdown) as exc:
+        pb.pipecg_solve(A, g["b"], g["x0"], pb.JacobiPreconditioner(g["inv_diag"]),
+                        _cfg(g, False), options=opts)
+    assert exc.value.quantity == "alpha denominator"

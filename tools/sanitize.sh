@@ -24,7 +24,7 @@ if eng in ("fused-d", "two"):
     print(eng, "powerlaw", rep.iterations)
 PY
 for tool in memcheck racecheck synccheck; do
-  for eng in fused-a fused-b fused-c fused-d two; do
+  for eng in fused-a fused-b fused-c fused-d fused-p two; do
     timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python /tmp/san_case.py $eng > $OUT/san_${tool}_${eng}.log 2>&1
     echo "$tool $eng rc=$? $(grep -c 'ERROR SUMMARY: 0 errors\|RACECHECK SUMMARY: 0 hazards' $OUT/san_${tool}_${eng}.log) $(grep 'SUMMARY' $OUT/san_${tool}_${eng}.log | tail -1)"
   done
