@@ -542,7 +542,10 @@ def run_b200(args):
         "config": {"workload": workload_name(kind, n, N, nnz) +
                                f" ({CONFIG_NAMES.get(args.config, 'custom')})",
                    "N": N, "nnz": nnz, "parallelism": "single GPU",
-                   "l2": f"inputs ({B / 1e9:.1f} GB/iteration) >> 126 MB L2; no flush needed",
+                   "l2": (f"inputs ({B / 1e9:.1f} GB/iteration) >> 126 MB L2; no flush needed"
+                          if B > 4 * 126e6 else
+                          f"working set ({B / 1e6:.0f} MB/iteration) is L2-sized: no flush, the "
+                          "number is the steady state a solve of this size also runs in"),
                    "engine": ENGINES.get(info["engine"], "?"),
                    "autotune_ms_per_iter": {"fused_A": info["tune_ms"][0],
                                             "fused_B": info["tune_ms"][1],
