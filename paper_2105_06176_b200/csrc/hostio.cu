@@ -101,12 +101,15 @@ class Pool {
 // ---------------------------------------------------------------------------
 // pinned staging ring (allocated once per process, per device)
 // ---------------------------------------------------------------------------
-constexpr int kSlots = 4;
-constexpr size_t kSlotBytes = 32u << 20;
+// ring geometry: kSlots slots of slot_bytes (env PIPECG_B200_H2D_SLOT_MB to
+// experiment); small slots let the host conversion of chunk k+1 overlap the
+// DMA of chunk k even for arrays of a few tens of MB
+constexpr int kSlots = 8;
 
 struct Ring {
   char* slot[kSlots] = {};
   cudaEvent_t ev[kSlots] = {};
+  size_t slot_bytes = 8u << 20;
   int device = -1;
   std::mutex mu;  // one transfer at a time per process
   int init() {
@@ -114,8 +117,10 @@ struct Ring {
     cudaGetDevice(&dev);
     if (device == dev) return PCG_OK;
     release();
+    if (const char* e = getenv("PIPECG_B200_H2D_SLOT_MB"))
+      slot_bytes = (size_t)std::max(1, atoi(e)) << 20;
     for (int s = 0; s < kSlots; ++s) {
-      if (cudaHostAlloc(reinterpret_cast<void**>(&slot[s]), kSlotBytes, cudaHostAllocPortable) !=
+      if (cudaHostAlloc(reinterpret_cast<void**>(&slot[s]), slot_bytes, cudaHostAllocPortable) !=
           cudaSuccess)
         return set_error(PCG_ENOMEM, "hostio: pinned staging allocation failed");
       if (cudaEventCreateWithFlags(&ev[s], cudaEventDisableTiming) != cudaSuccess)
@@ -184,7 +189,7 @@ extern "C" int pipecg_b200_h2d(void* dst_dev, const void* src_host, int64_t coun
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   const size_t out_es = kind == PCG_H2D_I64_TO_I32 ? 4 : 8;
-  const int64_t per_slot = (int64_t)(kSlotBytes / out_es);
+  const int64_t per_slot = (int64_t)(R.slot_bytes / out_es);
   const char* src = static_cast<const char*>(src_host);
   char* dst = static_cast<char*>(dst_dev);
   bool overflow = false;
@@ -213,13 +218,13 @@ extern "C" int pipecg_b200_d2h(void* dst_host, const void* src_dev, int64_t byte
   cudaStream_t st = (cudaStream_t)stream;
   const char* src = static_cast<const char*>(src_dev);
   char* dst = static_cast<char*>(dst_host);
-  const int64_t n_chunks = (bytes + kSlotBytes - 1) / kSlotBytes;
+  const int64_t n_chunks = (bytes + R.slot_bytes - 1) / R.slot_bytes;
   // keep up to kSlots chunks in flight; drain each into the caller's buffer
   for (int64_t c = 0; c < n_chunks + kSlots; ++c) {
     if (c < n_chunks) {
       const int s = (int)(c % kSlots);
-      const int64_t off = c * (int64_t)kSlotBytes;
-      const int64_t nb = std::min<int64_t>(kSlotBytes, bytes - off);
+      const int64_t off = c * (int64_t)R.slot_bytes;
+      const int64_t nb = std::min<int64_t>(R.slot_bytes, bytes - off);
       cudaError_t e = cudaEventSynchronize(R.ev[s]);
       if (e != cudaSuccess) return cuda_status(e, "d2h slot wait");
       e = cudaMemcpyAsync(R.slot[s], src + off, nb, cudaMemcpyDeviceToHost, st);
@@ -229,8 +234,8 @@ extern "C" int pipecg_b200_d2h(void* dst_host, const void* src_dev, int64_t byte
     const int64_t d = c - (kSlots - 1);  // chunk to drain now
     if (d >= 0 && d < n_chunks) {
       const int s = (int)(d % kSlots);
-      const int64_t off = d * (int64_t)kSlotBytes;
-      const int64_t nb = std::min<int64_t>(kSlotBytes, bytes - off);
+      const int64_t off = d * (int64_t)R.slot_bytes;
+      const int64_t nb = std::min<int64_t>(R.slot_bytes, bytes - off);
       cudaError_t e = cudaEventSynchronize(R.ev[s]);
       if (e != cudaSuccess) return cuda_status(e, "d2h wait");
       convert(dst + off, R.slot[s], nb / 8, PCG_H2D_COPY64);
