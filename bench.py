@@ -237,7 +237,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (manufactured solution x=1/sqrt(N))",
-        "config": {"workload": workload_name(kind, n, N, nnz),
+        "config": {"workload": workload_name(kind, n, N, nnz) +
+                               f" ({CONFIG_NAMES.get(args.config, 'custom')})",
                    "N": N, "nnz": nnz},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{args.steps} full PIPECG iterations of {kind} n={n} after "
