@@ -282,3 +282,45 @@ def test_persistent_chunks_breakdown_mid_chunk(cuda):
         pb.pipecg_solve(A, g["b"], g["x0"], pb.JacobiPreconditioner(g["inv_diag"]),
                         _cfg(g, False), options=opts)
     assert exc.value.quantity == "alpha denominator"
+
+
+def _rp64(A):
+    """The same device matrix with int64 row pointers (the layout shards with
+    >= 2^31 nonzeros use), to run the long-long instantiations at small size."""
+    d = pb.as_device_csr(A)
+    rp = torch.empty(d.rowptr.numel(), dtype=torch.int64, device=d.rowptr.device)
+    rp.copy_(d.rowptr.to(torch.int64))
+    return pb.DeviceCsr(d.n_rows, d.n_cols, d.nnz, rp, d.col, d.val)
+
+
+@pytest.mark.parametrize("engine", ["fused-a", "fused-b", "fused-c", "fused-d", "fused-p", "two"])
+def test_int64_row_pointers_bitwise(cuda, engine):
+    A = pb.stencil_host("3d7", 20)
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=5000)
+    D = _rp64(A)
+    assert D.rp64 == 1
+    bd = torch.from_numpy(b).cuda()
+    np.testing.assert_array_equal(pb.spmv(D, torch.from_numpy(x_true).cuda()).cpu().numpy(),
+                                  oracle.spmv(A, x_true))
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=5000, record_history=True)
+    x, rep = pb.pipecg_solve(D, bd, torch.zeros_like(bd), pb.JacobiPreconditioner(d), cfg,
+                             options=pb.DeviceOptions(dot_mode="seq", engine=engine))
+    assert rep.history == ref.history
+    np.testing.assert_array_equal(x.cpu().numpy(), ref.x)
+
+
+@pytest.mark.parametrize("engine", ["fused-d", "two"])
+def test_int64_row_pointers_irregular_bitwise(cuda, engine):
+    A = pb.generate_powerlaw(2**12)  # rows up to 205 nonzeros: no hub tiles
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=2000)
+    D = _rp64(A)
+    bd = torch.from_numpy(b).cuda()
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=2000, record_history=True)
+    x, rep = pb.pipecg_solve(D, bd, torch.zeros_like(bd), pb.JacobiPreconditioner(d), cfg,
+                             options=pb.DeviceOptions(dot_mode="seq", engine=engine))
+    assert rep.history == ref.history
+    np.testing.assert_array_equal(x.cpu().numpy(), ref.x)
