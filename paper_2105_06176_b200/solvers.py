@@ -400,13 +400,18 @@ def pipecg_solve(A, b, x0, pc, cfg: SolverConfig | None = None, *,
                               phase_times={"setup": 0.0, "iterations": 0.0},
                               drift_history=[] if cfg.drift_check_interval > 0 else None)
     require_cuda()
+    nvtx = torch.cuda.nvtx  # ranges for nsys / Nsight timelines (no-ops otherwise)
+    nvtx.range_push("pipecg.setup")
     solver = _solver_for(A, pc, options)
     bd, x0d = to_device_f64(b), to_device_f64(x0)
     solver.init(bd, x0d, cfg.tolerance, cfg.max_iterations, cfg.drift_check_interval)
     torch.cuda.synchronize()
+    nvtx.range_pop()
     t_setup = time.perf_counter()
+    nvtx.range_push("pipecg.iterations")
     res, hist, d_it, d_val = solver.run(cfg.record_history, cfg.max_iterations,
                                         cfg.drift_check_interval)
+    nvtx.range_pop()
     t_end = time.perf_counter()
     if res.status == _lib.PCG_BREAKDOWN:
         raise SolverBreakdown(_lib.BREAKDOWN_QUANTITY[res.breakdown_quantity],
