@@ -31,6 +31,7 @@
 #include <stdint.h>
 
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_radix_sort.cuh>
 
 #include <algorithm>
 #include <climits>
@@ -1369,6 +1370,85 @@ __global__ void __launch_bounds__(256) gated_spmv_rows(const Ctrl* C, long long 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Engine 2's K2 in SELL-C-sigma layout (irregular rows): rows sorted by
+// length inside windows of kSellSigma rows, packed in slices of 32 rows
+// whose k-th nonzeros are contiguous (column-major inside the slice).  One
+// warp per slice, one lane per row: a warp's load of "entry k" is one
+// coalesced 256-byte segment instead of 32 scattered ones, the rows of a
+// warp have similar lengths (little divergence), and every lane still sums
+// its own row strictly in CSR order -- bitwise the reference's _spmv.
+// Rows longer than kLongRow keep the block-per-row kernel (slen = -1 here).
+constexpr int kSellSigma = 1024;
+
+__global__ void __launch_bounds__(256) sell_spmv_kernel(const Ctrl* C, long long n, long long n_slices,
+                                                         const long long* __restrict__ sptr,
+                                                         const int* __restrict__ perm,
+                                                         const int* __restrict__ slen,
+                                                         const int* __restrict__ col,
+                                                         const double* __restrict__ val,
+                                                         const double* __restrict__ x,
+                                                         double* __restrict__ y) {
+  if (C && read_status(C) != PCG_RUNNING) return;
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long sl = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); sl < n_slices;
+       sl += warps) {
+    const long long p = sl * 32 + lane;
+    const bool valid = p < n;
+    const int r = valid ? perm[p] : 0;
+    const int len = valid ? slen[p] : -1;
+    int L = max(len, 0);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) L = max(L, __shfl_xor_sync(0xffffffffu, L, o));
+    const long long base = sptr[sl] + lane;
+    double acc = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < L; ++k)
+      if (k < len) acc = add(acc, mul(ldg_nc(val + base + 32LL * k), ldg_nc(x + ldg_nc(col + base + 32LL * k))));
+    if (valid && len >= 0) y[r] = acc;
+  }
+}
+
+// SELL build (setup): sort keys, slice widths, packing
+template <typename RP>
+__global__ void sell_keys_kernel(long long n, const RP* rp, long long thr, int* key, int* idx) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long len = (long long)rp[i + 1] - rp[i];
+    key[i] = len > thr ? (int)thr + 1 : (int)(thr - len);  // ascending key = descending length, long last
+    idx[i] = (int)i;
+  }
+}
+
+template <typename RP>
+__global__ void sell_len_kernel(long long n, const RP* rp, long long thr, const int* perm, int* slen,
+                                long long n_slices, long long* width) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int r = perm[p];
+    const long long len = (long long)rp[r + 1] - rp[r];
+    slen[p] = len > thr ? -1 : (int)len;
+    if ((p & 31) == 0) width[p >> 5] = 32LL * (len > thr ? 0 : len);  // first = longest of the slice
+  }
+}
+
+template <typename RP>
+__global__ void sell_fill_kernel(long long n, const RP* rp, const int* col, const double* val,
+                                 const int* perm, const int* slen, const long long* sptr,
+                                 int* col_s, double* val_s) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int len = slen[p];
+    if (len <= 0) continue;
+    const long long src = rp[perm[p]], dst = sptr[p >> 5] + (p & 31);
+    for (int k = 0; k < len; ++k) {
+      col_s[dst + 32LL * k] = col[src + k];
+      val_s[dst + 32LL * k] = val[src + k];
+    }
+  }
+}
+
 template <typename RP>
 __global__ void __launch_bounds__(256) gated_spmv_long(const Ctrl* C, const int* __restrict__ rows,
                                                         const RP* __restrict__ rp,
@@ -1793,6 +1873,14 @@ struct pcg_solver {
   bool pdl = true;                 // programmatic dependent launch of the fused kernels
   bool fused_xchg = false;         // distributed: halo + partial push inside the fused kernel
   unsigned long long* gbar = nullptr;  // variant P grid-barrier counter
+  // engine-2 K2 in SELL-C-sigma layout (irregular matrices)
+  bool sell = false;
+  long long sell_slices = 0;
+  long long* sell_ptr = nullptr;
+  int* sell_perm = nullptr;
+  int* sell_len = nullptr;
+  int* sell_col = nullptr;
+  double* sell_val = nullptr;
   int* x_ptr = nullptr;            // its per-tile send lists (sorted by row)
   int* x_row = nullptr;
   int* x_peer = nullptr;
@@ -2277,7 +2365,21 @@ int enqueue_step(pcg_solver* S, int k) {
         S->cp, R.C, k, use_fin(S) ? S->fin : S->partials, use_fin(S) ? 1 : S->grid,
         stored_m_fused(S) ? S->m : S->w[0],
         stored_m_fused(S) ? S->m2 : S->w[1], stored_m_fused(S) ? 9 : 7, stored_m_fused(S) ? 12 : 8);
-  if (S->engine == 2) {
+  if (S->engine == 2 && S->sell) {
+    sell_spmv_kernel<<<elementwise_grid(S->sell_slices * 32), 256, 0, st>>>(
+        R.C, n, S->sell_slices, S->sell_ptr, S->sell_perm, S->sell_len, S->sell_col, S->sell_val,
+        S->m, S->nv);
+    if (S->n_long > 0) {
+      if (S->A.rp64)
+        gated_spmv_long<long long><<<(unsigned)S->n_long, 256, 0, st>>>(
+            R.C, S->long_rows, static_cast<const long long*>(S->A.rowptr), S->A.col, S->A.val, S->m,
+            S->nv);
+      else
+        gated_spmv_long<int><<<(unsigned)S->n_long, 256, 0, st>>>(
+            R.C, S->long_rows, static_cast<const int*>(S->A.rowptr), S->A.col, S->A.val, S->m,
+            S->nv);
+    }
+  } else if (S->engine == 2) {
     const long long thr = S->n_long > 0 ? kLongRow : INT64_MAX;
     if (S->A.rp64) {
       gated_spmv_rows<long long><<<elementwise_grid(n), 256, 0, st>>>(
@@ -2446,7 +2548,8 @@ int preload_solver() {
   PCG_LOAD(tile_build_kernel<int>); PCG_LOAD(tile_build_kernel<long long>); PCG_LOAD(tile_close_kernel);
 
   PCG_LOAD(pipecg_k1_kernel); PCG_LOAD(gated_spmv_rows<int>); PCG_LOAD(gated_spmv_rows<long long>);
-  PCG_LOAD(gated_spmv_long<int>); PCG_LOAD(gated_spmv_long<long long>); PCG_LOAD(seq_dots_kernel);
+  PCG_LOAD(gated_spmv_long<int>); PCG_LOAD(gated_spmv_long<long long>);
+  PCG_LOAD(sell_spmv_kernel); PCG_LOAD(seq_dots_kernel);
   PCG_LOAD(drift_partial_kernel<int>); PCG_LOAD(drift_partial_kernel<long long>);
   PCG_LOAD(drift_finish_kernel); PCG_LOAD(advance_kernel); PCG_LOAD(init_ctrl_kernel);
   PCG_LOAD(iter_exchange_kernel); PCG_LOAD(vec_exchange_kernel);
@@ -2505,6 +2608,77 @@ __global__ void fill_kernel(double* p, long long n, double v) {
 // test) of every engine/variant that fits this matrix on this GPU and keep
 // the fastest.  Costs ~10 iterations once per solver; the state is
 // re-initialised by the caller's solver_init.
+__global__ void seg_offsets_kernel(long long n, int sigma, long long n_seg, int* offs) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k <= n_seg;
+       k += (long long)gridDim.x * blockDim.x)
+    offs[k] = (int)(k * sigma < n ? k * sigma : n);
+}
+
+// SELL-C-sigma copy of the matrix for engine 2's K2 (see sell_spmv_kernel)
+template <typename RP>
+int build_sell(pcg_solver* S) {
+  const long long n = S->A.n_rows;
+  const long long n_seg = (n + kSellSigma - 1) / kSellSigma;
+  const long long n_slices = (n + 31) / 32;
+  cudaStream_t st = S->stream;
+  const RP* rp = static_cast<const RP*>(S->A.rowptr);
+  int *key = nullptr, *key2 = nullptr, *idx = nullptr, *offs = nullptr;
+  long long* width = nullptr;
+  void* tmp = nullptr;
+  size_t b1 = 0, b2 = 0;
+  int rc = PCG_OK;
+  auto fail = [&](const char* w) { rc = set_error(PCG_ENOMEM, w); };
+  if (cudaMalloc(&key, n * 4) != cudaSuccess || cudaMalloc(&key2, n * 4) != cudaSuccess ||
+      cudaMalloc(&idx, n * 4) != cudaSuccess || cudaMalloc(&offs, (n_seg + 1) * 4) != cudaSuccess ||
+      cudaMalloc(&width, (n_slices + 1) * 8) != cudaSuccess ||
+      cudaMalloc(&S->sell_perm, n * 4) != cudaSuccess || cudaMalloc(&S->sell_len, n * 4) != cudaSuccess ||
+      cudaMalloc(&S->sell_ptr, (n_slices + 1) * 8) != cudaSuccess)
+    fail("SELL build workspace");
+  if (!rc) {
+    const unsigned g = elementwise_grid(n);
+    sell_keys_kernel<RP><<<g, 256, 0, st>>>(n, rp, kLongRow, key, idx);
+    seg_offsets_kernel<<<elementwise_grid(n_seg + 1), 256, 0, st>>>(n, kSellSigma, n_seg, offs);
+    int bits = 1;
+    while ((1LL << bits) <= kLongRow + 1) ++bits;
+    cub::DeviceSegmentedRadixSort::SortPairs(nullptr, b1, key, key2, idx, S->sell_perm, (int)n,
+                                             (int)n_seg, offs, offs + 1, 0, bits, st);
+    cub::DeviceScan::ExclusiveSum(nullptr, b2, width, S->sell_ptr, n_slices + 1, st);
+    if (cudaMalloc(&tmp, std::max(b1, b2)) != cudaSuccess) fail("SELL sort workspace");
+    if (!rc) {
+      size_t bt = std::max(b1, b2);
+      cub::DeviceSegmentedRadixSort::SortPairs(tmp, bt, key, key2, idx, S->sell_perm, (int)n,
+                                               (int)n_seg, offs, offs + 1, 0, bits, st);
+      cudaMemsetAsync(width, 0, (n_slices + 1) * 8, st);
+      sell_len_kernel<RP><<<g, 256, 0, st>>>(n, rp, kLongRow, S->sell_perm, S->sell_len, n_slices,
+                                             width);
+      bt = std::max(b1, b2);
+      cub::DeviceScan::ExclusiveSum(tmp, bt, width, S->sell_ptr, n_slices + 1, st);
+      long long total = 0;
+      cudaMemcpyAsync(&total, S->sell_ptr + n_slices, 8, cudaMemcpyDeviceToHost, st);
+      rc = cuda_status(cudaStreamSynchronize(st), "SELL build");
+      if (!rc && (cudaMalloc(&S->sell_col, (total + 64) * 4) != cudaSuccess ||
+                  cudaMalloc(&S->sell_val, (total + 64) * 8) != cudaSuccess))
+        fail("SELL arrays");
+      if (!rc) {
+        sell_fill_kernel<RP><<<g, 256, 0, st>>>(n, rp, S->A.col, S->A.val, S->sell_perm,
+                                                S->sell_len, S->sell_ptr, S->sell_col, S->sell_val);
+        rc = cuda_status(cudaStreamSynchronize(st), "SELL fill");
+      }
+    }
+  }
+  cudaFree(key);
+  cudaFree(key2);
+  cudaFree(idx);
+  cudaFree(offs);
+  cudaFree(width);
+  cudaFree(tmp);
+  if (!rc) {
+    S->sell = true;
+    S->sell_slices = n_slices;
+  }
+  return rc;
+}
+
 struct TuneKey {
   int dev;
   long long n_rows, n_cols, nnz;
@@ -2682,6 +2856,17 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
       }
     }
   }
+  {  // engine 2 on irregular rows reads a SELL-C-sigma copy (coalesced K2)
+    bool want = has_long && (req == 0 || req == 2 || !fused_ok);
+    if (const char* e = getenv("PIPECG_B200_SELL")) want = atoi(e) != 0 && (req == 0 || req == 2 || !fused_ok);
+    if (want) {
+      rc = A->rp64 ? build_sell<long long>(S) : build_sell<int>(S);
+      if (rc) {
+        pipecg_b200_solver_destroy(S);
+        return rc;
+      }
+    }
+  }
   const int grid2 = std::min<int>(kDotGrid, 4 * S->num_sms);
   S->grid = grid2;
   for (int v = 0; v < kVariants; ++v) S->grid = std::max(S->grid, S->plans[v].grid);
@@ -2764,6 +2949,11 @@ int pipecg_b200_solver_destroy(pcg_solver* S) {
   cudaFree(S->rec_dev);
   cudaFree(S->comm);
   cudaFree(S->long_rows);
+  cudaFree(S->sell_ptr);
+  cudaFree(S->sell_perm);
+  cudaFree(S->sell_len);
+  cudaFree(S->sell_col);
+  cudaFree(S->sell_val);
   cudaFree(S->x_ptr);
   cudaFree(S->x_row);
   cudaFree(S->x_peer);

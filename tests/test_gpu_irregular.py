@@ -121,3 +121,21 @@ def test_random_spd_tiles_bitwise(cuda, monkeypatch, dcap, max_len, engine):
     else:
         assert_within_envelope(x, rep, ref.iterations, ref.history, ref.x,
                                envelope(A, b, x0, d, tol, 3000))
+
+
+@pytest.mark.parametrize("n", [2**12, 3000])
+def test_sell_layout_bitwise(cuda, monkeypatch, n):
+    """Engine 2's SELL-C-sigma SpMV (rows length-sorted inside 1024-row
+    windows, 32-row column-major slices): every row still summed in CSR order,
+    so a sequential-dot solve is bitwise the reference's (incl. a ragged
+    last slice and window)."""
+    monkeypatch.setenv("PIPECG_B200_SELL", "1")
+    A = pb.generate_powerlaw(n) if n == 2**12 else _random_spd(n, 30, seed=4)
+    assert A.row_nnz().max() <= 256
+    b, x0, d, tol = _problem(A)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=3000)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=3000, record_history=True)
+    x, rep = pb.pipecg_solve(A, b, x0, pb.jacobi_setup(A), cfg,
+                             options=pb.DeviceOptions(dot_mode="seq", engine="two"))
+    assert rep.history == ref.history
+    np.testing.assert_array_equal(x, ref.x)
