@@ -1449,6 +1449,68 @@ __global__ void sell_fill_kernel(long long n, const RP* rp, const int* col, cons
   }
 }
 
+// Long rows split into chunks of at most kChunkNnz nonzeros, one CTA per
+// chunk (hub rows of 49k nonzeros no longer serialise one CTA): each CTA
+// reduces its chunk with a fixed tree; a row's last chunk to finish (atomic
+// ticket) sums the chunk partials in chunk order.  Deterministic.
+constexpr long long kChunkNnz = 2048;
+
+struct LongChunk {
+  long long lo, hi;  // nonzero range
+  int row;           // matrix row
+  int first;         // index of the row's first chunk
+  int n;             // chunks of this row
+  int slot;          // ticket counter of the row (multi-chunk rows)
+};
+
+__global__ void __launch_bounds__(256) gated_spmv_chunks(const Ctrl* C, const LongChunk* __restrict__ ch,
+                                                          const int* __restrict__ col,
+                                                          const double* __restrict__ val,
+                                                          const double* __restrict__ x,
+                                                          double* __restrict__ y, double* part,
+                                                          unsigned* ticket) {
+  __shared__ double red[9];
+  __shared__ int last;
+  if (cta_iteration(C, 0) < 0) return;
+  const LongChunk c = ch[blockIdx.x];
+  double v[1] = {0.0};
+  for (long long k0 = c.lo + threadIdx.x; k0 < c.hi; k0 += 4 * 256) {
+    double a[4], xv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long k = k0 + 256LL * u;
+      a[u] = 0.0;
+      xv[u] = 0.0;
+      if (k < c.hi) {
+        a[u] = ldg_nc(val + k);
+        xv[u] = ldg_nc(x + ldg_nc(col + k));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (k0 + 256LL * u < c.hi) v[0] = add(v[0], mul(a[u], xv[u]));
+  }
+  group_sum<1, 256>(v, threadIdx.x, red, 1);
+  if (c.n == 1) {
+    if (threadIdx.x == 0) y[c.row] = v[0];
+    return;
+  }
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = v[0];
+    __threadfence();
+    last = atomicAdd(ticket + c.slot, 1u) == (unsigned)(c.n - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    double s = 0.0;
+    for (int j = 0; j < c.n; ++j) s = add(s, __ldcg(part + c.first + j));
+    y[c.row] = s;
+    ticket[c.slot] = 0u;  // next iteration (stream-ordered)
+  }
+}
+
 template <typename RP>
 __global__ void __launch_bounds__(256) gated_spmv_long(const Ctrl* C, const int* __restrict__ rows,
                                                         const RP* __restrict__ rp,
@@ -1854,6 +1916,10 @@ struct pcg_solver {
   char* comm = nullptr;        // distributed exchange block (IPC-exported)
   int* long_rows = nullptr;
   long long n_long = 0;
+  LongChunk* chunks = nullptr;     // engine 2: long rows as nnz-bounded chunks
+  long long n_chunks = 0;
+  double* chunk_part = nullptr;
+  unsigned* chunk_ticket = nullptr;
   std::map<int, cudaGraphExec_t> graphs[2];
   long long host_base = 0;  // iterations enqueued so far
   bool initialized = false;
@@ -2369,7 +2435,11 @@ int enqueue_step(pcg_solver* S, int k) {
     sell_spmv_kernel<<<elementwise_grid(S->sell_slices * 32), 256, 0, st>>>(
         R.C, n, S->sell_slices, S->sell_ptr, S->sell_perm, S->sell_len, S->sell_col, S->sell_val,
         S->m, S->nv);
-    if (S->n_long > 0) {
+    if (S->n_chunks > 0) {
+      gated_spmv_chunks<<<(unsigned)S->n_chunks, 256, 0, st>>>(R.C, S->chunks, S->A.col, S->A.val,
+                                                               S->m, S->nv, S->chunk_part,
+                                                               S->chunk_ticket);
+    } else if (S->n_long > 0) {
       if (S->A.rp64)
         gated_spmv_long<long long><<<(unsigned)S->n_long, 256, 0, st>>>(
             R.C, S->long_rows, static_cast<const long long*>(S->A.rowptr), S->A.col, S->A.val, S->m,
@@ -2549,7 +2619,7 @@ int preload_solver() {
 
   PCG_LOAD(pipecg_k1_kernel); PCG_LOAD(gated_spmv_rows<int>); PCG_LOAD(gated_spmv_rows<long long>);
   PCG_LOAD(gated_spmv_long<int>); PCG_LOAD(gated_spmv_long<long long>);
-  PCG_LOAD(sell_spmv_kernel); PCG_LOAD(seq_dots_kernel);
+  PCG_LOAD(sell_spmv_kernel); PCG_LOAD(gated_spmv_chunks); PCG_LOAD(seq_dots_kernel);
   PCG_LOAD(drift_partial_kernel<int>); PCG_LOAD(drift_partial_kernel<long long>);
   PCG_LOAD(drift_finish_kernel); PCG_LOAD(advance_kernel); PCG_LOAD(init_ctrl_kernel);
   PCG_LOAD(iter_exchange_kernel); PCG_LOAD(vec_exchange_kernel);
@@ -2608,6 +2678,54 @@ __global__ void fill_kernel(double* p, long long n, double v) {
 // test) of every engine/variant that fits this matrix on this GPU and keep
 // the fastest.  Costs ~10 iterations once per solver; the state is
 // re-initialised by the caller's solver_init.
+__global__ void long_len_kernel(const int* rows, long long n, const void* rp, int rp64,
+                                long long* lo, long long* hi) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long i = rows[k];
+    lo[k] = rp64 ? ((const long long*)rp)[i] : (long long)((const int*)rp)[i];
+    hi[k] = rp64 ? ((const long long*)rp)[i + 1] : (long long)((const int*)rp)[i + 1];
+  }
+}
+
+// chunk table of the long rows (setup)
+int build_long_chunks(pcg_solver* S) {
+  const long long nl = S->n_long;
+  if (nl <= 0) return PCG_OK;
+  cudaStream_t st = S->stream;
+  long long* d = nullptr;
+  if (cudaMalloc(&d, 2 * nl * sizeof(long long)) != cudaSuccess)
+    return set_error(PCG_ENOMEM, "long chunks");
+  long_len_kernel<<<elementwise_grid(nl), 256, 0, st>>>(S->long_rows, nl, S->A.rowptr, S->A.rp64, d,
+                                                        d + nl);
+  std::vector<long long> lo(nl), hi(nl);
+  std::vector<int> rows(nl);
+  cudaMemcpyAsync(lo.data(), d, nl * 8, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(hi.data(), d + nl, nl * 8, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(rows.data(), S->long_rows, nl * 4, cudaMemcpyDeviceToHost, st);
+  int rc = cuda_status(cudaStreamSynchronize(st), "long chunks");
+  cudaFree(d);
+  if (rc) return rc;
+  std::vector<LongChunk> ch;
+  int slots = 0;
+  for (long long k = 0; k < nl; ++k) {
+    const long long len = hi[k] - lo[k];
+    const int n = (int)((len + kChunkNnz - 1) / kChunkNnz);
+    const int first = (int)ch.size();
+    const int slot = n > 1 ? slots++ : -1;
+    for (int j = 0; j < n; ++j)
+      ch.push_back(LongChunk{lo[k] + len * j / n, lo[k] + len * (j + 1) / n, rows[k], first, n, slot});
+  }
+  S->n_chunks = (long long)ch.size();
+  if (cudaMalloc(&S->chunks, ch.size() * sizeof(LongChunk)) != cudaSuccess ||
+      cudaMalloc(&S->chunk_part, ch.size() * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&S->chunk_ticket, std::max(slots, 1) * sizeof(unsigned)) != cudaSuccess)
+    return set_error(PCG_ENOMEM, "long chunks");
+  cudaMemcpyAsync(S->chunks, ch.data(), ch.size() * sizeof(LongChunk), cudaMemcpyHostToDevice, st);
+  cudaMemsetAsync(S->chunk_ticket, 0, std::max(slots, 1) * sizeof(unsigned), st);
+  return cuda_status(cudaStreamSynchronize(st), "long chunks");
+}
+
 __global__ void seg_offsets_kernel(long long n, int sigma, long long n_seg, int* offs) {
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k <= n_seg;
        k += (long long)gridDim.x * blockDim.x)
@@ -2861,6 +2979,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     if (const char* e = getenv("PIPECG_B200_SELL")) want = atoi(e) != 0 && (req == 0 || req == 2 || !fused_ok);
     if (want) {
       rc = A->rp64 ? build_sell<long long>(S) : build_sell<int>(S);
+      if (!rc && !getenv("PIPECG_B200_NO_CHUNKS")) rc = build_long_chunks(S);
       if (rc) {
         pipecg_b200_solver_destroy(S);
         return rc;
@@ -2949,6 +3068,9 @@ int pipecg_b200_solver_destroy(pcg_solver* S) {
   cudaFree(S->rec_dev);
   cudaFree(S->comm);
   cudaFree(S->long_rows);
+  cudaFree(S->chunks);
+  cudaFree(S->chunk_part);
+  cudaFree(S->chunk_ticket);
   cudaFree(S->sell_ptr);
   cudaFree(S->sell_perm);
   cudaFree(S->sell_len);

@@ -425,6 +425,7 @@ class DistributedSolver:
         # blocks -> adopt rank 0's choice
         names = {3: "fused-a", 4: "fused-b", 5: "fused-c", 6: "fused-d"}
         mine = int(self.solver.poll().engine)
+        mine = 5 if mine == 7 else mine  # P runs as C once connected
         chosen = group.all_gather_object(mine)[0]
         if mine != chosen:
             self.solver.close()
