@@ -324,3 +324,26 @@ def test_int64_row_pointers_irregular_bitwise(cuda, engine):
                              options=pb.DeviceOptions(dot_mode="seq", engine=engine))
     assert rep.history == ref.history
     np.testing.assert_array_equal(x.cpu().numpy(), ref.x)
+
+
+@pytest.mark.parametrize("bad", [float("nan"), float("inf")])
+def test_non_finite_rhs_exits_like_reference(cuda, bad):
+    """solvers.py:346: a NaN norm fails `norm >= tol` and exits unconverged at
+    once; an inf norm keeps iterating until the recurrence breaks down --
+    whatever the oracle does, the GPU must do the same."""
+    A = pb.stencil_host("2d5", 20)
+    x_true, b, x0, d = oracle.manufactured(A)
+    b = b.copy()
+    b[7] = bad
+    cfg = pb.SolverConfig(tolerance=1e-8, max_iterations=50, record_history=True)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=1e-8, max_iterations=50)
+    for eng in ("fused-c", "fused-p", "two"):
+        opts = pb.DeviceOptions(dot_mode="seq", engine=eng)
+        if ref.breakdown is not None:
+            with pytest.raises(pb.SolverBreakdown) as exc:
+                pb.pipecg_solve(A, b, x0, pb.JacobiPreconditioner(d), cfg, options=opts)
+            assert (exc.value.quantity, exc.value.iteration) == ref.breakdown[:2]
+            continue
+        x, rep = pb.pipecg_solve(A, b, x0, pb.JacobiPreconditioner(d), cfg, options=opts)
+        assert rep.iterations == ref.iterations and rep.converged == ref.converged
+        np.testing.assert_array_equal(np.array(rep.history), np.array(ref.history))
