@@ -405,7 +405,7 @@ struct FusedParams {
   int stages;
   int cap_val;  // doubles per stage
   int cap_col;  // ints per stage
-  int flags;    // experiment switches (PIPECG_B200_FLAGS): 2 = contiguous tile ranges per CTA
+  int flags;    // experiment switches (PIPECG_B200_FLAGS): 1 = gathers read the row itself, 2 = contiguous tile ranges
   FusedXchg X;                // fused peer exchange (X.ptr == nullptr: off)
   // variant D (nnz-balanced tiles)
   const int* tile_row;        // [n_tiles + 1] first row of each tile
@@ -813,7 +813,7 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_a(FusedParams<RP>
         for (int t = 0; t < 8; ++t) {
           const long long k = k0 + t;
           if (k < hi) {
-            const int c = col_s[k - cb];
+            const int c = (P.flags & 1) ? (int)i : col_s[k - cb];
             av[t] = val_s[k - vb];
             mv[t] = MG ? ldg_nc(P.m[it & 1] + c)                      // stored m
                        : mul(ldg_nc(P.dinv + c), ldg_nc(w_old + c));  // m = M^-1 w
