@@ -1951,6 +1951,7 @@ struct pcg_solver {
   bool irregular = false;          // some row longer than kLongRow
   bool pdl = true;                 // programmatic dependent launch of the fused kernels
   bool fused_xchg = false;         // distributed: halo + partial push inside the fused kernel
+  bool p_mg = true;                // variant P gathers the stored m (C) or dinv*w (A)
   unsigned long long* gbar = nullptr;  // variant P grid-barrier counter
   // engine-2 K2 in SELL-C-sigma layout (irregular matrices)
   bool sell = false;
@@ -2501,10 +2502,18 @@ int launch_persistent(pcg_solver* S, int K) {
   cfg.numAttrs = 1;
   unsigned long long* gbar = S->gbar;
   cudaError_t e;
-  switch (S->tr) {
-    case 256: e = cudaLaunchKernelEx(&cfg, pipecg_fused_kernel_p<RP, 256, true>, P, K, gbar); break;
-    case 128: e = cudaLaunchKernelEx(&cfg, pipecg_fused_kernel_p<RP, 128, true>, P, K, gbar); break;
-    default: e = cudaLaunchKernelEx(&cfg, pipecg_fused_kernel_p<RP, 64, true>, P, K, gbar); break;
+  if (S->p_mg) {
+    switch (S->tr) {
+      case 256: e = cudaLaunchKernelEx(&cfg, pipecg_fused_kernel_p<RP, 256, true>, P, K, gbar); break;
+      case 128: e = cudaLaunchKernelEx(&cfg, pipecg_fused_kernel_p<RP, 128, true>, P, K, gbar); break;
+      default: e = cudaLaunchKernelEx(&cfg, pipecg_fused_kernel_p<RP, 64, true>, P, K, gbar); break;
+    }
+  } else {
+    switch (S->tr) {
+      case 256: e = cudaLaunchKernelEx(&cfg, pipecg_fused_kernel_p<RP, 256, false>, P, K, gbar); break;
+      case 128: e = cudaLaunchKernelEx(&cfg, pipecg_fused_kernel_p<RP, 128, false>, P, K, gbar); break;
+      default: e = cudaLaunchKernelEx(&cfg, pipecg_fused_kernel_p<RP, 64, false>, P, K, gbar); break;
+    }
   }
   return cuda_status(e, "persistent launch");
 }
@@ -2622,6 +2631,9 @@ int preload_solver() {
   PCG_LOAD_X(int, 256); PCG_LOAD_X(int, 128); PCG_LOAD_X(int, 64);
   PCG_LOAD_X(long long, 256); PCG_LOAD_X(long long, 128); PCG_LOAD_X(long long, 64);
 #undef PCG_LOAD_X
+  PCG_LOAD((pipecg_fused_kernel_p<int, 256, false>)); PCG_LOAD((pipecg_fused_kernel_p<int, 128, false>));
+  PCG_LOAD((pipecg_fused_kernel_p<int, 64, false>)); PCG_LOAD((pipecg_fused_kernel_p<long long, 256, false>));
+  PCG_LOAD((pipecg_fused_kernel_p<long long, 128, false>)); PCG_LOAD((pipecg_fused_kernel_p<long long, 64, false>));
   PCG_LOAD((pipecg_fused_kernel_p<int, 256, true>)); PCG_LOAD((pipecg_fused_kernel_p<int, 128, true>));
   PCG_LOAD((pipecg_fused_kernel_p<int, 64, true>)); PCG_LOAD((pipecg_fused_kernel_p<long long, 256, true>));
   PCG_LOAD((pipecg_fused_kernel_p<long long, 128, true>)); PCG_LOAD((pipecg_fused_kernel_p<long long, 64, true>));
@@ -2658,6 +2670,9 @@ int preload_solver() {
   PCG_SMEM_X(int, 256); PCG_SMEM_X(int, 128); PCG_SMEM_X(int, 64);
   PCG_SMEM_X(long long, 256); PCG_SMEM_X(long long, 128); PCG_SMEM_X(long long, 64);
 #undef PCG_SMEM_X
+  PCG_SMEM((pipecg_fused_kernel_p<int, 256, false>)); PCG_SMEM((pipecg_fused_kernel_p<int, 128, false>));
+  PCG_SMEM((pipecg_fused_kernel_p<int, 64, false>)); PCG_SMEM((pipecg_fused_kernel_p<long long, 256, false>));
+  PCG_SMEM((pipecg_fused_kernel_p<long long, 128, false>)); PCG_SMEM((pipecg_fused_kernel_p<long long, 64, false>));
   PCG_SMEM((pipecg_fused_kernel_p<int, 256, true>)); PCG_SMEM((pipecg_fused_kernel_p<int, 128, true>));
   PCG_SMEM((pipecg_fused_kernel_p<int, 64, true>)); PCG_SMEM((pipecg_fused_kernel_p<long long, 256, true>));
   PCG_SMEM((pipecg_fused_kernel_p<long long, 128, true>)); PCG_SMEM((pipecg_fused_kernel_p<long long, 64, true>));
@@ -2908,6 +2923,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   S->A = *A;
   if (const char* f = getenv("PIPECG_B200_FLAGS")) S->flags = atoi(f);
   if (getenv("PIPECG_B200_NO_PDL")) S->pdl = false;
+  if (const char* e = getenv("PIPECG_B200_PA")) S->p_mg = atoi(e) == 0;  // experiment switch
   if (opts) S->opt = *opts;
   else {
     S->opt.dot_mode = PCG_DOT_TREE;
