@@ -1394,6 +1394,7 @@ __global__ void __launch_bounds__(256) gated_spmv_rows(const Ctrl* C, long long 
 // Rows longer than kLongRow keep the block-per-row kernel (slen = -1 here).
 constexpr int kSellSigma = 1024;
 
+template <int SB>
 __global__ void __launch_bounds__(256) sell_spmv_kernel(const Ctrl* C, long long n, long long n_slices,
                                                          const long long* __restrict__ sptr,
                                                          const int* __restrict__ perm,
@@ -1416,9 +1417,21 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(const Ctrl* C, long long
     for (int o = 16; o >= 1; o >>= 1) L = max(L, __shfl_xor_sync(0xffffffffu, L, o));
     const long long base = sptr[sl] + lane;
     double acc = 0.0;
-#pragma unroll 4
-    for (int k = 0; k < L; ++k)
-      if (k < len) acc = add(acc, mul(ldg_nc(val + base + 32LL * k), ldg_nc(x + ldg_nc(col + base + 32LL * k))));
+    for (int k0 = 0; k0 < L; k0 += SB) {  // batches: indices + values, gathers, ordered adds
+      int c[SB];
+      double a[SB], xv[SB];
+#pragma unroll
+      for (int u = 0; u < SB; ++u) {
+        const bool on = k0 + u < len;
+        c[u] = on ? ldg_nc(col + base + 32LL * (k0 + u)) : 0;
+        a[u] = on ? ldg_nc(val + base + 32LL * (k0 + u)) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < SB; ++u) xv[u] = k0 + u < len ? ldg_nc(x + c[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < SB; ++u)
+        if (k0 + u < len) acc = add(acc, mul(a[u], xv[u]));
+    }
     if (valid && len >= 0) y[r] = acc;
   }
 }
@@ -1955,6 +1968,7 @@ struct pcg_solver {
   unsigned long long* gbar = nullptr;  // variant P grid-barrier counter
   // engine-2 K2 in SELL-C-sigma layout (irregular matrices)
   bool sell = false;
+  int sell_batch = 2;              // nonzeros per lane per load batch in the SELL K2 (2 ~ 4 > 8, measured)
   long long sell_slices = 0;
   long long* sell_ptr = nullptr;
   int* sell_perm = nullptr;
@@ -2446,7 +2460,9 @@ int enqueue_step(pcg_solver* S, int k) {
         stored_m_fused(S) ? S->m : S->w[0],
         stored_m_fused(S) ? S->m2 : S->w[1], stored_m_fused(S) ? 9 : 7, stored_m_fused(S) ? 12 : 8);
   if (S->engine == 2 && S->sell) {
-    sell_spmv_kernel<<<elementwise_grid(S->sell_slices * 32), 256, 0, st>>>(
+    auto sk = S->sell_batch == 8 ? sell_spmv_kernel<8> : S->sell_batch == 2 ? sell_spmv_kernel<2>
+                                                                            : sell_spmv_kernel<4>;
+    sk<<<elementwise_grid(S->sell_slices * 32), 256, 0, st>>>(
         R.C, n, S->sell_slices, S->sell_ptr, S->sell_perm, S->sell_len, S->sell_col, S->sell_val,
         S->m, S->nv);
     if (S->n_chunks > 0) {
@@ -2644,7 +2660,8 @@ int preload_solver() {
 
   PCG_LOAD(pipecg_k1_kernel); PCG_LOAD(gated_spmv_rows<int>); PCG_LOAD(gated_spmv_rows<long long>);
   PCG_LOAD(gated_spmv_long<int>); PCG_LOAD(gated_spmv_long<long long>);
-  PCG_LOAD(sell_spmv_kernel); PCG_LOAD(gated_spmv_chunks); PCG_LOAD(seq_dots_kernel);
+  PCG_LOAD(sell_spmv_kernel<2>); PCG_LOAD(sell_spmv_kernel<4>); PCG_LOAD(sell_spmv_kernel<8>);
+  PCG_LOAD(gated_spmv_chunks); PCG_LOAD(seq_dots_kernel);
   PCG_LOAD(drift_partial_kernel<int>); PCG_LOAD(drift_partial_kernel<long long>);
   PCG_LOAD(drift_finish_kernel); PCG_LOAD(advance_kernel); PCG_LOAD(init_ctrl_kernel);
   PCG_LOAD(iter_exchange_kernel); PCG_LOAD(vec_exchange_kernel);
@@ -2923,6 +2940,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   S->A = *A;
   if (const char* f = getenv("PIPECG_B200_FLAGS")) S->flags = atoi(f);
   if (getenv("PIPECG_B200_NO_PDL")) S->pdl = false;
+  if (const char* e = getenv("PIPECG_B200_SELL_BATCH")) S->sell_batch = atoi(e);  // experiment
   if (const char* e = getenv("PIPECG_B200_PA")) S->p_mg = atoi(e) == 0;  // experiment switch
   if (opts) S->opt = *opts;
   else {
