@@ -35,7 +35,7 @@ def _cfg(g, record=True):
 CASES = [c for c in META["cases"] if c != "p125n6_pcg"]
 
 
-@pytest.mark.parametrize("engine", ["fused-a", "fused-b", "fused-c", "fused-d", "two"])
+@pytest.mark.parametrize("engine", ["fused-a", "fused-b", "fused-c", "fused-d", "fused-p", "two"])
 @pytest.mark.parametrize("case", CASES)
 def test_golden_bitwise_seq_mode(cuda, case, engine):
     """dot_mode='seq' reproduces the reference solve bit for bit."""
@@ -86,7 +86,7 @@ def assert_within_envelope(x, rep, ref_iters, ref_hist, ref_x, env):
     assert rel <= max(1e-8, 3 * x_gap), (rel, env)
 
 
-@pytest.mark.parametrize("engine", ["fused-a", "fused-b", "fused-c", "fused-d", "two"])
+@pytest.mark.parametrize("engine", ["fused-a", "fused-b", "fused-c", "fused-d", "fused-p", "two"])
 @pytest.mark.parametrize("case", CASES)
 def test_golden_tree_mode_tolerance(cuda, case, engine):
     """Default (tree dots): iterations, history and x within the larger of the
@@ -311,8 +311,9 @@ def test_int64_row_pointers_bitwise(cuda, engine):
     np.testing.assert_array_equal(x.cpu().numpy(), ref.x)
 
 
-@pytest.mark.parametrize("engine", ["fused-d", "two"])
-def test_int64_row_pointers_irregular_bitwise(cuda, engine):
+@pytest.mark.parametrize("engine,sell", [("fused-d", "0"), ("two", "0"), ("two", "1")])
+def test_int64_row_pointers_irregular_bitwise(cuda, monkeypatch, engine, sell):
+    monkeypatch.setenv("PIPECG_B200_SELL", sell)
     A = pb.generate_powerlaw(2**12)  # rows up to 205 nonzeros: no hub tiles
     x_true, b, x0, d = oracle.manufactured(A)
     tol = oracle.recipe_tolerance(A, b, d)
