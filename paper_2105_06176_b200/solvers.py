@@ -440,12 +440,16 @@ def true_residual_norm(A, x, b) -> float:
     return norm2(residual(A, x, b))
 
 
-def pcg_solve(A, b, x0, pc, cfg: SolverConfig | None = None):
+def pcg_solve(A, b, x0, pc, cfg: SolverConfig | None = None, *,
+              options: DeviceOptions | None = None):
     """Classic PCG (solvers.py:195-273) composed from the device operators.
 
     The reference's baseline algorithm; each
-    iteration synchronises once for its two dot products."""
+    iteration synchronises once for its dot products.  ``options.dot_mode``
+    as in :func:`pipecg_solve`: "tree" (default) or "seq" (the reference's
+    order: bitwise-identical history)."""
     cfg = cfg or SolverConfig()
+    mode = (options or DeviceOptions()).dot_mode
     t_start = time.perf_counter()
     _check_system(A, b, x0)
     on_dev = is_device_tensor(b)
@@ -456,10 +460,10 @@ def pcg_solve(A, b, x0, pc, cfg: SolverConfig | None = None):
     u = jacobi_apply(pc, r)
     p = torch.zeros_like(u)
     s = torch.empty_like(u)
-    gamma = dot(r, u)
+    gamma = dot(r, u, mode)
     gamma_prev = 0.0
-    norm = math.sqrt(dot(u, u))
-    b_norm = norm2(bd)
+    norm = math.sqrt(dot(u, u, mode))
+    b_norm = norm2(bd, mode)
     history = [norm] if cfg.record_history else None
     drift = [] if cfg.drift_check_interval > 0 else None
     t_setup = time.perf_counter()
@@ -469,7 +473,7 @@ def pcg_solve(A, b, x0, pc, cfg: SolverConfig | None = None):
         p.mul_(beta)  # np.multiply(p, beta, out=p)
         p.add_(u)
         spmv(A, p, out=s)
-        delta = dot(s, p)
+        delta = dot(s, p, mode)
         if delta <= 0.0 or not math.isfinite(delta):
             raise SolverBreakdown("delta", it, delta)
         alpha = gamma / delta
@@ -477,7 +481,7 @@ def pcg_solve(A, b, x0, pc, cfg: SolverConfig | None = None):
         r.sub_(alpha * s)
         jacobi_apply(pc, r, out=u)
         gamma_prev = gamma
-        gamma, uu = dots([(u, r), (u, u)], mode="seq")
+        gamma, uu = dots([(u, r), (u, u)], mode=mode)
         if gamma < 0.0 or not math.isfinite(gamma):
             raise SolverBreakdown("gamma", it, gamma)
         norm = math.sqrt(uu)
@@ -486,7 +490,7 @@ def pcg_solve(A, b, x0, pc, cfg: SolverConfig | None = None):
             history.append(norm)
         if drift is not None and it % cfg.drift_check_interval == 0:
             resid = residual(A, x, bd)
-            dv = norm2(resid - r)
+            dv = norm2(resid - r, mode)
             drift.append([it, dv / b_norm if b_norm > 0 else dv])
     t_end = time.perf_counter()
     report = SolveReport(

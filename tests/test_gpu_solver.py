@@ -348,3 +348,35 @@ def test_non_finite_rhs_exits_like_reference(cuda, bad):
         x, rep = pb.pipecg_solve(A, b, x0, pb.JacobiPreconditioner(d), cfg, options=opts)
         assert rep.iterations == ref.iterations and rep.converged == ref.converged
         np.testing.assert_array_equal(np.array(rep.history), np.array(ref.history))
+
+
+def test_pcg_solve_golden_bitwise_seq(cuda):
+    """Classic PCG (solvers.py:195-273) on the device operators, sequential
+    dots: the reference's own 5-iteration history bit for bit."""
+    g = load_golden("solve_p125n6_pcg.npz")
+    m = META["cases"]["p125n6_pcg"]
+    A = golden_matrix(g)
+    x, rep = pb.pcg_solve(A, g["b"], g["x0"], pb.JacobiPreconditioner(g["inv_diag"]),
+                          _cfg(g), options=pb.DeviceOptions(dot_mode="seq"))
+    assert rep.strategy == "pcg" and rep.iterations == m["iterations"]
+    np.testing.assert_array_equal(np.array(rep.history), g["history"])
+    np.testing.assert_array_equal(x, g["x"])
+
+
+@pytest.mark.parametrize("kind,n", [("3d7", 24), ("2d5", 100)])
+def test_pcg_solve_tree_vs_oracle_and_pipecg(cuda, kind, n):
+    """Tree dots within the oracle's envelope; PCG and PIPECG histories agree
+    over the first 20 iterations (acceptance #4, test_acceptance.py:136-154)."""
+    A = pb.stencil_host(kind, n)
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    ref = oracle.pcg_solve(A, b, x0, d, tol=tol, max_iterations=5000)
+    ref2 = oracle.pcg_solve(A, b, x0, d, tol=tol, max_iterations=5000, dot_mode="blocked")
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=5000, record_history=True)
+    x, rep = pb.pcg_solve(A, b, x0, pb.JacobiPreconditioner(d), cfg)
+    E = oracle.history_gap(ref2.history, ref.history)
+    assert abs(rep.iterations - ref.iterations) <= 1
+    assert oracle.history_gap(rep.history, ref.history) <= max(1e-10, 3 * E)
+    _, rp = pb.pipecg_solve(A, b, x0, pb.JacobiPreconditioner(d), cfg)
+    h1, h2 = np.array(rep.history[:20]), np.array(rp.history[:20])
+    assert np.max(np.abs(h1 - h2) / h1) <= 1e-6
