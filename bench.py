@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--no-tts", action="store_true", help="skip the time-to-solution leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--engine", default="auto",
-                    help="DeviceOptions.engine (auto | fused | fused-a | fused-b | fused-c | two)")
+                    help="DeviceOptions.engine (auto | fused | fused-a .. fused-f | fused-p | two)")
     return ap.parse_args()
 
 
@@ -262,10 +262,13 @@ def problem_device(pb, torch, kind, n, row_begin=0, row_end=None):
 ENGINES = {2: "two-kernel", 3: "fused-A (consumer gathers dinv*w)",
            4: "fused-B (gather warps)", 5: "fused-C (stored m, one gather per nonzero)",
            6: "fused-D (nnz-balanced tiles, cooperative gathers of the stored m)",
-           7: "fused-P (C with a chunk of iterations per persistent launch, grid barrier)"}
+           7: "fused-P (C with a chunk of iterations per persistent launch, grid barrier)",
+           8: "fused-E (A reading the row-pattern dictionary instead of the CSR)",
+           9: "fused-F (C reading the row-pattern dictionary instead of the CSR)"}
 KERNELS = {2: "gated_spmv_rows + pipecg_k1_kernel", 3: "pipecg_fused_kernel_a<int,TR,0>",
            4: "pipecg_fused_kernel<int,TR>", 5: "pipecg_fused_kernel_a<int,TR,1>",
-           6: "pipecg_fused_kernel_d<int,TR>", 7: "pipecg_fused_kernel_p<int,TR,1>"}
+           6: "pipecg_fused_kernel_d<int,TR>", 7: "pipecg_fused_kernel_p<int,TR,1>",
+           8: "pipecg_fused_kernel_s<TR,0>", 9: "pipecg_fused_kernel_s<TR,1>"}
 CONFIG_NAMES = {"3d7-256": "BASELINE.json configs[1]", "2d5-512": "BASELINE.json configs[0]",
                 "3d27-400": "BASELINE.json configs[2], single-GPU leg",
                 "3d7-400": "north_star headline (>= 64M rows)",
@@ -553,7 +556,9 @@ def run_b200(args):
                                             "fused_C": info["tune_ms"][2],
                                             "fused_D": info["tune_ms"][3],
                                             "fused_P": info["tune_ms"][4],
-                                            "two_kernel": info["tune_ms"][5]}},
+                                            "fused_E": info["tune_ms"][5],
+                                            "fused_F": info["tune_ms"][6],
+                                            "two_kernel": info["tune_ms"][7]}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "traffic_source": traffic_src,

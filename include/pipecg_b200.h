@@ -147,6 +147,16 @@ int pipecg_b200_find_long_rows(int64_t n_rows, int rp64, const void* rowptr, int
                                int32_t* long_rows, int64_t cap, int64_t* n_long_host,
                                void* stream);
 
+/* Lossless row-pattern dictionary (csrc/patterns.cu; what fused variants
+ * E/F read instead of the CSR): row i's entries are (i + off_k, v_k) for one
+ * of *n_pat distinct lists, *n_entries entries in all.  *n_pat = 0: the rows
+ * are too diverse (> 256 lists or > 2048 entries).  codes (device uint8[n_rows],
+ * optional) receives each row's list index, lists numbered by first row.
+ * Synchronous.  No reference counterpart (a storage format of sparse.py's CSR). */
+int pipecg_b200_row_patterns(int64_t n_rows, int rp64, const void* rowptr, const int32_t* col,
+                             const double* val, int64_t* n_pat, int64_t* n_entries,
+                             unsigned char* codes, void* stream);
+
 /* ---------------------------------------------------------------------- */
 /* On-device problem generators                   */
 /* kind: 5 = 2D 5-point, 7 = 3D 7-point, 27 = 3D 27-point (diag 26),      */
@@ -180,7 +190,9 @@ typedef struct {
 typedef struct {
   int dot_mode;        /* PCG_DOT_TREE (default) or PCG_DOT_SEQ */
   int engine;          /* 0 auto (autotuned for >= 64K rows), 1 fused (variant autotuned),
-                          2 two-kernel, 3..7 fused variant A/B/C/D/P */
+                          2 two-kernel, 3..9 fused variant A/B/C/D/P/E/F
+                          (E/F: A/C reading the matrix's row-pattern dictionary;
+                          only for matrices that have one) */
   int chunk;           /* iterations per CUDA-graph chunk (0 = auto) */
   int use_graphs;      /* 1 (default) or 0 (plain launches, debugging) */
   int max_sms;         /* size persistent grids for at most this many SMs (0 = all) */
@@ -197,9 +209,9 @@ typedef struct {
   double breakdown_value;
   int64_t n_history;   /* entries written to history_host */
   int64_t n_drift;     /* samples written to drift_*_host */
-  int engine;          /* engine used: 2 two-kernel, 3..7 fused variant A/B/C/D/P */
+  int engine;          /* engine used: 2 two-kernel, 3..9 fused variant A/B/C/D/P/E/F */
   int64_t graph_launches;
-  double tune_ms[8];   /* autotune ms/iteration: fused A, B, C, D, P, two-kernel, -, -
+  double tune_ms[8];   /* autotune ms/iteration: fused A, B, C, D, P, E, F, two-kernel
                           (0 = not run) */
 } pcg_result;
 

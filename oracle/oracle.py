@@ -295,6 +295,32 @@ def stencil(kind: str, n: int) -> Csr:
     return Csr(N, N, ro, ci, va)
 
 
+def row_patterns(A, max_pat=256, max_entries=2048):
+    """Checker for the device row-pattern dictionary (csrc/patterns.cu): the
+    distinct rows of A written relative to their own index -- (col - i,
+    value bits) in CSR order -- numbered by first occurrence.  Returns
+    (n_pat, n_entries, codes uint8[n]) or (0, 0, None) when there are more
+    than max_pat lists or max_entries entries.  Not a reference function:
+    the dictionary is a storage format of the reference's CSR
+    (sparse.py:43-132), whose SpMV order (kernels.py:64-70) it preserves."""
+    A = as_csr(A)
+    ro, ci, va = A.row_offsets, A.col_indices, np.ascontiguousarray(A.values).view(np.int64)
+    seen, codes, entries = {}, np.empty(A.n_rows, dtype=np.uint8), 0
+    for i in range(A.n_rows):
+        lo, hi = int(ro[i]), int(ro[i + 1])
+        key = (tuple((ci[lo:hi] - i).tolist()), tuple(va[lo:hi].tolist()))
+        c = seen.get(key)
+        if c is None:
+            if len(seen) == max_pat:
+                return 0, 0, None
+            c = seen[key] = len(seen)
+            entries += hi - lo
+        codes[i] = c
+    if entries > max_entries:
+        return 0, 0, None
+    return len(seen), entries, codes
+
+
 def manufactured(A):
     """cli.py:83-100: x_true = 1/sqrt(N), b = A x_true, x0 = 0, Jacobi."""
     N = A.n_rows

@@ -89,6 +89,7 @@ _SIGS = {
     "pipecg_b200_mm_to_csr": ([_vp, _int, _vp, _vp, _vp, _p_i64, _vp], _int),
     "pipecg_b200_mm_free": ([_vp], None),
     "pipecg_b200_find_long_rows": ([_i64, _int, _vp, _i64, _vp, _i64, _p_i64, _vp], _int),
+    "pipecg_b200_row_patterns": ([_i64, _int, _vp, _vp, _vp, _p_i64, _p_i64, _vp, _vp], _int),
     "pipecg_b200_stencil_shape": ([_int, _i64, _p_i64, _p_i64], _int),
     "pipecg_b200_stencil_prefix": ([_int, _i64, _i64, _p_i64], _int),
     "pipecg_b200_stencil_fill": ([_int, _i64, _i64, _i64, _int, _vp, _vp, _vp, _vp], _int),

@@ -25,6 +25,23 @@ int spmv_any(int64_t n_rows, int rp64, const void* rowptr, const int* col, const
              const double* x, const double* b, double* y, const int* long_rows, int64_t n_long,
              int mode, cudaStream_t st);
 int preload_ops();
+
+// Row-pattern dictionary of a CSR matrix (patterns.cu): row i's entries are
+// (i + off[k], val[k]) for k in [start[code[i]], start[code[i] + 1]), in
+// the CSR order, bit for bit.  n_pat == 0: the matrix has no dictionary.
+constexpr int kPatMax = 256;          // codes are one byte
+constexpr int kPatMaxEntries = 2048;  // dictionary entries (shared memory: 12 B each)
+struct RowPatterns {
+  int n_pat = 0, n_entries = 0, max_len = 0;
+  unsigned char* code = nullptr;  // [n + 256]
+  int* start = nullptr;           // [n_pat + 1]
+  int* off = nullptr;             // [n_entries] column - row
+  double* val = nullptr;          // [n_entries]
+};
+int build_row_patterns(long long n, int rp64, const void* rp, const int* col, const double* val,
+                       cudaStream_t st, RowPatterns* out);
+void free_row_patterns(RowPatterns* p);
+int preload_patterns();
 int dots_any(int64_t n, int npairs, const double* const* a, const double* const* b, int mode,
              double* out, double* workspace, cudaStream_t st);
 

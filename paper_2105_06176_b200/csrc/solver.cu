@@ -411,6 +411,12 @@ struct FusedParams {
   const int* tile_row;        // [n_tiles + 1] first row of each tile
   const long long* tile_e;    // [n_tiles + 1] first nonzero of each tile
   long long hub_len;          // rows longer than this are single-row hub tiles
+  // variants E/F (row-pattern dictionary, patterns.cu)
+  const unsigned char* pcode;  // [n] pattern code per row
+  const int* pstart;           // [n_pat + 1]
+  const int* poff;             // [n_pat_e] column - row
+  const double* pval;          // [n_pat_e]
+  int n_pat, n_pat_e;
 };
 
 template <typename RP, int TR>
@@ -861,6 +867,195 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_a(FusedParams<RP>
                         MG ? (((it + 1) & 1) ? 12 : 9) : 7 + (int)((it + 1) & 1), 1);
   }
   publish_partials<NT>(acc, lt, red, 1, P.pout, P.fin, P.counter, it, XG ? &P.X : nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// Variants E / F: the matrix read through its row-pattern dictionary
+// (patterns.cu).  Same CTA shape as A / C (producer warp + one consumer
+// thread per tile row), but a stage carries only the 7 streamed vectors and
+// one code byte per row: row i's nonzeros are (i + off[k], val[k]) for the
+// dictionary slice of its code, held in shared memory for the whole kernel.
+// The CSR is never read (12 bytes per nonzero + 4 per row less HBM traffic
+// per iteration); the sum runs over the same entries in the same order as
+// the CSR row, so the roundings are the reference's (kernels.py:64-70).
+//   E (MG = false): gathers dinv[c], w_old[c] (as A);
+//   F (MG = true):  gathers the stored m_old[c] (as C).
+// ---------------------------------------------------------------------------
+template <int TR>
+struct FusedLayoutS {
+  static constexpr int kVecBytes = TR * 8;
+  static constexpr int kStageBytes = 7 * kVecBytes + TR;  // 7 vectors + codes
+  static constexpr int kHeader = 1024;
+};
+
+// shared-memory bytes of a dictionary (start | off | val, 16-byte aligned parts)
+__host__ __device__ __forceinline__ int pat_smem_bytes(int n_pat, int n_e) {
+  return (int)(round_up(4LL * (n_pat + 1), 16) + round_up(4LL * n_e, 16) + 8LL * n_e);
+}
+
+template <int TR, bool MG>
+__global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_s(FusedParams<int> P, int step) {
+  using L = FusedLayoutS<TR>;
+  constexpr int NT = TR;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + 8;
+  double* red = reinterpret_cast<double*>(smem + 256);
+  volatile int* decision = reinterpret_cast<volatile int*>(smem + 512);
+  double* sc = reinterpret_cast<double*>(smem + 768);
+  long long* s_it = reinterpret_cast<long long*>(smem + 896);
+  int* pst = reinterpret_cast<int*>(smem + L::kHeader);
+  const int n_start = (int)round_up(P.n_pat + 1, 4), n_off = (int)round_up(P.n_pat_e, 4);
+  int* pof = pst + n_start;
+  double* pva = reinterpret_cast<double*>(pof + n_off);
+  unsigned char* stage0 = smem + L::kHeader + round_up(pat_smem_bytes(P.n_pat, P.n_pat_e), 128);
+  const int S = P.stages;
+
+  Ctrl* C = P.C;
+  const int tid = threadIdx.x;
+  const bool producer = tid < 32;
+  const long long t_lo = blockIdx.x, t_step = gridDim.x;
+  const long long my_tiles = P.n_tiles > t_lo ? (P.n_tiles - t_lo + t_step - 1) / t_step : 0;
+
+  pdl_trigger();
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NT / 32);
+    }
+    fence_barrier_init();
+  }
+  // the dictionary is constant: load it before waiting on the previous grid
+  for (int k = tid; k <= P.n_pat; k += blockDim.x) pst[k] = P.pstart[k];
+  for (int k = tid; k < P.n_pat_e; k += blockDim.x) {
+    pof[k] = P.poff[k];
+    pva[k] = P.pval[k];
+  }
+  pdl_wait();
+
+  uint64_t pol = 0;
+  auto issue = [&](long long j) {
+    const int s = (int)(j % S);
+    const long long t0 = (t_lo + j * t_step) * TR;
+    const long long rows = min((long long)TR, P.n - t0);
+    const uint32_t b_vec = (uint32_t)((rows * 8 + 15) / 16 * 16);
+    const uint32_t b_code = (uint32_t)((rows + 15) / 16 * 16);
+    unsigned char* sb = stage0 + (size_t)s * L::kStageBytes;
+    mbar_arrive_expect_tx(&full[s], 7 * b_vec + b_code);
+#pragma unroll
+    for (int k = 0; k < 7; ++k) bulk_g2s(sb + k * L::kVecBytes, P.vec[k] + t0, b_vec, &full[s], pol);
+    bulk_g2s_nohint(sb + 7 * L::kVecBytes, P.pcode + t0, b_code, &full[s]);
+  };
+  if (tid == 0) {
+    pol = policy_evict_first();
+    for (long long j = 0; j < my_tiles && j < S; ++j) issue(j);
+  }
+  if (tid == 32) *s_it = read_status(C) == PCG_RUNNING ? C->base_it + step : -1;
+  __syncthreads();
+  const long long it = *reinterpret_cast<volatile long long*>(s_it);
+  if (it < 0) {
+    if (tid == 0)
+      for (long long j = 0; j < my_tiles && j < S; ++j) mbar_wait(&full[j], 0);
+    return;
+  }
+  const double* w_old = P.w[it & 1];
+  double* w_new = P.w[(it + 1) & 1];
+  if (!producer) {
+    const Step stp = prologue<NT>(C, P.hist, P.rin, it, tid - 32, red, 1,
+                                  blockIdx.x == 0 && tid == 32);
+    if (tid == 32) {
+      sc[0] = stp.alpha;
+      sc[1] = stp.beta;
+      *decision = stp.go;
+    }
+  }
+  __syncthreads();
+  if (!*decision) {
+    if (tid == 0)
+      for (long long j = 0; j < my_tiles && j < S; ++j) mbar_wait(&full[j], 0);
+    return;
+  }
+  const double alpha = sc[0], beta = sc[1];
+  if (producer) {
+    if (tid == 0) {
+      for (long long j = S; j < my_tiles; ++j) {
+        mbar_wait(&empty[j % S], (uint32_t)((j / S - 1) & 1));
+        issue(j);
+      }
+    }
+    return;
+  }
+
+  const int lt = tid - 32;
+  const double* m_old = P.m[it & 1];
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (long long j = 0; j < my_tiles; ++j) {
+    const int s = (int)(j % S);
+    const long long t0 = (t_lo + j * t_step) * TR;
+    const long long rows = min((long long)TR, P.n - t0);
+    const unsigned char* sb = stage0 + (size_t)s * L::kStageBytes;
+    const double* v_s = reinterpret_cast<const double*>(sb);
+    const long long i = t0 + lt;
+    double wi = 0.0, di = 0.0;
+    if (lt < rows) {
+      wi = ldg_nc(w_old + i);
+      di = ldg_nc(P.dinv + i);
+    }
+    mbar_wait(&full[s], (uint32_t)((j / S) & 1));
+    if (lt < rows) {
+      const int code = sb[7 * L::kVecBytes + lt];
+      const int lo = pst[code], hi = pst[code + 1];
+      const int ii = (int)i;
+      // n_i = sum_k a_ik * m_ck over the row's dictionary entries (= its CSR
+      // entries, same order); three explicit phases per batch as in A
+      double nacc = 0.0;
+      for (int k0 = lo; k0 < hi; k0 += 8) {
+        double av[8], mv[8];
+        int cc[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int k = k0 + t < hi ? k0 + t : lo;
+          cc[t] = ii + pof[k];
+          av[t] = pva[k];
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if (k0 + t < hi) {
+            const int c = cc[t];
+            mv[t] = MG ? ldg_nc(m_old + c) : mul(ldg_nc(P.dinv + c), ldg_nc(w_old + c));
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if (k0 + t < hi) nacc = add(nacc, mul(av[t], mv[t]));
+      }
+      const double mi = mul(di, wi);
+      const double zi = add(nacc, mul(beta, v_s[0 * TR + lt]));
+      const double qi = add(mi, mul(beta, v_s[1 * TR + lt]));
+      const double si = add(wi, mul(beta, v_s[2 * TR + lt]));
+      const double ui = v_s[6 * TR + lt];
+      const double pi = add(ui, mul(beta, v_s[3 * TR + lt]));
+      const double xi = add(v_s[4 * TR + lt], mul(alpha, pi));
+      const double ri = sub(v_s[5 * TR + lt], mul(alpha, si));
+      const double un = sub(ui, mul(alpha, qi));
+      const double wn = sub(wi, mul(alpha, zi));
+      st_stream(P.vec[0] + i, zi);
+      st_stream(P.vec[1] + i, qi);
+      st_stream(P.vec[2] + i, si);
+      st_stream(P.vec[3] + i, pi);
+      st_stream(P.vec[4] + i, xi);
+      st_stream(P.vec[5] + i, ri);
+      st_stream(P.vec[6] + i, un);
+      st_stream(w_new + i, wn);
+      if (MG) P.m[(it + 1) & 1][i] = mul(di, wn);  // solvers.py:358
+      acc[0] = add(acc[0], mul(ri, un));
+      acc[1] = add(acc[1], mul(wn, un));
+      acc[2] = add(acc[2], mul(un, un));
+    }
+    __syncwarp();
+    if ((lt & 31) == 0) mbar_arrive(&empty[s]);
+  }
+  publish_partials<NT>(acc, lt, red, 1, P.pout, P.fin, P.counter, it);
 }
 
 // ---------------------------------------------------------------------------
@@ -1908,7 +2103,8 @@ struct FusedPlan {
   long long* tile_e = nullptr;
 };
 
-constexpr int kVariants = 5;  // A B C D P (= C in one persistent launch per chunk)
+constexpr int kVariants = 7;  // A B C D P (= C in one persistent launch per chunk) E F (A / C
+                               // reading the row-pattern dictionary instead of the CSR)
 constexpr long long kPersistMaxRows = 8LL << 20;  // P is a candidate up to this size
 
 struct pcg_solver {
@@ -1984,6 +2180,7 @@ struct pcg_solver {
   int* tile_row = nullptr;         // variant D/E tiles of the applied plan
   long long* tile_e = nullptr;
   long long hub_len = 0;
+  RowPatterns pat;                 // row-pattern dictionary (n_pat == 0: none)
 };
 
 namespace {
@@ -2179,6 +2376,69 @@ int plan_d(pcg_solver* S, const int* cv, FusedPlan* best) {
   return build_tiles_d<RP>(S, best);
 }
 
+// Variants E / F (row-pattern dictionary): stages are 7 vectors + one code
+// byte per row; the dictionary sits in front of them for the whole kernel.
+template <int TR, bool MG>
+int plan_one_s(pcg_solver* S, FusedPlan* out) {
+  FusedPlan p;
+  p.variant = MG ? 6 : 5;
+  p.tr = TR;
+  const size_t sb = FusedLayoutS<TR>::kStageBytes;
+  const size_t hdr = FusedLayoutS<TR>::kHeader +
+                     (size_t)round_up(pat_smem_bytes(S->pat.n_pat, S->pat.n_entries), 128);
+  const size_t sm_budget = 228 * 1024, cta_max = 227 * 1024;
+  const char* e_st = getenv("PIPECG_B200_STAGES");
+  const char* e_bps = getenv("PIPECG_B200_BPS");
+  for (int bps = e_bps ? atoi(e_bps) : 2; bps >= 1 && !p.stages; --bps) {
+    if (e_bps && bps != atoi(e_bps)) break;
+    for (int st = e_st ? atoi(e_st) : 3; st <= 8; ++st) {
+      const size_t need = hdr + st * sb;
+      if (need <= cta_max && (need + 1024) * bps <= sm_budget) {
+        p.stages = st;
+        p.bps = bps;
+        p.smem = need;
+        break;
+      }
+      if (e_st) break;
+    }
+  }
+  if (!p.stages) {
+    *out = p;
+    return PCG_OK;
+  }
+  int occ = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pipecg_fused_kernel_s<TR, MG>,
+                                                                TR + 32, p.smem);
+  if (e != cudaSuccess) return cuda_status(e, "pattern occupancy");
+  occ = std::min(occ, p.bps);
+  if (occ < 1) {
+    p.stages = 0;
+    *out = p;
+    return PCG_OK;
+  }
+  const long long n_tiles = (S->A.n_rows + TR - 1) / TR;
+  p.grid = (int)std::max<long long>(std::min<long long>((long long)occ * S->num_sms, n_tiles), 1);
+  p.score = occ * TR;
+  *out = p;
+  return PCG_OK;
+}
+
+template <bool MG>
+int plan_variant_s(pcg_solver* S, FusedPlan* best) {
+  FusedPlan p[3];
+  int rc = plan_one_s<256, MG>(S, &p[0]);
+  if (!rc) rc = plan_one_s<128, MG>(S, &p[1]);
+  if (!rc) rc = plan_one_s<64, MG>(S, &p[2]);
+  if (rc) return rc;
+  const char* e_tr = getenv("PIPECG_B200_TR");
+  *best = FusedPlan();
+  for (int k = 0; k < 3; ++k) {
+    if (!p[k].stages || (e_tr && atoi(e_tr) != p[k].tr)) continue;
+    if (p[k].score > best->score) *best = p[k];
+  }
+  return PCG_OK;
+}
+
 template <typename RP>
 int fused_setup(pcg_solver* S) {
   int cc[3], cv[3];
@@ -2204,6 +2464,9 @@ int fused_setup(pcg_solver* S) {
     if (e != cudaSuccess) return cuda_status(e, "persistent occupancy");
     if ((long long)occ * S->num_sms >= p.grid) S->plans[4] = p;
   }
+  // E / F: only when the matrix has a row-pattern dictionary (built by the caller)
+  if (!rc && S->pat.n_pat > 0) rc = plan_variant_s<false>(S, &S->plans[5]);
+  if (!rc && S->pat.n_pat > 0) rc = plan_variant_s<true>(S, &S->plans[6]);
   if (rc) return rc;
   bool any = false;
   for (int v = 0; v < kVariants; ++v) any = any || S->plans[v].stages > 0;
@@ -2213,7 +2476,7 @@ int fused_setup(pcg_solver* S) {
 void apply_plan(pcg_solver* S, const FusedPlan& p) {
   S->variant = p.variant;
   S->tr = p.tr;
-  S->n_tiles = p.variant == 3 ? p.n_tiles : (S->A.n_rows + p.tr - 1) / p.tr;
+  S->n_tiles = p.variant == 3 ? p.n_tiles : (S->A.n_rows + p.tr - 1) / p.tr;  // E/F: TR-row tiles
   S->tile_row = p.tile_row;
   S->tile_e = p.tile_e;
   S->hub_len = p.hub_len;
@@ -2337,6 +2600,12 @@ FusedParams<RP> fused_params(pcg_solver* S) {
   P.tile_row = S->tile_row;
   P.tile_e = S->tile_e;
   P.hub_len = S->hub_len;
+  P.pcode = S->pat.code;
+  P.pstart = S->pat.start;
+  P.poff = S->pat.off;
+  P.pval = S->pat.val;
+  P.n_pat = S->pat.n_pat;
+  P.n_pat_e = S->pat.n_entries;
   P.X = FusedXchg{};
   if (S->fused_xchg) {
     P.X.ptr = S->x_ptr;
@@ -2382,7 +2651,17 @@ void launch_fused(pcg_solver* S, int k) {
   const unsigned g = (unsigned)S->grid;
   const size_t sm = S->smem;
   const int variant = S->variant == 4 ? 2 : S->variant;  // P, launched per iteration, is C
-  if (variant == 1) {
+  if (variant == 5 || variant == 6) {
+    const FusedParams<int> PS = fused_params<int>(S);  // E/F never read the row pointers
+#define PCG_LS(MGV)                                                                             \
+  switch (S->tr) {                                                                              \
+    case 256: launch_k(pipecg_fused_kernel_s<256, MGV>, g, 256 + 32, sm, st, pdl, PS, k); break; \
+    case 128: launch_k(pipecg_fused_kernel_s<128, MGV>, g, 128 + 32, sm, st, pdl, PS, k); break; \
+    default: launch_k(pipecg_fused_kernel_s<64, MGV>, g, 64 + 32, sm, st, pdl, PS, k); break;    \
+  }
+    if (variant == 6) { PCG_LS(true) } else { PCG_LS(false) }
+#undef PCG_LS
+  } else if (variant == 1) {
     switch (S->tr) {
       case 256: launch_k(pipecg_fused_kernel<RP, 256>, g, FusedLayout<RP, 256>::kThreads, sm, st, pdl, P, k); break;
       case 128: launch_k(pipecg_fused_kernel<RP, 128>, g, FusedLayout<RP, 128>::kThreads, sm, st, pdl, P, k); break;
@@ -2415,7 +2694,9 @@ void launch_fused(pcg_solver* S, int k) {
 }
 
 // fused variants C and D gather a stored m (ping-pong m / m2) instead of w
-inline bool stored_m_fused(const pcg_solver* S) { return S->engine == 1 && S->variant >= 2; }
+inline bool stored_m_fused(const pcg_solver* S) {
+  return S->engine == 1 && S->variant >= 2 && S->variant != 5;
+}
 
 // enqueue graph step k (drift? -> iteration -> seq dots? -> exchange / SpMV)
 int enqueue_step(pcg_solver* S, int k) {
@@ -2657,6 +2938,9 @@ int preload_solver() {
   PCG_LOAD((pipecg_fused_kernel_d<int, 64>)); PCG_LOAD((pipecg_fused_kernel_d<long long, 256>));
   PCG_LOAD((pipecg_fused_kernel_d<long long, 128>)); PCG_LOAD((pipecg_fused_kernel_d<long long, 64>));
   PCG_LOAD(tile_build_kernel<int>); PCG_LOAD(tile_build_kernel<long long>); PCG_LOAD(tile_close_kernel);
+  PCG_LOAD((pipecg_fused_kernel_s<256, false>)); PCG_LOAD((pipecg_fused_kernel_s<128, false>));
+  PCG_LOAD((pipecg_fused_kernel_s<64, false>)); PCG_LOAD((pipecg_fused_kernel_s<256, true>));
+  PCG_LOAD((pipecg_fused_kernel_s<128, true>)); PCG_LOAD((pipecg_fused_kernel_s<64, true>));
 
   PCG_LOAD(pipecg_k1_kernel); PCG_LOAD(gated_spmv_rows<int>); PCG_LOAD(gated_spmv_rows<long long>);
   PCG_LOAD(gated_spmv_long<int>); PCG_LOAD(gated_spmv_long<long long>);
@@ -2696,8 +2980,13 @@ int preload_solver() {
   PCG_SMEM((pipecg_fused_kernel_d<int, 256>)); PCG_SMEM((pipecg_fused_kernel_d<int, 128>));
   PCG_SMEM((pipecg_fused_kernel_d<int, 64>)); PCG_SMEM((pipecg_fused_kernel_d<long long, 256>));
   PCG_SMEM((pipecg_fused_kernel_d<long long, 128>)); PCG_SMEM((pipecg_fused_kernel_d<long long, 64>));
+  PCG_SMEM((pipecg_fused_kernel_s<256, false>)); PCG_SMEM((pipecg_fused_kernel_s<128, false>));
+  PCG_SMEM((pipecg_fused_kernel_s<64, false>)); PCG_SMEM((pipecg_fused_kernel_s<256, true>));
+  PCG_SMEM((pipecg_fused_kernel_s<128, true>)); PCG_SMEM((pipecg_fused_kernel_s<64, true>));
 #undef PCG_SMEM
   if (e != cudaSuccess) return cuda_status(e, "preload solver kernels");
+  rc = preload_patterns();
+  if (rc) return rc;
   done_devices.insert(dev);
   return PCG_OK;
 }
@@ -2847,10 +3136,11 @@ struct TuneKey {
   long long n_rows, n_cols, nnz;
   int rp64;
   long long max_row;
-  int sms, dot_mode, req;
+  int sms, dot_mode, req, n_pat;
   bool operator<(const TuneKey& o) const {
-    return std::tie(dev, n_rows, n_cols, nnz, rp64, max_row, sms, dot_mode, req) <
-           std::tie(o.dev, o.n_rows, o.n_cols, o.nnz, o.rp64, o.max_row, o.sms, o.dot_mode, o.req);
+    return std::tie(dev, n_rows, n_cols, nnz, rp64, max_row, sms, dot_mode, req, n_pat) <
+           std::tie(o.dev, o.n_rows, o.n_cols, o.nnz, o.rp64, o.max_row, o.sms, o.dot_mode, o.req,
+                    o.n_pat);
   }
 };
 std::map<TuneKey, int>& tune_cache() {
@@ -2980,7 +3270,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     return rc;
   }
   // engine: 0 auto (autotuned), 1 fused (heuristic variant), 2 two-kernel,
-  // 3/4/5/6 fused variant A/B/C/D
+  // 3..9 fused variant A/B/C/D/P/E/F
   const int req = S->opt.engine;
   if (req < 0 || req > 3 + kVariants - 1) {
     pipecg_b200_solver_destroy(S);
@@ -2989,6 +3279,17 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   const bool has_long = max_row > (unsigned long long)kLongRow;
   S->irregular = has_long;
   bool fused_ok = false;
+  if (req == 0 || req == 1 || req == 8 || req == 9) {
+    // lossless row-pattern dictionary (variants E/F); none for irregular
+    // matrices or when the rows are too diverse (patterns.cu)
+    if (!has_long && !getenv("PIPECG_B200_NO_PATTERNS")) {
+      rc = build_row_patterns(A->n_rows, A->rp64, A->rowptr, A->col, A->val, S->stream, &S->pat);
+      if (rc) {
+        pipecg_b200_solver_destroy(S);
+        return rc;
+      }
+    }
+  }
   if (req != 2) {
     rc = A->rp64 ? fused_setup<long long>(S) : fused_setup<int>(S);
     if (rc && rc != PCG_EINVAL) {
@@ -2998,7 +3299,10 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     fused_ok = rc == PCG_OK;
     if (req >= 3 && !S->plans[req - 3].stages) fused_ok = false;
     if (!fused_ok && req != 0) {
+      const bool no_dict = S->pat.n_pat == 0;
       pipecg_b200_solver_destroy(S);
+      if (req >= 8 && no_dict)
+        return set_error(PCG_EINVAL, "fused variants E/F: the matrix has no row-pattern dictionary");
       return set_error(PCG_EINVAL, "fused engine: tiles exceed shared memory");
     }
   }
@@ -3052,7 +3356,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     // C for wide rows (> 12 nnz/row, one gather per nonzero) or A
     const bool wide = A->nnz > 12 * A->n_rows;
     // small problems are launch-latency bound: P (one launch per chunk) first
-    int order[kVariants] = {4, 0, 2, 3, 1};
+    int order[kVariants] = {4, 0, 2, 3, 1, 5, 6};
     if (has_long) order[0] = 3, order[1] = 4, order[2] = 2, order[3] = 0;
     else if (wide) order[1] = 2, order[2] = 0;
     S->engine = 1;
@@ -3066,7 +3370,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     // with the same shape and row-length profile on the same device reuses
     // the measured choice instead of re-timing every candidate
     const TuneKey key{dev, A->n_rows, A->n_cols, A->nnz, A->rp64, (long long)max_row,
-                      S->num_sms, S->opt.dot_mode, req};
+                      S->num_sms, S->opt.dot_mode, req, S->pat.n_pat};
     int cached = -1;
     if (!getenv("PIPECG_B200_NO_TUNE_CACHE")) {
       std::lock_guard<std::mutex> lk(tune_cache_mu());
@@ -3131,6 +3435,7 @@ int pipecg_b200_solver_destroy(pcg_solver* S) {
     cudaFree(S->plans[v].tile_row);
     cudaFree(S->plans[v].tile_e);
   }
+  free_row_patterns(&S->pat);
 
   if (S->ev_in) cudaEventDestroy(S->ev_in);
   if (S->stream) cudaStreamDestroy(S->stream);
@@ -3245,7 +3550,13 @@ int pipecg_b200_solver_connect(pcg_solver* S, int rank, int world, void* const* 
   cp.send_dst = reinterpret_cast<const long long*>(send_dst);
   S->cp = cp;
   S->connected = true;
-  if (S->variant == 4) S->variant = 2;  // per-iteration launches (the exchange needs them)
+  // per-iteration launches of the CSR kernels (the exchange needs them; the
+  // pattern dictionary holds global offsets, not the shard's column space)
+  if (S->engine == 1 && S->variant >= 4) {
+    const FusedPlan& csr = S->plans[S->variant == 5 ? 0 : 2];
+    if (!csr.stages) return set_error(PCG_EINVAL, "solver_connect: no CSR variant fits this shard");
+    apply_plan(S, csr);
+  }
   // fused exchange for variants A, C, D (B keeps the separate exchange kernel)
   S->fused_xchg = S->variant != 1 && !getenv("PIPECG_B200_SEPARATE_XCHG");
   if (S->fused_xchg) {

@@ -425,7 +425,8 @@ class DistributedSolver:
         # blocks -> adopt rank 0's choice
         names = {3: "fused-a", 4: "fused-b", 5: "fused-c", 6: "fused-d"}
         mine = int(self.solver.poll().engine)
-        mine = 5 if mine == 7 else mine  # P runs as C once connected
+        # once connected P and F run as C, E as A (per-iteration CSR launches)
+        mine = {7: 5, 8: 3, 9: 5}.get(mine, mine)
         chosen = group.all_gather_object(mine)[0]
         if mine != chosen:
             self.solver.close()

@@ -171,7 +171,10 @@ class DeviceOptions:
       "fused-c" / "fused-d" / "fused-p" (consumer gathers dinv*w / gather warps /
       stored m / nnz-balanced tiles with cooperative gathers, for irregular rows /
       C with a whole chunk of iterations in one persistent launch, for small
-      latency-bound problems) or "two" (update kernel +
+      latency-bound problems), "fused-e" / "fused-f" (A / C reading the
+      matrix through its lossless row-pattern dictionary: one byte per row
+      instead of the CSR, for constant-coefficient stencil-like matrices) or
+      "two" (update kernel +
       SpMV kernel; general matrices, very long rows).
     chunk: iterations per CUDA-graph chunk (0 = sized from the problem).
     use_graphs: capture chunks as CUDA graphs.
@@ -187,7 +190,8 @@ class DeviceOptions:
 
     def native(self) -> _lib.PcgOptions:
         eng = {"auto": 0, "fused": 1, "two": 2, "fused-a": 3, "fused-b": 4,
-               "fused-c": 5, "fused-d": 6, "fused-p": 7}[self.engine]
+               "fused-c": 5, "fused-d": 6, "fused-p": 7, "fused-e": 8,
+               "fused-f": 9}[self.engine]
         dm = {"tree": _lib.PCG_DOT_TREE, "seq": _lib.PCG_DOT_SEQ}[self.dot_mode]
         return _lib.PcgOptions(dm, eng, int(self.chunk), 1 if self.use_graphs else 0,
                                int(self.max_sms))

@@ -189,6 +189,20 @@ class DeviceCsr:
             self._n_long = n
         return (self._long_rows.data_ptr() if self._long_rows is not None else None, self._n_long)
 
+    def row_patterns(self, codes: bool = False):
+        """The matrix's lossless row-pattern dictionary (what fused variants
+        E/F read instead of the CSR): (number of distinct rows up to the row
+        index shift, dictionary entries[, uint8 code per row]).  (0, 0) when
+        the rows are too diverse for a dictionary."""
+        n_pat, n_e = ctypes.c_int64(0), ctypes.c_int64(0)
+        out = torch.empty(self.n_rows, dtype=torch.uint8, device=self.col.device) if codes else None
+        _lib.call("pipecg_b200_row_patterns", self.n_rows, self.rp64, self.rowptr.data_ptr(),
+                  self.col.data_ptr(), self.val.data_ptr(), ctypes.byref(n_pat), ctypes.byref(n_e),
+                  out.data_ptr() if out is not None else None, stream_ptr())
+        if codes:
+            return int(n_pat.value), int(n_e.value), (out if n_pat.value else None)
+        return int(n_pat.value), int(n_e.value)
+
     def to_host(self) -> CsrMatrix:
         ro = self.rowptr[: self.n_rows + 1].to(torch.int64).cpu().numpy()
         ci = self.col[: self.nnz].to(torch.int64).cpu().numpy()

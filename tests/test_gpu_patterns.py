@@ -1,0 +1,156 @@
+"""Fused variants E/F: the matrix read through its lossless row-pattern
+dictionary (csrc/patterns.cu) instead of the CSR.
+
+* The device dictionary equals the oracle's (oracle.row_patterns): same
+  number of lists, same entries, same code for every row.
+* With dot_mode="seq" every solve is bitwise the reference's: each row's
+  sum runs over the same (column, value) pairs in CSR order
+  (kernels.py:64-70, solvers.py:324-387).
+* Matrices without a dictionary (too many distinct rows / entries) keep
+  the CSR variants; asking for E/F on them fails loudly.
+"""
+
+from __future__ import annotations
+
+import json
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import GOLDEN, golden_matrix, load_golden
+
+pytestmark = pytest.mark.gpu
+
+pb = pytest.importorskip("paper_2105_06176_b200")
+torch = pytest.importorskip("torch")
+from test_gpu_irregular import _random_spd  # noqa: E402
+from test_gpu_solver import _rp64, assert_within_envelope, envelope  # noqa: E402
+
+META = json.loads((GOLDEN / "golden_meta.json").read_text())
+CASES = [c for c in META["cases"] if c != "p125n6_pcg"]
+
+
+def _perturbed(kind, n, rows):
+    """A stencil whose listed rows get a different diagonal (extra patterns)."""
+    A = pb.stencil_host(kind, n)
+    va = np.array(A.values, dtype=np.float64)
+    ro, ci = np.asarray(A.row_offsets), np.asarray(A.col_indices)
+    for i in rows:
+        for k in range(ro[i], ro[i + 1]):
+            if ci[k] == i:
+                va[k] += 0.5 + 0.25 * (i % 3)
+    return pb.CsrMatrix(A.n_rows, A.n_cols, ro, ci, va)
+
+
+DICT_CASES = [("2d5", 20), ("3d7", 12), ("3d27", 9), ("3d7", 3)]
+
+
+@pytest.mark.parametrize("kind,n", DICT_CASES)
+def test_dictionary_matches_oracle(cuda, kind, n):
+    A = pb.stencil_host(kind, n)
+    n_pat, n_e, codes = pb.as_device_csr(A).row_patterns(codes=True)
+    r_pat, r_e, r_codes = oracle.row_patterns(A)
+    assert (n_pat, n_e) == (r_pat, r_e)
+    assert n_pat == (9 if kind == "2d5" else 27)
+    np.testing.assert_array_equal(codes.cpu().numpy(), r_codes)
+
+
+def test_dictionary_perturbed_rows_and_rp64(cuda):
+    A = _perturbed("3d7", 10, [0, 17, 555, 999])
+    for D in (pb.as_device_csr(A), _rp64(A)):
+        n_pat, n_e, codes = D.row_patterns(codes=True)
+        r_pat, r_e, r_codes = oracle.row_patterns(A)
+        assert (n_pat, n_e) == (r_pat, r_e) and n_pat > 27
+        np.testing.assert_array_equal(codes.cpu().numpy(), r_codes)
+
+
+@pytest.mark.parametrize("make", [lambda: pb.stencil_host("p125", 7),
+                                  lambda: _random_spd(3000, 12, 5)])
+def test_no_dictionary_when_rows_are_diverse(cuda, make):
+    A = make()
+    assert oracle.row_patterns(A)[0] == 0
+    assert pb.as_device_csr(A).row_patterns() == (0, 0)
+    b = np.ones(A.n_rows)
+    with pytest.raises(Exception, match="row-pattern"):
+        pb.pipecg_solve(A, b, np.zeros(A.n_rows), pb.jacobi_setup(A),
+                        pb.SolverConfig(tolerance=1e-8, max_iterations=10),
+                        options=pb.DeviceOptions(engine="fused-e"))
+
+
+def _seq_vs_oracle(A, engine, max_it=5000, device_matrix=None):
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=max_it)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=max_it, record_history=True)
+    opts = pb.DeviceOptions(dot_mode="seq", engine=engine)
+    if device_matrix is None:
+        x, rep = pb.pipecg_solve(A, b, x0, pb.JacobiPreconditioner(d), cfg, options=opts)
+    else:
+        bd = torch.from_numpy(b).cuda()
+        x, rep = pb.pipecg_solve(device_matrix, bd, torch.zeros_like(bd),
+                                 pb.JacobiPreconditioner(d), cfg, options=opts)
+        x = x.cpu().numpy()
+    assert rep.iterations == ref.iterations
+    assert rep.history == ref.history
+    np.testing.assert_array_equal(x, ref.x)
+    return rep
+
+
+@pytest.mark.parametrize("engine", ["fused-e", "fused-f"])
+@pytest.mark.parametrize("kind,n", [("2d5", 40), ("3d7", 20), ("3d27", 12), ("3d7", 13), ("3d7", 2)])
+def test_stencil_seq_bitwise(cuda, kind, n, engine):
+    _seq_vs_oracle(pb.stencil_host(kind, n), engine)
+
+
+@pytest.mark.parametrize("engine", ["fused-e", "fused-f"])
+def test_perturbed_and_rp64_seq_bitwise(cuda, engine):
+    A = _perturbed("3d7", 14, [3, 100, 2000, 2743])
+    _seq_vs_oracle(A, engine)
+    _seq_vs_oracle(A, engine, device_matrix=_rp64(A))
+
+
+@pytest.mark.parametrize("engine", ["fused-e", "fused-f"])
+@pytest.mark.parametrize("case", CASES)
+def test_golden_cases_seq_bitwise(cuda, case, engine):
+    """Every golden case whose matrix has a dictionary, bit for bit."""
+    g = load_golden(f"solve_{case}.npz")
+    m = META["cases"][case]
+    A = golden_matrix(g)
+    if oracle.row_patterns(A)[0] == 0:
+        pytest.skip("no row-pattern dictionary for this matrix")
+    pc = pb.JacobiPreconditioner(g["inv_diag"])
+    cfg = pb.SolverConfig(tolerance=float(g["tol"]), max_iterations=int(g["max_iterations"]),
+                          record_history="breakdown" not in m,
+                          drift_check_interval=int(g["drift_k"]))
+    opts = pb.DeviceOptions(dot_mode="seq", engine=engine)
+    if "breakdown" in m:
+        with pytest.raises(pb.SolverBreakdown) as exc:
+            pb.pipecg_solve(A, g["b"], g["x0"], pc, cfg, options=opts)
+        assert exc.value.quantity == m["breakdown"]
+        assert exc.value.iteration == m["iteration"]
+        return
+    x, rep = pb.pipecg_solve(A, g["b"], g["x0"], pc, cfg, options=opts)
+    assert rep.iterations == m["iterations"]
+    np.testing.assert_array_equal(np.array(rep.history), g["history"])
+    np.testing.assert_array_equal(x, g["x"])
+
+
+@pytest.mark.parametrize("engine", ["fused-e", "fused-f"])
+def test_tree_mode_within_envelope(cuda, engine):
+    A = pb.stencil_host("3d7", 24)
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=5000)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=5000, record_history=True)
+    x, rep = pb.pipecg_solve(A, b, x0, pb.JacobiPreconditioner(d), cfg,
+                             options=pb.DeviceOptions(engine=engine))
+    assert_within_envelope(x, rep, ref.iterations, ref.history, ref.x,
+                           envelope(A, b, x0, d, tol, 5000))
+
+
+def test_autotuned_engine_bitwise(cuda):
+    """>= 64K rows: the autotuner times E/F beside the CSR variants; whatever
+    it picks is bitwise the reference in seq mode."""
+    rep = _seq_vs_oracle(pb.stencil_host("3d7", 48), "auto", max_it=3000)
+    assert rep.iterations > 10

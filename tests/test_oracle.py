@@ -158,3 +158,29 @@ def test_threaded_baseline_same_iterations():
         oracle.set_threads(1)
     assert abs(r1.iterations - r4.iterations) <= 1
     assert np.max(np.abs(r1.x - r4.x)) <= 1e-8 * np.max(np.abs(r1.x))
+
+
+@pytest.mark.parametrize("kind,n,expect", [("2d5", 10, 9), ("3d7", 6, 27), ("3d27", 5, 27),
+                                           ("3d7", 2, 8), ("p125", 6, 0)])
+def test_row_pattern_checker(kind, n, expect):
+    """oracle.row_patterns (the checker of csrc/patterns.cu): the boundary
+    classes of each stencil, codes by first occurrence, and every row
+    rebuilt from its dictionary entry is the CSR row bit for bit.  p125
+    (125 classes x up to 125 entries) exceeds the 2048-entry dictionary."""
+    A = oracle.stencil(kind, n)
+    n_pat, n_e, codes = oracle.row_patterns(A)
+    assert n_pat == expect
+    if not expect:
+        assert codes is None
+        return
+    ro, ci, va = A.row_offsets, A.col_indices, A.values
+    first = {}
+    for i in range(A.n_rows):
+        first.setdefault(int(codes[i]), i)
+    assert list(first) == list(range(n_pat))  # numbered by first occurrence
+    assert n_e == sum(int(ro[i + 1] - ro[i]) for i in first.values())
+    for i in range(A.n_rows):
+        r = first[int(codes[i])]
+        np.testing.assert_array_equal(ci[ro[i]:ro[i + 1]] - i, ci[ro[r]:ro[r + 1]] - r)
+        np.testing.assert_array_equal(va[ro[i]:ro[i + 1]].view(np.int64),
+                                      va[ro[r]:ro[r + 1]].view(np.int64))
