@@ -275,6 +275,23 @@ CONFIG_NAMES = {"3d7-256": "BASELINE.json configs[1]", "2d5-512": "BASELINE.json
                 "powerlaw-22": "BASELINE.json configs[3]"}
 
 
+def engine_bytes(engine: int, flags: int, N: int, nnz: int):
+    """Compulsory HBM bytes per iteration of the engine's kernel (vector
+    streams x 8N + the matrix as that engine stores it), or None (engine 2:
+    two kernels).  See DESIGN.md §4."""
+    csr = 12 * nnz + 4 * (N + 1)
+    win, dbc, uni = bool(flags & 2), bool(flags & 4), bool(flags & 8)
+    if engine in (3, 4):
+        return 17 * 8 * N + csr
+    if engine in (5, 6, 7):
+        return 19 * 8 * N + csr
+    if engine == 8:  # E: 16 streams with windows (dinv by code), else 17 (gathers)
+        return (16 if (win and dbc) else 17) * 8 * N + N
+    if engine == 9:  # F: 19 streams, 18 when dinv comes from the code
+        return (18 if (win and dbc) else 19) * 8 * N + N
+    return None
+
+
 def committed_traffic(config: str, engine: int):
     """DRAM bytes per launch of the dominant kernel from the committed ncu
     --set full capture (profiles/traffic.json, written by tools/ncu_summary.py)."""
@@ -316,7 +333,7 @@ def time_iterations(pb, torch, A, pc_d, warmup: int, steps: int, options=None):
     info = {"engine": res.engine, "graph_launches": res.graph_launches, "ok": bool(ok),
             "kernel_launches": steps * per_step + (res.graph_launches - g0),
             "status": res.status, "iterations_run": res.iterations,
-            "tune_ms": [round(v, 4) for v in res.tune_ms]}
+            "tune_ms": [round(v, 4) for v in res.tune_ms], "pattern_flags": res.pattern_flags}
     solver.close()
     del b, x0, x_true
     return ms, info
@@ -536,6 +553,7 @@ def run_b200(args):
     value = args.steps / (ms / 1e3)
     achieved = B / t_iter / 1e9
     traffic, traffic_src = committed_traffic(args.config, info["engine"])
+    kb = engine_bytes(info["engine"], info.get("pattern_flags", 0), N, nnz)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -566,6 +584,13 @@ def run_b200(args):
                      "bytes_formula": "176N + 12nnz + 4(N+1) (canonical, SURVEY.md §8(d))",
                      "peak_source": peak_src,
                      "frac_of_8TBs_spec": achieved / 8000.0,
+                     "kernel_bytes_per_iteration": kb,
+                     "kernel_achieved": kb / t_iter / 1e9 if kb else None,
+                     "kernel_frac": kb / t_iter / 1e9 / peak if kb else None,
+                     "kernel_bytes_note": "compulsory bytes of the engine's own data layout "
+                                          "(E/F: row-pattern dictionary, 1 code byte per row, "
+                                          "no CSR); frac > 1 above is in canonical bytes",
+                     "pattern_flags": info.get("pattern_flags"),
                      "kernel": KERNELS.get(info["engine"], "?") + " (one launch per iteration)"},
         "gpu_launches": info["kernel_launches"],
         "timing_ok": info["ok"],

@@ -213,6 +213,8 @@ typedef struct {
   int64_t graph_launches;
   double tune_ms[8];   /* autotune ms/iteration: fused A, B, C, D, P, E, F, two-kernel
                           (0 = not run) */
+  int pattern_flags;   /* row-pattern dictionary in use by E/F: 1 dictionary, 2 windows,
+                          4 dinv a function of the row's code, 8 ... one dinv for all rows */
 } pcg_result;
 
 int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_solver** out);

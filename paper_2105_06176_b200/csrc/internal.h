@@ -30,17 +30,22 @@ int preload_ops();
 // (i + off[k], val[k]) for k in [start[code[i]], start[code[i] + 1]), in
 // the CSR order, bit for bit.  n_pat == 0: the matrix has no dictionary.
 constexpr int kPatMax = 256;          // codes are one byte
-constexpr int kPatMaxEntries = 2048;  // dictionary entries (shared memory: 12 B each)
+constexpr int kPatMaxEntries = 2048;  // dictionary entries (shared memory: 16 B each)
 struct RowPatterns {
   int n_pat = 0, n_entries = 0, max_len = 0;
   unsigned char* code = nullptr;  // [n + 256]
   int* start = nullptr;           // [n_pat + 1]
+  int* rep = nullptr;             // [n_pat] first row of each code
   int* off = nullptr;             // [n_entries] column - row
   double* val = nullptr;          // [n_entries]
 };
 int build_row_patterns(long long n, int rp64, const void* rp, const int* col, const double* val,
                        cudaStream_t st, RowPatterns* out);
 void free_row_patterns(RowPatterns* p);
+// pdinv[k] = dinv[rep[k]]; *ok = dinv[i] == pdinv[code[i]] bitwise for every row;
+// *uniform: ok and every pdinv[k] == *value bitwise
+int check_dinv_by_code(const RowPatterns& p, long long n, const double* dinv, double* pdinv,
+                       bool* ok, bool* uniform, double* value, cudaStream_t st);
 int preload_patterns();
 int dots_any(int64_t n, int npairs, const double* const* a, const double* const* b, int mode,
              double* out, double* workspace, cudaStream_t st);

@@ -27,6 +27,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 #include "../../include/pipecg_b200.h"
@@ -201,6 +202,7 @@ int build(long long n, const RP* rp, const int* col, const double* val, cudaStre
     const int ne = h_start[u];
     if (cudaMalloc(&out->code, (size_t)n + 256) != cudaSuccess ||
         cudaMalloc(&out->start, (size_t)(u + 1) * 4) != cudaSuccess ||
+        cudaMalloc(&out->rep, (size_t)u * 4) != cudaSuccess ||
         cudaMalloc(&out->off, (size_t)std::max(ne, 1) * 4) != cudaSuccess ||
         cudaMalloc(&out->val, (size_t)std::max(ne, 1) * 8) != cudaSuccess)
       rc = set_error(PCG_ENOMEM, "row patterns: codes");
@@ -208,6 +210,7 @@ int build(long long n, const RP* rp, const int* col, const double* val, cudaStre
   if (usable && !rc) {
     cudaMemsetAsync(out->code + n, 0, 256, st);  // bulk-copy overrun of the last tile
     cudaMemcpyAsync(out->start, h_start.data(), (u + 1) * 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(out->rep, reps.data(), u * 4, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(d_start, h_start.data(), (u + 1) * 4, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(d_slot_code, slot_code.data(), kPatTable * 4, cudaMemcpyHostToDevice, st);
     pat_extract_kernel<RP><<<std::min(u, 256), 128, 0, st>>>(u, d_reps, rp, col, val, d_start,
@@ -232,7 +235,49 @@ int build(long long n, const RP* rp, const int* col, const double* val, cudaStre
   return rc;
 }
 
+__global__ void pat_dinv_gather_kernel(int u, const int* rep, const double* dinv, double* pdinv) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < u; k += gridDim.x * blockDim.x)
+    pdinv[k] = dinv[rep[k]];
+}
+
+__global__ void __launch_bounds__(256) pat_dinv_check_kernel(long long n, const unsigned char* code,
+                                                             const double* dinv, const double* pdinv,
+                                                             int* bad) {
+  bool ok = true;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    ok &= __double_as_longlong(dinv[i]) == __double_as_longlong(pdinv[code[i]]);
+  if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) *bad = 1;
+}
+
 }  // namespace
+
+int check_dinv_by_code(const RowPatterns& p, long long n, const double* dinv, double* pdinv,
+                       bool* ok, bool* uniform, double* value, cudaStream_t st) {
+  *ok = false;
+  *uniform = false;
+  *value = 0.0;
+  if (p.n_pat == 0) return PCG_OK;
+  int* bad = nullptr;
+  if (cudaMallocAsync(&bad, sizeof(int), st) != cudaSuccess)
+    return set_error(PCG_ENOMEM, "dinv check");
+  cudaMemsetAsync(bad, 0, sizeof(int), st);
+  pat_dinv_gather_kernel<<<1, 256, 0, st>>>(p.n_pat, p.rep, dinv, pdinv);
+  pat_dinv_check_kernel<<<elementwise_grid(n), 256, 0, st>>>(n, p.code, dinv, pdinv, bad);
+  int h = 1;
+  std::vector<double> pd(p.n_pat);
+  cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(pd.data(), pdinv, p.n_pat * sizeof(double), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(bad, st);
+  const int rc = cuda_status(cudaStreamSynchronize(st), "dinv check");
+  *ok = !rc && h == 0;
+  bool same = *ok;
+  for (int k = 1; k < p.n_pat && same; ++k)
+    same = std::memcmp(&pd[k], &pd[0], sizeof(double)) == 0;
+  *uniform = same;
+  *value = same ? pd[0] : 0.0;
+  return rc;
+}
 
 int build_row_patterns(long long n, int rp64, const void* rp, const int* col, const double* val,
                        cudaStream_t st, RowPatterns* out) {
@@ -247,6 +292,7 @@ int build_row_patterns(long long n, int rp64, const void* rp, const int* col, co
 void free_row_patterns(RowPatterns* p) {
   cudaFree(p->code);
   cudaFree(p->start);
+  cudaFree(p->rep);
   cudaFree(p->off);
   cudaFree(p->val);
   *p = RowPatterns{};
@@ -260,6 +306,7 @@ int preload_patterns() {
   PCG_LOAD(pat_len_kernel<int>); PCG_LOAD(pat_len_kernel<long long>);
   PCG_LOAD(pat_extract_kernel<int>); PCG_LOAD(pat_extract_kernel<long long>);
   PCG_LOAD(pat_verify_kernel<int>); PCG_LOAD(pat_verify_kernel<long long>);
+  PCG_LOAD(pat_dinv_gather_kernel); PCG_LOAD(pat_dinv_check_kernel);
 #undef PCG_LOAD
   return cuda_status(e, "preload pattern kernels");
 }

@@ -416,6 +416,8 @@ struct FusedParams {
   const int* pstart;           // [n_pat + 1]
   const int* poff;             // [n_pat_e] column - row
   const double* pval;          // [n_pat_e]
+  const unsigned char* pwin;   // [n_pat_e] window of each entry (WinTable)
+  const double* pdinv;         // [n_pat] dinv of each code (valid when WinTable.dinv_by_code)
   int n_pat, n_pat_e;
 };
 
@@ -872,31 +874,80 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_a(FusedParams<RP>
 // ---------------------------------------------------------------------------
 // Variants E / F: the matrix read through its row-pattern dictionary
 // (patterns.cu).  Same CTA shape as A / C (producer warp + one consumer
-// thread per tile row), but a stage carries only the 7 streamed vectors and
-// one code byte per row: row i's nonzeros are (i + off[k], val[k]) for the
+// thread per tile row), but instead of the tile's CSR a stage carries one
+// code byte per row: row i's nonzeros are (i + off[k], val[k]) for the
 // dictionary slice of its code, held in shared memory for the whole kernel.
-// The CSR is never read (12 bytes per nonzero + 4 per row less HBM traffic
-// per iteration); the sum runs over the same entries in the same order as
-// the CSR row, so the roundings are the reference's (kernels.py:64-70).
-//   E (MG = false): gathers dinv[c], w_old[c] (as A);
-//   F (MG = true):  gathers the stored m_old[c] (as C).
+// Every sum runs over the same entries in the same order as the CSR row, so
+// the roundings are the reference's (kernels.py:64-70).
+//
+// WIN (the dictionary's offsets form at most kMaxWin runs): the neighbour
+// values come from "windows" instead of per-nonzero gathers.  The distinct
+// offsets cluster into a few runs (3D 7-pt: -n^2 | -n | -1..1 | n | n^2);
+// for a tile [t0, t0 + TR) the values a run needs are one contiguous range
+// [t0 + lo, t0 + TR + hi), which the producer bulk-copies (TMA engine) into
+// the stage like the streamed vectors -- mostly L2 hits, since the other
+// tiles of the sweep read the same lines, so HBM sees each vector once.
+// Consumers then read everything from shared memory.
+//   F (MG = true):  the stored m_old = dinv * w_old (as C): windows of m,
+//                   plus w_old / dinv of the tile rows -> 19 vector streams
+//                   (18 when dinv is a function of the row's code);
+//   E (MG = false): m_c = dinv[c] * w_old[c] formed on the fly (as A) --
+//                   only with WIN when dinv is a function of the row's code
+//                   (Jacobi of a constant-coefficient stencil): windows of
+//                   w_old and of the codes, dinv[c] = pdinv[code[c]] from
+//                   shared memory -> 16 vector streams, the minimum (the 8
+//                   recurrence vectors read and written once).  Otherwise E
+//                   gathers dinv[c] and w_old[c] per nonzero (17 streams).
 // ---------------------------------------------------------------------------
+constexpr int kMaxWin = 16;  // windows per tile (more: per-nonzero gathers)
+
+struct WinTable {
+  int n;                // runs (0: per-nonzero gathers)
+  int elems;            // value-window elements per stage (sum of len)
+  int own;              // E: row lt's own w_old is at own + lt (the run holding offset 0)
+  int celems;           // E: code-window bytes per stage (sum of clen)
+  int cown;             // E: row lt's own code is at cown + lt
+  int w0;               // the run holding offset 0
+  int dinv_by_code;     // dinv[i] == pdinv[code[i]] for every row (checked)
+  int dinv_uniform;     // ... and every pdinv[k] is the same number: E needs no code windows
+  double dinv0;         // that number
+  long long ld;         // valid length of the windowed vectors (clamp)
+  long long code_ld;    // valid length of the code array (clamp)
+  int lo[kMaxWin];      // value windows: first offset, rounded down to even
+  int len[kMaxWin];     //   elements (even)
+  int base[kMaxWin];    //   first element in the stage's window area
+  int clo[kMaxWin];     // code windows (E): first offset, rounded down to 16
+  int clen[kMaxWin];    //   bytes (multiple of 16)
+  int cbase[kMaxWin];   //   first byte in the stage's code-window area
+};
+
 template <int TR>
 struct FusedLayoutS {
   static constexpr int kVecBytes = TR * 8;
-  static constexpr int kStageBytes = 7 * kVecBytes + TR;  // 7 vectors + codes
   static constexpr int kHeader = 1024;
+  // F+WIN: 7 vectors | w_old | dinv | codes | m windows
+  // E+WIN: 7 vectors | w_old windows | code windows
+  // gathers: 7 vectors | codes
+  __host__ __device__ static int stage_bytes(bool mg, bool win, int elems, int celems) {
+    if (win && mg) return 9 * kVecBytes + TR + elems * 8;
+    if (win) return 7 * kVecBytes + elems * 8 + celems;
+    return 7 * kVecBytes + TR;
+  }
 };
 
-// shared-memory bytes of a dictionary (start | off | val, 16-byte aligned parts)
+// shared-memory bytes of a dictionary: start | value index | code index |
+// val | per-code dinv (16-byte aligned parts)
 __host__ __device__ __forceinline__ int pat_smem_bytes(int n_pat, int n_e) {
-  return (int)(round_up(4LL * (n_pat + 1), 16) + round_up(4LL * n_e, 16) + 8LL * n_e);
+  return (int)(round_up(4LL * (n_pat + 1), 16) + 2 * round_up(4LL * n_e, 16) + 8LL * n_e +
+               round_up(8LL * n_pat, 16));
 }
 
-template <int TR, bool MG>
-__global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_s(FusedParams<int> P, int step) {
+template <int TR, bool MG, bool WIN>
+__global__ void __launch_bounds__(TR + 32, TR == 256 ? 3 : (TR == 128 ? 5 : 8)) pipecg_fused_kernel_s(FusedParams<int> P, WinTable W,
+                                                                 int step) {
   using L = FusedLayoutS<TR>;
   constexpr int NT = TR;
+  constexpr int VB = L::kVecBytes;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 8;
@@ -905,11 +956,15 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_s(FusedParams<int
   double* sc = reinterpret_cast<double*>(smem + 768);
   long long* s_it = reinterpret_cast<long long*>(smem + 896);
   int* pst = reinterpret_cast<int*>(smem + L::kHeader);
-  const int n_start = (int)round_up(P.n_pat + 1, 4), n_off = (int)round_up(P.n_pat_e, 4);
-  int* pof = pst + n_start;
-  double* pva = reinterpret_cast<double*>(pof + n_off);
+  const int n_start = (int)round_up(P.n_pat + 1, 4), n_e4 = (int)round_up(P.n_pat_e, 4);
+  int* pix = pst + n_start;  // WIN: value-window index of the entry for row 0; else the offset
+  int* pcx = pix + n_e4;     // E+WIN: code-window index of the entry for row 0
+  double* pva = reinterpret_cast<double*>(pcx + n_e4);
+  double* pdv = pva + P.n_pat_e;  // per-code dinv
   unsigned char* stage0 = smem + L::kHeader + round_up(pat_smem_bytes(P.n_pat, P.n_pat_e), 128);
+  const int SB = L::stage_bytes(MG, WIN, W.elems, W.celems);
   const int S = P.stages;
+  const bool dbc = W.dinv_by_code != 0;
 
   Ctrl* C = P.C;
   const int tid = threadIdx.x;
@@ -927,38 +982,99 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_s(FusedParams<int
   }
   // the dictionary is constant: load it before waiting on the previous grid
   for (int k = tid; k <= P.n_pat; k += blockDim.x) pst[k] = P.pstart[k];
+  for (int k = tid; k < P.n_pat; k += blockDim.x) pdv[k] = dbc ? P.pdinv[k] : 0.0;
   for (int k = tid; k < P.n_pat_e; k += blockDim.x) {
-    pof[k] = P.poff[k];
+    if (WIN) {
+      const int w = P.pwin[k];
+      pix[k] = W.base[w] + P.poff[k] - W.lo[w];
+      pcx[k] = W.cbase[w] + P.poff[k] - W.clo[w];
+    } else {
+      pix[k] = P.poff[k];
+    }
     pva[k] = P.pval[k];
   }
   pdl_wait();
 
+  // ---- producer ------------------------------------------------------------
+  // range [a, a + len) of an array of `esz`-byte elements, clamped to [0, lim)
+  auto range_copy = [&](unsigned char* dst, const unsigned char* src, long long a, int len,
+                        long long lim, int esz, uint64_t* bar, bool count_only) -> uint32_t {
+    const long long b = a + len;
+    const long long ca = a < 0 ? 0 : a, cb = b > lim ? lim : b;
+    if (cb <= ca) return 0;
+    const uint32_t bytes = (uint32_t)((cb - ca) * esz);
+    if (!count_only) bulk_g2s_nohint(dst + (ca - a) * esz, src + ca * esz, bytes, bar);
+    return bytes;
+  };
   uint64_t pol = 0;
-  auto issue = [&](long long j) {
+  // static part: expect the whole stage; copy what does not depend on the
+  // iteration (vectors, codes / code windows, F's dinv rows)
+  auto issue_static = [&](long long j) {
     const int s = (int)(j % S);
     const long long t0 = (t_lo + j * t_step) * TR;
     const long long rows = min((long long)TR, P.n - t0);
     const uint32_t b_vec = (uint32_t)((rows * 8 + 15) / 16 * 16);
     const uint32_t b_code = (uint32_t)((rows + 15) / 16 * 16);
-    unsigned char* sb = stage0 + (size_t)s * L::kStageBytes;
-    mbar_arrive_expect_tx(&full[s], 7 * b_vec + b_code);
+    unsigned char* sb = stage0 + (size_t)s * SB;
+    uint32_t tx = 7 * b_vec;
+    if (WIN && MG) {
+      tx += b_vec + (dbc ? 0 : b_vec) + b_code;
+      for (int w = 0; w < W.n; ++w)
+        tx += range_copy(nullptr, nullptr, t0 + W.lo[w], W.len[w], W.ld, 8, nullptr, true);
+    } else if (WIN) {
+      for (int w = 0; w < W.n; ++w) {
+        tx += range_copy(nullptr, nullptr, t0 + W.lo[w], W.len[w], W.ld, 8, nullptr, true);
+        if (!W.dinv_uniform || w == W.w0)
+          tx += range_copy(nullptr, nullptr, t0 + W.clo[w], W.clen[w], W.code_ld, 1, nullptr, true);
+      }
+    } else {
+      tx += b_code;
+    }
+    mbar_arrive_expect_tx(&full[s], tx);
 #pragma unroll
-    for (int k = 0; k < 7; ++k) bulk_g2s(sb + k * L::kVecBytes, P.vec[k] + t0, b_vec, &full[s], pol);
-    bulk_g2s_nohint(sb + 7 * L::kVecBytes, P.pcode + t0, b_code, &full[s]);
+    for (int k = 0; k < 7; ++k) bulk_g2s(sb + k * VB, P.vec[k] + t0, b_vec, &full[s], pol);
+    if (WIN && MG) {
+      if (!dbc) bulk_g2s_nohint(sb + 8 * VB, P.dinv + t0, b_vec, &full[s]);
+      bulk_g2s_nohint(sb + 9 * VB, P.pcode + t0, b_code, &full[s]);
+    } else if (WIN) {
+      unsigned char* carea = sb + 7 * VB + (size_t)W.elems * 8;
+      for (int w = 0; w < W.n; ++w)
+        if (!W.dinv_uniform || w == W.w0)
+          range_copy(carea + W.cbase[w], P.pcode, t0 + W.clo[w], W.clen[w], W.code_ld, 1, &full[s],
+                   false);
+    } else {
+      bulk_g2s_nohint(sb + 7 * VB, P.pcode + t0, b_code, &full[s]);
+    }
+  };
+  // iteration part: F: w_old rows + m_old windows; E: w_old windows
+  auto issue_dyn = [&](long long j, const double* w_src, const double* m_src) {
+    const int s = (int)(j % S);
+    const long long t0 = (t_lo + j * t_step) * TR;
+    const long long rows = min((long long)TR, P.n - t0);
+    unsigned char* sb = stage0 + (size_t)s * SB;
+    unsigned char* area = sb + (MG ? 9 * VB + TR : 7 * VB);
+    const unsigned char* src = reinterpret_cast<const unsigned char*>(MG ? m_src : w_src);
+    if (MG) bulk_g2s_nohint(sb + 7 * VB, w_src + t0, (uint32_t)((rows * 8 + 15) / 16 * 16), &full[s]);
+    for (int w = 0; w < W.n; ++w)
+      range_copy(area + (size_t)W.base[w] * 8, src, t0 + W.lo[w], W.len[w], W.ld, 8, &full[s], false);
   };
   if (tid == 0) {
     pol = policy_evict_first();
-    for (long long j = 0; j < my_tiles && j < S; ++j) issue(j);
+    for (long long j = 0; j < my_tiles && j < S; ++j) issue_static(j);
   }
   if (tid == 32) *s_it = read_status(C) == PCG_RUNNING ? C->base_it + step : -1;
   __syncthreads();
   const long long it = *reinterpret_cast<volatile long long*>(s_it);
+  const long long par = it < 0 ? 0 : it;
+  const double* w_old = P.w[par & 1];
+  const double* m_old = P.m[par & 1];
+  if (WIN && tid == 0)  // completes the first stages (also before an early exit)
+    for (long long j = 0; j < my_tiles && j < S; ++j) issue_dyn(j, w_old, m_old);
   if (it < 0) {
     if (tid == 0)
       for (long long j = 0; j < my_tiles && j < S; ++j) mbar_wait(&full[j], 0);
     return;
   }
-  const double* w_old = P.w[it & 1];
   double* w_new = P.w[(it + 1) & 1];
   if (!producer) {
     const Step stp = prologue<NT>(C, P.hist, P.rin, it, tid - 32, red, 1,
@@ -980,54 +1096,100 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_s(FusedParams<int
     if (tid == 0) {
       for (long long j = S; j < my_tiles; ++j) {
         mbar_wait(&empty[j % S], (uint32_t)((j / S - 1) & 1));
-        issue(j);
+        issue_static(j);
+        if (WIN) issue_dyn(j, w_old, m_old);
       }
     }
     return;
   }
 
+  // ---- consumers -----------------------------------------------------------
   const int lt = tid - 32;
-  const double* m_old = P.m[it & 1];
   double acc[3] = {0.0, 0.0, 0.0};
   for (long long j = 0; j < my_tiles; ++j) {
     const int s = (int)(j % S);
     const long long t0 = (t_lo + j * t_step) * TR;
     const long long rows = min((long long)TR, P.n - t0);
-    const unsigned char* sb = stage0 + (size_t)s * L::kStageBytes;
+    const unsigned char* sb = stage0 + (size_t)s * SB;
     const double* v_s = reinterpret_cast<const double*>(sb);
     const long long i = t0 + lt;
     double wi = 0.0, di = 0.0;
-    if (lt < rows) {
+    if (!WIN && lt < rows) {
       wi = ldg_nc(w_old + i);
       di = ldg_nc(P.dinv + i);
     }
     mbar_wait(&full[s], (uint32_t)((j / S) & 1));
     if (lt < rows) {
-      const int code = sb[7 * L::kVecBytes + lt];
-      const int lo = pst[code], hi = pst[code + 1];
-      const int ii = (int)i;
-      // n_i = sum_k a_ik * m_ck over the row's dictionary entries (= its CSR
-      // entries, same order); three explicit phases per batch as in A
       double nacc = 0.0;
-      for (int k0 = lo; k0 < hi; k0 += 8) {
-        double av[8], mv[8];
-        int cc[8];
+      if (WIN && MG) {
+        const double* win = reinterpret_cast<const double*>(sb + 9 * VB + TR);
+        const int code = sb[9 * VB + lt];
+        wi = v_s[7 * TR + lt];
+        di = dbc ? pdv[code] : v_s[8 * TR + lt];
+        const int lo = pst[code], hi = pst[code + 1];
+        for (int k = lo; k < hi; ++k) nacc = add(nacc, mul(pva[k], win[pix[k] + lt]));
+      } else if (WIN) {
+        const double* win = reinterpret_cast<const double*>(sb + 7 * VB);
+        const unsigned char* cwin = sb + 7 * VB + (size_t)W.elems * 8;
+        wi = win[W.own + lt];
+        const int code = cwin[W.cown + lt];
+        if (W.dinv_uniform) {  // one dinv for every row: only the own-row code window
+          di = W.dinv0;
+          const int lo = pst[code], hi = pst[code + 1];
+          for (int k0 = lo; k0 < hi; k0 += 8) {
+            double av[8], mv[8];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const int k = k0 + t < hi ? k0 + t : lo;
-          cc[t] = ii + pof[k];
-          av[t] = pva[k];
-        }
+            for (int t = 0; t < 8; ++t) {
+              const int k = k0 + t < hi ? k0 + t : lo;
+              av[t] = pva[k];
+              mv[t] = win[pix[k] + lt];
+            }
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          if (k0 + t < hi) {
-            const int c = cc[t];
-            mv[t] = MG ? ldg_nc(m_old + c) : mul(ldg_nc(P.dinv + c), ldg_nc(w_old + c));
+            for (int t = 0; t < 8; ++t)
+              if (k0 + t < hi) nacc = add(nacc, mul(av[t], mul(di, mv[t])));  // m = M^-1 w
+          }
+        } else {
+          di = pdv[code];
+          const int lo = pst[code], hi = pst[code + 1];
+          for (int k0 = lo; k0 < hi; k0 += 8) {
+            double av[8], mv[8], dv[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+              const int k = k0 + t < hi ? k0 + t : lo;
+              av[t] = pva[k];
+              mv[t] = win[pix[k] + lt];
+              dv[t] = pdv[cwin[pcx[k] + lt]];
+            }
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+              if (k0 + t < hi) nacc = add(nacc, mul(av[t], mul(dv[t], mv[t])));  // m = M^-1 w
           }
         }
+      } else {
+        // per-nonzero gathers, three explicit phases per batch as in A
+        const int code = sb[7 * VB + lt];
+        const int lo = pst[code], hi = pst[code + 1];
+        const int ii = (int)i;
+        for (int k0 = lo; k0 < hi; k0 += 8) {
+          double av[8], mv[8];
+          int cc[8];
 #pragma unroll
-        for (int t = 0; t < 8; ++t)
-          if (k0 + t < hi) nacc = add(nacc, mul(av[t], mv[t]));
+          for (int t = 0; t < 8; ++t) {
+            const int k = k0 + t < hi ? k0 + t : lo;
+            cc[t] = ii + pix[k];
+            av[t] = pva[k];
+          }
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            if (k0 + t < hi) {
+              const int c = cc[t];
+              mv[t] = MG ? ldg_nc(m_old + c) : mul(ldg_nc(P.dinv + c), ldg_nc(w_old + c));
+            }
+          }
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            if (k0 + t < hi) nacc = add(nacc, mul(av[t], mv[t]));
+        }
       }
       const double mi = mul(di, wi);
       const double zi = add(nacc, mul(beta, v_s[0 * TR + lt]));
@@ -2176,11 +2338,21 @@ struct pcg_solver {
   int* x_peer = nullptr;
   long long* x_dst = nullptr;
   FusedPlan plans[kVariants];      // per fused variant (stages == 0: does not fit)
+  std::vector<FusedPlan> alts[kVariants];  // E/F: occupancy alternatives the autotuner times
+  int alt_pick[kVariants] = {};    // ... and the one it picked
   double tune_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // autotune ms/iteration: fused A..E, engine 2
   int* tile_row = nullptr;         // variant D/E tiles of the applied plan
   long long* tile_e = nullptr;
   long long hub_len = 0;
   RowPatterns pat;                 // row-pattern dictionary (n_pat == 0: none)
+  // E/F windows: runs of the dictionary's offsets (patterns.cu; WinTable)
+  int n_runs = 0;                  // 0: per-nonzero gathers
+  int run_lo[kMaxWin] = {}, run_hi[kMaxWin] = {};
+  unsigned char* pwin = nullptr;   // [n_entries] run of each dictionary entry
+  double* pdinv = nullptr;         // [n_pat] dinv of each code's first row
+  bool dinv_by_code = false;       // dinv[i] == pdinv[code[i]] for every row (checked at init)
+  bool dinv_uniform = false;       // ... and all pdinv equal (dinv0)
+  double dinv0 = 0.0;
 };
 
 namespace {
@@ -2378,64 +2550,152 @@ int plan_d(pcg_solver* S, const int* cv, FusedPlan* best) {
 
 // Variants E / F (row-pattern dictionary): stages are 7 vectors + one code
 // byte per row; the dictionary sits in front of them for the whole kernel.
+// Runs of the dictionary's distinct offsets (gaps of at most kWinGap
+// elements are bridged): each run is one window per tile.  More than
+// kMaxWin runs -> E/F use per-nonzero gathers.
+constexpr int kWinGap = 16;
+int build_runs(pcg_solver* S) {
+  S->n_runs = 0;
+  const int ne = S->pat.n_entries;
+  if (S->pat.n_pat == 0 || getenv("PIPECG_B200_NO_WINDOWS")) return PCG_OK;
+  std::vector<int> off(ne);
+  int rc = cuda_status(cudaMemcpy(off.data(), S->pat.off, ne * sizeof(int), cudaMemcpyDeviceToHost),
+                       "pattern runs");
+  if (rc) return rc;
+  std::vector<int> d(off);
+  d.push_back(0);  // E reads each row's own w / dinv from the windows
+  std::sort(d.begin(), d.end());
+  d.erase(std::unique(d.begin(), d.end()), d.end());
+  int lo[kMaxWin], hi[kMaxWin], n = 0;
+  for (size_t k = 0; k < d.size(); ++k) {
+    if (n > 0 && d[k] - hi[n - 1] <= kWinGap) {
+      hi[n - 1] = d[k];
+      continue;
+    }
+    if (n == kMaxWin) return PCG_OK;  // too many runs: gathers
+    lo[n] = hi[n] = d[k];
+    ++n;
+  }
+  std::vector<unsigned char> run(ne);
+  for (int k = 0; k < ne; ++k)
+    for (int w = 0; w < n; ++w)
+      if (off[k] >= lo[w] && off[k] <= hi[w]) run[k] = (unsigned char)w;
+  if (cudaMalloc(&S->pwin, std::max(ne, 1)) != cudaSuccess)
+    return set_error(PCG_ENOMEM, "pattern runs");
+  rc = cuda_status(cudaMemcpy(S->pwin, run.data(), ne, cudaMemcpyHostToDevice), "pattern runs");
+  if (rc) return rc;
+  S->n_runs = n;
+  for (int w = 0; w < n; ++w) {
+    S->run_lo[w] = lo[w];
+    S->run_hi[w] = hi[w];
+  }
+  return PCG_OK;
+}
+
+// Window geometry of tile height tr (see pipecg_fused_kernel_s)
+WinTable win_table(const pcg_solver* S, int tr) {
+  WinTable W{};
+  W.n = S->n_runs;
+  W.ld = (long long)S->ld;
+  W.code_ld = (S->A.n_rows + 256) & ~15LL;
+  W.dinv_by_code = S->dinv_by_code ? 1 : 0;
+  W.dinv_uniform = S->dinv_by_code && S->dinv_uniform ? 1 : 0;
+  W.dinv0 = S->dinv0;
+  int base = 0, cbase = 0;
+  for (int w = 0; w < W.n; ++w) {
+    const int lo = S->run_lo[w], hi = S->run_hi[w];
+    W.lo[w] = lo - (((lo % 2) + 2) % 2);  // round down to even (16-byte copies)
+    W.len[w] = (int)round_up(tr + hi - W.lo[w], 2);
+    W.base[w] = base;
+    base += W.len[w];
+    W.clo[w] = lo - (((lo % 16) + 16) % 16);  // round down to 16
+    W.clen[w] = (int)round_up(tr + hi - W.clo[w], 16);
+    W.cbase[w] = cbase;
+    cbase += W.clen[w];
+    if (lo <= 0 && hi >= 0) {  // the run holding offset 0: each row's own value
+      W.own = W.base[w] - W.lo[w];
+      W.cown = W.cbase[w] - W.clo[w];
+      W.w0 = w;
+    }
+  }
+  W.elems = base;
+  W.celems = cbase;
+  return W;
+}
+
+// E reads windows only when dinv is a function of the row's code; F always
+inline bool s_windows(const pcg_solver* S, bool mg) {
+  return S->n_runs > 0 && (mg || S->dinv_by_code);
+}
+
+// One E/F plan: tile height TR with exactly `bps` CTAs per SM (3 stages if
+// they fit, else 2).  stages == 0: does not fit.
 template <int TR, bool MG>
-int plan_one_s(pcg_solver* S, FusedPlan* out) {
+int plan_one_s(pcg_solver* S, int bps, FusedPlan* out) {
   FusedPlan p;
   p.variant = MG ? 6 : 5;
   p.tr = TR;
-  const size_t sb = FusedLayoutS<TR>::kStageBytes;
+  const bool win = s_windows(S, MG);
+  const WinTable W = win_table(S, TR);
+  const size_t sb = FusedLayoutS<TR>::stage_bytes(MG, win, W.elems, W.celems);
   const size_t hdr = FusedLayoutS<TR>::kHeader +
                      (size_t)round_up(pat_smem_bytes(S->pat.n_pat, S->pat.n_entries), 128);
   const size_t sm_budget = 228 * 1024, cta_max = 227 * 1024;
   const char* e_st = getenv("PIPECG_B200_STAGES");
-  const char* e_bps = getenv("PIPECG_B200_BPS");
-  for (int bps = e_bps ? atoi(e_bps) : 2; bps >= 1 && !p.stages; --bps) {
-    if (e_bps && bps != atoi(e_bps)) break;
-    for (int st = e_st ? atoi(e_st) : 3; st <= 8; ++st) {
-      const size_t need = hdr + st * sb;
-      if (need <= cta_max && (need + 1024) * bps <= sm_budget) {
-        p.stages = st;
-        p.bps = bps;
-        p.smem = need;
-        break;
-      }
-      if (e_st) break;
+  for (int st = e_st ? atoi(e_st) : 3; st >= 2; --st) {
+    const size_t need = hdr + st * sb;
+    if (need <= cta_max && (need + 1024) * bps <= sm_budget) {
+      p.stages = st;
+      p.bps = bps;
+      p.smem = need;
+      break;
     }
+    if (e_st) break;
   }
   if (!p.stages) {
     *out = p;
     return PCG_OK;
   }
   int occ = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pipecg_fused_kernel_s<TR, MG>,
-                                                                TR + 32, p.smem);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &occ, win ? pipecg_fused_kernel_s<TR, MG, true> : pipecg_fused_kernel_s<TR, MG, false>,
+      TR + 32, p.smem);
   if (e != cudaSuccess) return cuda_status(e, "pattern occupancy");
-  occ = std::min(occ, p.bps);
-  if (occ < 1) {
+  if (occ < bps) {  // registers do not allow this many CTAs
     p.stages = 0;
     *out = p;
     return PCG_OK;
   }
   const long long n_tiles = (S->A.n_rows + TR - 1) / TR;
-  p.grid = (int)std::max<long long>(std::min<long long>((long long)occ * S->num_sms, n_tiles), 1);
-  p.score = occ * TR;
+  p.grid = (int)std::max<long long>(std::min<long long>((long long)bps * S->num_sms, n_tiles), 1);
+  p.score = bps * TR;
   *out = p;
   return PCG_OK;
 }
 
+// E/F candidates for the autotuner: 256-row tiles with 2, 3 and 4 CTAs per
+// SM (the best count depends on the stencil: 3D 7-pt E 256^3 0.366 ms with
+// 3 vs 0.460 ms with 2; 27-pt F 400^3 1.81 ms with 2 vs 2.03 ms with 4);
+// 128 / 64-row tiles only when 256 rows do not fit.  best = the first.
 template <bool MG>
-int plan_variant_s(pcg_solver* S, FusedPlan* best) {
-  FusedPlan p[3];
-  int rc = plan_one_s<256, MG>(S, &p[0]);
-  if (!rc) rc = plan_one_s<128, MG>(S, &p[1]);
-  if (!rc) rc = plan_one_s<64, MG>(S, &p[2]);
-  if (rc) return rc;
+int plan_variant_s(pcg_solver* S, FusedPlan* best, std::vector<FusedPlan>* alts) {
+  alts->clear();
   const char* e_tr = getenv("PIPECG_B200_TR");
-  *best = FusedPlan();
+  const char* e_bps = getenv("PIPECG_B200_BPS");
+  const int tr_pick = e_tr ? atoi(e_tr) : 0;
+  const int order[3] = {MG ? 2 : 3, MG ? 3 : 2, 4};  // default first
   for (int k = 0; k < 3; ++k) {
-    if (!p[k].stages || (e_tr && atoi(e_tr) != p[k].tr)) continue;
-    if (p[k].score > best->score) *best = p[k];
+    const int bps = e_bps ? atoi(e_bps) : order[k];
+    FusedPlan p;
+    int rc = PCG_OK;
+    if (!tr_pick || tr_pick == 256) rc = plan_one_s<256, MG>(S, bps, &p);
+    if (!rc && !p.stages && (!tr_pick || tr_pick == 128)) rc = plan_one_s<128, MG>(S, 2 * bps, &p);
+    if (!rc && !p.stages && (!tr_pick || tr_pick == 64)) rc = plan_one_s<64, MG>(S, 4 * bps, &p);
+    if (rc) return rc;
+    if (p.stages) alts->push_back(p);
+    if (e_bps) break;
   }
+  *best = alts->empty() ? FusedPlan() : alts->front();
   return PCG_OK;
 }
 
@@ -2465,8 +2725,8 @@ int fused_setup(pcg_solver* S) {
     if ((long long)occ * S->num_sms >= p.grid) S->plans[4] = p;
   }
   // E / F: only when the matrix has a row-pattern dictionary (built by the caller)
-  if (!rc && S->pat.n_pat > 0) rc = plan_variant_s<false>(S, &S->plans[5]);
-  if (!rc && S->pat.n_pat > 0) rc = plan_variant_s<true>(S, &S->plans[6]);
+  if (!rc && S->pat.n_pat > 0) rc = plan_variant_s<false>(S, &S->plans[5], &S->alts[5]);
+  if (!rc && S->pat.n_pat > 0) rc = plan_variant_s<true>(S, &S->plans[6], &S->alts[6]);
   if (rc) return rc;
   bool any = false;
   for (int v = 0; v < kVariants; ++v) any = any || S->plans[v].stages > 0;
@@ -2491,7 +2751,7 @@ void apply_plan(pcg_solver* S, const FusedPlan& p) {
 int alloc_state(pcg_solver* S) {
   const long long n = std::max(S->A.n_rows, S->A.n_cols);
   S->ld = (size_t)round_up(n + 32, 256);
-  const int nvec = 13;  // z q s p x r u w0 w1 m n b + spare
+  const int nvec = 13;  // z q s p x r u w0 w1 m n b m2
   cudaError_t e = cudaMalloc(&S->vbuf, S->ld * nvec * sizeof(double));
   if (e != cudaSuccess) return set_error(PCG_ENOMEM, "solver: vector allocation failed");
   cudaMemsetAsync(S->vbuf, 0, S->ld * nvec * sizeof(double), S->stream);
@@ -2604,6 +2864,8 @@ FusedParams<RP> fused_params(pcg_solver* S) {
   P.pstart = S->pat.start;
   P.poff = S->pat.off;
   P.pval = S->pat.val;
+  P.pwin = S->pwin;
+  P.pdinv = S->pdinv;
   P.n_pat = S->pat.n_pat;
   P.n_pat_e = S->pat.n_entries;
   P.X = FusedXchg{};
@@ -2653,13 +2915,18 @@ void launch_fused(pcg_solver* S, int k) {
   const int variant = S->variant == 4 ? 2 : S->variant;  // P, launched per iteration, is C
   if (variant == 5 || variant == 6) {
     const FusedParams<int> PS = fused_params<int>(S);  // E/F never read the row pointers
-#define PCG_LS(MGV)                                                                             \
-  switch (S->tr) {                                                                              \
-    case 256: launch_k(pipecg_fused_kernel_s<256, MGV>, g, 256 + 32, sm, st, pdl, PS, k); break; \
-    case 128: launch_k(pipecg_fused_kernel_s<128, MGV>, g, 128 + 32, sm, st, pdl, PS, k); break; \
-    default: launch_k(pipecg_fused_kernel_s<64, MGV>, g, 64 + 32, sm, st, pdl, PS, k); break;    \
+    const WinTable W = win_table(S, S->tr);
+#define PCG_LS(MGV, WV)                                                                                \
+  switch (S->tr) {                                                                                     \
+    case 256: launch_k(pipecg_fused_kernel_s<256, MGV, WV>, g, 256 + 32, sm, st, pdl, PS, W, k); break; \
+    case 128: launch_k(pipecg_fused_kernel_s<128, MGV, WV>, g, 128 + 32, sm, st, pdl, PS, W, k); break; \
+    default: launch_k(pipecg_fused_kernel_s<64, MGV, WV>, g, 64 + 32, sm, st, pdl, PS, W, k); break;    \
   }
-    if (variant == 6) { PCG_LS(true) } else { PCG_LS(false) }
+    const bool win = s_windows(S, variant == 6);
+    if (variant == 6 && win) { PCG_LS(true, true) }
+    else if (variant == 6) { PCG_LS(true, false) }
+    else if (win) { PCG_LS(false, true) }
+    else { PCG_LS(false, false) }
 #undef PCG_LS
   } else if (variant == 1) {
     switch (S->tr) {
@@ -2882,6 +3149,9 @@ void fill_result(pcg_solver* S, const Ctrl& c, pcg_result* res) {
   res->status = c.status;
   res->engine = S->engine == 1 ? 3 + S->variant : 2;
   for (int k = 0; k < 8; ++k) res->tune_ms[k] = S->tune_ms[k];
+  res->pattern_flags = S->pat.n_pat == 0 ? 0
+                       : 1 | (S->n_runs > 0 ? 2 : 0) | (S->dinv_by_code ? 4 : 0) |
+                             (S->dinv_by_code && S->dinv_uniform ? 8 : 0);
   res->graph_launches = S->graph_launches;
   res->norm0 = c.init.norm;
   res->breakdown_quantity = c.bd_code;
@@ -2938,9 +3208,11 @@ int preload_solver() {
   PCG_LOAD((pipecg_fused_kernel_d<int, 64>)); PCG_LOAD((pipecg_fused_kernel_d<long long, 256>));
   PCG_LOAD((pipecg_fused_kernel_d<long long, 128>)); PCG_LOAD((pipecg_fused_kernel_d<long long, 64>));
   PCG_LOAD(tile_build_kernel<int>); PCG_LOAD(tile_build_kernel<long long>); PCG_LOAD(tile_close_kernel);
-  PCG_LOAD((pipecg_fused_kernel_s<256, false>)); PCG_LOAD((pipecg_fused_kernel_s<128, false>));
-  PCG_LOAD((pipecg_fused_kernel_s<64, false>)); PCG_LOAD((pipecg_fused_kernel_s<256, true>));
-  PCG_LOAD((pipecg_fused_kernel_s<128, true>)); PCG_LOAD((pipecg_fused_kernel_s<64, true>));
+#define PCG_LOAD_S(MG, WV) \
+  PCG_LOAD((pipecg_fused_kernel_s<256, MG, WV>)); PCG_LOAD((pipecg_fused_kernel_s<128, MG, WV>)); \
+  PCG_LOAD((pipecg_fused_kernel_s<64, MG, WV>))
+  PCG_LOAD_S(false, false); PCG_LOAD_S(true, false); PCG_LOAD_S(false, true); PCG_LOAD_S(true, true);
+#undef PCG_LOAD_S
 
   PCG_LOAD(pipecg_k1_kernel); PCG_LOAD(gated_spmv_rows<int>); PCG_LOAD(gated_spmv_rows<long long>);
   PCG_LOAD(gated_spmv_long<int>); PCG_LOAD(gated_spmv_long<long long>);
@@ -2980,9 +3252,11 @@ int preload_solver() {
   PCG_SMEM((pipecg_fused_kernel_d<int, 256>)); PCG_SMEM((pipecg_fused_kernel_d<int, 128>));
   PCG_SMEM((pipecg_fused_kernel_d<int, 64>)); PCG_SMEM((pipecg_fused_kernel_d<long long, 256>));
   PCG_SMEM((pipecg_fused_kernel_d<long long, 128>)); PCG_SMEM((pipecg_fused_kernel_d<long long, 64>));
-  PCG_SMEM((pipecg_fused_kernel_s<256, false>)); PCG_SMEM((pipecg_fused_kernel_s<128, false>));
-  PCG_SMEM((pipecg_fused_kernel_s<64, false>)); PCG_SMEM((pipecg_fused_kernel_s<256, true>));
-  PCG_SMEM((pipecg_fused_kernel_s<128, true>)); PCG_SMEM((pipecg_fused_kernel_s<64, true>));
+#define PCG_SMEM_S(MG, WV) \
+  PCG_SMEM((pipecg_fused_kernel_s<256, MG, WV>)); PCG_SMEM((pipecg_fused_kernel_s<128, MG, WV>)); \
+  PCG_SMEM((pipecg_fused_kernel_s<64, MG, WV>))
+  PCG_SMEM_S(false, false); PCG_SMEM_S(true, false); PCG_SMEM_S(false, true); PCG_SMEM_S(true, true);
+#undef PCG_SMEM_S
 #undef PCG_SMEM
   if (e != cudaSuccess) return cuda_status(e, "preload solver kernels");
   rc = preload_patterns();
@@ -3136,15 +3410,16 @@ struct TuneKey {
   long long n_rows, n_cols, nnz;
   int rp64;
   long long max_row;
-  int sms, dot_mode, req, n_pat;
+  int sms, dot_mode, req, n_pat, dinv_mode;
   bool operator<(const TuneKey& o) const {
-    return std::tie(dev, n_rows, n_cols, nnz, rp64, max_row, sms, dot_mode, req, n_pat) <
+    return std::tie(dev, n_rows, n_cols, nnz, rp64, max_row, sms, dot_mode, req, n_pat, dinv_mode) <
            std::tie(o.dev, o.n_rows, o.n_cols, o.nnz, o.rp64, o.max_row, o.sms, o.dot_mode, o.req,
-                    o.n_pat);
+                    o.n_pat, o.dinv_mode);
   }
 };
-std::map<TuneKey, int>& tune_cache() {
-  static std::map<TuneKey, int> m;
+// value: variant (kVariants = engine 2) and the E/F alternative picked
+std::map<TuneKey, std::pair<int, int>>& tune_cache() {
+  static std::map<TuneKey, std::pair<int, int>> m;
   return m;
 }
 std::mutex& tune_cache_mu() {
@@ -3170,32 +3445,47 @@ int autotune(pcg_solver* S, int grid2, bool with_engine2, bool irregular) {
     if (cand < kVariants) {
       // B (gather warps) never won a measurement; D only pays for irregular rows
       if (!S->plans[cand].stages || cand == 1 || (cand == 3 && !irregular)) continue;
-      S->engine = 1;
-      apply_plan(S, S->plans[cand]);
-    } else {
-      S->engine = 2;
-      S->grid = S->n_partials = grid2;
     }
-    // b := n (ones), x0 := z (zeros); init copies them before overwriting
-    rc = pipecg_b200_solver_init(S, S->nv, S->z, 0.0, 1LL << 40, 0, st);
-    cudaGraphExec_t ge = nullptr;
-    if (!rc && S->opt.use_graphs) rc = chunk_graph(S, kTuneIters, 1, &ge);
-    if (!rc) rc = launch_chunk(S, 2, 0);
-    cudaEventRecord(e0, st);
-    if (!rc) rc = launch_chunk(S, kTuneIters, 1);
-    cudaEventRecord(e1, st);
-    if (!rc) rc = cuda_status(cudaEventSynchronize(e1), "autotune");
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    ms /= (float)kTuneIters;
-    S->tune_ms[cand] = ms;
-    for (int k = 0; k < 2; ++k) {  // graphs bake in this candidate's launch parameters
-      for (auto& kv : S->graphs[k]) cudaGraphExecDestroy(kv.second);
-      S->graphs[k].clear();
+    // E/F: every occupancy alternative; the fastest becomes the variant's plan
+    const int n_alt = cand < kVariants && !S->alts[cand].empty() ? (int)S->alts[cand].size() : 1;
+    float cand_ms = 0.f;
+    for (int a = 0; a < n_alt && !rc; ++a) {
+      if (cand < kVariants) {
+        S->engine = 1;
+        apply_plan(S, S->alts[cand].empty() ? S->plans[cand] : S->alts[cand][a]);
+      } else {
+        S->engine = 2;
+        S->grid = S->n_partials = grid2;
+      }
+      // b := n (ones), x0 := z (zeros); init copies them before overwriting
+      rc = pipecg_b200_solver_init(S, S->nv, S->z, 0.0, 1LL << 40, 0, st);
+      cudaGraphExec_t ge = nullptr;
+      if (!rc && S->opt.use_graphs) rc = chunk_graph(S, kTuneIters, 1, &ge);
+      if (!rc) rc = launch_chunk(S, 2, 0);
+      cudaEventRecord(e0, st);
+      if (!rc) rc = launch_chunk(S, kTuneIters, 1);
+      cudaEventRecord(e1, st);
+      if (!rc) rc = cuda_status(cudaEventSynchronize(e1), "autotune");
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ms /= (float)kTuneIters;
+      for (int k = 0; k < 2; ++k) {  // graphs bake in this candidate's launch parameters
+        for (auto& kv : S->graphs[k]) cudaGraphExecDestroy(kv.second);
+        S->graphs[k].clear();
+      }
+      if (rc) break;
+      if (a == 0 || ms < cand_ms) {
+        cand_ms = ms;
+        if (cand < kVariants && !S->alts[cand].empty()) {
+          S->plans[cand] = S->alts[cand][a];
+          S->alt_pick[cand] = a;
+        }
+      }
     }
-    if (!rc && (best < 0 || ms < best_ms)) {
+    S->tune_ms[cand] = cand_ms;
+    if (!rc && (best < 0 || cand_ms < best_ms)) {
       best = cand;
-      best_ms = ms;
+      best_ms = cand_ms;
     }
   }
   cudaEventDestroy(e0);
@@ -3284,6 +3574,14 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     // matrices or when the rows are too diverse (patterns.cu)
     if (!has_long && !getenv("PIPECG_B200_NO_PATTERNS")) {
       rc = build_row_patterns(A->n_rows, A->rp64, A->rowptr, A->col, A->val, S->stream, &S->pat);
+      if (!rc) rc = build_runs(S);
+      if (!rc && S->pat.n_pat > 0) {
+        if (cudaMalloc(&S->pdinv, S->pat.n_pat * sizeof(double)) != cudaSuccess)
+          rc = set_error(PCG_ENOMEM, "pattern dinv");
+        else
+          rc = check_dinv_by_code(S->pat, A->n_rows, A->inv_diag, S->pdinv, &S->dinv_by_code,
+                                  &S->dinv_uniform, &S->dinv0, S->stream);
+      }
       if (rc) {
         pipecg_b200_solver_destroy(S);
         return rc;
@@ -3370,13 +3668,16 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     // with the same shape and row-length profile on the same device reuses
     // the measured choice instead of re-timing every candidate
     const TuneKey key{dev, A->n_rows, A->n_cols, A->nnz, A->rp64, (long long)max_row,
-                      S->num_sms, S->opt.dot_mode, req, S->pat.n_pat};
-    int cached = -1;
+                      S->num_sms, S->opt.dot_mode, req, S->pat.n_pat,
+                      (S->dinv_by_code ? 1 : 0) + (S->dinv_uniform ? 2 : 0)};
+    int cached = -1, cached_alt = 0;
     if (!getenv("PIPECG_B200_NO_TUNE_CACHE")) {
       std::lock_guard<std::mutex> lk(tune_cache_mu());
       auto it = tune_cache().find(key);
-      if (it != tune_cache().end()) cached = it->second;
+      if (it != tune_cache().end()) std::tie(cached, cached_alt) = it->second;
     }
+    if (cached >= 0 && cached < kVariants && cached_alt < (int)S->alts[cached].size())
+      S->plans[cached] = S->alts[cached][cached_alt];
     if (cached >= 0 && (cached == kVariants || S->plans[cached].stages)) {
       if (cached < kVariants) {
         S->engine = 1;
@@ -3392,7 +3693,8 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
         return rc;
       }
       std::lock_guard<std::mutex> lk(tune_cache_mu());
-      tune_cache()[key] = S->engine == 2 ? kVariants : S->variant;
+      tune_cache()[key] = S->engine == 2 ? std::make_pair(kVariants, 0)
+                                         : std::make_pair(S->variant, S->alt_pick[S->variant]);
     }
   }
   *out = S;
@@ -3436,6 +3738,8 @@ int pipecg_b200_solver_destroy(pcg_solver* S) {
     cudaFree(S->plans[v].tile_e);
   }
   free_row_patterns(&S->pat);
+  cudaFree(S->pwin);
+  cudaFree(S->pdinv);
 
   if (S->ev_in) cudaEventDestroy(S->ev_in);
   if (S->stream) cudaStreamDestroy(S->stream);
@@ -3590,6 +3894,22 @@ int pipecg_b200_solver_init(pcg_solver* S, const double* b, const double* x0, do
   // solvers.py:305-321
   cudaMemcpyAsync(S->b, b, bytes, cudaMemcpyDeviceToDevice, st);
   cudaMemcpyAsync(S->x, x0, bytes, cudaMemcpyDeviceToDevice, st);
+  if (S->pat.n_pat > 0) {  // is dinv still a function of the row's code? (E/F read it so)
+    bool dbc = false, uni = false;
+    double d0 = 0.0;
+    int rc = check_dinv_by_code(S->pat, n, S->A.inv_diag, S->pdinv, &dbc, &uni, &d0, st);
+    if (rc) return rc;
+    if (dbc != S->dinv_by_code || uni != S->dinv_uniform ||
+        std::memcmp(&d0, &S->dinv0, sizeof(double)) != 0) {
+      S->dinv_by_code = dbc;
+      S->dinv_uniform = uni;
+      S->dinv0 = d0;
+      for (int k = 0; k < 2; ++k) {  // graphs bake the kernel choice in
+        for (auto& kv : S->graphs[k]) cudaGraphExecDestroy(kv.second);
+        S->graphs[k].clear();
+      }
+    }
+  }
   if (S->connected) {  // x halo (r = b - A x reads it)
     snapshot_arrive_kernel<<<1, 32, 0, st>>>(R.C, S->comm);
     vec_exchange_kernel<<<kXchgBlocks, 256, 0, st>>>(S->cp, 4, S->x);

@@ -154,3 +154,40 @@ def test_autotuned_engine_bitwise(cuda):
     it picks is bitwise the reference in seq mode."""
     rep = _seq_vs_oracle(pb.stencil_host("3d7", 48), "auto", max_it=3000)
     assert rep.iterations > 10
+
+
+def _seq_with_dinv(A, d, engine, opts_pc=None):
+    x_true, b, x0, _ = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=3000)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=3000, record_history=True)
+    pc = opts_pc if opts_pc is not None else pb.JacobiPreconditioner(d)
+    x, rep = pb.pipecg_solve(A, b, x0, pc, cfg, options=pb.DeviceOptions(dot_mode="seq", engine=engine))
+    assert rep.history == ref.history
+    np.testing.assert_array_equal(x, ref.x)
+
+
+@pytest.mark.parametrize("engine", ["fused-e", "fused-f"])
+def test_dinv_not_a_function_of_the_code(cuda, engine):
+    """A preconditioner that is not 1/diag of the pattern (some rows scaled):
+    E falls back to per-nonzero gathers, F stages dinv -- still bitwise."""
+    A = pb.stencil_host("3d7", 14)
+    d = oracle.jacobi_inv_diag(A).copy()
+    d[[5, 77, 1000]] *= 1.0 + 2.0**-20
+    _seq_with_dinv(A, d, engine)
+
+
+@pytest.mark.parametrize("engine", ["fused-e", "fused-f"])
+def test_dinv_changed_in_place_between_solves(cuda, engine):
+    """The cached solver re-checks dinv at every solve (solver_init)."""
+    A = pb.stencil_host("3d7", 12)
+    d0 = oracle.jacobi_inv_diag(A)
+    dev = torch.from_numpy(d0.copy()).cuda()
+    pc = pb.JacobiPreconditioner(dev)
+    _seq_with_dinv(A, d0, engine, pc)
+    d1 = d0.copy()
+    d1[[3, 500]] *= 1.0 - 2.0**-18
+    dev.copy_(torch.from_numpy(d1))
+    _seq_with_dinv(A, d1, engine, pc)
+    dev.copy_(torch.from_numpy(d0))
+    _seq_with_dinv(A, d0, engine, pc)
