@@ -367,9 +367,8 @@ __device__ __forceinline__ void publish_partials(double (&acc)[3], int lt, doubl
 // Halo rows of tile t -> the peers (see FusedXchg); consumers only (named
 // barrier `bar_id` makes the tile's new values visible CTA-wide first).
 template <int NT>
-__device__ __forceinline__ void tile_exchange(const FusedXchg& X, long long t, int lt,
-                                              const double* src, int vec, int bar_id) {
-  const int e0 = X.ptr[t], e1 = X.ptr[t + 1];
+__device__ __forceinline__ void tile_exchange_range(const FusedXchg& X, int e0, int e1, int lt,
+                                                    const double* src, int vec, int bar_id) {
   if (e1 <= e0) return;  // uniform across the CTA
   bar_sync(bar_id, NT);
   bool sent = false;
@@ -380,6 +379,11 @@ __device__ __forceinline__ void tile_exchange(const FusedXchg& X, long long t, i
     sent = true;
   }
   if (sent) __threadfence_system();  // before this CTA's ticket (publish_partials)
+}
+template <int NT>
+__device__ __forceinline__ void tile_exchange(const FusedXchg& X, long long t, int lt,
+                                              const double* src, int vec, int bar_id) {
+  tile_exchange_range<NT>(X, X.ptr[t], X.ptr[t + 1], lt, src, vec, bar_id);
 }
 
 // ===========================================================================
@@ -418,6 +422,7 @@ struct FusedParams {
   const double* pval;          // [n_pat_e]
   const unsigned char* pwin;   // [n_pat_e] window of each entry (WinTable)
   const double* pdinv;         // [n_pat] dinv of each code (valid when WinTable.dinv_by_code)
+  const unsigned short* tile_runs;  // [n_tiles] runs the tile's rows use (WinTable bit w)
   int n_pat, n_pat_e;
 };
 
@@ -935,6 +940,12 @@ struct FusedLayoutS {
   }
 };
 
+__device__ __forceinline__ unsigned tile_mask(const unsigned short* runs, long long t) {
+  unsigned short v;
+  asm volatile("ld.global.nc.u16 %0, [%1];" : "=h"(v) : "l"(runs + t));
+  return v;
+}
+
 // shared-memory bytes of a dictionary: start | value index | code index |
 // val | per-code dinv (16-byte aligned parts)
 __host__ __device__ __forceinline__ int pat_smem_bytes(int n_pat, int n_e) {
@@ -942,9 +953,13 @@ __host__ __device__ __forceinline__ int pat_smem_bytes(int n_pat, int n_e) {
                round_up(8LL * n_pat, 16));
 }
 
-template <int TR, bool MG, bool WIN>
-__global__ void __launch_bounds__(TR + 32, TR == 256 ? 3 : (TR == 128 ? 5 : 8)) pipecg_fused_kernel_s(FusedParams<int> P, WinTable W,
-                                                                 int step) {
+// XG: distributed (row-block shard, [owned | halo] columns): the tile's halo
+// rows of w (E) / m (F) are pushed to the peers after each tile, and the
+// windows of the first stages are requested only after the prologue has
+// seen every peer's previous iteration (they may cover halo rows).
+template <int TR, bool MG, bool WIN, bool XG = false>
+__global__ void __launch_bounds__(TR + 32, TR == 256 ? 3 : (TR == 128 ? 5 : 8))
+    pipecg_fused_kernel_s(FusedParams<int> P, WinTable W, int step) {
   using L = FusedLayoutS<TR>;
   constexpr int NT = TR;
   constexpr int VB = L::kVecBytes;
@@ -955,6 +970,7 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? 3 : (TR == 128 ? 5 : 8)) 
   volatile int* decision = reinterpret_cast<volatile int*>(smem + 512);
   double* sc = reinterpret_cast<double*>(smem + 768);
   long long* s_it = reinterpret_cast<long long*>(smem + 896);
+  unsigned* s_msk = reinterpret_cast<unsigned*>(smem + 128);  // run masks of the first stages
   int* pst = reinterpret_cast<int*>(smem + L::kHeader);
   const int n_start = (int)round_up(P.n_pat + 1, 4), n_e4 = (int)round_up(P.n_pat_e, 4);
   int* pix = pst + n_start;  // WIN: value-window index of the entry for row 0; else the offset
@@ -1009,7 +1025,12 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? 3 : (TR == 128 ? 5 : 8)) 
   uint64_t pol = 0;
   // static part: expect the whole stage; copy what does not depend on the
   // iteration (vectors, codes / code windows, F's dinv rows)
-  auto issue_static = [&](long long j) {
+  // msk: the runs the tile's rows use -- distributed only (a shard's halo
+  // runs are used by its boundary tiles alone); P.tile_runs is loaded
+  // ahead: a global load in front of each tile's copies stalled the
+  // producer (measured 0.366 -> 0.460 ms at 256^3).  On one GPU every run
+  // is copied (costs less than the mask bookkeeping, measured)
+  auto issue_static = [&](long long j, unsigned msk) {
     const int s = (int)(j % S);
     const long long t0 = (t_lo + j * t_step) * TR;
     const long long rows = min((long long)TR, P.n - t0);
@@ -1020,10 +1041,12 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? 3 : (TR == 128 ? 5 : 8)) 
     if (WIN && MG) {
       tx += b_vec + (dbc ? 0 : b_vec) + b_code;
       for (int w = 0; w < W.n; ++w)
-        tx += range_copy(nullptr, nullptr, t0 + W.lo[w], W.len[w], W.ld, 8, nullptr, true);
+        if ((msk >> w) & 1)
+          tx += range_copy(nullptr, nullptr, t0 + W.lo[w], W.len[w], W.ld, 8, nullptr, true);
     } else if (WIN) {
       for (int w = 0; w < W.n; ++w) {
-        tx += range_copy(nullptr, nullptr, t0 + W.lo[w], W.len[w], W.ld, 8, nullptr, true);
+        if ((msk >> w) & 1)
+          tx += range_copy(nullptr, nullptr, t0 + W.lo[w], W.len[w], W.ld, 8, nullptr, true);
         if (!W.dinv_uniform || w == W.w0)
           tx += range_copy(nullptr, nullptr, t0 + W.clo[w], W.clen[w], W.code_ld, 1, nullptr, true);
       }
@@ -1046,21 +1069,31 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? 3 : (TR == 128 ? 5 : 8)) 
       bulk_g2s_nohint(sb + 7 * VB, P.pcode + t0, b_code, &full[s]);
     }
   };
-  // iteration part: F: w_old rows + m_old windows; E: w_old windows
-  auto issue_dyn = [&](long long j, const double* w_src, const double* m_src) {
+  // iteration part: F: w_old rows + m_old windows; E: w_old windows.
+  // part 0: what this rank wrote itself (own rows), 1: windows reaching
+  // into the halo (written by the peers; distributed only), 2: both
+  auto issue_dyn = [&](long long j, const double* w_src, const double* m_src, int part,
+                       unsigned msk) {
     const int s = (int)(j % S);
     const long long t0 = (t_lo + j * t_step) * TR;
     const long long rows = min((long long)TR, P.n - t0);
     unsigned char* sb = stage0 + (size_t)s * SB;
     unsigned char* area = sb + (MG ? 9 * VB + TR : 7 * VB);
     const unsigned char* src = reinterpret_cast<const unsigned char*>(MG ? m_src : w_src);
-    if (MG) bulk_g2s_nohint(sb + 7 * VB, w_src + t0, (uint32_t)((rows * 8 + 15) / 16 * 16), &full[s]);
-    for (int w = 0; w < W.n; ++w)
-      range_copy(area + (size_t)W.base[w] * 8, src, t0 + W.lo[w], W.len[w], W.ld, 8, &full[s], false);
+    if (MG && part != 1)
+      bulk_g2s_nohint(sb + 7 * VB, w_src + t0, (uint32_t)((rows * 8 + 15) / 16 * 16), &full[s]);
+    for (int w = 0; w < W.n; ++w) {
+      const bool halo = XG && t0 + W.lo[w] + W.len[w] > P.n;
+      if (((msk >> w) & 1) && (part == 2 || halo == (part == 1)))
+        range_copy(area + (size_t)W.base[w] * 8, src, t0 + W.lo[w], W.len[w], W.ld, 8, &full[s],
+                   false);
+    }
   };
   if (tid == 0) {
     pol = policy_evict_first();
-    for (long long j = 0; j < my_tiles && j < S; ++j) issue_static(j);
+    for (long long j = 0; j < my_tiles && j < S; ++j)  // the masks first: one latency
+      s_msk[j] = XG && WIN ? tile_mask(P.tile_runs, t_lo + j * t_step) : ~0u;
+    for (long long j = 0; j < my_tiles && j < S; ++j) issue_static(j, XG ? s_msk[j] : ~0u);
   }
   if (tid == 32) *s_it = read_status(C) == PCG_RUNNING ? C->base_it + step : -1;
   __syncthreads();
@@ -1068,9 +1101,16 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? 3 : (TR == 128 ? 5 : 8)) 
   const long long par = it < 0 ? 0 : it;
   const double* w_old = P.w[par & 1];
   const double* m_old = P.m[par & 1];
-  if (WIN && tid == 0)  // completes the first stages (also before an early exit)
-    for (long long j = 0; j < my_tiles && j < S; ++j) issue_dyn(j, w_old, m_old);
+  // completes the first stages (before the prologue on one GPU; after it
+  // -- the peers' halo rows have arrived -- when distributed)
+  auto issue_first_dyn = [&](int part) {
+    if (WIN && tid == 0)
+      for (long long j = 0; j < my_tiles && j < S; ++j)
+        issue_dyn(j, w_old, m_old, part, XG ? s_msk[j] : ~0u);
+  };
+  issue_first_dyn(XG ? 0 : 2);
   if (it < 0) {
+    if (XG) issue_first_dyn(1);  // (stale data, never read: lets the stages complete)
     if (tid == 0)
       for (long long j = 0; j < my_tiles && j < S; ++j) mbar_wait(&full[j], 0);
     return;
@@ -1086,6 +1126,9 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? 3 : (TR == 128 ? 5 : 8)) 
     }
   }
   __syncthreads();
+  if (XG && WIN && tid == 0)  // peers' halo stores (acquired in the prologue) before TMA reads
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  if (XG) issue_first_dyn(1);
   if (!*decision) {
     if (tid == 0)
       for (long long j = 0; j < my_tiles && j < S; ++j) mbar_wait(&full[j], 0);
@@ -1094,10 +1137,14 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? 3 : (TR == 128 ? 5 : 8)) 
   const double alpha = sc[0], beta = sc[1];
   if (producer) {
     if (tid == 0) {
+      unsigned nmsk = XG && WIN && S < my_tiles ? tile_mask(P.tile_runs, t_lo + S * t_step) : ~0u;
       for (long long j = S; j < my_tiles; ++j) {
+        const unsigned msk = nmsk;
+        if (XG && WIN && j + 1 < my_tiles)  // in flight while the stage drains
+          nmsk = tile_mask(P.tile_runs, t_lo + (j + 1) * t_step);
         mbar_wait(&empty[j % S], (uint32_t)((j / S - 1) & 1));
-        issue_static(j);
-        if (WIN) issue_dyn(j, w_old, m_old);
+        issue_static(j, msk);
+        if (WIN) issue_dyn(j, w_old, m_old, 2, msk);
       }
     }
     return;
@@ -1117,6 +1164,14 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? 3 : (TR == 128 ? 5 : 8)) 
     if (!WIN && lt < rows) {
       wi = ldg_nc(w_old + i);
       di = ldg_nc(P.dinv + i);
+    }
+    // the tile's send range, loaded now so its latency hides under the tile
+    // (loaded after the tile it stalled every tile: +0.085 ms per iteration
+    // for 2 virtual ranks at 256^3)
+    int xe0 = 0, xe1 = 0;
+    if (XG) {
+      xe0 = ldg_nc(P.X.ptr + t0 / TR);
+      xe1 = ldg_nc(P.X.ptr + t0 / TR + 1);
     }
     mbar_wait(&full[s], (uint32_t)((j / S) & 1));
     if (lt < rows) {
@@ -1216,8 +1271,11 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? 3 : (TR == 128 ? 5 : 8)) 
     }
     __syncwarp();
     if ((lt & 31) == 0) mbar_arrive(&empty[s]);
+    if (XG)  // the tile's halo rows of the vector the peers read next
+      tile_exchange_range<NT>(P.X, xe0, xe1, lt, MG ? P.m[(it + 1) & 1] : w_new,
+                              MG ? (((it + 1) & 1) ? 12 : 9) : 7 + (int)((it + 1) & 1), 1);
   }
-  publish_partials<NT>(acc, lt, red, 1, P.pout, P.fin, P.counter, it);
+  publish_partials<NT>(acc, lt, red, 1, P.pout, P.fin, P.counter, it, XG ? &P.X : nullptr);
 }
 
 // ---------------------------------------------------------------------------
@@ -2247,6 +2305,29 @@ __global__ void tile_close_kernel(long long n, long long n_tiles, long long nnz,
   tile_e[n_tiles] = nnz;
 }
 
+__global__ void __launch_bounds__(256) uniform_check_kernel(long long n, const double* d, double v,
+                                                            int* bad) {
+  bool ok = true;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    ok &= __double_as_longlong(d[i]) == __double_as_longlong(v);
+  if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) *bad = 1;
+}
+
+// runs used by each tile of tr rows: OR of its rows' code masks
+__global__ void __launch_bounds__(256) tile_runs_kernel(long long n, int tr, const unsigned char* code,
+                                                        const unsigned short* code_runs,
+                                                        unsigned short* out) {
+  const long long nt = (n + tr - 1) / tr;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nt;
+       t += (long long)gridDim.x * blockDim.x) {
+    unsigned m = 0;
+    const long long e = min(n, (t + 1) * tr);
+    for (long long i = t * tr; i < e; ++i) m |= code_runs[code[i]];
+    out[t] = (unsigned short)m;
+  }
+}
+
 }  // namespace pcg
 
 using namespace pcg;
@@ -2350,6 +2431,7 @@ struct pcg_solver {
   int run_lo[kMaxWin] = {}, run_hi[kMaxWin] = {};
   unsigned char* pwin = nullptr;   // [n_entries] run of each dictionary entry
   double* pdinv = nullptr;         // [n_pat] dinv of each code's first row
+  unsigned short* tile_runs[3] = {nullptr, nullptr, nullptr};  // per tile height 256/128/64
   bool dinv_by_code = false;       // dinv[i] == pdinv[code[i]] for every row (checked at init)
   bool dinv_uniform = false;       // ... and all pdinv equal (dinv0)
   double dinv0 = 0.0;
@@ -2577,12 +2659,44 @@ int build_runs(pcg_solver* S) {
     ++n;
   }
   std::vector<unsigned char> run(ne);
+  int w0 = 0;
+  for (int w = 0; w < n; ++w)
+    if (lo[w] <= 0 && hi[w] >= 0) w0 = w;
   for (int k = 0; k < ne; ++k)
     for (int w = 0; w < n; ++w)
       if (off[k] >= lo[w] && off[k] <= hi[w]) run[k] = (unsigned char)w;
-  if (cudaMalloc(&S->pwin, std::max(ne, 1)) != cudaSuccess)
+  // runs each code uses (+ the own-row run) -> runs each tile uses, per tile height
+  std::vector<int> start(S->pat.n_pat + 1);
+  rc = cuda_status(cudaMemcpy(start.data(), S->pat.start, start.size() * sizeof(int),
+                              cudaMemcpyDeviceToHost), "pattern runs");
+  if (rc) return rc;
+  std::vector<unsigned short> code_runs(S->pat.n_pat);
+  for (int c = 0; c < S->pat.n_pat; ++c) {
+    unsigned m = 1u << w0;
+    for (int k = start[c]; k < start[c + 1]; ++k) m |= 1u << run[k];
+    code_runs[c] = (unsigned short)m;
+  }
+  unsigned short* d_cr = nullptr;
+  const long long nr = S->A.n_rows;
+  if (cudaMalloc(&S->pwin, std::max(ne, 1)) != cudaSuccess ||
+      cudaMalloc(&d_cr, code_runs.size() * sizeof(unsigned short)) != cudaSuccess)
     return set_error(PCG_ENOMEM, "pattern runs");
   rc = cuda_status(cudaMemcpy(S->pwin, run.data(), ne, cudaMemcpyHostToDevice), "pattern runs");
+  if (!rc)
+    rc = cuda_status(cudaMemcpy(d_cr, code_runs.data(), code_runs.size() * sizeof(unsigned short),
+                                cudaMemcpyHostToDevice), "pattern runs");
+  for (int k = 0; k < 3 && !rc; ++k) {
+    const int tr = 256 >> k;
+    const long long nt = (nr + tr - 1) / tr;
+    if (cudaMalloc(&S->tile_runs[k], nt * sizeof(unsigned short)) != cudaSuccess) {
+      rc = set_error(PCG_ENOMEM, "pattern tile runs");
+      break;
+    }
+    tile_runs_kernel<<<elementwise_grid(nt), 256, 0, S->stream>>>(nr, tr, S->pat.code, d_cr,
+                                                                  S->tile_runs[k]);
+  }
+  if (!rc) rc = cuda_status(cudaStreamSynchronize(S->stream), "pattern tile runs");
+  cudaFree(d_cr);
   if (rc) return rc;
   S->n_runs = n;
   for (int w = 0; w < n; ++w) {
@@ -2593,6 +2707,10 @@ int build_runs(pcg_solver* S) {
 }
 
 // Window geometry of tile height tr (see pipecg_fused_kernel_s)
+inline const unsigned short* tile_runs_for(const pcg_solver* S, int tr) {
+  return S->tile_runs[tr == 256 ? 0 : tr == 128 ? 1 : 2];
+}
+
 WinTable win_table(const pcg_solver* S, int tr) {
   WinTable W{};
   W.n = S->n_runs;
@@ -2866,6 +2984,7 @@ FusedParams<RP> fused_params(pcg_solver* S) {
   P.pval = S->pat.val;
   P.pwin = S->pwin;
   P.pdinv = S->pdinv;
+  P.tile_runs = S->n_runs > 0 ? tile_runs_for(S, S->tr) : nullptr;
   P.n_pat = S->pat.n_pat;
   P.n_pat_e = S->pat.n_entries;
   P.X = FusedXchg{};
@@ -2923,7 +3042,16 @@ void launch_fused(pcg_solver* S, int k) {
     default: launch_k(pipecg_fused_kernel_s<64, MGV, WV>, g, 64 + 32, sm, st, pdl, PS, W, k); break;    \
   }
     const bool win = s_windows(S, variant == 6);
-    if (variant == 6 && win) { PCG_LS(true, true) }
+    if (S->fused_xchg) {  // connect keeps E/F only with windows
+#define PCG_LSX(MGV)                                                                                         \
+  switch (S->tr) {                                                                                           \
+    case 256: launch_k(pipecg_fused_kernel_s<256, MGV, true, true>, g, 256 + 32, sm, st, pdl, PS, W, k); break; \
+    case 128: launch_k(pipecg_fused_kernel_s<128, MGV, true, true>, g, 128 + 32, sm, st, pdl, PS, W, k); break; \
+    default: launch_k(pipecg_fused_kernel_s<64, MGV, true, true>, g, 64 + 32, sm, st, pdl, PS, W, k); break;    \
+  }
+      if (variant == 6) { PCG_LSX(true) } else { PCG_LSX(false) }
+#undef PCG_LSX
+    } else if (variant == 6 && win) { PCG_LS(true, true) }
     else if (variant == 6) { PCG_LS(true, false) }
     else if (win) { PCG_LS(false, true) }
     else { PCG_LS(false, false) }
@@ -3213,6 +3341,10 @@ int preload_solver() {
   PCG_LOAD((pipecg_fused_kernel_s<64, MG, WV>))
   PCG_LOAD_S(false, false); PCG_LOAD_S(true, false); PCG_LOAD_S(false, true); PCG_LOAD_S(true, true);
 #undef PCG_LOAD_S
+  PCG_LOAD((pipecg_fused_kernel_s<256, false, true, true>)); PCG_LOAD((pipecg_fused_kernel_s<128, false, true, true>));
+  PCG_LOAD((pipecg_fused_kernel_s<64, false, true, true>)); PCG_LOAD((pipecg_fused_kernel_s<256, true, true, true>));
+  PCG_LOAD((pipecg_fused_kernel_s<128, true, true, true>)); PCG_LOAD((pipecg_fused_kernel_s<64, true, true, true>));
+  PCG_LOAD(tile_runs_kernel); PCG_LOAD(uniform_check_kernel);
 
   PCG_LOAD(pipecg_k1_kernel); PCG_LOAD(gated_spmv_rows<int>); PCG_LOAD(gated_spmv_rows<long long>);
   PCG_LOAD(gated_spmv_long<int>); PCG_LOAD(gated_spmv_long<long long>);
@@ -3257,6 +3389,9 @@ int preload_solver() {
   PCG_SMEM((pipecg_fused_kernel_s<64, MG, WV>))
   PCG_SMEM_S(false, false); PCG_SMEM_S(true, false); PCG_SMEM_S(false, true); PCG_SMEM_S(true, true);
 #undef PCG_SMEM_S
+  PCG_SMEM((pipecg_fused_kernel_s<256, false, true, true>)); PCG_SMEM((pipecg_fused_kernel_s<128, false, true, true>));
+  PCG_SMEM((pipecg_fused_kernel_s<64, false, true, true>)); PCG_SMEM((pipecg_fused_kernel_s<256, true, true, true>));
+  PCG_SMEM((pipecg_fused_kernel_s<128, true, true, true>)); PCG_SMEM((pipecg_fused_kernel_s<64, true, true, true>));
 #undef PCG_SMEM
   if (e != cudaSuccess) return cuda_status(e, "preload solver kernels");
   rc = preload_patterns();
@@ -3697,6 +3832,15 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
                                          : std::make_pair(S->variant, S->alt_pick[S->variant]);
     }
   }
+  if (getenv("PIPECG_B200_DEBUG_PLAN")) {  // experiment aid: the plan in use + the E/F alternatives
+    fprintf(stderr, "[pipecg_b200] engine %d variant %d tr %d stages %d grid %d smem %zu n_pat %d "
+            "runs %d dinv_by_code %d uniform %d\n", S->engine, S->variant, S->tr, S->stages, S->grid,
+            S->smem, S->pat.n_pat, S->n_runs, (int)S->dinv_by_code, (int)S->dinv_uniform);
+    for (int v = 5; v <= 6; ++v)
+      for (const FusedPlan& p : S->alts[v])
+        fprintf(stderr, "[pipecg_b200]   alt %c: tr %d bps %d stages %d grid %d smem %zu\n",
+                v == 5 ? 'E' : 'F', p.tr, p.bps, p.stages, p.grid, p.smem);
+  }
   *out = S;
   return PCG_OK;
 }
@@ -3739,6 +3883,7 @@ int pipecg_b200_solver_destroy(pcg_solver* S) {
   }
   free_row_patterns(&S->pat);
   cudaFree(S->pwin);
+  for (int k = 0; k < 3; ++k) cudaFree(S->tile_runs[k]);
   cudaFree(S->pdinv);
 
   if (S->ev_in) cudaEventDestroy(S->ev_in);
@@ -3829,6 +3974,19 @@ int build_tile_sends(pcg_solver* S) {
   return cuda_status(cudaStreamSynchronize(st), "fused exchange lists");
 }
 
+// every inv_diag entry of [0, n_cols) (owned + halo) equal to dinv0?
+int uniform_dinv(pcg_solver* S, int* bad) {
+  int* d = nullptr;
+  if (cudaMalloc(&d, sizeof(int)) != cudaSuccess) return set_error(PCG_ENOMEM, "dinv check");
+  cudaMemsetAsync(d, 0, sizeof(int), S->stream);
+  uniform_check_kernel<<<elementwise_grid(S->A.n_cols), 256, 0, S->stream>>>(
+      S->A.n_cols, S->A.inv_diag, S->dinv0, d);
+  cudaMemcpyAsync(bad, d, sizeof(int), cudaMemcpyDeviceToHost, S->stream);
+  const int rc = cuda_status(cudaStreamSynchronize(S->stream), "dinv check");
+  cudaFree(d);
+  return rc;
+}
+
 int pipecg_b200_solver_connect(pcg_solver* S, int rank, int world, void* const* peer_vbuf,
                                const int64_t* peer_ld, void* const* peer_comm, int64_t n_send,
                                const int32_t* send_row, const int32_t* send_peer,
@@ -3854,9 +4012,21 @@ int pipecg_b200_solver_connect(pcg_solver* S, int rank, int world, void* const* 
   cp.send_dst = reinterpret_cast<const long long*>(send_dst);
   S->cp = cp;
   S->connected = true;
-  // per-iteration launches of the CSR kernels (the exchange needs them; the
-  // pattern dictionary holds global offsets, not the shard's column space)
-  if (S->engine == 1 && S->variant >= 4) {
+  // The shard's row-pattern dictionary is valid in its [owned | halo]
+  // column space (the halo mapping is affine per contiguous halo range), so
+  // E/F keep running with windows and the fused exchange.  E needs one dinv
+  // for every column, halo included (it never sees the halo rows' codes).
+  // Otherwise -> the CSR variant of the same exchange class (E -> A, F -> C,
+  // both push the same vector) in per-iteration launches (P -> C).
+  bool keep = S->engine == 1 && (S->variant == 5 || S->variant == 6) && S->n_runs > 0 &&
+              !getenv("PIPECG_B200_SEPARATE_XCHG");
+  if (keep && S->variant == 5) {
+    int bad = 1;
+    int rc = uniform_dinv(S, &bad);
+    if (rc) return rc;
+    keep = S->dinv_by_code && S->dinv_uniform && !bad;
+  }
+  if (S->engine == 1 && S->variant >= 4 && !keep) {
     const FusedPlan& csr = S->plans[S->variant == 5 ? 0 : 2];
     if (!csr.stages) return set_error(PCG_EINVAL, "solver_connect: no CSR variant fits this shard");
     apply_plan(S, csr);
@@ -3899,6 +4069,10 @@ int pipecg_b200_solver_init(pcg_solver* S, const double* b, const double* x0, do
     double d0 = 0.0;
     int rc = check_dinv_by_code(S->pat, n, S->A.inv_diag, S->pdinv, &dbc, &uni, &d0, st);
     if (rc) return rc;
+    if (S->connected && S->engine == 1 && S->variant == 5 &&
+        (!dbc || !uni || std::memcmp(&d0, &S->dinv0, sizeof(double)) != 0))
+      return set_error(PCG_ESTATE, "solver_init: inv_diag changed after solver_connect "
+                                   "(variant E reads one dinv for every column)");
     if (dbc != S->dinv_by_code || uni != S->dinv_uniform ||
         std::memcmp(&d0, &S->dinv0, sizeof(double)) != 0) {
       S->dinv_by_code = dbc;

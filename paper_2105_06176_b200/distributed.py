@@ -418,21 +418,42 @@ class DistributedSolver:
         engine = opts.engine if opts.engine.startswith("fused") else "fused"
         opts = DeviceOptions(dot_mode=opts.dot_mode, engine=engine, chunk=opts.chunk,
                              use_graphs=opts.use_graphs, max_sms=opts.max_sms)
-        self.solver = PipecgSolver(problem.A, problem.inv_diag, opts)
+        try:
+            self.solver = PipecgSolver(problem.A, problem.inv_diag, opts)
+        except _lib.NativeError:
+            # E/F asked for, but this shard has no row-pattern dictionary
+            if engine not in ("fused-e", "fused-f"):
+                raise
+            opts.engine = "fused-a" if engine == "fused-e" else "fused-c"
+            self.solver = PipecgSolver(problem.A, problem.inv_diag, opts)
         # every rank must run the same fused variant: the exchange pushes the
         # vector the variant gathers (w for A/B, the stored m for C/D), and
         # per-rank autotuning could pick differently on differently shaped
         # blocks -> adopt rank 0's choice
-        names = {3: "fused-a", 4: "fused-b", 5: "fused-c", 6: "fused-d"}
+        # (E/F keep their row-pattern windows across the shard's halo; a rank
+        # that cannot run rank 0's E/F runs the CSR variant that pushes the
+        # same vector: E -> A (w), F -> C (m))
+        names = {3: "fused-a", 4: "fused-b", 5: "fused-c", 6: "fused-d", 8: "fused-e",
+                 9: "fused-f"}
         mine = int(self.solver.poll().engine)
-        # once connected P and F run as C, E as A (per-iteration CSR launches)
-        mine = {7: 5, 8: 3, 9: 5}.get(mine, mine)
+        mine = 5 if mine == 7 else mine  # P runs as C once connected
         chosen = group.all_gather_object(mine)[0]
+        # E (autotuned on the shard alone) trails F once the halo exchange is
+        # live (2 virtual ranks at 256^3: F 0.55, A 0.64, E 0.70 ms/iteration;
+        # tools/dist1.py) -> F, unless E was asked for explicitly
+        if chosen == 8 and engine != "fused-e":
+            chosen = 9
         if mine != chosen:
             self.solver.close()
             opts = DeviceOptions(dot_mode=opts.dot_mode, engine=names[chosen], chunk=opts.chunk,
                                  use_graphs=opts.use_graphs, max_sms=opts.max_sms)
-            self.solver = PipecgSolver(problem.A, problem.inv_diag, opts)
+            try:
+                self.solver = PipecgSolver(problem.A, problem.inv_diag, opts)
+            except _lib.NativeError:
+                if chosen not in (8, 9):
+                    raise
+                opts.engine = names[3 if chosen == 8 else 5]
+                self.solver = PipecgSolver(problem.A, problem.inv_diag, opts)
         vbuf, ld, comm = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_void_p()
         _lib.call("pipecg_b200_solver_comm_info", self.solver._h, ctypes.byref(vbuf),
                   ctypes.byref(ld), ctypes.byref(comm))

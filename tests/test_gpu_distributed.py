@@ -54,7 +54,10 @@ def run_virtual(world, make_problem, cfg, chunk=0, engine="fused"):
 
 @pytest.mark.parametrize("world,kind,n,engine", [(2, "3d7", 40, "fused-a"), (3, "3d7", 33, "fused-b"),
                                                  (2, "2d5", 200, "fused-c"), (4, "3d27", 24, "fused"),
-                                                 (3, "3d27", 20, "fused-c"), (2, "3d7", 30, "fused-d")])
+                                                 (3, "3d27", 20, "fused-c"), (2, "3d7", 30, "fused-d"),
+                                                 (2, "3d7", 40, "fused-e"), (3, "3d7", 33, "fused-f"),
+                                                 (2, "2d5", 200, "fused-e"), (4, "3d7", 36, "fused-e"),
+                                                 (3, "3d27", 20, "fused-f")])
 def test_virtual_ranks_match_single_gpu(cuda, world, kind, n, engine):
     A = oracle.stencil(kind, n)
     x_true, b, x0, d = oracle.manufactured(A)
@@ -177,3 +180,37 @@ def test_virtual_ranks_e2e_host_blocks_and_autotune_agreement(cuda):
     assert abs(it - ref.iterations) <= 1 and secs > 0
     assert err < 1e-6
     assert sum(o[3] for o in out) == 8 * A.n_rows
+
+
+@pytest.mark.parametrize("engine,code", [("fused-e", 8), ("fused-f", 9)])
+def test_virtual_ranks_keep_row_pattern_variants(cuda, engine, code):
+    """A stencil shard's dictionary is valid in its [owned | halo] column
+    space: E/F stay in use once connected (windows over the halo ranges)."""
+    world, n = 2, 40
+    G = D.LocalGroup(world)
+    opts = pb.DeviceOptions(max_sms=max(8, 148 // world - 10), engine=engine)
+    got, errs = [None] * world, []
+
+    def work(r):
+        try:
+            torch.cuda.set_device(0)
+            g = G.view(r)
+            prob = D.shard_stencil("3d7", n, g)
+            s = D.DistributedSolver(prob, g, opts)
+            xt, b = D.manufactured_local(prob)
+            s.init(b, torch.zeros_like(b), 1e-30, 30)
+            res = s.run(False, 30)[0]
+            got[r] = (res.engine, res.pattern_flags, res.iterations)
+            s.close()
+        except BaseException as e:  # noqa: BLE001
+            errs.append((r, repr(e)))
+            G._barrier.abort()
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    assert not errs, errs
+    for eng, flags, its in got:
+        assert eng == code and flags & 3 == 3 and its == 30
