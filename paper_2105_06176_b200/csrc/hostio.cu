@@ -173,6 +173,32 @@ bool convert(void* dst, const void* src, int64_t n, int kind) {
 }
 
 }  // namespace
+
+thread_local cudaStream_t t_alloc_stream = nullptr;
+
+AllocStream::AllocStream(cudaStream_t st) : prev(t_alloc_stream) { t_alloc_stream = st; }
+AllocStream::~AllocStream() { t_alloc_stream = prev; }
+
+cudaError_t pool_malloc_bytes(void** p, size_t bytes) {
+  if (!t_alloc_stream) return cudaMalloc(p, bytes);
+  return cudaMallocAsync(p, bytes, t_alloc_stream);
+}
+
+void pool_free(void* p) {
+  if (!p) return;
+  if (t_alloc_stream) cudaFreeAsync(p, t_alloc_stream);
+  else cudaFree(p);
+}
+
+void pool_init() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+  unsigned long long keep = 2ULL << 30;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+}
+
 }  // namespace pcg
 
 using namespace pcg;

@@ -12,6 +12,24 @@ constexpr int64_t kGridCap = 64 * kNumSMs; // grid-stride cap for row kernels
 constexpr int64_t kLongRow = 256;          // rows longer than this use the block path
 
 int set_error(int code, const char* what);
+
+// Setup-time device allocations come from the device's stream-ordered pool
+// (cudaMallocAsync on the solver's stream, set for the calling thread with
+// AllocStream): creating and destroying solvers call after call (the
+// reference-facing API builds one per matrix) then costs no cudaMalloc /
+// cudaFree round trips.  Memory exported over CUDA IPC stays on cudaMalloc.
+struct AllocStream {
+  explicit AllocStream(cudaStream_t st);
+  ~AllocStream();
+  cudaStream_t prev;
+};
+cudaError_t pool_malloc_bytes(void** p, size_t bytes);
+template <typename T>
+inline cudaError_t pool_malloc(T** p, size_t bytes) {
+  return pool_malloc_bytes(reinterpret_cast<void**>(p), bytes);
+}
+void pool_free(void* p);
+void pool_init();  // once per device: keep up to 2 GB cached in the pool
 int cuda_status(cudaError_t e, const char* where);
 
 inline unsigned elementwise_grid(int64_t n) {

@@ -154,8 +154,8 @@ int build(long long n, const RP* rp, const int* col, const double* val, cudaStre
   unsigned long long* tab = nullptr;
   int *rep = nullptr, *fail = nullptr, *dev_small = nullptr;
   int rc = PCG_OK;
-  if (cudaMalloc(&tab, kPatTable * 8) != cudaSuccess || cudaMalloc(&rep, kPatTable * 4) != cudaSuccess ||
-      cudaMalloc(&fail, 8) != cudaSuccess)
+  if (pool_malloc(&tab, kPatTable * 8) != cudaSuccess || pool_malloc(&rep, kPatTable * 4) != cudaSuccess ||
+      pool_malloc(&fail, 8) != cudaSuccess)
     rc = set_error(PCG_ENOMEM, "row patterns: workspace");
   std::vector<unsigned long long> h_tab(kPatTable);
   std::vector<int> h_rep(kPatTable);
@@ -183,7 +183,7 @@ int build(long long n, const RP* rp, const int* col, const double* val, cudaStre
       slot_code[slots[k]] = k;
       reps[k] = h_rep[slots[k]];
     }
-    if (cudaMalloc(&dev_small, (size_t)(3 * u + 1 + kPatTable) * 4) != cudaSuccess)
+    if (pool_malloc(&dev_small, (size_t)(3 * u + 1 + kPatTable) * 4) != cudaSuccess)
       rc = set_error(PCG_ENOMEM, "row patterns: dictionary");
   }
   int* d_reps = dev_small;
@@ -200,11 +200,11 @@ int build(long long n, const RP* rp, const int* col, const double* val, cudaStre
   }
   if (usable && !rc) {
     const int ne = h_start[u];
-    if (cudaMalloc(&out->code, (size_t)n + 256) != cudaSuccess ||
-        cudaMalloc(&out->start, (size_t)(u + 1) * 4) != cudaSuccess ||
-        cudaMalloc(&out->rep, (size_t)u * 4) != cudaSuccess ||
-        cudaMalloc(&out->off, (size_t)std::max(ne, 1) * 4) != cudaSuccess ||
-        cudaMalloc(&out->val, (size_t)std::max(ne, 1) * 8) != cudaSuccess)
+    if (pool_malloc(&out->code, (size_t)n + 256) != cudaSuccess ||
+        pool_malloc(&out->start, (size_t)(u + 1) * 4) != cudaSuccess ||
+        pool_malloc(&out->rep, (size_t)u * 4) != cudaSuccess ||
+        pool_malloc(&out->off, (size_t)std::max(ne, 1) * 4) != cudaSuccess ||
+        pool_malloc(&out->val, (size_t)std::max(ne, 1) * 8) != cudaSuccess)
       rc = set_error(PCG_ENOMEM, "row patterns: codes");
   }
   if (usable && !rc) {
@@ -227,10 +227,10 @@ int build(long long n, const RP* rp, const int* col, const double* val, cudaStre
       out->max_len = *std::max_element(h_len.begin(), h_len.end());
     }
   }
-  cudaFree(tab);
-  cudaFree(rep);
-  cudaFree(fail);
-  cudaFree(dev_small);
+  pool_free(tab);
+  pool_free(rep);
+  pool_free(fail);
+  pool_free(dev_small);
   if (!usable || rc) free_row_patterns(out);
   return rc;
 }
@@ -290,11 +290,11 @@ int build_row_patterns(long long n, int rp64, const void* rp, const int* col, co
 }
 
 void free_row_patterns(RowPatterns* p) {
-  cudaFree(p->code);
-  cudaFree(p->start);
-  cudaFree(p->rep);
-  cudaFree(p->off);
-  cudaFree(p->val);
+  pool_free(p->code);
+  pool_free(p->start);
+  pool_free(p->rep);
+  pool_free(p->off);
+  pool_free(p->val);
   *p = RowPatterns{};
 }
 

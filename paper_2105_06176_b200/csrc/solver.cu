@@ -34,6 +34,7 @@
 #include <cub/device/device_segmented_radix_sort.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -2566,11 +2567,11 @@ int build_tiles_d(pcg_solver* S, FusedPlan* p) {
   void* tmp = nullptr;
   size_t tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, offs, n_blocks, st);
-  if (cudaMalloc(&counts, n_blocks * sizeof(int)) != cudaSuccess ||
-      cudaMalloc(&offs, (n_blocks + 1) * sizeof(long long)) != cudaSuccess ||
-      cudaMalloc(&tmp, tmp_bytes) != cudaSuccess) {
-    cudaFree(counts);
-    cudaFree(offs);
+  if (pool_malloc(&counts, n_blocks * sizeof(int)) != cudaSuccess ||
+      pool_malloc(&offs, (n_blocks + 1) * sizeof(long long)) != cudaSuccess ||
+      pool_malloc(&tmp, tmp_bytes) != cudaSuccess) {
+    pool_free(counts);
+    pool_free(offs);
     return set_error(PCG_ENOMEM, "variant D tiles: workspace");
   }
   const RP* rp = static_cast<const RP*>(S->A.rowptr);
@@ -2585,8 +2586,8 @@ int build_tiles_d(pcg_solver* S, FusedPlan* p) {
   int rc = cuda_status(cudaStreamSynchronize(st), "variant D tile count");
   const long long n_tiles = last_off + last_cnt;
   if (!rc) {
-    if (cudaMalloc(&p->tile_row, (n_tiles + 1) * sizeof(int)) != cudaSuccess ||
-        cudaMalloc(&p->tile_e, (n_tiles + 1) * sizeof(long long)) != cudaSuccess)
+    if (pool_malloc(&p->tile_row, (n_tiles + 1) * sizeof(int)) != cudaSuccess ||
+        pool_malloc(&p->tile_e, (n_tiles + 1) * sizeof(long long)) != cudaSuccess)
       rc = set_error(PCG_ENOMEM, "variant D tiles");
   }
   if (!rc) {
@@ -2595,9 +2596,9 @@ int build_tiles_d(pcg_solver* S, FusedPlan* p) {
     tile_close_kernel<<<1, 1, 0, st>>>(n, n_tiles, S->A.nnz, p->tile_row, p->tile_e);
     rc = cuda_status(cudaStreamSynchronize(st), "variant D tile build");
   }
-  cudaFree(counts);
-  cudaFree(offs);
-  cudaFree(tmp);
+  pool_free(counts);
+  pool_free(offs);
+  pool_free(tmp);
   if (rc) return rc;
   p->n_tiles = n_tiles;
   p->grid = (int)std::max<long long>(std::min<long long>(p->grid, n_tiles), 1);
@@ -2678,8 +2679,8 @@ int build_runs(pcg_solver* S) {
   }
   unsigned short* d_cr = nullptr;
   const long long nr = S->A.n_rows;
-  if (cudaMalloc(&S->pwin, std::max(ne, 1)) != cudaSuccess ||
-      cudaMalloc(&d_cr, code_runs.size() * sizeof(unsigned short)) != cudaSuccess)
+  if (pool_malloc(&S->pwin, std::max(ne, 1)) != cudaSuccess ||
+      pool_malloc(&d_cr, code_runs.size() * sizeof(unsigned short)) != cudaSuccess)
     return set_error(PCG_ENOMEM, "pattern runs");
   rc = cuda_status(cudaMemcpy(S->pwin, run.data(), ne, cudaMemcpyHostToDevice), "pattern runs");
   if (!rc)
@@ -2688,7 +2689,7 @@ int build_runs(pcg_solver* S) {
   for (int k = 0; k < 3 && !rc; ++k) {
     const int tr = 256 >> k;
     const long long nt = (nr + tr - 1) / tr;
-    if (cudaMalloc(&S->tile_runs[k], nt * sizeof(unsigned short)) != cudaSuccess) {
+    if (pool_malloc(&S->tile_runs[k], nt * sizeof(unsigned short)) != cudaSuccess) {
       rc = set_error(PCG_ENOMEM, "pattern tile runs");
       break;
     }
@@ -2696,7 +2697,7 @@ int build_runs(pcg_solver* S) {
                                                                   S->tile_runs[k]);
   }
   if (!rc) rc = cuda_status(cudaStreamSynchronize(S->stream), "pattern tile runs");
-  cudaFree(d_cr);
+  pool_free(d_cr);
   if (rc) return rc;
   S->n_runs = n;
   for (int w = 0; w < n; ++w) {
@@ -2866,6 +2867,34 @@ void apply_plan(pcg_solver* S, const FusedPlan& p) {
   S->n_partials = p.grid;
 }
 
+// pinned kRecBytes records, recycled across solvers (page-locking memory
+// costs milliseconds; the reference-facing call creates a solver per matrix)
+std::mutex& pinned_mu() {
+  static std::mutex mu;
+  return mu;
+}
+std::vector<char*>& pinned_free() {
+  static std::vector<char*> v;
+  return v;
+}
+char* pinned_record() {
+  {
+    std::lock_guard<std::mutex> lk(pinned_mu());
+    if (!pinned_free().empty()) {
+      char* p = pinned_free().back();
+      pinned_free().pop_back();
+      return p;
+    }
+  }
+  char* p = nullptr;
+  return cudaMallocHost(&p, kRecBytes) == cudaSuccess ? p : nullptr;
+}
+void pinned_record_release(char* p) {
+  std::lock_guard<std::mutex> lk(pinned_mu());
+  if (pinned_free().size() < 64) pinned_free().push_back(p);
+  else cudaFreeHost(p);
+}
+
 int alloc_state(pcg_solver* S) {
   const long long n = std::max(S->A.n_rows, S->A.n_cols);
   S->ld = (size_t)round_up(n + 32, 256);
@@ -2888,26 +2917,26 @@ int alloc_state(pcg_solver* S) {
   S->b = v + 11 * S->ld;
   S->m2 = v + 12 * S->ld;
   const int maxp = std::max(S->grid, 1);
-  e = cudaMalloc(&S->partials, (size_t)2 * maxp * 4 * sizeof(double));
+  e = pool_malloc(&S->partials, (size_t)2 * maxp * 4 * sizeof(double));
   if (e != cudaSuccess) return set_error(PCG_ENOMEM, "solver: partials allocation failed");
   cudaMemsetAsync(S->partials, 0, (size_t)2 * maxp * 4 * sizeof(double), S->stream);
-  if (cudaMalloc(&S->gbar, sizeof(unsigned long long)) != cudaSuccess ||
-      cudaMalloc(&S->fin, 8 * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&S->counter, 2 * sizeof(unsigned)) != cudaSuccess)
+  if (pool_malloc(&S->gbar, sizeof(unsigned long long)) != cudaSuccess ||
+      pool_malloc(&S->fin, 8 * sizeof(double)) != cudaSuccess ||
+      pool_malloc(&S->counter, 2 * sizeof(unsigned)) != cudaSuccess)
     return set_error(PCG_ENOMEM, "solver: partials allocation failed");
   cudaMemsetAsync(S->fin, 0, 8 * sizeof(double), S->stream);
   cudaMemsetAsync(S->counter, 0, 2 * sizeof(unsigned), S->stream);
-  if (cudaMalloc(&S->seqbuf, 8 * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&S->dpart, kDotGrid * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&S->dots_ws, (size_t)kDotGrid * 4 * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&S->dots4, 4 * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&S->rec_dev, kRecBytes) != cudaSuccess ||
+  if (pool_malloc(&S->seqbuf, 8 * sizeof(double)) != cudaSuccess ||
+      pool_malloc(&S->dpart, kDotGrid * sizeof(double)) != cudaSuccess ||
+      pool_malloc(&S->dots_ws, (size_t)kDotGrid * 4 * sizeof(double)) != cudaSuccess ||
+      pool_malloc(&S->dots4, 4 * sizeof(double)) != cudaSuccess ||
+      pool_malloc(&S->rec_dev, kRecBytes) != cudaSuccess ||
       cudaMalloc(&S->comm, kCommBytes) != cudaSuccess)
     return set_error(PCG_ENOMEM, "solver: workspace allocation failed");
   cudaMemsetAsync(S->rec_dev, 0, kRecBytes, S->stream);
   cudaMemsetAsync(S->comm, 0, kCommBytes, S->stream);
   for (int k = 0; k < 2; ++k)
-    if (cudaMallocHost(&S->rec_host[k], kRecBytes) != cudaSuccess)
+    if (!(S->rec_host[k] = pinned_record()))
       return set_error(PCG_ENOMEM, "solver: pinned record allocation failed");
   return cuda_status(cudaStreamSynchronize(S->stream), "solver: workspace init");
 }
@@ -3307,6 +3336,7 @@ int preload_solver() {
   if (done_devices.count(dev)) return PCG_OK;
   int rc = preload_ops();
   if (rc) return rc;
+  pool_init();
   cudaFuncAttributes a;
   cudaError_t e = cudaSuccess;
 #define PCG_LOAD(k) if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void*)(k))
@@ -3437,7 +3467,7 @@ int build_long_chunks(pcg_solver* S) {
   if (nl <= 0) return PCG_OK;
   cudaStream_t st = S->stream;
   long long* d = nullptr;
-  if (cudaMalloc(&d, 2 * nl * sizeof(long long)) != cudaSuccess)
+  if (pool_malloc(&d, 2 * nl * sizeof(long long)) != cudaSuccess)
     return set_error(PCG_ENOMEM, "long chunks");
   long_len_kernel<<<elementwise_grid(nl), 256, 0, st>>>(S->long_rows, nl, S->A.rowptr, S->A.rp64, d,
                                                         d + nl);
@@ -3447,7 +3477,7 @@ int build_long_chunks(pcg_solver* S) {
   cudaMemcpyAsync(hi.data(), d + nl, nl * 8, cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(rows.data(), S->long_rows, nl * 4, cudaMemcpyDeviceToHost, st);
   int rc = cuda_status(cudaStreamSynchronize(st), "long chunks");
-  cudaFree(d);
+  pool_free(d);
   if (rc) return rc;
   std::vector<LongChunk> ch;
   int slots = 0;
@@ -3460,9 +3490,9 @@ int build_long_chunks(pcg_solver* S) {
       ch.push_back(LongChunk{lo[k] + len * j / n, lo[k] + len * (j + 1) / n, rows[k], first, n, slot});
   }
   S->n_chunks = (long long)ch.size();
-  if (cudaMalloc(&S->chunks, ch.size() * sizeof(LongChunk)) != cudaSuccess ||
-      cudaMalloc(&S->chunk_part, ch.size() * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&S->chunk_ticket, std::max(slots, 1) * sizeof(unsigned)) != cudaSuccess)
+  if (pool_malloc(&S->chunks, ch.size() * sizeof(LongChunk)) != cudaSuccess ||
+      pool_malloc(&S->chunk_part, ch.size() * sizeof(double)) != cudaSuccess ||
+      pool_malloc(&S->chunk_ticket, std::max(slots, 1) * sizeof(unsigned)) != cudaSuccess)
     return set_error(PCG_ENOMEM, "long chunks");
   cudaMemcpyAsync(S->chunks, ch.data(), ch.size() * sizeof(LongChunk), cudaMemcpyHostToDevice, st);
   cudaMemsetAsync(S->chunk_ticket, 0, std::max(slots, 1) * sizeof(unsigned), st);
@@ -3489,11 +3519,11 @@ int build_sell(pcg_solver* S) {
   size_t b1 = 0, b2 = 0;
   int rc = PCG_OK;
   auto fail = [&](const char* w) { rc = set_error(PCG_ENOMEM, w); };
-  if (cudaMalloc(&key, n * 4) != cudaSuccess || cudaMalloc(&key2, n * 4) != cudaSuccess ||
-      cudaMalloc(&idx, n * 4) != cudaSuccess || cudaMalloc(&offs, (n_seg + 1) * 4) != cudaSuccess ||
-      cudaMalloc(&width, (n_slices + 1) * 8) != cudaSuccess ||
-      cudaMalloc(&S->sell_perm, n * 4) != cudaSuccess || cudaMalloc(&S->sell_len, n * 4) != cudaSuccess ||
-      cudaMalloc(&S->sell_ptr, (n_slices + 1) * 8) != cudaSuccess)
+  if (pool_malloc(&key, n * 4) != cudaSuccess || pool_malloc(&key2, n * 4) != cudaSuccess ||
+      pool_malloc(&idx, n * 4) != cudaSuccess || pool_malloc(&offs, (n_seg + 1) * 4) != cudaSuccess ||
+      pool_malloc(&width, (n_slices + 1) * 8) != cudaSuccess ||
+      pool_malloc(&S->sell_perm, n * 4) != cudaSuccess || pool_malloc(&S->sell_len, n * 4) != cudaSuccess ||
+      pool_malloc(&S->sell_ptr, (n_slices + 1) * 8) != cudaSuccess)
     fail("SELL build workspace");
   if (!rc) {
     const unsigned g = elementwise_grid(n);
@@ -3504,7 +3534,7 @@ int build_sell(pcg_solver* S) {
     cub::DeviceSegmentedRadixSort::SortPairs(nullptr, b1, key, key2, idx, S->sell_perm, (int)n,
                                              (int)n_seg, offs, offs + 1, 0, bits, st);
     cub::DeviceScan::ExclusiveSum(nullptr, b2, width, S->sell_ptr, n_slices + 1, st);
-    if (cudaMalloc(&tmp, std::max(b1, b2)) != cudaSuccess) fail("SELL sort workspace");
+    if (pool_malloc(&tmp, std::max(b1, b2)) != cudaSuccess) fail("SELL sort workspace");
     if (!rc) {
       size_t bt = std::max(b1, b2);
       cub::DeviceSegmentedRadixSort::SortPairs(tmp, bt, key, key2, idx, S->sell_perm, (int)n,
@@ -3517,8 +3547,8 @@ int build_sell(pcg_solver* S) {
       long long total = 0;
       cudaMemcpyAsync(&total, S->sell_ptr + n_slices, 8, cudaMemcpyDeviceToHost, st);
       rc = cuda_status(cudaStreamSynchronize(st), "SELL build");
-      if (!rc && (cudaMalloc(&S->sell_col, (total + 64) * 4) != cudaSuccess ||
-                  cudaMalloc(&S->sell_val, (total + 64) * 8) != cudaSuccess))
+      if (!rc && (pool_malloc(&S->sell_col, (total + 64) * 4) != cudaSuccess ||
+                  pool_malloc(&S->sell_val, (total + 64) * 8) != cudaSuccess))
         fail("SELL arrays");
       if (!rc) {
         sell_fill_kernel<RP><<<g, 256, 0, st>>>(n, rp, S->A.col, S->A.val, S->sell_perm,
@@ -3527,12 +3557,12 @@ int build_sell(pcg_solver* S) {
       }
     }
   }
-  cudaFree(key);
-  cudaFree(key2);
-  cudaFree(idx);
-  cudaFree(offs);
-  cudaFree(width);
-  cudaFree(tmp);
+  pool_free(key);
+  pool_free(key2);
+  pool_free(idx);
+  pool_free(offs);
+  pool_free(width);
+  pool_free(tmp);
   if (!rc) {
     S->sell = true;
     S->sell_slices = n_slices;
@@ -3653,6 +3683,13 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   if (prc) return prc;
   pcg_solver* S = new pcg_solver();
   S->A = *A;
+  // setup phase times (PIPECG_B200_DEBUG_PLAN)
+  const auto t_start = std::chrono::steady_clock::now();
+  std::vector<std::pair<const char*, double>> phases;
+  auto phase = [&](const char* name) {
+    phases.emplace_back(name, std::chrono::duration<double, std::milli>(
+                                  std::chrono::steady_clock::now() - t_start).count());
+  };
   if (const char* f = getenv("PIPECG_B200_FLAGS")) S->flags = atoi(f);
   if (getenv("PIPECG_B200_NO_PDL")) S->pdl = false;
   if (const char* e = getenv("PIPECG_B200_SELL_BATCH")) S->sell_batch = atoi(e);  // experiment
@@ -3681,6 +3718,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     pipecg_b200_solver_destroy(S);
     return rc;
   }
+  AllocStream alloc_on(S->stream);  // setup allocations: the stream-ordered pool
   // long rows (> kLongRow entries) -> engine 2 with the block-per-row path
   unsigned long long* mx = nullptr;
   cudaMallocAsync(&mx, sizeof(unsigned long long), S->stream);
@@ -3703,6 +3741,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   }
   const bool has_long = max_row > (unsigned long long)kLongRow;
   S->irregular = has_long;
+  phase("stream+max_row");
   bool fused_ok = false;
   if (req == 0 || req == 1 || req == 8 || req == 9) {
     // lossless row-pattern dictionary (variants E/F); none for irregular
@@ -3711,7 +3750,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
       rc = build_row_patterns(A->n_rows, A->rp64, A->rowptr, A->col, A->val, S->stream, &S->pat);
       if (!rc) rc = build_runs(S);
       if (!rc && S->pat.n_pat > 0) {
-        if (cudaMalloc(&S->pdinv, S->pat.n_pat * sizeof(double)) != cudaSuccess)
+        if (pool_malloc(&S->pdinv, S->pat.n_pat * sizeof(double)) != cudaSuccess)
           rc = set_error(PCG_ENOMEM, "pattern dinv");
         else
           rc = check_dinv_by_code(S->pat, A->n_rows, A->inv_diag, S->pdinv, &S->dinv_by_code,
@@ -3723,6 +3762,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
       }
     }
   }
+  phase("patterns");
   if (req != 2) {
     rc = A->rp64 ? fused_setup<long long>(S) : fused_setup<int>(S);
     if (rc && rc != PCG_EINVAL) {
@@ -3745,7 +3785,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
       rc = pipecg_b200_find_long_rows(A->n_rows, A->rp64, A->rowptr, kLongRow, nullptr, 0, &cnt,
                                       S->stream);
       if (!rc && cnt > 0) {
-        if (cudaMalloc(&S->long_rows, cnt * sizeof(int)) != cudaSuccess)
+        if (pool_malloc(&S->long_rows, cnt * sizeof(int)) != cudaSuccess)
           rc = set_error(PCG_ENOMEM, "long rows alloc");
         else
           rc = pipecg_b200_find_long_rows(A->n_rows, A->rp64, A->rowptr, kLongRow, S->long_rows,
@@ -3773,7 +3813,9 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   const int grid2 = std::min<int>(kDotGrid, 4 * S->num_sms);
   S->grid = grid2;
   for (int v = 0; v < kVariants; ++v) S->grid = std::max(S->grid, S->plans[v].grid);
+  phase("fused_setup+long+sell");
   rc = alloc_state(S);
+  phase("alloc_state");
   if (rc) {
     pipecg_b200_solver_destroy(S);
     return rc;
@@ -3832,7 +3874,9 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
                                          : std::make_pair(S->variant, S->alt_pick[S->variant]);
     }
   }
+  phase("engine choice");
   if (getenv("PIPECG_B200_DEBUG_PLAN")) {  // experiment aid: the plan in use + the E/F alternatives
+    for (auto& ph : phases) fprintf(stderr, "[pipecg_b200] t=%.2f ms after %s\n", ph.second, ph.first);
     fprintf(stderr, "[pipecg_b200] engine %d variant %d tr %d stages %d grid %d smem %zu n_pat %d "
             "runs %d dinv_by_code %d uniform %d\n", S->engine, S->variant, S->tr, S->stages, S->grid,
             S->smem, S->pat.n_pat, S->n_runs, (int)S->dinv_by_code, (int)S->dinv_uniform);
@@ -3848,43 +3892,44 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
 int pipecg_b200_solver_destroy(pcg_solver* S) {
   if (!S) return PCG_OK;
   if (S->stream) cudaStreamSynchronize(S->stream);
+  AllocStream alloc_on(S->stream);  // (null stream: plain cudaFree)
   for (int k = 0; k < 2; ++k) {
     for (auto& kv : S->graphs[k]) cudaGraphExecDestroy(kv.second);
-    if (S->rec_host[k]) cudaFreeHost(S->rec_host[k]);
+    if (S->rec_host[k]) pinned_record_release(S->rec_host[k]);
     if (S->ev_rec[k]) cudaEventDestroy(S->ev_rec[k]);
   }
   cudaFree(S->vbuf);
-  cudaFree(S->partials);
-  cudaFree(S->fin);
-  cudaFree(S->gbar);
-  cudaFree(S->counter);
-  cudaFree(S->seqbuf);
-  cudaFree(S->dpart);
-  cudaFree(S->dots_ws);
-  cudaFree(S->dots4);
-  cudaFree(S->rec_dev);
+  pool_free(S->partials);
+  pool_free(S->fin);
+  pool_free(S->gbar);
+  pool_free(S->counter);
+  pool_free(S->seqbuf);
+  pool_free(S->dpart);
+  pool_free(S->dots_ws);
+  pool_free(S->dots4);
+  pool_free(S->rec_dev);
   cudaFree(S->comm);
-  cudaFree(S->long_rows);
-  cudaFree(S->chunks);
-  cudaFree(S->chunk_part);
-  cudaFree(S->chunk_ticket);
-  cudaFree(S->sell_ptr);
-  cudaFree(S->sell_perm);
-  cudaFree(S->sell_len);
-  cudaFree(S->sell_col);
-  cudaFree(S->sell_val);
-  cudaFree(S->x_ptr);
-  cudaFree(S->x_row);
-  cudaFree(S->x_peer);
-  cudaFree(S->x_dst);
+  pool_free(S->long_rows);
+  pool_free(S->chunks);
+  pool_free(S->chunk_part);
+  pool_free(S->chunk_ticket);
+  pool_free(S->sell_ptr);
+  pool_free(S->sell_perm);
+  pool_free(S->sell_len);
+  pool_free(S->sell_col);
+  pool_free(S->sell_val);
+  pool_free(S->x_ptr);
+  pool_free(S->x_row);
+  pool_free(S->x_peer);
+  pool_free(S->x_dst);
   for (int v = 0; v < kVariants; ++v) {
-    cudaFree(S->plans[v].tile_row);
-    cudaFree(S->plans[v].tile_e);
+    pool_free(S->plans[v].tile_row);
+    pool_free(S->plans[v].tile_e);
   }
   free_row_patterns(&S->pat);
-  cudaFree(S->pwin);
-  for (int k = 0; k < 3; ++k) cudaFree(S->tile_runs[k]);
-  cudaFree(S->pdinv);
+  pool_free(S->pwin);
+  for (int k = 0; k < 3; ++k) pool_free(S->tile_runs[k]);
+  pool_free(S->pdinv);
 
   if (S->ev_in) cudaEventDestroy(S->ev_in);
   if (S->stream) cudaStreamDestroy(S->stream);
@@ -3954,16 +3999,16 @@ int build_tile_sends(pcg_solver* S) {
   }
   for (long long t = 0; t <= nt; ++t)
     ptr[t] = (int)(std::lower_bound(srow.begin(), srow.end(), tstart[t]) - srow.begin());
-  cudaFree(S->x_ptr);
-  cudaFree(S->x_row);
-  cudaFree(S->x_peer);
-  cudaFree(S->x_dst);
+  pool_free(S->x_ptr);
+  pool_free(S->x_row);
+  pool_free(S->x_peer);
+  pool_free(S->x_dst);
   S->x_ptr = S->x_row = S->x_peer = nullptr;
   S->x_dst = nullptr;
-  if (cudaMalloc(&S->x_ptr, (nt + 1) * sizeof(int)) != cudaSuccess ||
-      cudaMalloc(&S->x_row, std::max<long long>(ns, 1) * sizeof(int)) != cudaSuccess ||
-      cudaMalloc(&S->x_peer, std::max<long long>(ns, 1) * sizeof(int)) != cudaSuccess ||
-      cudaMalloc(&S->x_dst, std::max<long long>(ns, 1) * sizeof(long long)) != cudaSuccess)
+  if (pool_malloc(&S->x_ptr, (nt + 1) * sizeof(int)) != cudaSuccess ||
+      pool_malloc(&S->x_row, std::max<long long>(ns, 1) * sizeof(int)) != cudaSuccess ||
+      pool_malloc(&S->x_peer, std::max<long long>(ns, 1) * sizeof(int)) != cudaSuccess ||
+      pool_malloc(&S->x_dst, std::max<long long>(ns, 1) * sizeof(long long)) != cudaSuccess)
     return set_error(PCG_ENOMEM, "fused exchange lists");
   cudaMemcpyAsync(S->x_ptr, ptr.data(), (nt + 1) * sizeof(int), cudaMemcpyHostToDevice, st);
   if (ns) {
@@ -3977,13 +4022,13 @@ int build_tile_sends(pcg_solver* S) {
 // every inv_diag entry of [0, n_cols) (owned + halo) equal to dinv0?
 int uniform_dinv(pcg_solver* S, int* bad) {
   int* d = nullptr;
-  if (cudaMalloc(&d, sizeof(int)) != cudaSuccess) return set_error(PCG_ENOMEM, "dinv check");
+  if (pool_malloc(&d, sizeof(int)) != cudaSuccess) return set_error(PCG_ENOMEM, "dinv check");
   cudaMemsetAsync(d, 0, sizeof(int), S->stream);
   uniform_check_kernel<<<elementwise_grid(S->A.n_cols), 256, 0, S->stream>>>(
       S->A.n_cols, S->A.inv_diag, S->dinv0, d);
   cudaMemcpyAsync(bad, d, sizeof(int), cudaMemcpyDeviceToHost, S->stream);
   const int rc = cuda_status(cudaStreamSynchronize(S->stream), "dinv check");
-  cudaFree(d);
+  pool_free(d);
   return rc;
 }
 
@@ -4012,6 +4057,7 @@ int pipecg_b200_solver_connect(pcg_solver* S, int rank, int world, void* const* 
   cp.send_dst = reinterpret_cast<const long long*>(send_dst);
   S->cp = cp;
   S->connected = true;
+  AllocStream alloc_on(S->stream);
   // The shard's row-pattern dictionary is valid in its [owned | halo]
   // column space (the halo mapping is affine per contiguous halo range), so
   // E/F keep running with windows and the fused exchange.  E needs one dinv
