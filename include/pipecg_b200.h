@@ -210,7 +210,7 @@ typedef struct {
   int64_t n_history;   /* entries written to history_host */
   int64_t n_drift;     /* samples written to drift_*_host */
   int engine;          /* engine used: 2 two-kernel, 3..9 fused variant A/B/C/D/P/E/F */
-  int64_t graph_launches;
+  int64_t graph_launches;  /* iteration chunks launched (CUDA graphs, or directly) */
   double tune_ms[8];   /* autotune ms/iteration: fused A, B, C, D, P, E, F, two-kernel
                           (0 = not run) */
   int pattern_flags;   /* row-pattern dictionary in use by E/F: 1 dictionary, 2 windows,

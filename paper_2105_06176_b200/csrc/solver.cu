@@ -424,6 +424,7 @@ struct FusedParams {
   const unsigned char* pwin;   // [n_pat_e] window of each entry (WinTable)
   const double* pdinv;         // [n_pat] dinv of each code (valid when WinTable.dinv_by_code)
   const unsigned short* tile_runs;  // [n_tiles] runs the tile's rows use (WinTable bit w)
+  int l2_prefetch;             // E/F: prefetch the streams of the tile this many stages ahead into L2 (0: off)
   int n_pat, n_pat_e;
 };
 
@@ -941,6 +942,10 @@ struct FusedLayoutS {
   }
 };
 
+__device__ __forceinline__ void l2_prefetch_bulk(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ unsigned tile_mask(const unsigned short* runs, long long t) {
   unsigned short v;
   asm volatile("ld.global.nc.u16 %0, [%1];" : "=h"(v) : "l"(runs + t));
@@ -1143,6 +1148,21 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? 3 : (TR == 128 ? 5 : 8))
         const unsigned msk = nmsk;
         if (XG && WIN && j + 1 < my_tiles)  // in flight while the stage drains
           nmsk = tile_mask(P.tile_runs, t_lo + (j + 1) * t_step);
+        if (P.l2_prefetch && j + P.l2_prefetch < my_tiles) {
+          // HBM -> L2 for a tile that is loaded l2_prefetch stages from now:
+          // more bytes in flight than the shared-memory ring holds
+          const long long tp = (t_lo + (j + P.l2_prefetch) * t_step) * TR;
+          const uint32_t bp = (uint32_t)((min((long long)TR, P.n - tp) * 8 + 15) / 16 * 16);
+#pragma unroll
+          for (int k = 0; k < 7; ++k) l2_prefetch_bulk(P.vec[k] + tp, bp);
+          if (MG) l2_prefetch_bulk(w_old + tp, bp);
+          if (WIN) {  // the leading run: the only window not yet in L2
+            const int w = W.n - 1;
+            const long long a = tp + W.lo[w], b = min(a + W.len[w], W.ld);
+            if (b > a && a >= 0)
+              l2_prefetch_bulk((MG ? m_old : w_old) + a, (uint32_t)((b - a) * 8));
+          }
+        }
         mbar_wait(&empty[j % S], (uint32_t)((j / S - 1) & 1));
         issue_static(j, msk);
         if (WIN) issue_dyn(j, w_old, m_old, 2, msk);
@@ -2405,6 +2425,7 @@ struct pcg_solver {
   bool pdl = true;                 // programmatic dependent launch of the fused kernels
   bool fused_xchg = false;         // distributed: halo + partial push inside the fused kernel
   bool p_mg = true;                // variant P gathers the stored m (C) or dinv*w (A)
+  int l2_prefetch = 0;             // E/F L2 prefetch distance in stages (experiment switch)
   unsigned long long* gbar = nullptr;  // variant P grid-barrier counter
   // engine-2 K2 in SELL-C-sigma layout (irregular matrices)
   bool sell = false;
@@ -3014,6 +3035,7 @@ FusedParams<RP> fused_params(pcg_solver* S) {
   P.pwin = S->pwin;
   P.pdinv = S->pdinv;
   P.tile_runs = S->n_runs > 0 ? tile_runs_for(S, S->tr) : nullptr;
+  P.l2_prefetch = S->l2_prefetch;
   P.n_pat = S->pat.n_pat;
   P.n_pat_e = S->pat.n_entries;
   P.X = FusedXchg{};
@@ -3280,23 +3302,36 @@ int launch_chunk(pcg_solver* S, int K, int parity) {
   if (!S->opt.use_graphs) {
     int rc = enqueue_chunk_body(S, K, parity);
     if (rc) return rc;
-  } else {
-    cudaGraphExec_t exec = nullptr;
-    int rc = chunk_graph(S, K, parity, &exec);
-    if (rc) return rc;
-    cudaError_t e = cudaGraphLaunch(exec, S->stream);
+  } else if (S->graphs[parity].count(K)) {
+    cudaError_t e = cudaGraphLaunch(S->graphs[parity][K], S->stream);
     if (e != cudaSuccess) return cuda_status(e, "graph launch");
+  } else {
+    // first chunk of this shape: launch it directly, then capture and
+    // instantiate its graph while the GPU runs it (the host would otherwise
+    // stall the GPU for the instantiation, measured ~5 ms per fresh solver)
+    int rc = enqueue_chunk_body(S, K, parity);
+    if (rc) return rc;
+    rc = cuda_status(cudaEventRecord(S->ev_rec[parity], S->stream), "record event");
+    cudaGraphExec_t exec = nullptr;
+    if (!rc) rc = chunk_graph(S, K, parity, &exec);
     S->graph_launches++;
+    return rc;
   }
+  S->graph_launches++;  // chunks launched (graph or direct)
   return cuda_status(cudaEventRecord(S->ev_rec[parity], S->stream), "record event");
 }
 
 int auto_chunk(pcg_solver* S) {
   if (S->opt.chunk > 0) return std::min(S->opt.chunk, kMaxChunk);
-  // aim for ~2 ms of GPU work per chunk (HBM estimate at ~5 TB/s)
+  // aim for ~4 ms of GPU work per chunk: the autotuner's time for the
+  // engine in use, else an HBM estimate at ~5 TB/s.  A chunk boundary costs a
+  // drain + graph launch + record copy (~15 us); a larger chunk costs up to
+  // K-1 early-exit launches after convergence (~3 us each)
   const double bytes = 136.0 * S->A.n_rows + 12.0 * S->A.nnz + 4.0 * S->A.n_rows;
-  const double t_iter = bytes / 5.0e12 + 4e-6;
-  int K = (int)(2e-3 / t_iter);
+  double t_iter = bytes / 5.0e12 + 4e-6;
+  const double tuned = S->engine == 2 ? S->tune_ms[kVariants] : S->tune_ms[S->variant];
+  if (tuned > 0) t_iter = tuned * 1e-3;
+  int K = (int)(4e-3 / t_iter);
   int p = 4;
   while (p * 2 <= K && p < kMaxChunk) p *= 2;
   return std::max(4, std::min(p, kMaxChunk));
@@ -3694,6 +3729,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   if (getenv("PIPECG_B200_NO_PDL")) S->pdl = false;
   if (const char* e = getenv("PIPECG_B200_SELL_BATCH")) S->sell_batch = atoi(e);  // experiment
   if (const char* e = getenv("PIPECG_B200_PA")) S->p_mg = atoi(e) == 0;  // experiment switch
+  if (const char* e = getenv("PIPECG_B200_L2PF")) S->l2_prefetch = atoi(e);  // experiment switch
   if (opts) S->opt = *opts;
   else {
     S->opt.dot_mode = PCG_DOT_TREE;
