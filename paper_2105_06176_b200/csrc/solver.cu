@@ -964,7 +964,7 @@ __host__ __device__ __forceinline__ int pat_smem_bytes(int n_pat, int n_e) {
 // windows of the first stages are requested only after the prologue has
 // seen every peer's previous iteration (they may cover halo rows).
 template <int TR, bool MG, bool WIN, bool XG = false>
-__global__ void __launch_bounds__(TR + 32, TR == 256 ? 3 : (TR == 128 ? 5 : 8))
+__global__ void __launch_bounds__(TR + 32, TR == 256 ? (WIN ? 4 : 3) : (TR == 128 ? 6 : 8))
     pipecg_fused_kernel_s(FusedParams<int> P, WinTable W, int step) {
   using L = FusedLayoutS<TR>;
   constexpr int NT = TR;
@@ -1227,18 +1227,9 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? 3 : (TR == 128 ? 5 : 8))
         } else {
           di = pdv[code];
           const int lo = pst[code], hi = pst[code + 1];
-          for (int k0 = lo; k0 < hi; k0 += 8) {
-            double av[8], mv[8], dv[8];
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-              const int k = k0 + t < hi ? k0 + t : lo;
-              av[t] = pva[k];
-              mv[t] = win[pix[k] + lt];
-              dv[t] = pdv[cwin[pcx[k] + lt]];
-            }
-#pragma unroll
-            for (int t = 0; t < 8; ++t)
-              if (k0 + t < hi) nacc = add(nacc, mul(av[t], mul(dv[t], mv[t])));  // m = M^-1 w
+          for (int k = lo; k < hi; ++k) {
+            const double mc = mul(pdv[cwin[pcx[k] + lt]], win[pix[k] + lt]);  // m = M^-1 w
+            nacc = add(nacc, mul(pva[k], mc));
           }
         }
       } else {

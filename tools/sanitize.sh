@@ -17,6 +17,18 @@ for kind, n in (("3d7", 20), ("2d5", 64)):
     print(eng, kind, n, rep.iterations, float(np.abs(x - xt).max()))
 P = pb.generate_powerlaw(2**13)
 xt = np.full(P.n_rows, 1 / math.sqrt(P.n_rows)); b = pb.spmv(P, xt)
+if eng in ("fused-e", "fused-f"):  # diagonal varies by row class: E's code windows
+    A = pb.stencil_host("3d7", 14)
+    va = np.array(A.values); ro = np.asarray(A.row_offsets); ci = np.asarray(A.col_indices)
+    for i in (3, 100, 2000):
+        for k in range(ro[i], ro[i + 1]):
+            if ci[k] == i: va[k] += 0.5
+    A = pb.CsrMatrix(A.n_rows, A.n_cols, ro, ci, va)
+    xt = np.full(A.n_rows, 1 / math.sqrt(A.n_rows)); b = pb.spmv(A, xt)
+    x, rep = pb.pipecg_solve(A, b, np.zeros(A.n_rows), pb.jacobi_setup(A),
+                             pb.SolverConfig(tolerance=1e-9, max_iterations=400),
+                             options=pb.DeviceOptions(engine=eng, chunk=8))
+    print(eng, "perturbed 3d7", rep.iterations, float(np.abs(x - xt).max()))
 if eng in ("fused-d", "two"):
     x, rep = pb.pipecg_solve(P, b, np.zeros(P.n_rows), pb.jacobi_setup(P),
                              pb.SolverConfig(tolerance=1e-9, max_iterations=100),
@@ -24,7 +36,7 @@ if eng in ("fused-d", "two"):
     print(eng, "powerlaw", rep.iterations)
 PY
 for tool in memcheck racecheck synccheck; do
-  for eng in fused-a fused-b fused-c fused-d fused-p two; do
+  for eng in ${ENGINES:-fused-a fused-b fused-c fused-d fused-p fused-e fused-f two}; do
     timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python /tmp/san_case.py $eng > $OUT/san_${tool}_${eng}.log 2>&1
     echo "$tool $eng rc=$? $(grep -c 'ERROR SUMMARY: 0 errors\|RACECHECK SUMMARY: 0 hazards' $OUT/san_${tool}_${eng}.log) $(grep 'SUMMARY' $OUT/san_${tool}_${eng}.log | tail -1)"
   done
