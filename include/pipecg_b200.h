@@ -271,6 +271,9 @@ int pipecg_b200_solver_comm_info(pcg_solver* s, void** vbuf, int64_t* ld, void**
 int pipecg_b200_ipc_get_handle(void* dev_ptr, void* handle_out);
 int pipecg_b200_ipc_open(const void* handle, void** dev_ptr_out);
 int pipecg_b200_ipc_close(void* dev_ptr);
+/* One process driving several GPUs (pipecg_solve(..., devices=[...])): let
+ * `device` load/store `peer`'s memory (idempotent). */
+int pipecg_b200_enable_peer_access(int device, int peer);
 /* peer_*: world entries (this rank's own at [rank]); send_*: device arrays
  * of n_send entries: local row, destination rank, destination local column */
 int pipecg_b200_solver_connect(pcg_solver* s, int rank, int world, void* const* peer_vbuf,

@@ -109,6 +109,7 @@ _SIGS = {
     "pipecg_b200_ipc_get_handle": ([_vp, _vp], _int),
     "pipecg_b200_ipc_open": ([_vp, ctypes.POINTER(_vp)], _int),
     "pipecg_b200_ipc_close": ([_vp], _int),
+    "pipecg_b200_enable_peer_access": ([_int, _int], _int),
     "pipecg_b200_solver_connect": ([_vp, _int, _int, _vp, _vp, _vp, _i64, _vp, _vp, _vp], _int),
     "pipecg_b200_solve_host": ([_i64, _p_i64, _p_i64, _p_dbl, _p_dbl, _p_dbl, _p_dbl, _dbl, _i64,
                                 _i64, _int, _p_dbl, _p_dbl, _i64, _p_i64, _p_dbl, _i64,

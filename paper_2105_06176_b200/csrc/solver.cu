@@ -3993,6 +3993,22 @@ int pipecg_b200_ipc_close(void* dev_ptr) {
   return cuda_status(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
 }
 
+int pipecg_b200_enable_peer_access(int device, int peer) {
+  int prev = 0, can = 0;
+  cudaGetDevice(&prev);
+  cudaError_t e = cudaDeviceCanAccessPeer(&can, device, peer);
+  if (e != cudaSuccess) return cuda_status(e, "cudaDeviceCanAccessPeer");
+  if (!can) return set_error(PCG_EINVAL, "enable_peer_access: the devices cannot access each other");
+  e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();  // clear the sticky-free status
+    e = cudaSuccess;
+  }
+  cudaSetDevice(prev);
+  return cuda_status(e, "cudaDeviceEnablePeerAccess");
+}
+
 // Per-tile send lists for the fused exchange: the plan's send entries sorted
 // by local row, and for every tile of the applied plan the range of entries
 // whose row it owns.

@@ -571,3 +571,74 @@ def pipecg_solve_distributed(problem: ShardedProblem, b_local, x0_local, cfg, gr
         partition=problem.plan.summary(),
     )
     return x, rep
+
+
+def pipecg_solve_devices(A, b, x0, pc, cfg, devices, options=None):
+    """``pipecg_solve(..., devices=[d0, d1, ...])`` from ONE process (the
+    reference's ``devices=`` keyword, hybrid.py:78,235,424):
+    one thread per device, the host CSR split into nnz-balanced row blocks
+    (``shard_csr``), peer access enabled between the devices, and the same
+    fused exchange as the one-process-per-GPU path -- every device pushes its
+    halo rows and dot partials straight into the others' memory.  Returns the
+    gathered x (host ndarray, or a CUDA tensor on devices[0] for CUDA inputs)
+    and rank 0's SolveReport (identical on every rank).  A device listed
+    twice shares that GPU (grids sized for co-residency; used by the tests)."""
+    import torch
+
+    from . import _lib
+    from .solvers import DeviceOptions, SolverBreakdown, SolverConfig, is_device_tensor
+
+    cfg = cfg or SolverConfig()
+    devices = [int(d) for d in devices]
+    W = len(devices)
+    on_dev = is_device_tensor(b)
+    host = A.to_host() if hasattr(A, "to_host") else A
+    bh = b.detach().cpu().numpy() if on_dev else np.ascontiguousarray(b, dtype=np.float64)
+    xh = (x0.detach().cpu().numpy() if is_device_tensor(x0)
+          else np.ascontiguousarray(x0, dtype=np.float64))
+    d = pc.inv_diag
+    dh = d.detach().cpu().numpy() if is_device_tensor(d) else np.asarray(d, dtype=np.float64)
+    opts = options or DeviceOptions()
+    if len(set(devices)) < W:  # a GPU shared by several ranks: co-resident grids
+        opts = DeviceOptions(dot_mode=opts.dot_mode, engine=opts.engine, chunk=opts.chunk,
+                             use_graphs=opts.use_graphs, max_sms=max(8, 148 // W - 10))
+    for dv in set(devices):
+        for q in set(devices):
+            if q != dv:
+                _lib.call("pipecg_b200_enable_peer_access", dv, q)
+    G = LocalGroup(W)
+    out, errs = [None] * W, []
+
+    def work(r):
+        try:
+            torch.cuda.set_device(devices[r])
+            g = G.view(r)
+            prob = shard_csr(host, g)
+            r0, r1 = prob.plan.row_begin, prob.plan.row_end
+            # the caller's preconditioner on [owned | halo] (not the shard's own Jacobi)
+            dl = np.concatenate([dh[r0:r1], dh[prob.plan.halo_cols]])
+            prob.inv_diag.copy_(torch.from_numpy(dl))
+            dev = prob.inv_diag.device
+            bl = torch.from_numpy(bh[r0:r1].copy()).to(dev)
+            xl = torch.from_numpy(xh[r0:r1].copy()).to(dev)
+            x, rep = pipecg_solve_distributed(prob, bl, xl, cfg, g, opts)
+            out[r] = (x.cpu().numpy(), rep)
+        except BaseException as e:  # noqa: BLE001
+            errs.append((r, e))
+            G._barrier.abort()
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(W)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errs:
+        first = sorted(errs, key=lambda e: isinstance(e[1], threading.BrokenBarrierError))[0][1]
+        if isinstance(first, SolverBreakdown):
+            raise first
+        raise RuntimeError(f"pipecg_solve(devices={devices}) failed: {first!r}") from first
+    x = np.concatenate([o[0] for o in out])
+    rep = out[0][1]
+    if on_dev:
+        x = torch.from_numpy(x).to(torch.device("cuda", devices[0]))
+    return x, rep

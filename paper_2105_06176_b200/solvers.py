@@ -382,7 +382,7 @@ def pipecg_init(A, b, x0, pc) -> PipecgState:
 
 
 def pipecg_solve(A, b, x0, pc, cfg: SolverConfig | None = None, *,
-                 options: DeviceOptions | None = None):
+                 options: DeviceOptions | None = None, devices=None):
     """Solve Ax = b by pipelined preconditioned CG on the GPU (solvers.py:324-387).
 
     Same contract and stopping rule as the reference: convergence when
@@ -390,11 +390,23 @@ def pipecg_solve(A, b, x0, pc, cfg: SolverConfig | None = None, *,
     ``history`` has iterations+1 entries; drift samples every k iterations;
     :class:`SolverBreakdown` on a broken recurrence.  Returns ``(x,
     report)``; x is a host ndarray for host inputs, a CUDA tensor for CUDA
-    inputs."""
+    inputs.
+
+    devices: None (the current GPU) or a list of CUDA device ids; with more
+    than one the rows are sharded over them from this process (the
+    reference's ``devices=`` keyword, hybrid.py:78; see
+    ``distributed.pipecg_solve_devices``)."""
     cfg = cfg or SolverConfig()
     options = options or DeviceOptions()
     t_start = time.perf_counter()
     _check_system(A, b, x0)
+    if devices is not None and len(devices) > 1:
+        from .distributed import pipecg_solve_devices
+
+        return pipecg_solve_devices(A, b, x0, pc, cfg, devices, options)
+    if devices is not None and len(devices) == 1:
+        with torch.cuda.device(int(devices[0])):
+            return pipecg_solve(A, b, x0, pc, cfg, options=options)
     n = int(A.n_rows)
     on_dev = is_device_tensor(b)
     if n == 0:

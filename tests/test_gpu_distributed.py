@@ -214,3 +214,36 @@ def test_virtual_ranks_keep_row_pattern_variants(cuda, engine, code):
     assert not errs, errs
     for eng, flags, its in got:
         assert eng == code and flags & 3 == 3 and its == 30
+
+
+@pytest.mark.parametrize("kind,n", [("3d7", 24), ("2d5", 120)])
+def test_pipecg_solve_devices_keyword(cuda, kind, n):
+    """pipecg_solve(..., devices=[0, 0]): the one-process multi-device entry
+    (the reference's devices= keyword) -- here two ranks sharing the one
+    GPU; same iterations and x as the single-device solve, within the
+    oracle's reorder envelope."""
+    A = pb.stencil_host(kind, n)
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=20000, record_history=True)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=20000)
+    x, rep = pb.pipecg_solve(A, b, x0, pb.JacobiPreconditioner(d), cfg, devices=[0, 0])
+    assert isinstance(x, np.ndarray) and x.shape == (A.n_rows,)
+    assert rep.converged and abs(rep.iterations - ref.iterations) <= 1
+    assert oracle.history_gap(rep.history, ref.history) <= 1e-10
+    assert np.max(np.abs(x - ref.x)) / np.max(np.abs(ref.x)) <= 1e-8
+    assert rep.partition["world"] == 2
+
+
+def test_pipecg_solve_devices_custom_preconditioner(cuda):
+    """The caller's inv_diag (not the shard's own Jacobi) is used on every rank."""
+    A = pb.stencil_host("3d7", 20)
+    x_true, b, x0, d = oracle.manufactured(A)
+    d = d.copy()
+    d[::7] *= 0.9
+    tol = oracle.recipe_tolerance(A, b, d)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=20000, record_history=True)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=20000)
+    x, rep = pb.pipecg_solve(A, b, x0, pb.JacobiPreconditioner(d), cfg, devices=[0, 0, 0])
+    assert abs(rep.iterations - ref.iterations) <= 1
+    assert np.max(np.abs(x - ref.x)) / np.max(np.abs(ref.x)) <= 1e-8
