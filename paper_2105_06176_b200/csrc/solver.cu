@@ -110,6 +110,7 @@ __host__ __device__ inline Record record_at(char* base) {
 struct Step {
   int go;
   double alpha, beta;
+  double alpha_prev;  // alpha of iteration it-1 (it >= 1)
 };
 
 // What the prologue of iteration `it` reduces: pin[(it-1)&1][0..n_pin)[0..2]
@@ -179,7 +180,7 @@ __device__ __forceinline__ long long cta_iteration(const Ctrl* C, int step) {
 template <int NT>
 __device__ Step prologue(Ctrl* C, double* hist, const ReduceIn& R, long long it, int lt,
                          double* red, int bar_id, bool leader) {
-  Step st{0, 0.0, 0.0};
+  Step st{0, 0.0, 0.0, 0.0};
   double gamma, delta, norm, gamma_prev = 0.0, alpha_prev = 0.0;
   if (it == 0) {
     gamma = C->init.gamma;
@@ -219,6 +220,7 @@ __device__ Step prologue(Ctrl* C, double* hist, const ReduceIn& R, long long it,
     const Slot* prev = &C->slot[(it - 1) & 1];
     gamma_prev = __ldcg(&prev->gamma);
     alpha_prev = __ldcg(&prev->alpha);
+    st.alpha_prev = alpha_prev;
     // solvers.py:354-357 (iteration it-1's guards)
     if (gamma < 0.0 || !isfinite(gamma)) {
       if (leader) {
@@ -424,6 +426,7 @@ struct FusedParams {
   const unsigned char* pwin;   // [n_pat_e] window of each entry (WinTable)
   const double* pdinv;         // [n_pat] dinv of each code (valid when WinTable.dinv_by_code)
   const unsigned short* tile_runs;  // [n_tiles] runs the tile's rows use (WinTable bit w)
+  int defer_x;                 // E/F: x updated every other iteration (see pipecg_fused_kernel_s)
   int l2_prefetch;             // E/F: prefetch the streams of the tile this many stages ahead into L2 (0: off)
   int n_pat, n_pat_e;
 };
@@ -964,7 +967,7 @@ __host__ __device__ __forceinline__ int pat_smem_bytes(int n_pat, int n_e) {
 // windows of the first stages are requested only after the prologue has
 // seen every peer's previous iteration (they may cover halo rows).
 template <int TR, bool MG, bool WIN, bool XG = false>
-__global__ void __launch_bounds__(TR + 32, TR == 256 ? (WIN ? 4 : 3) : (TR == 128 ? 6 : 8))
+__global__ void __launch_bounds__(TR + 32, TR == 256 ? (WIN && !XG ? 4 : 3) : (TR == 128 ? 6 : 8))
     pipecg_fused_kernel_s(FusedParams<int> P, WinTable W, int step) {
   using L = FusedLayoutS<TR>;
   constexpr int NT = TR;
@@ -1036,14 +1039,15 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (WIN ? 4 : 3) : (TR == 12
   // ahead: a global load in front of each tile's copies stalled the
   // producer (measured 0.366 -> 0.460 ms at 256^3).  On one GPU every run
   // is copied (costs less than the mask bookkeeping, measured)
-  auto issue_static = [&](long long j, unsigned msk) {
+  // skip_x: x is neither read nor written this iteration (deferred update)
+  auto issue_static = [&](long long j, unsigned msk, bool skip_x) {
     const int s = (int)(j % S);
     const long long t0 = (t_lo + j * t_step) * TR;
     const long long rows = min((long long)TR, P.n - t0);
     const uint32_t b_vec = (uint32_t)((rows * 8 + 15) / 16 * 16);
     const uint32_t b_code = (uint32_t)((rows + 15) / 16 * 16);
     unsigned char* sb = stage0 + (size_t)s * SB;
-    uint32_t tx = 7 * b_vec;
+    uint32_t tx = (skip_x ? 6 : 7) * b_vec;
     if (WIN && MG) {
       tx += b_vec + (dbc ? 0 : b_vec) + b_code;
       for (int w = 0; w < W.n; ++w)
@@ -1061,7 +1065,8 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (WIN ? 4 : 3) : (TR == 12
     }
     mbar_arrive_expect_tx(&full[s], tx);
 #pragma unroll
-    for (int k = 0; k < 7; ++k) bulk_g2s(sb + k * VB, P.vec[k] + t0, b_vec, &full[s], pol);
+    for (int k = 0; k < 7; ++k)
+      if (k != 4 || !skip_x) bulk_g2s(sb + k * VB, P.vec[k] + t0, b_vec, &full[s], pol);
     if (WIN && MG) {
       if (!dbc) bulk_g2s_nohint(sb + 8 * VB, P.dinv + t0, b_vec, &full[s]);
       bulk_g2s_nohint(sb + 9 * VB, P.pcode + t0, b_code, &full[s]);
@@ -1095,15 +1100,25 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (WIN ? 4 : 3) : (TR == 12
                    false);
     }
   };
+  // Deferred x (defer_x): x_{it+1} = x_it + alpha_it p_it only feeds the
+  // result, so even iterations skip it and odd iterations apply both
+  // updates in order, x = (x + alpha_{it-1} p_{it-1}) + alpha_it p_it (p_{it-1}
+  // is the staged p_old) -- the reference's roundings, one x read + write
+  // saved every other iteration.  The kernel whose prologue stops the solve
+  // applies a pending update.  The producer reads the iteration itself so
+  // the first stages know whether to copy x.
   if (tid == 0) {
     pol = policy_evict_first();
+    const long long it0 = read_status(C) == PCG_RUNNING ? C->base_it + step : -1;
+    const bool skip0 = P.defer_x && it0 >= 0 && (it0 & 1) == 0;
     for (long long j = 0; j < my_tiles && j < S; ++j)  // the masks first: one latency
       s_msk[j] = XG && WIN ? tile_mask(P.tile_runs, t_lo + j * t_step) : ~0u;
-    for (long long j = 0; j < my_tiles && j < S; ++j) issue_static(j, XG ? s_msk[j] : ~0u);
+    for (long long j = 0; j < my_tiles && j < S; ++j) issue_static(j, XG ? s_msk[j] : ~0u, skip0);
   }
   if (tid == 32) *s_it = read_status(C) == PCG_RUNNING ? C->base_it + step : -1;
   __syncthreads();
   const long long it = *reinterpret_cast<volatile long long*>(s_it);
+  const bool skip_x = P.defer_x && it >= 0 && (it & 1) == 0;
   const long long par = it < 0 ? 0 : it;
   const double* w_old = P.w[par & 1];
   const double* m_old = P.m[par & 1];
@@ -1128,6 +1143,7 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (WIN ? 4 : 3) : (TR == 12
     if (tid == 32) {
       sc[0] = stp.alpha;
       sc[1] = stp.beta;
+      sc[2] = stp.alpha_prev;
       *decision = stp.go;
     }
   }
@@ -1138,9 +1154,17 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (WIN ? 4 : 3) : (TR == 12
   if (!*decision) {
     if (tid == 0)
       for (long long j = 0; j < my_tiles && j < S; ++j) mbar_wait(&full[j], 0);
+    // the solve stops here: apply the pending update of iteration it-1
+    if (P.defer_x && it >= 1 && ((it - 1) & 1) == 0 && !producer) {
+      const double ap = sc[2];
+      for (long long j = 0; j < my_tiles; ++j) {
+        const long long i = (t_lo + j * t_step) * TR + (tid - 32);
+        if (i < P.n) P.vec[4][i] = add(P.vec[4][i], mul(ap, P.vec[3][i]));
+      }
+    }
     return;
   }
-  const double alpha = sc[0], beta = sc[1];
+  const double alpha = sc[0], beta = sc[1], alpha_prev = sc[2];
   if (producer) {
     if (tid == 0) {
       unsigned nmsk = XG && WIN && S < my_tiles ? tile_mask(P.tile_runs, t_lo + S * t_step) : ~0u;
@@ -1164,7 +1188,7 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (WIN ? 4 : 3) : (TR == 12
           }
         }
         mbar_wait(&empty[j % S], (uint32_t)((j / S - 1) & 1));
-        issue_static(j, msk);
+        issue_static(j, msk, skip_x);
         if (WIN) issue_dyn(j, w_old, m_old, 2, msk);
       }
     }
@@ -1263,8 +1287,13 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (WIN ? 4 : 3) : (TR == 12
       const double qi = add(mi, mul(beta, v_s[1 * TR + lt]));
       const double si = add(wi, mul(beta, v_s[2 * TR + lt]));
       const double ui = v_s[6 * TR + lt];
-      const double pi = add(ui, mul(beta, v_s[3 * TR + lt]));
-      const double xi = add(v_s[4 * TR + lt], mul(alpha, pi));
+      const double p_old = v_s[3 * TR + lt];
+      const double pi = add(ui, mul(beta, p_old));
+      // (deferred x: odd iterations first apply iteration it-1's update)
+      const double xi = skip_x ? 0.0
+                        : add(P.defer_x ? add(v_s[4 * TR + lt], mul(alpha_prev, p_old))
+                                        : v_s[4 * TR + lt],
+                              mul(alpha, pi));
       const double ri = sub(v_s[5 * TR + lt], mul(alpha, si));
       const double un = sub(ui, mul(alpha, qi));
       const double wn = sub(wi, mul(alpha, zi));
@@ -1272,7 +1301,7 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (WIN ? 4 : 3) : (TR == 12
       st_stream(P.vec[1] + i, qi);
       st_stream(P.vec[2] + i, si);
       st_stream(P.vec[3] + i, pi);
-      st_stream(P.vec[4] + i, xi);
+      if (!skip_x) st_stream(P.vec[4] + i, xi);
       st_stream(P.vec[5] + i, ri);
       st_stream(P.vec[6] + i, un);
       st_stream(w_new + i, wn);
@@ -2417,6 +2446,7 @@ struct pcg_solver {
   bool fused_xchg = false;         // distributed: halo + partial push inside the fused kernel
   bool p_mg = true;                // variant P gathers the stored m (C) or dinv*w (A)
   int l2_prefetch = 0;             // E/F L2 prefetch distance in stages (experiment switch)
+  bool no_defer_x = false;         // E/F: update x every iteration (experiment switch)
   unsigned long long* gbar = nullptr;  // variant P grid-barrier counter
   // engine-2 K2 in SELL-C-sigma layout (irregular matrices)
   bool sell = false;
@@ -3027,6 +3057,9 @@ FusedParams<RP> fused_params(pcg_solver* S) {
   P.pdinv = S->pdinv;
   P.tile_runs = S->n_runs > 0 ? tile_runs_for(S, S->tr) : nullptr;
   P.l2_prefetch = S->l2_prefetch;
+  // E/F deferred x update: not with drift samples (they read x every k
+  // iterations) and not when switched off (experiment / A-B measurement)
+  P.defer_x = S->drift_k == 0 && !S->no_defer_x ? 1 : 0;
   P.n_pat = S->pat.n_pat;
   P.n_pat_e = S->pat.n_entries;
   P.X = FusedXchg{};
@@ -3721,6 +3754,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   if (const char* e = getenv("PIPECG_B200_SELL_BATCH")) S->sell_batch = atoi(e);  // experiment
   if (const char* e = getenv("PIPECG_B200_PA")) S->p_mg = atoi(e) == 0;  // experiment switch
   if (const char* e = getenv("PIPECG_B200_L2PF")) S->l2_prefetch = atoi(e);  // experiment switch
+  if (getenv("PIPECG_B200_NO_DEFER_X")) S->no_defer_x = true;                 // experiment switch
   if (opts) S->opt = *opts;
   else {
     S->opt.dot_mode = PCG_DOT_TREE;
@@ -4146,6 +4180,13 @@ int pipecg_b200_solver_init(pcg_solver* S, const double* b, const double* x0, do
   const size_t bytes = (size_t)n * sizeof(double);
   S->tol = tolerance;
   S->max_it = max_iterations;
+  if ((drift_check_interval > 0) != (S->drift_k > 0)) {
+    // the chunk graphs bake in the drift kernels and the deferred-x mode
+    for (int k = 0; k < 2; ++k) {
+      for (auto& kv : S->graphs[k]) cudaGraphExecDestroy(kv.second);
+      S->graphs[k].clear();
+    }
+  }
   S->drift_k = drift_check_interval;
   Record R = record_at(S->rec_dev);
   cudaMemsetAsync(&R.C->comm_error, 0, sizeof(int), st);

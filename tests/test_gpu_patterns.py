@@ -191,3 +191,40 @@ def test_dinv_changed_in_place_between_solves(cuda, engine):
     _seq_with_dinv(A, d1, engine, pc)
     dev.copy_(torch.from_numpy(d0))
     _seq_with_dinv(A, d0, engine, pc)
+
+
+@pytest.mark.parametrize("engine", ["fused-e", "fused-f"])
+@pytest.mark.parametrize("max_it", [1, 2, 3, 10, 11])
+def test_deferred_x_every_stop_parity(cuda, engine, max_it):
+    """E/F update x every other iteration (both updates, in order, on odd
+    iterations; the stopping kernel applies a pending one): x after a stop at
+    either parity -- max_iterations or convergence -- is bitwise the reference's."""
+    A = pb.stencil_host("3d7", 16)
+    x_true, b, x0, d = oracle.manufactured(A)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=1e-300, max_iterations=max_it)
+    cfg = pb.SolverConfig(tolerance=1e-300, max_iterations=max_it, record_history=True)
+    for chunk in (0, 3):
+        x, rep = pb.pipecg_solve(A, b, x0, pb.JacobiPreconditioner(d), cfg,
+                                 options=pb.DeviceOptions(dot_mode="seq", engine=engine,
+                                                          chunk=chunk))
+        assert rep.iterations == max_it
+        np.testing.assert_array_equal(x, ref.x)
+
+
+@pytest.mark.parametrize("engine", ["fused-e", "fused-f"])
+def test_drift_samples_with_row_patterns(cuda, engine):
+    """Drift samples read x: E/F then update x every iteration; the cached
+    solver switches between the two modes across solves."""
+    A = pb.stencil_host("3d7", 14)
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=3000, drift_check_interval=5)
+    pc = pb.JacobiPreconditioner(d)
+    opts = pb.DeviceOptions(dot_mode="seq", engine=engine)
+    for k in (0, 5, 0):
+        cfg = pb.SolverConfig(tolerance=tol, max_iterations=3000, record_history=True,
+                              drift_check_interval=k)
+        x, rep = pb.pipecg_solve(A, b, x0, pc, cfg, options=opts)
+        np.testing.assert_array_equal(x, ref.x)
+        if k:
+            assert [t[0] for t in rep.drift_history] == [t[0] for t in ref.drift_history]
