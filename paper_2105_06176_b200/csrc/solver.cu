@@ -1790,6 +1790,8 @@ struct TwoParams {
 __global__ void __launch_bounds__(256) pipecg_k1_kernel(TwoParams P, int step) {
   __shared__ double red[3 * 8 + 1];
   Ctrl* C = P.C;
+  pdl_trigger();
+  pdl_wait();  // n from the SpMV kernels of the previous iteration
   const long long it = cta_iteration(C, step);
   if (it < 0) return;
   const Step stp = prologue<256>(C, P.hist, P.rin, it, threadIdx.x, red, 1,
@@ -1859,6 +1861,8 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(const Ctrl* C, long long
                                                          const double* __restrict__ val,
                                                          const double* __restrict__ x,
                                                          double* __restrict__ y) {
+  pdl_wait();     // m from K1
+  pdl_trigger();  // ... then the hub-row chunks may start beside this kernel
   if (C && read_status(C) != PCG_RUNNING) return;
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
@@ -1953,6 +1957,13 @@ __global__ void __launch_bounds__(256) gated_spmv_chunks(const Ctrl* C, const Lo
                                                           unsigned* ticket) {
   __shared__ double red[9];
   __shared__ int last;
+  // Launched (programmatically) while the SELL kernel still runs: the hub
+  // rows only need K1's m, which SELL waited for before letting this kernel
+  // start.  Every thread waits for SELL to complete before it exits, so the
+  // next K1 -- ordered after this grid -- sees all of n.
+  struct WaitOnExit {
+    __device__ ~WaitOnExit() { pdl_wait(); }
+  } wait_on_exit;
   if (cta_iteration(C, 0) < 0) return;
   const LongChunk c = ch[blockIdx.x];
   double v[1] = {0.0};
@@ -3200,7 +3211,7 @@ int enqueue_step(pcg_solver* S, int k) {
     P.pout = S->partials;
     P.fin = S->fin;
     P.counter = use_fin(S) ? S->counter : nullptr;
-    pipecg_k1_kernel<<<S->grid, 256, 0, st>>>(P, k);
+    launch_k(pipecg_k1_kernel, (unsigned)S->grid, 256, 0, st, S->pdl, P, k);
   }
   if (S->opt.dot_mode == PCG_DOT_SEQ && !S->connected)
     seq_dots_kernel<<<1, 32, 0, st>>>(R.C, n, S->r, S->u, S->w[0], S->w[1], S->engine == 1,
@@ -3213,13 +3224,14 @@ int enqueue_step(pcg_solver* S, int k) {
   if (S->engine == 2 && S->sell) {
     auto sk = S->sell_batch == 8 ? sell_spmv_kernel<8> : S->sell_batch == 2 ? sell_spmv_kernel<2>
                                                                             : sell_spmv_kernel<4>;
-    sk<<<elementwise_grid(S->sell_slices * 32), 256, 0, st>>>(
-        R.C, n, S->sell_slices, S->sell_ptr, S->sell_perm, S->sell_len, S->sell_col, S->sell_val,
-        S->m, S->nv);
+    launch_k(sk, elementwise_grid(S->sell_slices * 32), 256, 0, st, S->pdl, (const Ctrl*)R.C, n,
+             S->sell_slices, (const long long*)S->sell_ptr, (const int*)S->sell_perm,
+             (const int*)S->sell_len, (const int*)S->sell_col, (const double*)S->sell_val,
+             (const double*)S->m, S->nv);
     if (S->n_chunks > 0) {
-      gated_spmv_chunks<<<(unsigned)S->n_chunks, 256, 0, st>>>(R.C, S->chunks, S->A.col, S->A.val,
-                                                               S->m, S->nv, S->chunk_part,
-                                                               S->chunk_ticket);
+      launch_k(gated_spmv_chunks, (unsigned)S->n_chunks, 256, 0, st, S->pdl, (const Ctrl*)R.C,
+               (const LongChunk*)S->chunks, (const int*)S->A.col, (const double*)S->A.val,
+               (const double*)S->m, S->nv, S->chunk_part, S->chunk_ticket);
     } else if (S->n_long > 0) {
       if (S->A.rp64)
         gated_spmv_long<long long><<<(unsigned)S->n_long, 256, 0, st>>>(
