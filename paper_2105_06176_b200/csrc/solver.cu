@@ -132,6 +132,11 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -1660,7 +1665,9 @@ __global__ void __launch_bounds__(TR + 32) pipecg_fused_kernel_p(FusedParams<RP>
     if (step > 0) {  // grid barrier: every CTA finished iteration it - 1
       if (lt == 0) {
         const unsigned long long target = (unsigned long long)step * gridDim.x;
-        while (ld_acquire_sys(gbar) < target) __nanosleep(32);
+        // GPU-scope acquire spin (P is single-GPU only): 2D 512^2 11.2 -> 11.0 us/it
+        while (ld_acquire_gpu(gbar) < target) {
+        }
       }
       bar_sync(1, NT);
     }
