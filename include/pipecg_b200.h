@@ -246,7 +246,11 @@ void* pipecg_b200_solver_stream(pcg_solver* s);
 /* Poll the result after pipecg_b200_solver_enqueue (synchronises). */
 int pipecg_b200_solver_poll(pcg_solver* s, pcg_result* res);
 
-/* Device pointer of the iterate x (valid after solver_run / poll). */
+/* Device pointer of the iterate x (valid after solver_run / poll).  With the
+ * row-pattern variants E/F, x is updated every other iteration (both updates
+ * in order, bitwise the reference's) and is final once the solve has STOPPED
+ * (convergence or max_iterations); after a solver_enqueue that ends with the
+ * solve still RUNNING it may lag one update. */
 double* pipecg_b200_solver_x(pcg_solver* s);
 
 /* Device pointers of the state vectors in PipecgState field order
