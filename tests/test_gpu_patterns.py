@@ -228,3 +228,47 @@ def test_drift_samples_with_row_patterns(cuda, engine):
         np.testing.assert_array_equal(x, ref.x)
         if k:
             assert [t[0] for t in rep.drift_history] == [t[0] for t in ref.drift_history]
+
+
+def _nine_point(n):
+    """2D 9-point Laplacian-like SPD matrix (diag 8, 8 neighbours -1),
+    assembled here: a stencil the generators do not produce."""
+    rows, cols, vals = [], [], []
+    for y in range(n):
+        for x in range(n):
+            i = y * n + x
+            for dy in (-1, 0, 1):
+                for dx in (-1, 0, 1):
+                    xx, yy = x + dx, y + dy
+                    if 0 <= xx < n and 0 <= yy < n:
+                        rows.append(i)
+                        cols.append(yy * n + xx)
+                        vals.append(8.0 if (dx, dy) == (0, 0) else -1.0)
+    ro = np.zeros(n * n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=n * n), out=ro[1:])
+    return pb.CsrMatrix(n * n, n * n, ro, np.array(cols, dtype=np.int64), np.array(vals))
+
+
+def _tridiag(n):
+    ro = np.zeros(n + 1, dtype=np.int64)
+    cols, vals = [], []
+    for i in range(n):
+        for j in (i - 1, i, i + 1):
+            if 0 <= j < n:
+                cols.append(j)
+                vals.append(2.5 if j == i else -1.0)
+        ro[i + 1] = len(cols)
+    return pb.CsrMatrix(n, n, ro, np.array(cols, dtype=np.int64), np.array(vals))
+
+
+@pytest.mark.parametrize("engine", ["fused-e", "fused-f", "auto"])
+@pytest.mark.parametrize("make", [lambda: _nine_point(45), lambda: _tridiag(37),
+                                  lambda: _tridiag(300000)])
+def test_assembled_matrices_seq_bitwise(cuda, make, engine):
+    """Matrices assembled outside the generators (9-point 2D, tridiagonal
+    with n not a multiple of any tile height, one with >= 64K rows so the
+    autotuner runs): dictionary = oracle's, solves bitwise."""
+    A = make()
+    n_pat, n_e = pb.as_device_csr(A).row_patterns()
+    assert (n_pat, n_e) == oracle.row_patterns(A)[:2]
+    _seq_vs_oracle(A, engine, max_it=400)
