@@ -411,6 +411,7 @@ def e2e_host(pb, torch, kind, n, reps: int = 3):
             "h2d_bytes_per_call": h2d, "d2h_bytes_per_call": d2h,
             "iterations_per_call": per_call_it, "seconds_per_call": total_s / reps,
             "calls": reps, "seconds_each_call": per_call, "warmup_call_seconds": round(warm_s, 4),
+            "value_median_call": (total_it / reps) / sorted(per_call)[len(per_call) // 2],
             "call": "paper_2105_06176_b200.pipecg_solve(A host CsrMatrix int64, b, x0 numpy, "
                     "JacobiPreconditioner(numpy), SolverConfig(tol=1e-8*norm0)) -> (x numpy, report)",
             "host_memory": "pageable numpy (the reference's own int64/float64 arrays); staged by the "

@@ -1241,18 +1241,10 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? 3 : (TR == 128 ? 6 : 8))
         if (W.dinv_uniform) {  // one dinv for every row: only the own-row code window
           di = W.dinv0;
           const int lo = pst[code], hi = pst[code + 1];
-          for (int k0 = lo; k0 < hi; k0 += 8) {
-            double av[8], mv[8];
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-              const int k = k0 + t < hi ? k0 + t : lo;
-              av[t] = pva[k];
-              mv[t] = win[pix[k] + lt];
-            }
-#pragma unroll
-            for (int t = 0; t < 8; ++t)
-              if (k0 + t < hi) nacc = add(nacc, mul(av[t], mul(di, mv[t])));  // m = M^-1 w
-          }
+          // a plain loop: batching the loads 8 at a time measured 8% slower
+          // at 256^3 (0.369 vs 0.339 ms, same box) and 15% at 27-pt
+          for (int k = lo; k < hi; ++k)
+            nacc = add(nacc, mul(pva[k], mul(di, win[pix[k] + lt])));  // m = M^-1 w
         } else {
           di = pdv[code];
           const int lo = pst[code], hi = pst[code + 1];
