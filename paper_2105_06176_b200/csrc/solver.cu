@@ -3316,20 +3316,31 @@ int chunk_graph(pcg_solver* S, int K, int parity, cudaGraphExec_t* out) {
     *out = it->second;
     return PCG_OK;
   }
-  cudaGraph_t g = nullptr;
-  cudaGraphExec_t exec = nullptr;
-  cudaError_t e = cudaStreamBeginCapture(S->stream, cudaStreamCaptureModeThreadLocal);
-  if (e != cudaSuccess) return cuda_status(e, "begin capture");
-  int rc = enqueue_chunk_body(S, K, parity);
-  e = cudaStreamEndCapture(S->stream, &g);
-  if (rc) return rc;
-  if (e != cudaSuccess) return cuda_status(e, "end capture");
-  e = cudaGraphInstantiate(&exec, g, 0);
-  cudaGraphDestroy(g);
-  if (e != cudaSuccess) return cuda_status(e, "graph instantiate");
-  S->graphs[parity][K] = exec;
-  *out = exec;
-  return PCG_OK;
+  // A capture can be invalidated from outside this solver: another thread
+  // synchronising the whole device (cudaDeviceSynchronize, a cudaFree) while
+  // this stream captures -- e.g. several solvers sharing one GPU from one
+  // process.  Retry a few times; the caller falls back to direct launches.
+  cudaError_t e = cudaSuccess;
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    e = cudaStreamBeginCapture(S->stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) break;
+    const int rc = enqueue_chunk_body(S, K, parity);
+    e = cudaStreamEndCapture(S->stream, &g);
+    if (!rc && e == cudaSuccess) {
+      e = cudaGraphInstantiate(&exec, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return cuda_status(e, "graph instantiate");
+      S->graphs[parity][K] = exec;
+      *out = exec;
+      return PCG_OK;
+    }
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();  // the invalidation is not sticky
+    if (e == cudaSuccess) e = cudaErrorStreamCaptureInvalidated;
+  }
+  return cuda_status(e, "graph capture");
 }
 
 int launch_chunk(pcg_solver* S, int K, int parity) {
@@ -3348,7 +3359,8 @@ int launch_chunk(pcg_solver* S, int K, int parity) {
     if (rc) return rc;
     rc = cuda_status(cudaEventRecord(S->ev_rec[parity], S->stream), "record event");
     cudaGraphExec_t exec = nullptr;
-    if (!rc) rc = chunk_graph(S, K, parity, &exec);
+    if (!rc && chunk_graph(S, K, parity, &exec) != PCG_OK)
+      cudaGetLastError();  // no graph this time: the next chunk of this shape launches directly
     S->graph_launches++;
     return rc;
   }
@@ -3695,7 +3707,8 @@ int autotune(pcg_solver* S, int grid2, bool with_engine2, bool irregular) {
       // b := n (ones), x0 := z (zeros); init copies them before overwriting
       rc = pipecg_b200_solver_init(S, S->nv, S->z, 0.0, 1LL << 40, 0, st);
       cudaGraphExec_t ge = nullptr;
-      if (!rc && S->opt.use_graphs) rc = chunk_graph(S, kTuneIters, 1, &ge);
+      if (!rc && S->opt.use_graphs && chunk_graph(S, kTuneIters, 1, &ge) != PCG_OK)
+        cudaGetLastError();  // timed with direct launches instead
       if (!rc) rc = launch_chunk(S, 2, 0);
       cudaEventRecord(e0, st);
       if (!rc) rc = launch_chunk(S, kTuneIters, 1);
@@ -4364,8 +4377,8 @@ int pipecg_b200_solver_prepare(pcg_solver* S, int64_t count) {
   for (int k : sizes)
     for (int parity = 0; parity < 2 && k > 0; ++parity) {
       cudaGraphExec_t exec = nullptr;
-      int rc = chunk_graph(S, k, parity, &exec);
-      if (rc) return rc;
+      if (chunk_graph(S, k, parity, &exec) != PCG_OK)
+        cudaGetLastError();  // launched directly instead (see chunk_graph)
     }
   return PCG_OK;
 }

@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 import threading
 import time
 from dataclasses import dataclass, field
@@ -441,7 +442,7 @@ class DistributedSolver:
         # E (autotuned on the shard alone) trails F once the halo exchange is
         # live (2 virtual ranks at 256^3: F 0.55, A 0.64, E 0.70 ms/iteration;
         # tools/dist1.py) -> F, unless E was asked for explicitly
-        if chosen == 8 and engine != "fused-e":
+        if chosen == 8 and engine != "fused-e" and not os.environ.get("PIPECG_B200_DIST_KEEP_E"):
             chosen = 9
         if mine != chosen:
             self.solver.close()
@@ -553,7 +554,10 @@ def pipecg_solve_distributed(problem: ShardedProblem, b_local, x0_local, cfg, gr
     solver.init(b_local, x0_local, cfg.tolerance, cfg.max_iterations)
     import torch
 
-    torch.cuda.synchronize()
+    # the solver's own stream, not the device: another rank sharing this GPU
+    # (devices=[0, 0], virtual ranks) may be capturing a CUDA graph, and a
+    # device-wide synchronize would invalidate that capture
+    torch.cuda.ExternalStream(solver.stream).synchronize()
     t1 = time.perf_counter()
     res, hist, _, _ = solver.run(cfg.record_history, cfg.max_iterations)
     t2 = time.perf_counter()

@@ -421,7 +421,9 @@ def pipecg_solve(A, b, x0, pc, cfg: SolverConfig | None = None, *,
     solver = _solver_for(A, pc, options)
     bd, x0d = to_device_f64(b), to_device_f64(x0)
     solver.init(bd, x0d, cfg.tolerance, cfg.max_iterations, cfg.drift_check_interval)
-    torch.cuda.synchronize()
+    # the solver's stream only: a device-wide synchronize would break a CUDA
+    # graph capture of a solver driven from another thread on this GPU
+    torch.cuda.ExternalStream(solver.stream).synchronize()
     nvtx.range_pop()
     t_setup = time.perf_counter()
     nvtx.range_push("pipecg.iterations")

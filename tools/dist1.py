@@ -30,7 +30,8 @@ for eng in engines:
             s = D.DistributedSolver(prob, g, opts)
             xt, b = D.manufactured_local(prob)
             s.init(b, torch.zeros_like(b), 0.0, 1000)
-            s.solver.enqueue(5); s.solver.prepare(100); torch.cuda.synchronize()
+            s.solver.enqueue(5); s.solver.prepare(100)
+            torch.cuda.ExternalStream(s.stream).synchronize()  # not the device: peers may capture
             g.barrier()
             st = torch.cuda.ExternalStream(s.stream)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
