@@ -439,10 +439,13 @@ class DistributedSolver:
         mine = int(self.solver.poll().engine)
         mine = 5 if mine == 7 else mine  # P runs as C once connected
         chosen = group.all_gather_object(mine)[0]
-        # E (autotuned on the shard alone) trails F once the halo exchange is
-        # live (2 virtual ranks at 256^3: F 0.55, A 0.64, E 0.70 ms/iteration;
-        # tools/dist1.py) -> F, unless E was asked for explicitly
-        if chosen == 8 and engine != "fused-e" and not os.environ.get("PIPECG_B200_DIST_KEEP_E"):
+        # Ranks sharing one GPU (max_sms > 0: virtual ranks, tests): E trails
+        # F there (2 ranks on one B200 at 256^3: F 0.55, E 0.59-0.60
+        # ms/iteration, tools/dist1.py) -> F.  With a GPU per rank the
+        # shard's own autotuning stands (one connected rank at 256^3: E 0.387,
+        # F 0.445 ms/iteration).
+        if (chosen == 8 and engine != "fused-e" and opts.max_sms > 0
+                and not os.environ.get("PIPECG_B200_DIST_KEEP_E")):
             chosen = 9
         if mine != chosen:
             self.solver.close()
