@@ -30,6 +30,7 @@ JSON line fields (rank 0):
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -382,7 +383,8 @@ def e2e_host(pb, torch, kind, n, reps: int = 3):
 
     warm_transfers()  # one-time pinned-ring / thread-pool start, like CUDA context creation
     total_it, total_s, per_call = 0, 0.0, []
-    for call in range(reps + 1):  # call 0: untimed warm-up (allocator growth, page-in)
+    warmup_calls = 2  # untimed: allocator / pool growth, page-in of the host arrays
+    for call in range(reps + warmup_calls):
         # a fresh CsrMatrix each call: nothing cached on the device
         A = pb.CsrMatrix.__new__(pb.CsrMatrix)
         for k, v in (("n_rows", N), ("n_cols", N), ("row_offsets", ro), ("col_indices", ci),
@@ -395,7 +397,12 @@ def e2e_host(pb, torch, kind, n, reps: int = 3):
         x, rep = pb.pipecg_solve(A, b, x0, pc, cfg)
         dt = time.perf_counter() - t0
         del A
-        if call == 0:
+        # the call's device matrix and solver form a reference cycle (the
+        # solver cache lives on the matrix): collect it here, not inside the
+        # next timed call (a cyclic-GC pass freeing ~2 GB of device memory
+        # mid-call measured +40..200 ms outliers)
+        gc.collect()
+        if call < warmup_calls:
             warm_s = dt
             continue
         total_it += rep.iterations
@@ -418,7 +425,7 @@ def e2e_host(pb, torch, kind, n, reps: int = 3):
                            "native pinned pipeline (csrc/hostio.cu), indices narrowed to int32 "
                            "on the host side",
             "not_timed": "process start-up: CUDA context, pinned staging ring + host thread pool "
-                         "(warm_transfers) and one untimed warm-up call (device allocator growth); "
+                         "(warm_transfers) and two untimed warm-up calls (device allocator growth); "
                          "every timed call still uploads a fresh CsrMatrix, builds a new solver, "
                          "solves and downloads x; the engine choice comes from the process tuning "
                          "cache when an identically shaped matrix was tuned earlier in the process"}
