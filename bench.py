@@ -358,7 +358,7 @@ def time_to_solution(pb, torch, A, pc_d):
             "tolerance": tol, "verify_inf_err": err}
 
 
-def e2e_host(pb, torch, kind, n, reps: int = 3):
+def e2e_host(pb, torch, kind, n, reps: int = 5):
     """The reference-facing drop-in call with host numpy buffers."""
     import numpy as np
 
