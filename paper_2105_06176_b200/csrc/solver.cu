@@ -972,7 +972,7 @@ __host__ __device__ __forceinline__ int pat_smem_bytes(int n_pat, int n_e) {
 // windows of the first stages are requested only after the prologue has
 // seen every peer's previous iteration (they may cover halo rows).
 template <int TR, bool MG, bool WIN, bool XG = false>
-__global__ void __launch_bounds__(TR + 32, TR == 256 ? 3 : (TR == 128 ? 6 : 8))
+__global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128 ? 6 : 8))
     pipecg_fused_kernel_s(FusedParams<int> P, WinTable W, int step) {
   using L = FusedLayoutS<TR>;
   constexpr int NT = TR;
