@@ -3897,7 +3897,12 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   }
   const int grid2 = std::min<int>(kDotGrid, 4 * S->num_sms);
   S->grid = grid2;
-  for (int v = 0; v < kVariants; ++v) S->grid = std::max(S->grid, S->plans[v].grid);
+  // partials are sized for the largest grid any candidate (plan or autotune
+  // alternative) can launch with
+  for (int v = 0; v < kVariants; ++v) {
+    S->grid = std::max(S->grid, S->plans[v].grid);
+    for (const FusedPlan& p : S->alts[v]) S->grid = std::max(S->grid, p.grid);
+  }
   phase("fused_setup+long+sell");
   rc = alloc_state(S);
   phase("alloc_state");

@@ -272,3 +272,24 @@ def test_assembled_matrices_seq_bitwise(cuda, make, engine):
     n_pat, n_e = pb.as_device_csr(A).row_patterns()
     assert (n_pat, n_e) == oracle.row_patterns(A)[:2]
     _seq_vs_oracle(A, engine, max_it=400)
+
+
+@pytest.mark.parametrize("max_sms", [0, 64, 20])
+def test_autotune_alternatives_fit_the_partials(cuda, max_sms):
+    """Regression: an autotune alternative (F at 128-row tiles, 6 CTAs/SM)
+    launched a larger grid than any variant's default plan and wrote its
+    block partials past the buffer (illegal access with max_sms=64).  The
+    autotuned solve must run and stay bitwise in seq mode."""
+    A = pb.stencil_host("3d7", 48)
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=3000)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=3000, record_history=True)
+    for dot_mode in ("seq", "tree"):
+        opts = pb.DeviceOptions(dot_mode=dot_mode, engine="auto", max_sms=max_sms)
+        x, rep = pb.pipecg_solve(A, b, x0, pb.JacobiPreconditioner(d), cfg, options=opts)
+        if dot_mode == "seq":
+            assert rep.history == ref.history
+            np.testing.assert_array_equal(x, ref.x)
+        else:
+            assert abs(rep.iterations - ref.iterations) <= 1
