@@ -182,6 +182,7 @@ def cpu_baseline(kind: str, n: int, seconds: float, warmup: int = 1, steps: int 
     oracle.build()
     threads = os.cpu_count() or 1
     oracle.set_threads(threads)
+    oracle.set_exact_dots(False)  # timing mode: chunked parallel dots
     A = oracle.as_csr(host_problem(kind, n))
     x_true, b, x0, d = oracle.manufactured(A)
     st = oracle.Stepper(A, b, d)
@@ -203,6 +204,7 @@ def cpu_baseline(kind: str, n: int, seconds: float, warmup: int = 1, steps: int 
         dt = time.perf_counter() - t0
     st.close()
     oracle.set_threads(1)
+    oracle.set_exact_dots(True)
     return {
         "value": done / dt, "unit": UNIT, "cores": threads, "kind": "port",
         "sample": f"oracle/pipecg_oracle.c (reference algorithm, kernels.py/solvers.py restated "
@@ -223,6 +225,7 @@ def run_reference(args):
     oracle.build()
     threads = os.cpu_count() or 1
     oracle.set_threads(threads)
+    oracle.set_exact_dots(False)  # timing mode: chunked parallel dots
     A = oracle.as_csr(host_problem(kind, n))
     x_true, b, x0, d = oracle.manufactured(A)
     st = oracle.Stepper(A, b, d)
@@ -277,20 +280,31 @@ CONFIG_NAMES = {"3d7-256": "BASELINE.json configs[1]", "2d5-512": "BASELINE.json
 
 
 def engine_bytes(engine: int, flags: int, N: int, nnz: int):
-    """Compulsory HBM bytes per iteration of the engine's kernel (vector
-    streams x 8N + the matrix as that engine stores it), or None (engine 2:
-    two kernels).  See DESIGN.md §4."""
-    csr = 12 * nnz + 4 * (N + 1)
-    win, dbc, uni = bool(flags & 2), bool(flags & 4), bool(flags & 8)
-    if engine in (3, 4):
-        return 17 * 8 * N + csr
-    if engine in (5, 6, 7):
-        return 19 * 8 * N + csr
-    if engine == 8:  # E: 16 streams with windows (dinv by code), else 17 (gathers)
-        return (16 if (win and dbc) else 17) * 8 * N + N
-    if engine == 9:  # F: 19 streams, 18 when dinv comes from the code
-        return (18 if (win and dbc) else 19) * 8 * N + N
-    return None
+    """ALGORITHMIC HBM bytes per iteration of the engine in use: the vectors
+    and matrix data one iteration of that engine must move at minimum, in
+    the engine's own layout, averaged over an even/odd
+    iteration pair when the deferred x update is on (flags & 16: E/F read
+    and write x every other iteration).  Returns (bytes, formula)."""
+    rp = 8 if nnz >= 2**31 else 4
+    csr = 12 * nnz + rp * (N + 1)
+    win, dbc, defer = bool(flags & 2), bool(flags & 4), bool(flags & 16)
+    if engine in (3, 4):  # A/B: 17 streams + CSR
+        return 17 * 8 * N + csr, "17 vector streams x 8N + CSR (12 nnz + 4(N+1))"
+    if engine in (5, 6, 7):  # C/D/P: 19 streams + CSR
+        return 19 * 8 * N + csr, "19 vector streams x 8N + CSR (12 nnz + 4(N+1))"
+    if engine in (8, 9):
+        # E: 16 streams with windows + dinv from the code, else 17 (gathers)
+        # F: 18 streams when dinv comes from the code, else 19
+        streams = (16 if (win and dbc) else 17) if engine == 8 else (18 if (win and dbc) else 19)
+        if defer:
+            streams -= 1  # x read + write on odd iterations only: 2 streams / 2
+        sname = "E" if engine == 8 else "F"
+        return (int(streams * 8 * N + N),
+                f"{sname}: {streams} vector streams x 8N (averaged over the deferred-x pair) "
+                "+ 1 B/row code" if defer else f"{sname}: {streams} vector streams x 8N + 1 B/row code")
+    # engine 2: K1 (10 vectors read + 9 written + ... = 20 streams) + SpMV
+    # (m gathered once, n written, CSR) = the canonical 22 streams + CSR
+    return canonical_bytes(N, nnz), "two kernels: 22 vector streams x 8N + CSR (canonical)"
 
 
 def committed_traffic(config: str, engine: int):
@@ -382,8 +396,14 @@ def e2e_host(pb, torch, kind, n, reps: int = 5):
     from paper_2105_06176_b200._device import warm_transfers
 
     warm_transfers()  # one-time pinned-ring / thread-pool start, like CUDA context creation
+    from paper_2105_06176_b200 import _lib
+
+    # the first call of the process for this matrix shape pays the autotuner
+    # (and graph instantiation): forget what the device-timed leg tuned
+    _lib.load().pipecg_b200_tune_cache_clear()
     total_it, total_s, per_call = 0, 0.0, []
     warmup_calls = 2  # untimed: allocator / pool growth, page-in of the host arrays
+    first = None
     for call in range(reps + warmup_calls):
         # a fresh CsrMatrix each call: nothing cached on the device
         A = pb.CsrMatrix.__new__(pb.CsrMatrix)
@@ -402,12 +422,21 @@ def e2e_host(pb, torch, kind, n, reps: int = 5):
         # next timed call (a cyclic-GC pass freeing ~2 GB of device memory
         # mid-call measured +40..200 ms outliers)
         gc.collect()
+        if call == 0:
+            first = {"seconds": round(dt, 4), "iterations": rep.iterations,
+                     "value": rep.iterations / dt,
+                     "setup_s": round(rep.phase_times["setup"], 4),
+                     "iterations_s": round(rep.phase_times["iterations"], 4),
+                     "note": "first call for this matrix shape in the process: upload + "
+                             "autotune (every candidate engine timed on ~10 iterations) + "
+                             "graph capture + solve + download"}
         if call < warmup_calls:
             warm_s = dt
             continue
         total_it += rep.iterations
         total_s += dt
         per_call.append(round(dt, 4))
+    phases = e2e_phases(pb, torch, N, ro, ci, va, b, d, tol)
     # bytes that cross PCIe: int32 row offsets / columns (narrowed on the host
     # side of the pinned pipeline), float64 values, b, x0 and inv_diag
     h2d = (8 if nnz >= 2**31 else 4) * (N + 1) + 12 * nnz + 3 * 8 * N
@@ -418,6 +447,7 @@ def e2e_host(pb, torch, kind, n, reps: int = 5):
             "h2d_bytes_per_call": h2d, "d2h_bytes_per_call": d2h,
             "iterations_per_call": per_call_it, "seconds_per_call": total_s / reps,
             "calls": reps, "seconds_each_call": per_call, "warmup_call_seconds": round(warm_s, 4),
+            "first_call": first, "phases_ms": phases,
             "value_median_call": (total_it / reps) / sorted(per_call)[len(per_call) // 2],
             "call": "paper_2105_06176_b200.pipecg_solve(A host CsrMatrix int64, b, x0 numpy, "
                     "JacobiPreconditioner(numpy), SolverConfig(tol=1e-8*norm0)) -> (x numpy, report)",
@@ -429,6 +459,47 @@ def e2e_host(pb, torch, kind, n, reps: int = 5):
                          "every timed call still uploads a fresh CsrMatrix, builds a new solver, "
                          "solves and downloads x; the engine choice comes from the process tuning "
                          "cache when an identically shaped matrix was tuned earlier in the process"}
+
+
+def e2e_phases(pb, torch, N, ro, ci, va, b, d, tol):
+    """Where one steady-state host-buffer call spends its time: the steps of
+    pipecg_solve (solvers.py) timed one by one, synchronising between them
+    (one extra call, outside the e2e value)."""
+    import numpy as np
+
+    from paper_2105_06176_b200 import kernels as K, solvers as S, sparse as SP
+
+    A = pb.CsrMatrix.__new__(pb.CsrMatrix)
+    for k, v in (("n_rows", N), ("n_cols", N), ("row_offsets", ro), ("col_indices", ci),
+                 ("values", va)):
+        object.__setattr__(A, k, v)
+    pc = pb.JacobiPreconditioner(d)
+    names = ("csr_upload", "inv_diag_upload", "solver_create", "b_x0_upload", "init", "iterations",
+             "x_download")
+    torch.cuda.synchronize()
+    t = [time.perf_counter()]
+
+    def mark():
+        torch.cuda.synchronize()
+        t.append(time.perf_counter())
+
+    SP.as_device_csr(A); mark()
+    K.device_inv_diag(pc); mark()
+    s, cached = S._solver_for(A, pc, pb.DeviceOptions()); mark()
+    try:
+        bd, x0d = S.to_device_f64(b), S.to_device_f64(np.zeros(N)); mark()
+        s.init(bd, x0d, tol, 20000, 0); mark()
+        res = s.run(False, 20000, 0)[0]; mark()
+        s.x_host(); mark()
+    finally:
+        s.lock.release()
+    out = {nm: round(1e3 * (t[i + 1] - t[i]), 2) for i, nm in enumerate(names)}
+    out["iterations_run"] = int(res.iterations)
+    out["solver_create_note"] = ("SELL-C-sigma / long-row chunk / row-pattern setup + state "
+                                 "allocation; the engine comes from the process tuning cache")
+    del A, pc, s, bd, x0d
+    gc.collect()
+    return out
 
 
 def run_distributed(args):
@@ -453,7 +524,9 @@ def run_distributed(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     group = D.TorchGroup()
     kind, n = parse_config(args.config)
-    opts = pb.DeviceOptions(engine=args.engine, max_sms=max(8, 148 // ws - 10) if same else 0)
+    from paper_2105_06176_b200._device import shared_max_sms
+
+    opts = pb.DeviceOptions(engine=args.engine, max_sms=shared_max_sms(ws) if same else 0)
     prob = D.shard_stencil(kind, n, group)
     solver = D.DistributedSolver(prob, group, opts)
     xt, b = D.manufactured_local(prob)
@@ -563,9 +636,9 @@ def run_b200(args):
                                    pb.DeviceOptions(engine=args.engine))
     t_iter = ms / 1e3 / args.steps
     value = args.steps / (ms / 1e3)
-    achieved = B / t_iter / 1e9
     traffic, traffic_src = committed_traffic(args.config, info["engine"])
-    kb = engine_bytes(info["engine"], info.get("pattern_flags", 0), N, nnz)
+    kb, kb_formula = engine_bytes(info["engine"], info.get("pattern_flags", 0), N, nnz)
+    achieved = kb / t_iter / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -589,19 +662,21 @@ def run_b200(args):
                                             "fused_E": info["tune_ms"][5],
                                             "fused_F": info["tune_ms"][6],
                                             "two_kernel": info["tune_ms"][7]}},
+        # achieved = the engine's ALGORITHMIC bytes per iteration (its own
+        # layout: what one iteration must move at minimum) / the measured
+        # iteration time; `canonical_equivalent` re-states the same time in
+        # SURVEY.md §8(d)'s fixed 22-stream CSR bytes (not moved by E/F, so
+        # its frac can exceed 1: a speed, not a roofline fraction)
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "traffic_source": traffic_src,
-                     "bytes_per_iteration": B,
-                     "bytes_formula": "176N + 12nnz + 4(N+1) (canonical, SURVEY.md §8(d))",
+                     "bytes_per_iteration": kb, "bytes_formula": kb_formula,
                      "peak_source": peak_src,
                      "frac_of_8TBs_spec": achieved / 8000.0,
-                     "kernel_bytes_per_iteration": kb,
-                     "kernel_achieved": kb / t_iter / 1e9 if kb else None,
-                     "kernel_frac": kb / t_iter / 1e9 / peak if kb else None,
-                     "kernel_bytes_note": "compulsory bytes of the engine's own data layout "
-                                          "(E/F: row-pattern dictionary, 1 code byte per row, "
-                                          "no CSR); frac > 1 above is in canonical bytes",
+                     "canonical_equivalent": {
+                         "bytes_per_iteration": B,
+                         "bytes_formula": "176N + 12nnz + 4(N+1) (SURVEY.md §8(d), 22 streams + CSR)",
+                         "achieved": B / t_iter / 1e9, "frac": B / t_iter / 1e9 / peak},
                      "pattern_flags": info.get("pattern_flags"),
                      "kernel": KERNELS.get(info["engine"], "?") + " (one launch per iteration)"},
         "gpu_launches": info["kernel_launches"],
@@ -621,11 +696,17 @@ def run_b200(args):
             pc4 = pb.jacobi_setup(A4).inv_diag
             ms4, info4 = time_iterations(pb, torch, A4, pc4, 3, 40)
             B4 = canonical_bytes(A4.n_rows, A4.nnz)
+            kb4, _ = engine_bytes(info4["engine"], info4.get("pattern_flags", 0), A4.n_rows, A4.nnz)
             t4 = ms4 / 1e3 / 40
             line["north_star"] = {"workload": "3d7 Poisson n=400 (N=64,000,000, nnz=447,040,000)",
                                   "iters_per_s": 1 / t4, "ms_per_iter": t4 * 1e3,
-                                  "achieved_gbs": B4 / t4 / 1e9, "frac": B4 / t4 / 1e9 / peak,
-                                  "target_frac": 0.75, "ok": info4["ok"]}
+                                  "engine": ENGINES.get(info4["engine"], "?"),
+                                  "achieved_gbs": kb4 / t4 / 1e9, "frac": kb4 / t4 / 1e9 / peak,
+                                  "bytes_per_iteration": kb4,
+                                  "canonical_equivalent_frac": B4 / t4 / 1e9 / peak,
+                                  "target": ">= 75% of the HBM roofline = 291 it/s "
+                                            "(SURVEY.md §8(d), canonical bytes)",
+                                  "ok": info4["ok"]}
             del A4, pc4
             torch.cuda.empty_cache()
         except Exception as e:  # report, do not hide

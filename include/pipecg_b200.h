@@ -214,7 +214,8 @@ typedef struct {
   double tune_ms[8];   /* autotune ms/iteration: fused A, B, C, D, P, E, F, two-kernel
                           (0 = not run) */
   int pattern_flags;   /* row-pattern dictionary in use by E/F: 1 dictionary, 2 windows,
-                          4 dinv a function of the row's code, 8 ... one dinv for all rows */
+                          4 dinv a function of the row's code, 8 ... one dinv for all rows,
+                          16 deferred x update (x read + written every other iteration) */
 } pcg_result;
 
 int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_solver** out);
@@ -245,6 +246,10 @@ int pipecg_b200_solver_enqueue(pcg_solver* s, int64_t count);
 void* pipecg_b200_solver_stream(pcg_solver* s);
 /* Poll the result after pipecg_b200_solver_enqueue (synchronises). */
 int pipecg_b200_solver_poll(pcg_solver* s, pcg_result* res);
+/* Forget the process-wide autotuning cache (engine / variant picked per
+ * matrix shape and row profile): the next solver_create re-tunes.  Used to
+ * measure a first call including its autotuning. */
+void pipecg_b200_tune_cache_clear(void);
 
 /* Device pointer of the iterate x (valid after solver_run / poll).  With the
  * row-pattern variants E/F, x is updated every other iteration (both updates

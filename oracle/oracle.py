@@ -77,6 +77,7 @@ def lib():
         )
         L.or_pcg_solve.restype = ctypes.c_int
         L.or_set_threads.argtypes = [ctypes.c_int]
+        L.or_set_exact_dots.argtypes = [ctypes.c_int]
         L.or_max_threads.restype = ctypes.c_int
         L.or_gen_csr.argtypes = [ctypes.c_int, ctypes.c_int64, _p_i64, _p_i64, _p_f64]
         L.or_gen_csr.restype = ctypes.c_int
@@ -103,6 +104,13 @@ def set_threads(t: int) -> int:
     """Thread count for the CPU baseline (1 = the reference's own orders)."""
     lib().or_set_threads(int(t))
     return int(t)
+
+
+def set_exact_dots(exact: bool) -> None:
+    """True (default): dots in the requested order (seq = the reference's)
+    for any thread count.  False: static-chunked parallel dots -- only for
+    the CPU-baseline timing (bench.py), never for parity."""
+    lib().or_set_exact_dots(1 if exact else 0)
 
 
 def max_threads() -> int:

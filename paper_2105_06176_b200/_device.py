@@ -21,6 +21,19 @@ def require_cuda() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+def shared_max_sms(ranks_on_device: int, device: int | None = None) -> int:
+    """``DeviceOptions.max_sms`` for one of ``ranks_on_device`` solvers that
+    share a GPU: the device's SM count split between them (less a margin),
+    so every rank's persistent grid stays co-resident while its prologue
+    waits for the peers."""
+    k = max(1, int(ranks_on_device))
+    if k == 1:
+        return 0
+    dev = torch.cuda.current_device() if device is None else int(device)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    return max(8, sms // k - 10)
+
+
 def stream_ptr() -> int:
     return torch.cuda.current_stream().cuda_stream
 

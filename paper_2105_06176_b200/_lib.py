@@ -103,6 +103,7 @@ _SIGS = {
     "pipecg_b200_solver_prepare": ([_vp, _i64], _int),
     "pipecg_b200_solver_stream": ([_vp], _vp),
     "pipecg_b200_solver_poll": ([_vp, ctypes.POINTER(PcgResult)], _int),
+    "pipecg_b200_tune_cache_clear": ([], None),
     "pipecg_b200_solver_x": ([_vp], _vp),
     "pipecg_b200_solver_state": ([_vp, ctypes.POINTER(_vp)], _int),
     "pipecg_b200_solver_comm_info": ([_vp, ctypes.POINTER(_vp), _p_i64, ctypes.POINTER(_vp)], _int),
@@ -121,7 +122,7 @@ EXPORTED = tuple(_SIGS)
 
 def build(verbose: bool = False) -> Path:
     """Compile the CUDA library in-tree (nvcc, sm_100a)."""
-    r = subprocess.run(["make", "-C", str(CSRC)], capture_output=not verbose, text=True)
+    r = subprocess.run(["make", "-j8", "-C", str(CSRC)], capture_output=not verbose, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"building {LIB_PATH} failed:\n{r.stdout}\n{r.stderr}")
     return LIB_PATH

@@ -84,6 +84,8 @@ struct Ctrl {
   int diag_where;                  // 1 = iteration wait, 2 = setup wait timed out
   unsigned long long diag_seen;    // counter value at the timeout
   unsigned long long diag_target;  // value waited for
+  int x_final;                     // deferred x: pending update applied after the stop
+  int pad_;
 };
 static_assert(sizeof(Ctrl) <= 256, "Ctrl must fit its 256-byte record slot");
 
@@ -1159,14 +1161,11 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
   if (!*decision) {
     if (tid == 0)
       for (long long j = 0; j < my_tiles && j < S; ++j) mbar_wait(&full[j], 0);
-    // the solve stops here: apply the pending update of iteration it-1
-    if (P.defer_x && it >= 1 && ((it - 1) & 1) == 0 && !producer) {
-      const double ap = sc[2];
-      for (long long j = 0; j < my_tiles; ++j) {
-        const long long i = (t_lo + j * t_step) * TR + (tid - 32);
-        if (i < P.n) P.vec[4][i] = add(P.vec[4][i], mul(ap, P.vec[3][i]));
-      }
-    }
+    // the solve stops here.  A pending deferred x update (it odd) is NOT
+    // applied by this kernel: block 0's prologue has already published the
+    // stop, so a CTA that starts after that reads it = -1 and could not tell
+    // it had rows to finish.  finalize_x_kernel, enqueued by the host after
+    // the run, applies it from the control block instead.
     return;
   }
   const double alpha = sc[0], beta = sc[1], alpha_prev = sc[2];
@@ -2108,6 +2107,26 @@ __global__ void __launch_bounds__(256) drift_finish_kernel(const Ctrl* C, int st
   }
 }
 
+// Deferred x (variants E/F, see pipecg_fused_kernel_s): when the solve
+// stopped at an odd iteration `it`, iteration it-1 skipped its x update, so
+// x_it = x_{it-1} + alpha_{it-1} p_{it-1} is still pending: p holds p_{it-1}
+// (the stopping kernel writes nothing) and slot[(it-1)&1] its alpha.  Runs
+// once per solve (x_final), after every iteration kernel of the run.
+__global__ void __launch_bounds__(256) finalize_x_kernel(Ctrl* C, long long n, double* x,
+                                                         const double* p) {
+  if (C->status != PCG_STOPPED || C->x_final) return;
+  const long long it = C->final_it;
+  if (it >= 1 && ((it - 1) & 1) == 0) {
+    const double a = C->slot[(it - 1) & 1].alpha;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+      x[i] = add(x[i], mul(a, p[i]));  // kernels.py:108 (x += alpha p)
+  }
+}
+__global__ void finalize_mark_kernel(Ctrl* C) {
+  if (threadIdx.x == 0 && C->status == PCG_STOPPED) C->x_final = 1;
+}
+
 __global__ void advance_kernel(Ctrl* C, int k) {
   if (threadIdx.x == 0) C->base_it += k;
 }
@@ -2133,6 +2152,7 @@ __global__ void init_ctrl_kernel(Ctrl* C, const double* dots, int nranks, double
     C->bd_val = 0.0;
     C->final_it = -1;
     C->final_norm = 0.0;
+    C->x_final = 0;
     C->slot[0] = Slot{0, 0, 0, 0};
     C->slot[1] = Slot{0, 0, 0, 0};
     if (!arrive) C->arrive_base = 0ull;  // distributed: snapshot taken at init start
@@ -2457,6 +2477,7 @@ struct pcg_solver {
   bool p_mg = true;                // variant P gathers the stored m (C) or dinv*w (A)
   int l2_prefetch = 0;             // E/F L2 prefetch distance in stages (experiment switch)
   bool no_defer_x = false;         // E/F: update x every iteration (experiment switch)
+  long long chunk_nnz = kChunkNnz; // engine 2: nonzeros per long-row chunk (test switch)
   unsigned long long* gbar = nullptr;  // variant P grid-barrier counter
   // engine-2 K2 in SELL-C-sigma layout (irregular matrices)
   bool sell = false;
@@ -3025,6 +3046,13 @@ ReduceIn reduce_in(pcg_solver* S) {
   return R;
 }
 
+// E/F deferred x update: not with drift samples (they read x every k
+// iterations) and not when switched off (experiment / A-B measurement)
+inline bool defer_x_active(const pcg_solver* S) {
+  return S->engine == 1 && (S->variant == 5 || S->variant == 6) && S->drift_k == 0 &&
+         !S->no_defer_x;
+}
+
 template <typename RP>
 FusedParams<RP> fused_params(pcg_solver* S) {
   FusedParams<RP> P;
@@ -3067,9 +3095,7 @@ FusedParams<RP> fused_params(pcg_solver* S) {
   P.pdinv = S->pdinv;
   P.tile_runs = S->n_runs > 0 ? tile_runs_for(S, S->tr) : nullptr;
   P.l2_prefetch = S->l2_prefetch;
-  // E/F deferred x update: not with drift samples (they read x every k
-  // iterations) and not when switched off (experiment / A-B measurement)
-  P.defer_x = S->drift_k == 0 && !S->no_defer_x ? 1 : 0;
+  P.defer_x = defer_x_active(S) ? 1 : 0;
   P.n_pat = S->pat.n_pat;
   P.n_pat_e = S->pat.n_entries;
   P.X = FusedXchg{};
@@ -3390,7 +3416,8 @@ void fill_result(pcg_solver* S, const Ctrl& c, pcg_result* res) {
   for (int k = 0; k < 8; ++k) res->tune_ms[k] = S->tune_ms[k];
   res->pattern_flags = S->pat.n_pat == 0 ? 0
                        : 1 | (S->n_runs > 0 ? 2 : 0) | (S->dinv_by_code ? 4 : 0) |
-                             (S->dinv_by_code && S->dinv_uniform ? 8 : 0);
+                             (S->dinv_by_code && S->dinv_uniform ? 8 : 0) |
+                             (defer_x_active(S) ? 16 : 0);
   res->graph_launches = S->graph_launches;
   res->norm0 = c.init.norm;
   res->breakdown_quantity = c.bd_code;
@@ -3464,6 +3491,7 @@ int preload_solver() {
   PCG_LOAD(gated_spmv_chunks); PCG_LOAD(seq_dots_kernel);
   PCG_LOAD(drift_partial_kernel<int>); PCG_LOAD(drift_partial_kernel<long long>);
   PCG_LOAD(drift_finish_kernel); PCG_LOAD(advance_kernel); PCG_LOAD(init_ctrl_kernel);
+  PCG_LOAD(finalize_x_kernel); PCG_LOAD(finalize_mark_kernel);
   PCG_LOAD(iter_exchange_kernel); PCG_LOAD(vec_exchange_kernel);
   PCG_LOAD(init_dots_exchange_kernel); PCG_LOAD(snapshot_arrive_kernel); PCG_LOAD(xwait_kernel);
   PCG_LOAD(tile_span_kernel<int>); PCG_LOAD(tile_span_kernel<long long>); PCG_LOAD(max_row_kernel);
@@ -3565,7 +3593,7 @@ int build_long_chunks(pcg_solver* S) {
   int slots = 0;
   for (long long k = 0; k < nl; ++k) {
     const long long len = hi[k] - lo[k];
-    const int n = (int)((len + kChunkNnz - 1) / kChunkNnz);
+    const int n = (int)((len + S->chunk_nnz - 1) / S->chunk_nnz);
     const int first = (int)ch.size();
     const int slot = n > 1 ? slots++ : -1;
     for (int j = 0; j < n; ++j)
@@ -3779,6 +3807,8 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   if (const char* e = getenv("PIPECG_B200_PA")) S->p_mg = atoi(e) == 0;  // experiment switch
   if (const char* e = getenv("PIPECG_B200_L2PF")) S->l2_prefetch = atoi(e);  // experiment switch
   if (getenv("PIPECG_B200_NO_DEFER_X")) S->no_defer_x = true;                 // experiment switch
+  if (const char* v = getenv("PIPECG_B200_CHUNK_NNZ"))  // test switch: many chunks on small rows
+    S->chunk_nnz = std::max(32LL, atoll(v));
   if (opts) S->opt = *opts;
   else {
     S->opt.dot_mode = PCG_DOT_TREE;
@@ -4228,10 +4258,19 @@ int pipecg_b200_solver_init(pcg_solver* S, const double* b, const double* x0, do
     double d0 = 0.0;
     int rc = check_dinv_by_code(S->pat, n, S->A.inv_diag, S->pdinv, &dbc, &uni, &d0, st);
     if (rc) return rc;
-    if (S->connected && S->engine == 1 && S->variant == 5 &&
-        (!dbc || !uni || std::memcmp(&d0, &S->dinv0, sizeof(double)) != 0))
-      return set_error(PCG_ESTATE, "solver_init: inv_diag changed after solver_connect "
-                                   "(variant E reads one dinv for every column)");
+    if (S->connected && S->engine == 1 && S->variant == 5) {
+      // E reads one dinv for every column, the halo columns included: the
+      // owned rows (check_dinv_by_code) and all n_cols entries must still
+      // hold the number solver_connect checked
+      int bad = 0;
+      if (dbc && uni && std::memcmp(&d0, &S->dinv0, sizeof(double)) == 0) {
+        rc = uniform_dinv(S, &bad);
+        if (rc) return rc;
+      }
+      if (!dbc || !uni || bad || std::memcmp(&d0, &S->dinv0, sizeof(double)) != 0)
+        return set_error(PCG_ESTATE, "solver_init: inv_diag changed after solver_connect "
+                                     "(variant E reads one dinv for every column)");
+    }
     if (dbc != S->dinv_by_code || uni != S->dinv_uniform ||
         std::memcmp(&d0, &S->dinv0, sizeof(double)) != 0) {
       S->dinv_by_code = dbc;
@@ -4362,6 +4401,12 @@ int pipecg_b200_solver_run(pcg_solver* S, pcg_result* res, double* history_host,
     if (c.status != PCG_RUNNING || !more) break;
     cur = nxt;
   }
+  if (defer_x_active(S)) {  // after every queued iteration kernel (stream order)
+    Ctrl* Cd = record_at(S->rec_dev).C;
+    finalize_x_kernel<<<elementwise_grid(S->A.n_rows), 256, 0, S->stream>>>(Cd, S->A.n_rows,
+                                                                            S->x, S->p);
+    finalize_mark_kernel<<<1, 32, 0, S->stream>>>(Cd);
+  }
   {
     cudaError_t e = cudaStreamSynchronize(S->stream);
     if (e != cudaSuccess) return cuda_status(e, "solve sync");
@@ -4416,6 +4461,11 @@ int pipecg_b200_solver_poll(pcg_solver* S, pcg_result* res) {
   memset(res, 0, sizeof(*res));
   fill_result(S, c, res);
   return comm_failed(c);
+}
+
+void pipecg_b200_tune_cache_clear(void) {
+  std::lock_guard<std::mutex> lock(tune_cache_mu());
+  tune_cache().clear();
 }
 
 int pipecg_b200_solver_state(pcg_solver* S, double** ptrs) {

@@ -607,8 +607,12 @@ def pipecg_solve_devices(A, b, x0, pc, cfg, devices, options=None):
     dh = d.detach().cpu().numpy() if is_device_tensor(d) else np.asarray(d, dtype=np.float64)
     opts = options or DeviceOptions()
     if len(set(devices)) < W:  # a GPU shared by several ranks: co-resident grids
+        from ._device import shared_max_sms
+
+        share = max(devices.count(dv) for dv in set(devices))
+        busiest = max(set(devices), key=devices.count)
         opts = DeviceOptions(dot_mode=opts.dot_mode, engine=opts.engine, chunk=opts.chunk,
-                             use_graphs=opts.use_graphs, max_sms=max(8, 148 // W - 10))
+                             use_graphs=opts.use_graphs, max_sms=shared_max_sms(share, busiest))
     for dv in set(devices):
         for q in set(devices):
             if q != dv:

@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import threading
 import time
 from dataclasses import dataclass, field
 from typing import Any
@@ -229,6 +230,7 @@ class PipecgSolver:
         _lib.call("pipecg_b200_solver_create", ctypes.byref(m), ctypes.byref(opts), ctypes.byref(h))
         self._h = h
         self.n = self.A.n_rows
+        self.lock = threading.Lock()  # held by the thread driving a solve
 
     def close(self):
         if getattr(self, "_h", None) and self._h.value:
@@ -326,18 +328,37 @@ def _cuda_memcpy_d2d(dst: int, src: int, nbytes: int) -> None:
     torch.cuda.current_stream().synchronize()
 
 
-def _solver_for(A, pc, options: DeviceOptions) -> PipecgSolver:
-    """Cached native solver for (matrix, preconditioner, options)."""
+_CACHE_LOCK = threading.Lock()
+
+
+def _solver_for(A, pc, options: DeviceOptions) -> tuple[PipecgSolver, bool]:
+    """A native solver for (matrix, preconditioner, options), LOCKED for the
+    caller: ``(solver, cached)``.
+
+    The matrix caches one solver (its state vectors and graphs stay resident
+    across solves).  A solver handle is single-threaded state, so the caller
+    holds ``solver.lock`` from init to the x download; a second thread
+    solving the same matrix concurrently gets a private solver instead of
+    sharing the busy one (the reference's solvers are re-entrant: numba
+    ``nogil`` kernels on caller-owned arrays).  ``cached`` False: the caller
+    closes the private solver when done."""
     dA = as_device_csr(A)
     d = device_inv_diag(pc)
-    cache = dA.__dict__.setdefault("_solvers", {})
     key = (options.key(), d.data_ptr())
-    s = cache.get(key)
-    if s is None:
-        s = PipecgSolver(dA, d, options)
-        cache.clear()  # one resident solver per matrix bounds HBM use
-        cache[key] = s
-    return s
+    with _CACHE_LOCK:
+        cache = dA.__dict__.setdefault("_solvers", {})
+        s = cache.get(key)
+        if s is not None and s.lock.acquire(blocking=False):
+            return s, True
+        if s is None and not any(v.lock.locked() for v in cache.values()):
+            s = PipecgSolver(dA, d, options)
+            cache.clear()  # one resident solver per matrix bounds HBM use
+            cache[key] = s
+            s.lock.acquire()
+            return s, True
+    s = PipecgSolver(dA, d, options)  # busy: a private solver for this call
+    s.lock.acquire()
+    return s, False
 
 
 def pipecg_scalars(gamma: float, gamma_prev: float, delta: float, alpha_prev: float,
@@ -418,27 +439,32 @@ def pipecg_solve(A, b, x0, pc, cfg: SolverConfig | None = None, *,
     require_cuda()
     nvtx = torch.cuda.nvtx  # ranges for nsys / Nsight timelines (no-ops otherwise)
     nvtx.range_push("pipecg.setup")
-    solver = _solver_for(A, pc, options)
-    bd, x0d = to_device_f64(b), to_device_f64(x0)
-    solver.init(bd, x0d, cfg.tolerance, cfg.max_iterations, cfg.drift_check_interval)
-    # the solver's stream only: a device-wide synchronize would break a CUDA
-    # graph capture of a solver driven from another thread on this GPU
-    torch.cuda.ExternalStream(solver.stream).synchronize()
-    nvtx.range_pop()
-    t_setup = time.perf_counter()
-    nvtx.range_push("pipecg.iterations")
-    res, hist, d_it, d_val = solver.run(cfg.record_history, cfg.max_iterations,
-                                        cfg.drift_check_interval)
-    nvtx.range_pop()
-    t_end = time.perf_counter()
-    if res.status == _lib.PCG_BREAKDOWN:
-        raise SolverBreakdown(_lib.BREAKDOWN_QUANTITY[res.breakdown_quantity],
-                              int(res.breakdown_iteration), float(res.breakdown_value))
-    history = hist[: res.n_history].tolist() if hist is not None else None
-    drift = None
-    if cfg.drift_check_interval > 0:
-        drift = [[int(d_it[k]), float(d_val[k])] for k in range(res.n_drift)]
-    x = solver.x_tensor() if on_dev else solver.x_host()
+    solver, cached = _solver_for(A, pc, options)
+    try:
+        bd, x0d = to_device_f64(b), to_device_f64(x0)
+        solver.init(bd, x0d, cfg.tolerance, cfg.max_iterations, cfg.drift_check_interval)
+        # the solver's stream only: a device-wide synchronize would break a CUDA
+        # graph capture of a solver driven from another thread on this GPU
+        torch.cuda.ExternalStream(solver.stream).synchronize()
+        nvtx.range_pop()
+        t_setup = time.perf_counter()
+        nvtx.range_push("pipecg.iterations")
+        res, hist, d_it, d_val = solver.run(cfg.record_history, cfg.max_iterations,
+                                            cfg.drift_check_interval)
+        nvtx.range_pop()
+        t_end = time.perf_counter()
+        if res.status == _lib.PCG_BREAKDOWN:
+            raise SolverBreakdown(_lib.BREAKDOWN_QUANTITY[res.breakdown_quantity],
+                                  int(res.breakdown_iteration), float(res.breakdown_value))
+        history = hist[: res.n_history].tolist() if hist is not None else None
+        drift = None
+        if cfg.drift_check_interval > 0:
+            drift = [[int(d_it[k]), float(d_val[k])] for k in range(res.n_drift)]
+        x = solver.x_tensor() if on_dev else solver.x_host()
+    finally:
+        solver.lock.release()
+        if not cached:
+            solver.close()
     report = SolveReport(
         converged=bool(res.converged),
         iterations=int(res.iterations),

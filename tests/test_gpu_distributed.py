@@ -23,13 +23,14 @@ pytestmark = pytest.mark.gpu
 pb = pytest.importorskip("paper_2105_06176_b200")
 torch = pytest.importorskip("torch")
 from paper_2105_06176_b200 import distributed as D  # noqa: E402
+from paper_2105_06176_b200._device import shared_max_sms  # noqa: E402
 
 
 def run_virtual(world, make_problem, cfg, chunk=0, engine="fused"):
     G = D.LocalGroup(world)
     out = [None] * world
     errs = []
-    opts = pb.DeviceOptions(max_sms=max(8, 148 // world - 10), chunk=chunk, engine=engine)
+    opts = pb.DeviceOptions(max_sms=shared_max_sms(world), chunk=chunk, engine=engine)
 
     def work(r):
         try:
@@ -188,7 +189,7 @@ def test_virtual_ranks_keep_row_pattern_variants(cuda, engine, code):
     space: E/F stay in use once connected (windows over the halo ranges)."""
     world, n = 2, 40
     G = D.LocalGroup(world)
-    opts = pb.DeviceOptions(max_sms=max(8, 148 // world - 10), engine=engine)
+    opts = pb.DeviceOptions(max_sms=shared_max_sms(world), engine=engine)
     got, errs = [None] * world, []
 
     def work(r):

@@ -139,3 +139,70 @@ def test_sell_layout_bitwise(cuda, monkeypatch, n):
                              options=pb.DeviceOptions(dot_mode="seq", engine="two"))
     assert rep.history == ref.history
     np.testing.assert_array_equal(x, ref.x)
+
+
+def _hub_spd(n, hub_rows, hub_len, seed):
+    """Symmetric, strictly diagonally dominant; `hub_rows` rows coupled to
+    `hub_len` random columns each (rows of > 2,048 nonzeros: several chunks
+    of the engine-2 long-row path, like the 49,349-nonzero rows of the
+    2^22 power-law config), plus a sparse random background."""
+    rng = np.random.default_rng(seed)
+    r = [np.repeat(np.arange(hub_rows), hub_len)]
+    c = [rng.integers(0, n, size=hub_rows * hub_len)]
+    bg = rng.integers(0, n, size=(2, 4 * n))
+    r.append(bg[0])
+    c.append(bg[1])
+    r, c = np.concatenate(r), np.concatenate(c)
+    keep = r != c
+    key = np.unique(np.minimum(r[keep], c[keep]) * n + np.maximum(r[keep], c[keep]))
+    a, b = key // n, key % n
+    v = -rng.uniform(0.1, 1.0, size=a.size)
+    rows = np.concatenate([a, b, np.arange(n)])
+    cols = np.concatenate([b, a, np.arange(n)])
+    vals = np.concatenate([v, v, np.zeros(n)])
+    order = np.lexsort((cols, rows))
+    rows, cols, vals = rows[order], cols[order], vals[order]
+    vals[rows == cols] = np.bincount(rows, weights=np.abs(vals), minlength=n) + 1.0
+    ro = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=ro[1:])
+    return pb.CsrMatrix(n, n, ro, cols, vals)
+
+
+@pytest.mark.parametrize("chunk_nnz", [None, 300, 64])
+def test_hub_rows_multi_chunk(cuda, monkeypatch, chunk_nnz):
+    """Engine 2's long-row path with several chunks per row (kChunkNnz =
+    2,048 by default; PIPECG_B200_CHUNK_NNZ shrinks it so every row > 256
+    nonzeros splits into many chunks): the last chunk to finish (atomic
+    ticket) sums the chunk partials in chunk order.  Within the oracle's
+    reorder envelope in both dot modes, and bitwise repeatable."""
+    if chunk_nnz:
+        monkeypatch.setenv("PIPECG_B200_CHUNK_NNZ", str(chunk_nnz))
+    A = _hub_spd(60000, 6, 9000, seed=11)
+    lens = A.row_nnz()
+    assert lens.max() > 4 * 2048  # >= 5 chunks per hub row at the default size
+    b, x0, d, tol = _problem(A)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=3000)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=3000, record_history=True)
+    env = envelope(A, b, x0, d, tol, 3000)
+    for mode in ("tree", "seq"):
+        opts = pb.DeviceOptions(engine="two", dot_mode=mode)
+        x, rep = pb.pipecg_solve(A, b, x0, pb.jacobi_setup(A), cfg, options=opts)
+        assert_within_envelope(x, rep, ref.iterations, ref.history, ref.x, env)
+        x2, rep2 = pb.pipecg_solve(A, b, x0, pb.jacobi_setup(A), cfg, options=opts)
+        assert rep2.history == rep.history
+        np.testing.assert_array_equal(x2, x)
+
+
+def test_powerlaw_multi_chunk_small_chunks(cuda, monkeypatch):
+    """Power-law 2^16 (rows up to ~1,800 nonzeros) with 64-nonzero chunks:
+    every row above 256 nonzeros becomes 5..29 chunks."""
+    monkeypatch.setenv("PIPECG_B200_CHUNK_NNZ", "64")
+    A = pb.generate_powerlaw(2**16)
+    assert A.row_nnz().max() > 20 * 64
+    b, x0, d, tol = _problem(A)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=2000)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=2000, record_history=True)
+    x, rep = pb.pipecg_solve(A, b, x0, pb.jacobi_setup(A), cfg,
+                             options=pb.DeviceOptions(engine="two"))
+    assert_within_envelope(x, rep, ref.iterations, ref.history, ref.x,
+                           envelope(A, b, x0, d, tol, 2000))

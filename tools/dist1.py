@@ -12,6 +12,7 @@ import sys, threading
 sys.path.insert(0, ".")
 import torch
 import paper_2105_06176_b200 as pb
+from paper_2105_06176_b200._device import shared_max_sms
 from paper_2105_06176_b200 import distributed as D
 
 kind, n = sys.argv[1], int(sys.argv[2])
@@ -19,7 +20,7 @@ engines = sys.argv[3].split(",") if len(sys.argv) > 3 else ["fused-a", "fused-c"
 world = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 for eng in engines:
     G = D.LocalGroup(world)
-    opts = pb.DeviceOptions(engine=eng, max_sms=0 if world == 1 else max(8, 148 // world - 10))
+    opts = pb.DeviceOptions(engine=eng, max_sms=0 if world == 1 else shared_max_sms(world))
     ms, info, errs = [0.0] * world, [None] * world, []
 
     def work(r):

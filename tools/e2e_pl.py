@@ -21,7 +21,7 @@ for rep in range(3):
     torch.cuda.synchronize(); t = [time.perf_counter()]
     SP.as_device_csr(A); torch.cuda.synchronize(); t.append(time.perf_counter())
     K.device_inv_diag(pc); torch.cuda.synchronize(); t.append(time.perf_counter())
-    s = S._solver_for(A, pc, pb.DeviceOptions()); torch.cuda.synchronize(); t.append(time.perf_counter())
+    s, _ = S._solver_for(A, pc, pb.DeviceOptions()); s.lock.release(); torch.cuda.synchronize(); t.append(time.perf_counter())
     bd, x0d = S.to_device_f64(b), S.to_device_f64(np.zeros(N)); torch.cuda.synchronize(); t.append(time.perf_counter())
     s.init(bd, x0d, tol, 20000, 0); torch.cuda.synchronize(); t.append(time.perf_counter())
     res = s.run(False, 20000, 0)[0]; t.append(time.perf_counter())
