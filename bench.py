@@ -268,11 +268,13 @@ ENGINES = {2: "two-kernel", 3: "fused-A (consumer gathers dinv*w)",
            6: "fused-D (nnz-balanced tiles, cooperative gathers of the stored m)",
            7: "fused-P (C with a chunk of iterations per persistent launch, grid barrier)",
            8: "fused-E (A reading the row-pattern dictionary instead of the CSR)",
-           9: "fused-F (C reading the row-pattern dictionary instead of the CSR)"}
+           9: "fused-F (C reading the row-pattern dictionary instead of the CSR)",
+           10: "fused-G (one SELL-C-sigma kernel per iteration, hub rows as chunks inside it)"}
 KERNELS = {2: "gated_spmv_rows + pipecg_k1_kernel", 3: "pipecg_fused_kernel_a<int,TR,0>",
            4: "pipecg_fused_kernel<int,TR>", 5: "pipecg_fused_kernel_a<int,TR,1>",
            6: "pipecg_fused_kernel_d<int,TR>", 7: "pipecg_fused_kernel_p<int,TR,1>",
-           8: "pipecg_fused_kernel_s<TR,0>", 9: "pipecg_fused_kernel_s<TR,1>"}
+           8: "pipecg_fused_kernel_s<TR,0>", 9: "pipecg_fused_kernel_s<TR,1>",
+           10: "pipecg_fused_kernel_g<2>"}
 CONFIG_NAMES = {"3d7-256": "BASELINE.json configs[1]", "2d5-512": "BASELINE.json configs[0]",
                 "3d27-400": "BASELINE.json configs[2], single-GPU leg",
                 "3d7-400": "north_star headline (>= 64M rows)",
@@ -302,6 +304,12 @@ def engine_bytes(engine: int, flags: int, N: int, nnz: int):
         return (int(streams * 8 * N + N),
                 f"{sname}: {streams} vector streams x 8N (averaged over the deferred-x pair) "
                 "+ 1 B/row code" if defer else f"{sname}: {streams} vector streams x 8N + 1 B/row code")
+    if engine == 10:
+        # G: z q s p x r u w read + written, dinv read, m_new written (18
+        # streams), the SELL copy's column + value per nonzero, its row
+        # permutation + length per row (the gathers of m are L2 traffic)
+        return (18 * 8 * N + 12 * nnz + 8 * N,
+                "G: 18 vector streams x 8N + SELL 12 B/nnz + 8 B/row (permutation, length)")
     # engine 2: K1 (10 vectors read + 9 written + ... = 20 streams) + SpMV
     # (m gathered once, n written, CSR) = the canonical 22 streams + CSR
     return canonical_bytes(N, nnz), "two kernels: 22 vector streams x 8N + CSR (canonical)"
@@ -661,7 +669,8 @@ def run_b200(args):
                                             "fused_P": info["tune_ms"][4],
                                             "fused_E": info["tune_ms"][5],
                                             "fused_F": info["tune_ms"][6],
-                                            "two_kernel": info["tune_ms"][7]}},
+                                            "two_kernel": info["tune_ms"][7],
+                                            "fused_G": info["tune_ms"][8]}},
         # achieved = the engine's ALGORITHMIC bytes per iteration (its own
         # layout: what one iteration must move at minimum) / the measured
         # iteration time; `canonical_equivalent` re-states the same time in

@@ -192,7 +192,9 @@ typedef struct {
   int engine;          /* 0 auto (autotuned for >= 64K rows), 1 fused (variant autotuned),
                           2 two-kernel, 3..9 fused variant A/B/C/D/P/E/F
                           (E/F: A/C reading the matrix's row-pattern dictionary;
-                          only for matrices that have one) */
+                          only for matrices that have one), 10 fused-g (one
+                          SELL-C-sigma kernel per iteration for irregular rows,
+                          hub rows as chunks inside it) */
   int chunk;           /* iterations per CUDA-graph chunk (0 = auto) */
   int use_graphs;      /* 1 (default) or 0 (plain launches, debugging) */
   int max_sms;         /* size persistent grids for at most this many SMs (0 = all) */
@@ -209,9 +211,11 @@ typedef struct {
   double breakdown_value;
   int64_t n_history;   /* entries written to history_host */
   int64_t n_drift;     /* samples written to drift_*_host */
-  int engine;          /* engine used: 2 two-kernel, 3..9 fused variant A/B/C/D/P/E/F */
+  int engine;          /* engine used: 2 two-kernel, 3..9 fused variant A/B/C/D/P/E/F,
+                          10 fused-g */
   int64_t graph_launches;  /* iteration chunks launched (CUDA graphs, or directly) */
-  double tune_ms[8];   /* autotune ms/iteration: fused A, B, C, D, P, E, F, two-kernel
+  double tune_ms[9];   /* autotune ms/iteration: fused A, B, C, D, P, E, F, two-kernel,
+                          fused-g
                           (0 = not run) */
   int pattern_flags;   /* row-pattern dictionary in use by E/F: 1 dictionary, 2 windows,
                           4 dinv a function of the row's code, 8 ... one dinv for all rows,

@@ -50,7 +50,7 @@ class PcgResult(ctypes.Structure):
         ("status", _int), ("converged", _int), ("iterations", _i64), ("final_norm", _dbl),
         ("norm0", _dbl), ("breakdown_quantity", _int), ("breakdown_iteration", _i64),
         ("breakdown_value", _dbl), ("n_history", _i64), ("n_drift", _i64), ("engine", _int),
-        ("graph_launches", _i64), ("tune_ms", _dbl * 8), ("pattern_flags", _int),
+        ("graph_launches", _i64), ("tune_ms", _dbl * 9), ("pattern_flags", _int),
     ]
 
 

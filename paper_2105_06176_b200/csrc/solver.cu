@@ -1785,6 +1785,9 @@ struct TwoParams {
   unsigned* counter;
 };
 
+// POL: L2 hints -- the streams evict-first, m (gathered by the SpMV next)
+// stored evict-last
+template <bool POL>
 __global__ void __launch_bounds__(256) pipecg_k1_kernel(TwoParams P, int step) {
   __shared__ double red[3 * 8 + 1];
   Ctrl* C = P.C;
@@ -1797,14 +1800,16 @@ __global__ void __launch_bounds__(256) pipecg_k1_kernel(TwoParams P, int step) {
   if (!stp.go) return;
   const double alpha = stp.alpha, beta = stp.beta;
   double acc[3] = {0.0, 0.0, 0.0};
+  const uint64_t pf = POL ? policy_l2(1) : 0, pl = POL ? policy_l2(2) : 0;
+  auto ld = [&](const double* a) { return POL ? ld_hint(a, pf) : *a; };
   for (long long i = blockIdx.x * 256LL + threadIdx.x; i < P.n; i += (long long)gridDim.x * 256) {
-    const double zi = add(P.nv[i], mul(beta, P.z[i]));
-    const double qi = add(P.m[i], mul(beta, P.q[i]));
-    const double wi = P.w[i], ui = P.u[i];
-    const double si = add(wi, mul(beta, P.s[i]));
-    const double pi = add(ui, mul(beta, P.p[i]));
-    const double xi = add(P.x[i], mul(alpha, pi));
-    const double ri = sub(P.r[i], mul(alpha, si));
+    const double zi = add(ld(P.nv + i), mul(beta, ld(P.z + i)));
+    const double qi = add(ld(P.m + i), mul(beta, ld(P.q + i)));
+    const double wi = ld(P.w + i), ui = ld(P.u + i);
+    const double si = add(wi, mul(beta, ld(P.s + i)));
+    const double pi = add(ui, mul(beta, ld(P.p + i)));
+    const double xi = add(ld(P.x + i), mul(alpha, pi));
+    const double ri = sub(ld(P.r + i), mul(alpha, si));
     const double un = sub(ui, mul(alpha, qi));
     const double wn = sub(wi, mul(alpha, zi));
     P.z[i] = zi;
@@ -1815,7 +1820,8 @@ __global__ void __launch_bounds__(256) pipecg_k1_kernel(TwoParams P, int step) {
     P.r[i] = ri;
     P.u[i] = un;
     P.w[i] = wn;
-    P.m[i] = mul(P.dinv[i], wn);  // solvers.py:358
+    if (POL) st_hint(P.m + i, mul(ld(P.dinv + i), wn), pl);  // solvers.py:358
+    else P.m[i] = mul(P.dinv[i], wn);
     acc[0] = add(acc[0], mul(ri, un));
     acc[1] = add(acc[1], mul(wn, un));
     acc[2] = add(acc[2], mul(un, un));
@@ -1848,9 +1854,11 @@ __global__ void __launch_bounds__(256) gated_spmv_rows(const Ctrl* C, long long 
 // warp have similar lengths (little divergence), and every lane still sums
 // its own row strictly in CSR order -- bitwise the reference's _spmv.
 // Rows longer than kLongRow keep the block-per-row kernel (slen = -1 here).
+// 256 = engine 3's window (one CTA); engine 2 reads the same copy (1024
+// measured within noise for engine 2's SELL kernel alone)
 constexpr int kSellSigma = 1024;
 
-template <int SB>
+template <int SB, bool POL>
 __global__ void __launch_bounds__(256) sell_spmv_kernel(const Ctrl* C, long long n, long long n_slices,
                                                          const long long* __restrict__ sptr,
                                                          const int* __restrict__ perm,
@@ -1864,6 +1872,7 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(const Ctrl* C, long long
   if (C && read_status(C) != PCG_RUNNING) return;
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const uint64_t pf = POL ? policy_l2(1) : 0, pl = POL ? policy_l2(2) : 0;
   for (long long sl = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); sl < n_slices;
        sl += warps) {
     const long long p = sl * 32 + lane;
@@ -1881,11 +1890,12 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(const Ctrl* C, long long
 #pragma unroll
       for (int u = 0; u < SB; ++u) {
         const bool on = k0 + u < len;
-        c[u] = on ? ldg_nc(col + base + 32LL * (k0 + u)) : 0;
-        a[u] = on ? ldg_nc(val + base + 32LL * (k0 + u)) : 0.0;
+        c[u] = on ? (POL ? ld_hint(col + base + 32LL * (k0 + u), pf) : ldg_nc(col + base + 32LL * (k0 + u))) : 0;
+        a[u] = on ? (POL ? ld_hint(val + base + 32LL * (k0 + u), pf) : ldg_nc(val + base + 32LL * (k0 + u))) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < SB; ++u) xv[u] = k0 + u < len ? ldg_nc(x + c[u]) : 0.0;
+      for (int u = 0; u < SB; ++u)
+        xv[u] = k0 + u < len ? (POL ? ld_gather(x + c[u], pl) : ldg_nc(x + c[u])) : 0.0;
 #pragma unroll
       for (int u = 0; u < SB; ++u)
         if (k0 + u < len) acc = add(acc, mul(a[u], xv[u]));
@@ -1945,6 +1955,8 @@ struct LongChunk {
   int first;         // index of the row's first chunk
   int n;             // chunks of this row
   int slot;          // ticket counter of the row (multi-chunk rows)
+  int hub;           // index of the row in the long-row list (engine 3: its dot slot)
+  int pad_;
 };
 
 __global__ void __launch_bounds__(256) gated_spmv_chunks(const Ctrl* C, const LongChunk* __restrict__ ch,
@@ -2021,14 +2033,334 @@ __global__ void __launch_bounds__(256) gated_spmv_long(const Ctrl* C, const int*
 }
 
 // ===========================================================================
+// Engine 3 ("fused-g"): irregular matrices, ONE kernel per iteration
+// ===========================================================================
+// Engine 2 runs an irregular matrix as K1 (20 vector streams) + a SELL SpMV
+// (n written, then re-read by the next K1) + hub-row chunks.  Engine 3 makes
+// the SpMV of iteration it+1 and the update of iteration it one pass, as the
+// fused engine does, keeping engine 2's irregular-row machinery:
+//
+//   * the solver state lives in SELL order: position p holds row perm[p]
+//     (rows sorted by length inside 256-row windows), so the lane that sums
+//     row perm[p] -- one lane per row, 32-row slices whose k-th nonzeros
+//     are contiguous (coalesced column / value loads) -- also updates
+//     position p of every vector with coalesced loads and stores.  Warps
+//     are independent: no shared memory, no CTA barrier per slice.  The
+//     SELL copy's columns are renumbered into positions (iperm[col]); the
+//     permutation stays inside each window, so the gathers keep the matrix's
+//     locality.  b and the caller-facing x are natural order (init permutes
+//     the state in, solver_x / solver_state permute out).
+//   * the eight recurrences (kernels.py:100-111), with m_p = dinv_p * w_p
+//     formed from the w the lane reads anyway (bit for bit the stored m),
+//     m_new = dinv * w_new stored for the next iteration's gathers
+//     (ping-pong m), dot partials;
+//   * rows longer than kLongRow ("hubs", SELL length -1) are packed
+//     (positions, values) at setup and cut into chunks of <= kGChunkNnz
+//     nonzeros, one WARP each; the row's last chunk to finish (atomic
+//     ticket) sums the chunk partials in chunk order and applies the row's
+//     update, its three dot terms going into the row's slot; the grid's
+//     last CTA sums the block partials and then the hub slots in a fixed
+//     order (deterministic).
+//
+// Bytes per iteration: z q s p x r u w read + written, dinv read, m_new
+// written (18 streams) + the SELL copy (12 B per nonzero) + the m gathers,
+// which L2 serves when the streams are marked evict-first.
+// Every row sums its nonzeros in CSR order (bitwise the reference's _spmv,
+// kernels.py:64-70); only the order of the dot partials is a tree.
+constexpr int kGRows = 256;              // SELL sigma (window) and CTA size
+constexpr long long kGChunkNnz = 512;    // hub chunk = one warp
+// rows longer than this leave the lane-per-row SELL path for warp chunks: a
+// lane's row is a chain of dependent (index -> gather) loads, and a slice
+// of 256-nonzero rows would be the kernel's critical path
+constexpr long long kGLaneRow = 64;
+
+struct GParams {
+  long long n;
+  long long n_slices;       // ceil(n / 32)
+  long long n_chunks;       // hub-row chunks (0: no hub rows)
+  const long long* sptr;    // SELL slice starts (elements)
+  const int* slen;          // SELL position -> row length (-1: hub row)
+  const int* scol;          // SELL columns as positions
+  const double* sval;
+  const LongChunk* chunks;  // hub chunks: ranges of hcol / hval, row = position
+  const int* hcol;          // hub rows packed: columns as positions
+  const double* hval;
+  double* chunk_part;
+  unsigned* chunk_ticket;
+  double* hubdot;           // [n_hub][4]: dot terms of each multi-chunk row
+  int n_hub;
+  const double* dinv;       // inv_diag in SELL order
+  double *z, *q, *s, *p, *x, *r, *u, *w;
+  double* m[2];             // ping-pong: gather m[it&1], write m[(it+1)&1]
+  Ctrl* C;
+  double* hist;
+  ReduceIn rin;
+  double* pout;             // block partials [2][grid][4]
+  double* fin;              // [2][4]
+  unsigned* counter;        // [2]
+};
+
+struct GRow {
+  double z, q, s, p, x, r, u, w, d;
+};
+
+__device__ __forceinline__ GRow g_load(const GParams& P, long long i, uint64_t pol) {
+  GRow v;
+  v.z = ld_hint(P.z + i, pol);
+  v.q = ld_hint(P.q + i, pol);
+  v.s = ld_hint(P.s + i, pol);
+  v.p = ld_hint(P.p + i, pol);
+  v.x = ld_hint(P.x + i, pol);
+  v.r = ld_hint(P.r + i, pol);
+  v.u = ld_hint(P.u + i, pol);
+  v.w = ld_hint(P.w + i, pol);
+  v.d = ld_hint(P.dinv + i, pol);
+  return v;
+}
+
+// kernels.py:100-111 (order and roundings of _fused_update), m = M^-1 w
+// (solvers.py:358) and the three dot terms of position i
+__device__ __forceinline__ void g_update(const GParams& P, long long i, const GRow& v, double nval,
+                                         double alpha, double beta, double* m_new, uint64_t pst,
+                                         uint64_t pm, double (&acc)[3]) {
+  const double mi = mul(v.d, v.w);  // = the stored m_old bit for bit
+  const double zi = add(nval, mul(beta, v.z));
+  const double qi = add(mi, mul(beta, v.q));
+  const double si = add(v.w, mul(beta, v.s));
+  const double pi = add(v.u, mul(beta, v.p));
+  const double xi = add(v.x, mul(alpha, pi));
+  const double ri = sub(v.r, mul(alpha, si));
+  const double un = sub(v.u, mul(alpha, qi));
+  const double wn = sub(v.w, mul(alpha, zi));
+  st_hint(P.z + i, zi, pst);
+  st_hint(P.q + i, qi, pst);
+  st_hint(P.s + i, si, pst);
+  st_hint(P.p + i, pi, pst);
+  st_hint(P.x + i, xi, pst);
+  st_hint(P.r + i, ri, pst);
+  st_hint(P.u + i, un, pst);
+  st_hint(P.w + i, wn, pst);
+  st_hint(m_new + i, mul(v.d, wn), pm);
+  acc[0] = add(acc[0], mul(ri, un));
+  acc[1] = add(acc[1], mul(wn, un));
+  acc[2] = add(acc[2], mul(un, un));
+}
+
+// SB: SELL nonzeros per lane per load batch; MB: CTAs per SM compiled for;
+// PF: the lane's update operands are loaded before its SpMV (in flight during
+// the gathers, 18 more live registers) or after it
+template <int SB, int MB, bool PF>
+__global__ void __launch_bounds__(kGRows, MB) pipecg_fused_kernel_g(GParams P, int step) {
+  __shared__ double red[3 * (kGRows / 32) + 1];
+  __shared__ int s_last;
+  __shared__ long long s_it;
+  Ctrl* C = P.C;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  pdl_trigger();
+  pdl_wait();  // m_old, the vectors and the partials of the previous iteration
+  const long long it = cta_iteration(C, step, &s_it);
+  if (it < 0) return;
+  const Step stp = prologue<kGRows>(C, P.hist, P.rin, it, tid, red, 1, blockIdx.x == 0 && tid == 0);
+  if (!stp.go) return;
+  const double alpha = stp.alpha, beta = stp.beta;
+  const double* m_old = P.m[it & 1];
+  double* m_new = P.m[(it + 1) & 1];
+  // L2: everything streamed once per iteration (SELL copy, the state
+  // vectors) evict-first; m (stored now, gathered next iteration) and its
+  // gathers evict-last, so the randomly gathered vector stays L2-resident
+  const uint64_t p_sell = policy_l2(1), p_str = p_sell;
+  const uint64_t p_m = policy_l2(2), p_g = p_m;
+  const long long gwarp = (long long)blockIdx.x * (kGRows / 32) + warp;
+  const long long n_warps = (long long)gridDim.x * (kGRows / 32);
+  double acc[3] = {0.0, 0.0, 0.0};
+
+  // ---- hub rows: chunks of <= kGChunkNnz nonzeros, one warp each -------
+  for (long long c = gwarp; c < P.n_chunks; c += n_warps) {
+    const LongChunk ch = P.chunks[c];
+    // products 32 at a time (lane l: entry 32 r + l), summed IN ORDER by
+    // every lane through shuffles: the chunk's sum is a left-to-right sum
+    // of its entries, so a one-chunk row is the reference's _spmv row
+    double v = 0.0;
+    for (long long k0 = ch.lo + lane; k0 < ch.hi + lane; k0 += 32LL * 4) {
+      double pr[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const long long k = k0 + 32LL * t;
+        pr[t] = 0.0;
+        if (k < ch.hi) pr[t] = mul(ld_hint(P.hval + k, p_sell), ld_gather(m_old + ld_hint(P.hcol + k, p_sell), p_g));
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const long long r0 = k0 - lane + 32LL * t;  // entry of lane 0 in this round
+        const int cnt = (int)max(0LL, min(32LL, ch.hi - r0));
+        for (int l = 0; l < cnt; ++l) v = add(v, __shfl_sync(0xffffffffu, pr[t], l));
+      }
+    }
+    if (lane == 0) {
+      double nrow = v;
+      bool mine = true;
+      if (ch.n > 1) {  // the row's last chunk to finish sums the chunk partials in order
+        P.chunk_part[c] = v;
+        __threadfence();
+        mine = atomicAdd(P.chunk_ticket + ch.slot, 1u) == (unsigned)(ch.n - 1);
+        if (mine) {
+          __threadfence();
+          nrow = 0.0;
+          for (int j = 0; j < ch.n; ++j) nrow = add(nrow, __ldcg(P.chunk_part + ch.first + j));
+          P.chunk_ticket[ch.slot] = 0u;  // next iteration (stream-ordered)
+        }
+      }
+      if (ch.n == 1) {
+        // a one-chunk row is always this warp's (static chunk -> warp map):
+        // its dot terms join this lane's partial, deterministically
+        const GRow rv = g_load(P, ch.row, p_str);
+        g_update(P, ch.row, rv, nrow, alpha, beta, m_new, p_str, p_m, acc);
+      } else if (mine) {  // whichever warp finished the row: the row's own slot
+        const GRow rv = g_load(P, ch.row, p_str);
+        double hd[3] = {0.0, 0.0, 0.0};
+        g_update(P, ch.row, rv, nrow, alpha, beta, m_new, p_str, p_m, hd);
+        double* slot = P.hubdot + (size_t)ch.slot * 4;
+        slot[0] = hd[0];
+        slot[1] = hd[1];
+        slot[2] = hd[2];
+      }
+    }
+  }
+
+  // ---- 32-row slices: one warp each, one lane per position ---------------
+  for (long long sl = gwarp; sl < P.n_slices; sl += n_warps) {
+    const long long i = sl * 32 + lane;
+    const int len = i < P.n ? ldg_nc(P.slen + i) : -1;
+    GRow rv{};
+    if (PF && len >= 0) rv = g_load(P, i, p_str);
+    int L = max(len, 0);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) L = max(L, __shfl_xor_sync(0xffffffffu, L, o));
+    const long long eb = (L > 0 ? P.sptr[sl] : 0) + lane;
+    double nacc = 0.0;
+    // software pipeline: the next batch's indices and values are in flight
+    // while this batch's gathers run (one dependent latency per batch)
+    int cc[SB];
+    double a[SB];
+#pragma unroll
+    for (int t = 0; t < SB; ++t) {
+      const bool on = t < len;
+      cc[t] = on ? ld_hint(P.scol + eb + 32LL * t, p_sell) : 0;
+      a[t] = on ? ld_hint(P.sval + eb + 32LL * t, p_sell) : 0.0;
+    }
+    for (int k0 = 0; k0 < L; k0 += SB) {
+      double mv[SB];
+#pragma unroll
+      for (int t = 0; t < SB; ++t) mv[t] = k0 + t < len ? ld_gather(m_old + cc[t], p_g) : 0.0;
+      int cn[SB];
+      double an[SB];
+#pragma unroll
+      for (int t = 0; t < SB; ++t) {
+        const bool on = k0 + SB + t < len;
+        cn[t] = on ? ld_hint(P.scol + eb + 32LL * (k0 + SB + t), p_sell) : 0;
+        an[t] = on ? ld_hint(P.sval + eb + 32LL * (k0 + SB + t), p_sell) : 0.0;
+      }
+#pragma unroll
+      for (int t = 0; t < SB; ++t)
+        if (k0 + t < len) nacc = add(nacc, mul(a[t], mv[t]));
+#pragma unroll
+      for (int t = 0; t < SB; ++t) {
+        cc[t] = cn[t];
+        a[t] = an[t];
+      }
+    }
+    if (len >= 0) {
+      if (!PF) rv = g_load(P, i, p_str);
+      g_update(P, i, rv, nacc, alpha, beta, m_new, p_str, p_m, acc);
+    }
+  }
+
+  // ---- dot partials: block partials, then the hub slots (fixed order) ----
+  group_sum<3, kGRows>(acc, tid, red, 1);
+  double* part = P.pout + (size_t)(it & 1) * (size_t)gridDim.x * 4;
+  if (tid == 0) {
+    double* out = part + (size_t)blockIdx.x * 4;
+    out[0] = acc[0];
+    out[1] = acc[1];
+    out[2] = acc[2];
+    out[3] = 0.0;
+    __threadfence();  // this CTA's hub slots and partial before its ticket
+    s_last = atomicAdd(P.counter + (it & 1), 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double v[3] = {0.0, 0.0, 0.0};
+  for (int j = tid; j < (int)gridDim.x; j += kGRows) {
+    v[0] = add(v[0], __ldcg(part + j * 4 + 0));
+    v[1] = add(v[1], __ldcg(part + j * 4 + 1));
+    v[2] = add(v[2], __ldcg(part + j * 4 + 2));
+  }
+  for (int h = tid; h < P.n_hub; h += kGRows) {
+    v[0] = add(v[0], __ldcg(P.hubdot + h * 4 + 0));
+    v[1] = add(v[1], __ldcg(P.hubdot + h * 4 + 1));
+    v[2] = add(v[2], __ldcg(P.hubdot + h * 4 + 2));
+  }
+  group_sum<3, kGRows>(v, tid, red, 1);
+  if (tid == 0) {
+    double* f = P.fin + (size_t)(it & 1) * 4;
+    f[0] = v[0];
+    f[1] = v[1];
+    f[2] = v[2];
+    f[3] = 0.0;
+    P.counter[it & 1] = 0u;  // reused by iteration it + 2 (stream-ordered)
+  }
+}
+
+// SELL-order (position) <-> natural-order (row) copies of a vector
+__global__ void __launch_bounds__(256) gather_perm_kernel(long long n, const int* __restrict__ perm,
+                                                          const double* __restrict__ src,
+                                                          double* __restrict__ dst) {
+  for (long long p = blockIdx.x * 256LL + threadIdx.x; p < n; p += (long long)gridDim.x * 256)
+    dst[p] = src[perm[p]];
+}
+__global__ void __launch_bounds__(256) scatter_perm_kernel(long long n, const int* __restrict__ perm,
+                                                           const double* __restrict__ src,
+                                                           double* __restrict__ dst) {
+  for (long long p = blockIdx.x * 256LL + threadIdx.x; p < n; p += (long long)gridDim.x * 256)
+    dst[perm[p]] = src[p];
+}
+__global__ void __launch_bounds__(256) iperm_kernel(long long n, const int* __restrict__ perm,
+                                                    int* __restrict__ iperm) {
+  for (long long p = blockIdx.x * 256LL + threadIdx.x; p < n; p += (long long)gridDim.x * 256)
+    iperm[perm[p]] = (int)p;
+}
+__global__ void __launch_bounds__(256) renumber_kernel(long long m, const int* __restrict__ iperm,
+                                                       const int* __restrict__ col, int* __restrict__ out) {
+  for (long long e = blockIdx.x * 256LL + threadIdx.x; e < m; e += (long long)gridDim.x * 256)
+    out[e] = iperm[col[e]];
+}
+// hub row k's CSR entries -> packed [hoff[k], hoff[k+1]) with positions
+__global__ void __launch_bounds__(256) hub_pack_kernel(const long long* __restrict__ lo,
+                                                       const long long* __restrict__ hoff,
+                                                       const int* __restrict__ iperm,
+                                                       const int* __restrict__ col,
+                                                       const double* __restrict__ val,
+                                                       int* __restrict__ hcol, double* __restrict__ hval) {
+  const long long k = blockIdx.x;
+  const long long n = hoff[k + 1] - hoff[k];
+  for (long long j = threadIdx.x; j < n; j += 256) {
+    hcol[hoff[k] + j] = iperm[col[lo[k] + j]];
+    hval[hoff[k] + j] = val[lo[k] + j];
+  }
+}
+
+// ===========================================================================
 // sequential-dot mode (bitwise reference order) and drift samples
 // ===========================================================================
 // After F(it)/K1(it): overwrite partial 0 with the three strictly sequential
 // dots; the next prologue then reduces exactly one partial.
+// ip (engine 3): the state is in SELL order, row i lives at position ip[i]
 __global__ void __launch_bounds__(32) seq_dots_kernel(const Ctrl* C, long long n, const double* r,
                                                        const double* u, const double* w0,
                                                        const double* w1, int pingpong,
-                                                       double* seqbuf, int step) {
+                                                       double* seqbuf, int step, const int* ip) {
   constexpr int CH = 256;
   __shared__ double prod[3][CH];
   const long long it = cta_iteration(C, step);
@@ -2039,11 +2371,12 @@ __global__ void __launch_bounds__(32) seq_dots_kernel(const Ctrl* C, long long n
   for (long long base = 0; base < n; base += CH) {
 #pragma unroll
     for (int j = 0; j < CH / 32; ++j) {
-      const long long i = base + j * 32 + lane;
-      const double ui = i < n ? u[i] : 0.0;
-      prod[0][j * 32 + lane] = i < n ? mul(r[i], ui) : 0.0;
-      prod[1][j * 32 + lane] = i < n ? mul(w[i], ui) : 0.0;
-      prod[2][j * 32 + lane] = i < n ? mul(ui, ui) : 0.0;
+      const long long i0 = base + j * 32 + lane;
+      const long long i = ip && i0 < n ? ip[i0] : i0;
+      const double ui = i0 < n ? u[i] : 0.0;
+      prod[0][j * 32 + lane] = i0 < n ? mul(r[i], ui) : 0.0;
+      prod[1][j * 32 + lane] = i0 < n ? mul(w[i], ui) : 0.0;
+      prod[2][j * 32 + lane] = i0 < n ? mul(ui, ui) : 0.0;
     }
     __syncwarp();
     if (lane == 0) {
@@ -2074,7 +2407,8 @@ __global__ void __launch_bounds__(256) drift_partial_kernel(const Ctrl* C, int s
                                                              const double* __restrict__ x,
                                                              const double* __restrict__ b,
                                                              const double* __restrict__ r,
-                                                             double* __restrict__ dpart) {
+                                                             double* __restrict__ dpart,
+                                                             const int* __restrict__ ip) {
   __shared__ double red[8];
   const long long it = cta_iteration(C, step);
   if (it < 0) return;
@@ -2082,8 +2416,9 @@ __global__ void __launch_bounds__(256) drift_partial_kernel(const Ctrl* C, int s
   double v[1] = {0.0};
   for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
     double acc = 0.0;
-    for (long long k = rp[i]; k < rp[i + 1]; ++k) acc = add(acc, mul(val[k], x[col[k]]));
-    const double e = sub(sub(b[i], acc), r[i]);
+    for (long long k = rp[i]; k < rp[i + 1]; ++k)
+      acc = add(acc, mul(val[k], x[ip ? ip[col[k]] : col[k]]));
+    const double e = sub(sub(b[i], acc), r[ip ? ip[i] : i]);
     v[0] = add(v[0], mul(e, e));
   }
   group_sum<1, 256>(v, threadIdx.x, red, 1);
@@ -2420,6 +2755,20 @@ struct FusedPlan {
 constexpr int kVariants = 7;  // A B C D P (= C in one persistent launch per chunk) E F (A / C
                                // reading the row-pattern dictionary instead of the CSR)
 constexpr long long kPersistMaxRows = 8LL << 20;  // P is a candidate up to this size
+// opt.engine request / result code of engine 3 (fused-g, irregular rows)
+constexpr int kReqG = 3 + kVariants;
+
+// a SELL-C-sigma copy of the matrix (rows sorted by length inside windows of
+// sigma rows, 32-row slices, column-major inside a slice; rows longer than
+// the copy's threshold have length -1 and are not stored)
+struct Sell {
+  long long slices = 0, total = 0;  // slices, elements incl. padding
+  long long* ptr = nullptr;         // [slices + 1] slice starts
+  int* perm = nullptr;              // position -> row
+  int* len = nullptr;               // position -> length (-1: longer than the threshold)
+  int* col = nullptr;
+  double* val = nullptr;
+};
 
 struct pcg_solver {
   pcg_matrix A{};
@@ -2482,12 +2831,8 @@ struct pcg_solver {
   // engine-2 K2 in SELL-C-sigma layout (irregular matrices)
   bool sell = false;
   int sell_batch = 2;              // nonzeros per lane per load batch in the SELL K2 (2 ~ 4 > 8, measured)
-  long long sell_slices = 0;
-  long long* sell_ptr = nullptr;
-  int* sell_perm = nullptr;
-  int* sell_len = nullptr;
-  int* sell_col = nullptr;
-  double* sell_val = nullptr;
+  Sell sell2;                      // engine 2's copy (rows <= kLongRow, sigma kSellSigma)
+  Sell gsell;                      // engine 3's copy (rows <= g_thr, sigma kGRows)
   int* x_ptr = nullptr;            // its per-tile send lists (sorted by row)
   int* x_row = nullptr;
   int* x_peer = nullptr;
@@ -2495,7 +2840,28 @@ struct pcg_solver {
   FusedPlan plans[kVariants];      // per fused variant (stages == 0: does not fit)
   std::vector<FusedPlan> alts[kVariants];  // E/F: occupancy alternatives the autotuner times
   int alt_pick[kVariants] = {};    // ... and the one it picked
-  double tune_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // autotune ms/iteration: fused A..E, engine 2
+  double tune_ms[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // autotune ms/iteration: fused A..F, engine 2, 3
+  double* hubdot = nullptr;        // engine 3: dot terms of each multi-chunk row [n_gmulti][4]
+  int n_gmulti = 0;
+  LongChunk* gchunks = nullptr;    // engine 3: long rows as warp-sized chunks
+  long long n_gchunks = 0;
+  double* gchunk_part = nullptr;
+  unsigned* gchunk_ticket = nullptr;
+  long long g_chunk_nnz = kGChunkNnz;
+  bool g_built = false;            // engine 3 data below exists
+  int* iperm = nullptr;            // row -> SELL position
+  int* sell_colp = nullptr;        // engine 3 SELL columns renumbered to positions
+  long long g_thr = kGLaneRow;     // engine 3: rows longer than this are warp chunks
+  int* g_long_rows = nullptr;      // ... those rows
+  long long n_glong = 0;
+  int* hcol = nullptr;             // hub rows packed (positions, values)
+  double* hval = nullptr;
+  double* dinvp = nullptr;         // inv_diag in SELL order (every init)
+  double* natbuf = nullptr;        // solver_state: natural-order copies (engine 3)
+  int g_batch = 2;                 // engine 3 SELL nonzeros per lane per load batch (2 or 4)
+  bool e2_pol = false;             // engine 2: L2 hints (streams evict-first, m evict-last)
+  int g_mb = 4;                    // engine 3 CTAs per SM the kernel is compiled for (4 or 6)
+  bool g_pf = false;               // engine 3 update operands loaded before the row's SpMV
   int* tile_row = nullptr;         // variant D/E tiles of the applied plan
   long long* tile_e = nullptr;
   long long hub_len = 0;
@@ -3016,7 +3382,7 @@ int alloc_state(pcg_solver* S) {
 
 // grids above this many blocks publish one fixed-order sum (last block)
 constexpr int kFinGrid = 512;
-inline bool use_fin(const pcg_solver* S) { return S->grid > kFinGrid; }
+inline bool use_fin(const pcg_solver* S) { return S->grid > kFinGrid || S->engine == 3; }
 
 // Variant P: the whole chunk in one cooperative (co-resident) launch.
 // Only single-GPU, tree dots, no drift samples; otherwise P runs as C.
@@ -3204,6 +3570,46 @@ inline bool stored_m_fused(const pcg_solver* S) {
   return S->engine == 1 && S->variant >= 2 && S->variant != 5;
 }
 
+// engine 3 kernel instance: SELL nonzeros per lane per batch x CTAs per SM
+using GKern = void (*)(GParams, int);
+inline GKern g_kernel(const pcg_solver* S) {
+  if (S->g_pf) return S->g_batch == 4 ? pipecg_fused_kernel_g<4, 3, true> : pipecg_fused_kernel_g<2, 4, true>;
+  if (S->g_mb == 6) return S->g_batch == 4 ? pipecg_fused_kernel_g<4, 6, false> : pipecg_fused_kernel_g<2, 6, false>;
+  return S->g_batch == 4 ? pipecg_fused_kernel_g<4, 4, false> : pipecg_fused_kernel_g<2, 4, false>;
+}
+
+// engine 3: one fused SELL kernel per iteration (pipecg_fused_kernel_g)
+void launch_g(pcg_solver* S, int k, const Record& R) {
+  GParams P;
+  P.n = S->A.n_rows;
+  P.n_slices = (S->A.n_rows + 31) / 32;
+  P.n_chunks = S->n_gchunks;
+  P.sptr = S->gsell.ptr;
+  P.slen = S->gsell.len;
+  P.scol = S->sell_colp;
+  P.sval = S->gsell.val;
+  P.chunks = S->gchunks;
+  P.hcol = S->hcol;
+  P.hval = S->hval;
+  P.chunk_part = S->gchunk_part;
+  P.chunk_ticket = S->gchunk_ticket;
+  P.hubdot = S->hubdot;
+  P.n_hub = S->hubdot ? S->n_gmulti : 0;
+  P.dinv = S->dinvp;
+  P.z = S->z; P.q = S->q; P.s = S->s; P.p = S->p; P.x = S->x;
+  P.r = S->r; P.u = S->u; P.w = S->w[0];
+  P.m[0] = S->m;
+  P.m[1] = S->m2;
+  P.C = R.C;
+  P.hist = R.hist;
+  P.rin = reduce_in(S);
+  P.pout = S->partials;
+  P.fin = S->fin;
+  P.counter = S->counter;
+  auto kern = g_kernel(S);
+  launch_k(kern, (unsigned)S->grid, kGRows, 0, S->stream, S->pdl, P, k);
+}
+
 // enqueue graph step k (drift? -> iteration -> seq dots? -> exchange / SpMV)
 int enqueue_step(pcg_solver* S, int k) {
   Record R = record_at(S->rec_dev);
@@ -3213,17 +3619,19 @@ int enqueue_step(pcg_solver* S, int k) {
     if (S->A.rp64)
       drift_partial_kernel<long long><<<kDotGrid, 256, 0, st>>>(
           R.C, k, n, static_cast<const long long*>(S->A.rowptr), S->A.col, S->A.val, S->x, S->b,
-          S->r, S->dpart);
+          S->r, S->dpart, S->engine == 3 ? S->iperm : nullptr);
     else
       drift_partial_kernel<int><<<kDotGrid, 256, 0, st>>>(R.C, k, n,
                                                            static_cast<const int*>(S->A.rowptr),
                                                            S->A.col, S->A.val, S->x, S->b, S->r,
-                                                           S->dpart);
+                                                           S->dpart, S->engine == 3 ? S->iperm : nullptr);
     drift_finish_kernel<<<1, 256, 0, st>>>(R.C, k, S->dpart, kDotGrid, R.dval, R.dit);
   }
   if (S->engine == 1) {
     if (S->A.rp64) launch_fused<long long>(S, k);
     else launch_fused<int>(S, k);
+  } else if (S->engine == 3) {
+    launch_g(S, k, R);
   } else {
     TwoParams P;
     P.n = n;
@@ -3236,22 +3644,25 @@ int enqueue_step(pcg_solver* S, int k) {
     P.pout = S->partials;
     P.fin = S->fin;
     P.counter = use_fin(S) ? S->counter : nullptr;
-    launch_k(pipecg_k1_kernel, (unsigned)S->grid, 256, 0, st, S->pdl, P, k);
+    launch_k(S->e2_pol ? pipecg_k1_kernel<true> : pipecg_k1_kernel<false>, (unsigned)S->grid, 256, 0, st,
+             S->pdl, P, k);
   }
   if (S->opt.dot_mode == PCG_DOT_SEQ && !S->connected)
     seq_dots_kernel<<<1, 32, 0, st>>>(R.C, n, S->r, S->u, S->w[0], S->w[1], S->engine == 1,
-                                      S->seqbuf, k);
+                                      S->seqbuf, k, S->engine == 3 ? S->iperm : nullptr);
   if (S->connected && !S->fused_xchg)
     iter_exchange_kernel<<<kXchgBlocks, 256, 0, st>>>(
         S->cp, R.C, k, use_fin(S) ? S->fin : S->partials, use_fin(S) ? 1 : S->grid,
         stored_m_fused(S) ? S->m : S->w[0],
         stored_m_fused(S) ? S->m2 : S->w[1], stored_m_fused(S) ? 9 : 7, stored_m_fused(S) ? 12 : 8);
   if (S->engine == 2 && S->sell) {
-    auto sk = S->sell_batch == 8 ? sell_spmv_kernel<8> : S->sell_batch == 2 ? sell_spmv_kernel<2>
-                                                                            : sell_spmv_kernel<4>;
-    launch_k(sk, elementwise_grid(S->sell_slices * 32), 256, 0, st, S->pdl, (const Ctrl*)R.C, n,
-             S->sell_slices, (const long long*)S->sell_ptr, (const int*)S->sell_perm,
-             (const int*)S->sell_len, (const int*)S->sell_col, (const double*)S->sell_val,
+    auto sk = S->e2_pol ? (S->sell_batch == 4 ? sell_spmv_kernel<4, true> : sell_spmv_kernel<2, true>)
+                        : (S->sell_batch == 8   ? sell_spmv_kernel<8, false>
+                           : S->sell_batch == 2 ? sell_spmv_kernel<2, false>
+                                                : sell_spmv_kernel<4, false>);
+    launch_k(sk, elementwise_grid(S->sell2.slices * 32), 256, 0, st, S->pdl, (const Ctrl*)R.C, n,
+             S->sell2.slices, (const long long*)S->sell2.ptr, (const int*)S->sell2.perm,
+             (const int*)S->sell2.len, (const int*)S->sell2.col, (const double*)S->sell2.val,
              (const double*)S->m, S->nv);
     if (S->n_chunks > 0) {
       launch_k(gated_spmv_chunks, (unsigned)S->n_chunks, 256, 0, st, S->pdl, (const Ctrl*)R.C,
@@ -3402,7 +3813,9 @@ int auto_chunk(pcg_solver* S) {
   // K-1 early-exit launches after convergence (~3 us each)
   const double bytes = 136.0 * S->A.n_rows + 12.0 * S->A.nnz + 4.0 * S->A.n_rows;
   double t_iter = bytes / 5.0e12 + 4e-6;
-  const double tuned = S->engine == 2 ? S->tune_ms[kVariants] : S->tune_ms[S->variant];
+  const double tuned = S->engine == 2   ? S->tune_ms[kVariants]
+                       : S->engine == 3 ? S->tune_ms[kVariants + 1]
+                                        : S->tune_ms[S->variant];
   if (tuned > 0) t_iter = tuned * 1e-3;
   int K = (int)(4e-3 / t_iter);
   int p = 4;
@@ -3412,8 +3825,8 @@ int auto_chunk(pcg_solver* S) {
 
 void fill_result(pcg_solver* S, const Ctrl& c, pcg_result* res) {
   res->status = c.status;
-  res->engine = S->engine == 1 ? 3 + S->variant : 2;
-  for (int k = 0; k < 8; ++k) res->tune_ms[k] = S->tune_ms[k];
+  res->engine = S->engine == 1 ? 3 + S->variant : S->engine == 3 ? kReqG : 2;
+  for (int k = 0; k < 9; ++k) res->tune_ms[k] = S->tune_ms[k];
   res->pattern_flags = S->pat.n_pat == 0 ? 0
                        : 1 | (S->n_runs > 0 ? 2 : 0) | (S->dinv_by_code ? 4 : 0) |
                              (S->dinv_by_code && S->dinv_uniform ? 8 : 0) |
@@ -3485,13 +3898,20 @@ int preload_solver() {
   PCG_LOAD((pipecg_fused_kernel_s<128, true, true, true>)); PCG_LOAD((pipecg_fused_kernel_s<64, true, true, true>));
   PCG_LOAD(tile_runs_kernel); PCG_LOAD(uniform_check_kernel);
 
-  PCG_LOAD(pipecg_k1_kernel); PCG_LOAD(gated_spmv_rows<int>); PCG_LOAD(gated_spmv_rows<long long>);
+  PCG_LOAD(pipecg_k1_kernel<false>); PCG_LOAD(pipecg_k1_kernel<true>); PCG_LOAD(gated_spmv_rows<int>); PCG_LOAD(gated_spmv_rows<long long>);
   PCG_LOAD(gated_spmv_long<int>); PCG_LOAD(gated_spmv_long<long long>);
-  PCG_LOAD(sell_spmv_kernel<2>); PCG_LOAD(sell_spmv_kernel<4>); PCG_LOAD(sell_spmv_kernel<8>);
+  PCG_LOAD((sell_spmv_kernel<2, false>)); PCG_LOAD((sell_spmv_kernel<4, false>));
+  PCG_LOAD((sell_spmv_kernel<8, false>)); PCG_LOAD((sell_spmv_kernel<2, true>));
+  PCG_LOAD((sell_spmv_kernel<4, true>));
   PCG_LOAD(gated_spmv_chunks); PCG_LOAD(seq_dots_kernel);
   PCG_LOAD(drift_partial_kernel<int>); PCG_LOAD(drift_partial_kernel<long long>);
   PCG_LOAD(drift_finish_kernel); PCG_LOAD(advance_kernel); PCG_LOAD(init_ctrl_kernel);
   PCG_LOAD(finalize_x_kernel); PCG_LOAD(finalize_mark_kernel);
+  PCG_LOAD((pipecg_fused_kernel_g<4, 3, true>)); PCG_LOAD((pipecg_fused_kernel_g<2, 4, true>));
+  PCG_LOAD((pipecg_fused_kernel_g<2, 4, false>)); PCG_LOAD((pipecg_fused_kernel_g<4, 4, false>));
+  PCG_LOAD((pipecg_fused_kernel_g<2, 6, false>)); PCG_LOAD((pipecg_fused_kernel_g<4, 6, false>));
+  PCG_LOAD(gather_perm_kernel); PCG_LOAD(scatter_perm_kernel); PCG_LOAD(iperm_kernel);
+  PCG_LOAD(renumber_kernel); PCG_LOAD(hub_pack_kernel);
   PCG_LOAD(iter_exchange_kernel); PCG_LOAD(vec_exchange_kernel);
   PCG_LOAD(init_dots_exchange_kernel); PCG_LOAD(snapshot_arrive_kernel); PCG_LOAD(xwait_kernel);
   PCG_LOAD(tile_span_kernel<int>); PCG_LOAD(tile_span_kernel<long long>); PCG_LOAD(max_row_kernel);
@@ -3572,6 +3992,35 @@ __global__ void long_len_kernel(const int* rows, long long n, const void* rp, in
 }
 
 // chunk table of the long rows (setup)
+// nnz-bounded chunks of the long rows: engine 2 (one CTA per chunk of
+// chunk_nnz) and engine 3 (one warp per chunk of g_chunk_nnz)
+int build_chunk_list(pcg_solver* S, long long chunk_nnz, const std::vector<long long>& lo,
+                     const std::vector<long long>& hi, const std::vector<int>& rows,
+                     LongChunk** out, long long* n_out, double** part, unsigned** ticket,
+                     int* n_multi = nullptr) {
+  const long long nl = (long long)lo.size();
+  std::vector<LongChunk> ch;
+  int slots = 0;
+  for (long long k = 0; k < nl; ++k) {
+    const long long len = hi[k] - lo[k];
+    const int n = (int)((len + chunk_nnz - 1) / chunk_nnz);
+    const int first = (int)ch.size();
+    const int slot = n > 1 ? slots++ : -1;
+    for (int j = 0; j < n; ++j)
+      ch.push_back(LongChunk{lo[k] + len * j / n, lo[k] + len * (j + 1) / n, rows[k], first, n, slot,
+                             (int)k, 0});
+  }
+  *n_out = (long long)ch.size();
+  if (n_multi) *n_multi = slots;
+  if (pool_malloc(out, ch.size() * sizeof(LongChunk)) != cudaSuccess ||
+      pool_malloc(part, ch.size() * sizeof(double)) != cudaSuccess ||
+      pool_malloc(ticket, std::max(slots, 1) * sizeof(unsigned)) != cudaSuccess)
+    return set_error(PCG_ENOMEM, "long chunks");
+  cudaMemcpyAsync(*out, ch.data(), ch.size() * sizeof(LongChunk), cudaMemcpyHostToDevice, S->stream);
+  cudaMemsetAsync(*ticket, 0, std::max(slots, 1) * sizeof(unsigned), S->stream);
+  return cuda_status(cudaStreamSynchronize(S->stream), "long chunks");
+}
+
 int build_long_chunks(pcg_solver* S) {
   const long long nl = S->n_long;
   if (nl <= 0) return PCG_OK;
@@ -3589,24 +4038,69 @@ int build_long_chunks(pcg_solver* S) {
   int rc = cuda_status(cudaStreamSynchronize(st), "long chunks");
   pool_free(d);
   if (rc) return rc;
-  std::vector<LongChunk> ch;
-  int slots = 0;
-  for (long long k = 0; k < nl; ++k) {
-    const long long len = hi[k] - lo[k];
-    const int n = (int)((len + S->chunk_nnz - 1) / S->chunk_nnz);
-    const int first = (int)ch.size();
-    const int slot = n > 1 ? slots++ : -1;
-    for (int j = 0; j < n; ++j)
-      ch.push_back(LongChunk{lo[k] + len * j / n, lo[k] + len * (j + 1) / n, rows[k], first, n, slot});
+  return build_chunk_list(S, S->chunk_nnz, lo, hi, rows, &S->chunks, &S->n_chunks, &S->chunk_part,
+                          &S->chunk_ticket);
+}
+
+__global__ void gather_int_kernel(long long n, const int* __restrict__ idx, const int* __restrict__ src,
+                                  int* __restrict__ dst) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x)
+    dst[k] = src[idx[k]];
+}
+
+// Engine 3 data (needs the SELL copy): row -> position map, the SELL
+// columns as positions, the hub rows packed with positions, their warp
+// chunks (row = position) and dot slots.
+int build_g(pcg_solver* S) {
+  const long long n = S->A.n_rows, nl = S->n_glong;
+  cudaStream_t st = S->stream;
+  if (pool_malloc(&S->iperm, n * 4) != cudaSuccess ||
+      pool_malloc(&S->sell_colp, (S->gsell.total + 64) * 4) != cudaSuccess ||
+      pool_malloc(&S->dinvp, (n + 32) * 8) != cudaSuccess)
+    return set_error(PCG_ENOMEM, "engine 3 setup");
+  iperm_kernel<<<elementwise_grid(n), 256, 0, st>>>(n, S->gsell.perm, S->iperm);
+  renumber_kernel<<<elementwise_grid(S->gsell.total + 64), 256, 0, st>>>(S->gsell.total + 64, S->iperm,
+                                                                         S->gsell.col, S->sell_colp);
+  if (nl > 0) {
+    long long* d = nullptr;
+    int* pos = nullptr;
+    if (pool_malloc(&d, 2 * nl * sizeof(long long)) != cudaSuccess ||
+        pool_malloc(&pos, nl * sizeof(int)) != cudaSuccess)
+      return set_error(PCG_ENOMEM, "engine 3 setup");
+    long_len_kernel<<<elementwise_grid(nl), 256, 0, st>>>(S->g_long_rows, nl, S->A.rowptr, S->A.rp64,
+                                                          d, d + nl);
+    gather_int_kernel<<<elementwise_grid(nl), 256, 0, st>>>(nl, S->g_long_rows, S->iperm, pos);
+    std::vector<long long> lo(nl), hi(nl), hoff(nl + 1, 0);
+    std::vector<int> prow(nl);
+    cudaMemcpyAsync(lo.data(), d, nl * 8, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(hi.data(), d + nl, nl * 8, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(prow.data(), pos, nl * 4, cudaMemcpyDeviceToHost, st);
+    int rc = cuda_status(cudaStreamSynchronize(st), "engine 3 setup");
+    if (rc) return rc;
+    for (long long k = 0; k < nl; ++k) hoff[k + 1] = hoff[k] + (hi[k] - lo[k]);
+    long long* hoff_d = nullptr;
+    if (pool_malloc(&hoff_d, (nl + 1) * 8) != cudaSuccess ||
+        pool_malloc(&S->hcol, (hoff[nl] + 16) * 4) != cudaSuccess ||
+        pool_malloc(&S->hval, (hoff[nl] + 16) * 8) != cudaSuccess)
+      return set_error(PCG_ENOMEM, "engine 3 hub rows");
+    cudaMemcpyAsync(hoff_d, hoff.data(), (nl + 1) * 8, cudaMemcpyHostToDevice, st);
+    hub_pack_kernel<<<(unsigned)nl, 256, 0, st>>>(d, hoff_d, S->iperm, S->A.col, S->A.val, S->hcol,
+                                                  S->hval);
+    rc = cuda_status(cudaStreamSynchronize(st), "engine 3 hub rows");
+    pool_free(d);
+    pool_free(pos);
+    pool_free(hoff_d);
+    if (rc) return rc;
+    std::vector<long long> plo(hoff.begin(), hoff.end() - 1), phi(hoff.begin() + 1, hoff.end());
+    rc = build_chunk_list(S, S->g_chunk_nnz, plo, phi, prow, &S->gchunks, &S->n_gchunks,
+                          &S->gchunk_part, &S->gchunk_ticket, &S->n_gmulti);
+    if (rc) return rc;
+    if (pool_malloc(&S->hubdot, std::max(S->n_gmulti, 1) * 4 * sizeof(double)) != cudaSuccess)
+      return set_error(PCG_ENOMEM, "engine 3 hub rows");
   }
-  S->n_chunks = (long long)ch.size();
-  if (pool_malloc(&S->chunks, ch.size() * sizeof(LongChunk)) != cudaSuccess ||
-      pool_malloc(&S->chunk_part, ch.size() * sizeof(double)) != cudaSuccess ||
-      pool_malloc(&S->chunk_ticket, std::max(slots, 1) * sizeof(unsigned)) != cudaSuccess)
-    return set_error(PCG_ENOMEM, "long chunks");
-  cudaMemcpyAsync(S->chunks, ch.data(), ch.size() * sizeof(LongChunk), cudaMemcpyHostToDevice, st);
-  cudaMemsetAsync(S->chunk_ticket, 0, std::max(slots, 1) * sizeof(unsigned), st);
-  return cuda_status(cudaStreamSynchronize(st), "long chunks");
+  S->g_built = true;
+  return cuda_status(cudaStreamSynchronize(st), "engine 3 setup");
 }
 
 __global__ void seg_offsets_kernel(long long n, int sigma, long long n_seg, int* offs) {
@@ -3617,9 +4111,9 @@ __global__ void seg_offsets_kernel(long long n, int sigma, long long n_seg, int*
 
 // SELL-C-sigma copy of the matrix for engine 2's K2 (see sell_spmv_kernel)
 template <typename RP>
-int build_sell(pcg_solver* S) {
+int build_sell(pcg_solver* S, int sigma, long long thr, Sell* out) {
   const long long n = S->A.n_rows;
-  const long long n_seg = (n + kSellSigma - 1) / kSellSigma;
+  const long long n_seg = (n + sigma - 1) / sigma;
   const long long n_slices = (n + 31) / 32;
   cudaStream_t st = S->stream;
   const RP* rp = static_cast<const RP*>(S->A.rowptr);
@@ -3632,37 +4126,42 @@ int build_sell(pcg_solver* S) {
   if (pool_malloc(&key, n * 4) != cudaSuccess || pool_malloc(&key2, n * 4) != cudaSuccess ||
       pool_malloc(&idx, n * 4) != cudaSuccess || pool_malloc(&offs, (n_seg + 1) * 4) != cudaSuccess ||
       pool_malloc(&width, (n_slices + 1) * 8) != cudaSuccess ||
-      pool_malloc(&S->sell_perm, n * 4) != cudaSuccess || pool_malloc(&S->sell_len, n * 4) != cudaSuccess ||
-      pool_malloc(&S->sell_ptr, (n_slices + 1) * 8) != cudaSuccess)
+      pool_malloc(&out->perm, n * 4) != cudaSuccess || pool_malloc(&out->len, n * 4) != cudaSuccess ||
+      pool_malloc(&out->ptr, (n_slices + 1) * 8) != cudaSuccess)
     fail("SELL build workspace");
   if (!rc) {
     const unsigned g = elementwise_grid(n);
-    sell_keys_kernel<RP><<<g, 256, 0, st>>>(n, rp, kLongRow, key, idx);
-    seg_offsets_kernel<<<elementwise_grid(n_seg + 1), 256, 0, st>>>(n, kSellSigma, n_seg, offs);
+    sell_keys_kernel<RP><<<g, 256, 0, st>>>(n, rp, thr, key, idx);
+    seg_offsets_kernel<<<elementwise_grid(n_seg + 1), 256, 0, st>>>(n, sigma, n_seg, offs);
     int bits = 1;
-    while ((1LL << bits) <= kLongRow + 1) ++bits;
-    cub::DeviceSegmentedRadixSort::SortPairs(nullptr, b1, key, key2, idx, S->sell_perm, (int)n,
+    while ((1LL << bits) <= thr + 1) ++bits;
+    cub::DeviceSegmentedRadixSort::SortPairs(nullptr, b1, key, key2, idx, out->perm, (int)n,
                                              (int)n_seg, offs, offs + 1, 0, bits, st);
-    cub::DeviceScan::ExclusiveSum(nullptr, b2, width, S->sell_ptr, n_slices + 1, st);
+    cub::DeviceScan::ExclusiveSum(nullptr, b2, width, out->ptr, n_slices + 1, st);
     if (pool_malloc(&tmp, std::max(b1, b2)) != cudaSuccess) fail("SELL sort workspace");
     if (!rc) {
       size_t bt = std::max(b1, b2);
-      cub::DeviceSegmentedRadixSort::SortPairs(tmp, bt, key, key2, idx, S->sell_perm, (int)n,
+      cub::DeviceSegmentedRadixSort::SortPairs(tmp, bt, key, key2, idx, out->perm, (int)n,
                                                (int)n_seg, offs, offs + 1, 0, bits, st);
       cudaMemsetAsync(width, 0, (n_slices + 1) * 8, st);
-      sell_len_kernel<RP><<<g, 256, 0, st>>>(n, rp, kLongRow, S->sell_perm, S->sell_len, n_slices,
+      sell_len_kernel<RP><<<g, 256, 0, st>>>(n, rp, thr, out->perm, out->len, n_slices,
                                              width);
       bt = std::max(b1, b2);
-      cub::DeviceScan::ExclusiveSum(tmp, bt, width, S->sell_ptr, n_slices + 1, st);
+      cub::DeviceScan::ExclusiveSum(tmp, bt, width, out->ptr, n_slices + 1, st);
       long long total = 0;
-      cudaMemcpyAsync(&total, S->sell_ptr + n_slices, 8, cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(&total, out->ptr + n_slices, 8, cudaMemcpyDeviceToHost, st);
       rc = cuda_status(cudaStreamSynchronize(st), "SELL build");
-      if (!rc && (pool_malloc(&S->sell_col, (total + 64) * 4) != cudaSuccess ||
-                  pool_malloc(&S->sell_val, (total + 64) * 8) != cudaSuccess))
+      out->total = total;
+      if (!rc && (pool_malloc(&out->col, (total + 64) * 4) != cudaSuccess ||
+                  pool_malloc(&out->val, (total + 64) * 8) != cudaSuccess))
         fail("SELL arrays");
       if (!rc) {
-        sell_fill_kernel<RP><<<g, 256, 0, st>>>(n, rp, S->A.col, S->A.val, S->sell_perm,
-                                                S->sell_len, S->sell_ptr, S->sell_col, S->sell_val);
+        // padding entries: column 0, value 0 (engine 3 gathers them without
+        // summing; engine 2 skips them)
+        cudaMemsetAsync(out->col, 0, (total + 64) * 4, st);
+        cudaMemsetAsync(out->val, 0, (total + 64) * 8, st);
+        sell_fill_kernel<RP><<<g, 256, 0, st>>>(n, rp, S->A.col, S->A.val, out->perm,
+                                                out->len, out->ptr, out->col, out->val);
         rc = cuda_status(cudaStreamSynchronize(st), "SELL fill");
       }
     }
@@ -3673,10 +4172,7 @@ int build_sell(pcg_solver* S) {
   pool_free(offs);
   pool_free(width);
   pool_free(tmp);
-  if (!rc) {
-    S->sell = true;
-    S->sell_slices = n_slices;
-  }
+  if (!rc) out->slices = n_slices;
   return rc;
 }
 
@@ -3702,7 +4198,7 @@ std::mutex& tune_cache_mu() {
   return mu;
 }
 
-int autotune(pcg_solver* S, int grid2, bool with_engine2, bool irregular) {
+int autotune(pcg_solver* S, int grid2, int grid3, bool with_engine2, bool irregular) {
   const long long n = S->A.n_rows;
   cudaStream_t st = S->stream;
   fill_kernel<<<elementwise_grid(n), 256, 0, st>>>(S->nv, n, 1.0);
@@ -3716,7 +4212,11 @@ int autotune(pcg_solver* S, int grid2, bool with_engine2, bool irregular) {
   int best = -1;
   float best_ms = 0.f;
   int rc = PCG_OK;
-  for (int cand = 0; cand < (with_engine2 ? kVariants + 1 : kVariants) && !rc; ++cand) {
+  // candidates: fused variants 0..kVariants-1, engine 2 (kVariants), engine 3
+  // (kVariants + 1: irregular rows, when its SELL copy exists)
+  const bool g_ok = irregular && S->g_built;
+  const int n_cand = with_engine2 ? (g_ok ? kVariants + 2 : kVariants + 1) : kVariants;
+  for (int cand = 0; cand < n_cand && !rc; ++cand) {
     if (cand < kVariants) {
       // B (gather warps) never won a measurement; D only pays for irregular rows
       if (!S->plans[cand].stages || cand == 1 || (cand == 3 && !irregular)) continue;
@@ -3728,9 +4228,12 @@ int autotune(pcg_solver* S, int grid2, bool with_engine2, bool irregular) {
       if (cand < kVariants) {
         S->engine = 1;
         apply_plan(S, S->alts[cand].empty() ? S->plans[cand] : S->alts[cand][a]);
-      } else {
+      } else if (cand == kVariants) {
         S->engine = 2;
         S->grid = S->n_partials = grid2;
+      } else {
+        S->engine = 3;
+        S->grid = S->n_partials = grid3;
       }
       // b := n (ones), x0 := z (zeros); init copies them before overwriting
       rc = pipecg_b200_solver_init(S, S->nv, S->z, 0.0, 1LL << 40, 0, st);
@@ -3772,9 +4275,12 @@ int autotune(pcg_solver* S, int grid2, bool with_engine2, bool irregular) {
   if (best < kVariants) {
     S->engine = 1;
     apply_plan(S, S->plans[best]);
-  } else {
+  } else if (best == kVariants) {
     S->engine = 2;
     S->grid = S->n_partials = grid2;
+  } else {
+    S->engine = 3;
+    S->grid = S->n_partials = grid3;
   }
   return PCG_OK;
 }
@@ -3804,11 +4310,16 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   if (const char* f = getenv("PIPECG_B200_FLAGS")) S->flags = atoi(f);
   if (getenv("PIPECG_B200_NO_PDL")) S->pdl = false;
   if (const char* e = getenv("PIPECG_B200_SELL_BATCH")) S->sell_batch = atoi(e);  // experiment
+  if (const char* e = getenv("PIPECG_B200_G_BATCH")) S->g_batch = atoi(e);         // experiment
+  if (const char* e = getenv("PIPECG_B200_G_MB")) S->g_mb = atoi(e);               // experiment
+  if (const char* e = getenv("PIPECG_B200_E2POL")) S->e2_pol = atoi(e) != 0;      // experiment
+  if (const char* e = getenv("PIPECG_B200_G_PF")) S->g_pf = atoi(e) != 0;          // experiment
+  if (const char* e = getenv("PIPECG_B200_G_THR")) S->g_thr = std::max(8LL, atoll(e)); // experiment
   if (const char* e = getenv("PIPECG_B200_PA")) S->p_mg = atoi(e) == 0;  // experiment switch
   if (const char* e = getenv("PIPECG_B200_L2PF")) S->l2_prefetch = atoi(e);  // experiment switch
   if (getenv("PIPECG_B200_NO_DEFER_X")) S->no_defer_x = true;                 // experiment switch
   if (const char* v = getenv("PIPECG_B200_CHUNK_NNZ"))  // test switch: many chunks on small rows
-    S->chunk_nnz = std::max(32LL, atoll(v));
+    S->chunk_nnz = S->g_chunk_nnz = std::max(32LL, atoll(v));
   if (opts) S->opt = *opts;
   else {
     S->opt.dot_mode = PCG_DOT_TREE;
@@ -3850,7 +4361,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   // engine: 0 auto (autotuned), 1 fused (heuristic variant), 2 two-kernel,
   // 3..9 fused variant A/B/C/D/P/E/F
   const int req = S->opt.engine;
-  if (req < 0 || req > 3 + kVariants - 1) {
+  if (req < 0 || req > kReqG) {
     pipecg_b200_solver_destroy(S);
     return set_error(PCG_EINVAL, "solver_create: unknown engine");
   }
@@ -3878,7 +4389,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     }
   }
   phase("patterns");
-  if (req != 2) {
+  if (req != 2 && req != kReqG) {
     rc = A->rp64 ? fused_setup<long long>(S) : fused_setup<int>(S);
     if (rc && rc != PCG_EINVAL) {
       pipecg_b200_solver_destroy(S);
@@ -3917,7 +4428,9 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     bool want = has_long && (req == 0 || req == 2 || !fused_ok);
     if (const char* e = getenv("PIPECG_B200_SELL")) want = atoi(e) != 0 && (req == 0 || req == 2 || !fused_ok);
     if (want) {
-      rc = A->rp64 ? build_sell<long long>(S) : build_sell<int>(S);
+      rc = A->rp64 ? build_sell<long long>(S, kSellSigma, kLongRow, &S->sell2)
+                   : build_sell<int>(S, kSellSigma, kLongRow, &S->sell2);
+      S->sell = rc == PCG_OK;
       if (!rc && !getenv("PIPECG_B200_NO_CHUNKS")) rc = build_long_chunks(S);
       if (rc) {
         pipecg_b200_solver_destroy(S);
@@ -3925,8 +4438,37 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
       }
     }
   }
+  // engine 3: an autotune candidate for irregular rows (req 0), or asked for
+  if (req == kReqG || (req == 0 && has_long && !getenv("PIPECG_B200_NO_G"))) {
+    int64_t cnt = 0;
+    rc = pipecg_b200_find_long_rows(A->n_rows, A->rp64, A->rowptr, S->g_thr, nullptr, 0, &cnt, S->stream);
+    if (!rc && cnt > 0) {
+      if (pool_malloc(&S->g_long_rows, cnt * sizeof(int)) != cudaSuccess)
+        rc = set_error(PCG_ENOMEM, "engine 3 long rows");
+      else
+        rc = pipecg_b200_find_long_rows(A->n_rows, A->rp64, A->rowptr, S->g_thr, S->g_long_rows, cnt,
+                                        &cnt, S->stream);
+    }
+    S->n_glong = cnt;
+    if (!rc)
+      rc = A->rp64 ? build_sell<long long>(S, kGRows, S->g_thr, &S->gsell)
+                   : build_sell<int>(S, kGRows, S->g_thr, &S->gsell);
+    if (!rc) rc = build_g(S);
+    if (rc) {
+      pipecg_b200_solver_destroy(S);
+      return rc;
+    }
+  }
   const int grid2 = std::min<int>(kDotGrid, 4 * S->num_sms);
-  S->grid = grid2;
+  int grid3 = 0;  // engine 3: resident CTAs (256 threads each), at most one per window
+  if (S->g_built) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, g_kernel(S), kGRows, 0);
+    const long long n_win = (A->n_rows + kGRows - 1) / kGRows;  // 8 slices (warps) each
+    grid3 = (int)std::max<long long>(1, std::min<long long>((long long)std::max(occ, 1) * S->num_sms,
+                                                            n_win));
+  }
+  S->grid = std::max(grid2, grid3);
   // partials are sized for the largest grid any candidate (plan or autotune
   // alternative) can launch with
   for (int v = 0; v < kVariants; ++v) {
@@ -3940,7 +4482,10 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     pipecg_b200_solver_destroy(S);
     return rc;
   }
-  if (!fused_ok) {
+  if (req == kReqG) {
+    S->engine = 3;
+    S->grid = S->n_partials = grid3;
+  } else if (!fused_ok) {
     S->engine = 2;
     S->grid = S->n_partials = grid2;
   } else if (req >= 3) {
@@ -3975,23 +4520,29 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     }
     if (cached >= 0 && cached < kVariants && cached_alt < (int)S->alts[cached].size())
       S->plans[cached] = S->alts[cached][cached_alt];
-    if (cached >= 0 && (cached == kVariants || S->plans[cached].stages)) {
+    if (cached >= 0 && (cached == kVariants ||
+                        (cached == kVariants + 1 && S->g_built) ||
+                        (cached < kVariants && S->plans[cached].stages))) {
       if (cached < kVariants) {
         S->engine = 1;
         apply_plan(S, S->plans[cached]);
-      } else {
+      } else if (cached == kVariants) {
         S->engine = 2;
         S->grid = S->n_partials = grid2;
+      } else {
+        S->engine = 3;
+        S->grid = S->n_partials = grid3;
       }
     } else {
-      rc = autotune(S, grid2, req == 0, has_long);
+      rc = autotune(S, grid2, grid3, req == 0, has_long);
       if (rc) {
         pipecg_b200_solver_destroy(S);
         return rc;
       }
       std::lock_guard<std::mutex> lk(tune_cache_mu());
-      tune_cache()[key] = S->engine == 2 ? std::make_pair(kVariants, 0)
-                                         : std::make_pair(S->variant, S->alt_pick[S->variant]);
+      tune_cache()[key] = S->engine == 2   ? std::make_pair(kVariants, 0)
+                          : S->engine == 3 ? std::make_pair(kVariants + 1, 0)
+                                           : std::make_pair(S->variant, S->alt_pick[S->variant]);
     }
   }
   phase("engine choice");
@@ -4000,6 +4551,10 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
     fprintf(stderr, "[pipecg_b200] engine %d variant %d tr %d stages %d grid %d smem %zu n_pat %d "
             "runs %d dinv_by_code %d uniform %d\n", S->engine, S->variant, S->tr, S->stages, S->grid,
             S->smem, S->pat.n_pat, S->n_runs, (int)S->dinv_by_code, (int)S->dinv_uniform);
+    if (S->g_built)
+      fprintf(stderr, "[pipecg_b200] engine 3: lane rows <= %lld, %lld warp-chunk rows (%lld chunks, %d "
+              "multi-chunk), SELL %lld slices %lld elements, grid %d\n", S->g_thr, S->n_glong,
+              S->n_gchunks, S->n_gmulti, S->gsell.slices, S->gsell.total, S->engine == 3 ? S->grid : 0);
     for (int v = 5; v <= 6; ++v)
       for (const FusedPlan& p : S->alts[v])
         fprintf(stderr, "[pipecg_b200]   alt %c: tr %d bps %d stages %d grid %d smem %zu\n",
@@ -4033,11 +4588,24 @@ int pipecg_b200_solver_destroy(pcg_solver* S) {
   pool_free(S->chunks);
   pool_free(S->chunk_part);
   pool_free(S->chunk_ticket);
-  pool_free(S->sell_ptr);
-  pool_free(S->sell_perm);
-  pool_free(S->sell_len);
-  pool_free(S->sell_col);
-  pool_free(S->sell_val);
+  pool_free(S->hubdot);
+  pool_free(S->gchunks);
+  pool_free(S->iperm);
+  pool_free(S->sell_colp);
+  pool_free(S->hcol);
+  pool_free(S->hval);
+  pool_free(S->dinvp);
+  pool_free(S->natbuf);
+  pool_free(S->gchunk_part);
+  pool_free(S->gchunk_ticket);
+  for (Sell* c : {&S->sell2, &S->gsell}) {
+    pool_free(c->ptr);
+    pool_free(c->perm);
+    pool_free(c->len);
+    pool_free(c->col);
+    pool_free(c->val);
+  }
+  pool_free(S->g_long_rows);
   pool_free(S->x_ptr);
   pool_free(S->x_row);
   pool_free(S->x_peer);
@@ -4156,16 +4724,20 @@ int build_tile_sends(pcg_solver* S) {
 }
 
 // every inv_diag entry of [0, n_cols) (owned + halo) equal to dinv0?
+// Stream-ordered allocation only: solver_init calls this while a peer rank
+// sharing the GPU may already be spinning in its iteration kernel, and a
+// plain cudaFree would wait for that kernel (device-wide sync -> the peer
+// times out waiting for this rank).
 int uniform_dinv(pcg_solver* S, int* bad) {
   int* d = nullptr;
-  if (pool_malloc(&d, sizeof(int)) != cudaSuccess) return set_error(PCG_ENOMEM, "dinv check");
+  if (cudaMallocAsync(&d, sizeof(int), S->stream) != cudaSuccess)
+    return set_error(PCG_ENOMEM, "dinv check");
   cudaMemsetAsync(d, 0, sizeof(int), S->stream);
   uniform_check_kernel<<<elementwise_grid(S->A.n_cols), 256, 0, S->stream>>>(
       S->A.n_cols, S->A.inv_diag, S->dinv0, d);
   cudaMemcpyAsync(bad, d, sizeof(int), cudaMemcpyDeviceToHost, S->stream);
-  const int rc = cuda_status(cudaStreamSynchronize(S->stream), "dinv check");
-  pool_free(d);
-  return rc;
+  cudaFreeAsync(d, S->stream);
+  return cuda_status(cudaStreamSynchronize(S->stream), "dinv check");
 }
 
 int pipecg_b200_solver_connect(pcg_solver* S, int rank, int world, void* const* peer_vbuf,
@@ -4312,6 +4884,10 @@ int pipecg_b200_solver_init(pcg_solver* S, const double* b, const double* x0, do
     S->xtarget += (unsigned long long)S->world * kXchgBlocks;
     xwait_kernel<<<1, 32, 0, st>>>(S->comm, S->xtarget, R.C);
   }
+  if (S->engine == 3) {  // the kernel gathers the stored m (n = A m is formed in the kernel)
+    rc = pipecg_b200_jacobi_apply(n, S->A.inv_diag, S->w[0], S->m, st);  // m = M^-1 w
+    if (rc) return rc;
+  }
   if (S->engine == 2) {
     rc = pipecg_b200_jacobi_apply(n, S->A.inv_diag, S->w[0], S->m, st);  // m = M^-1 w
     if (rc) return rc;
@@ -4328,6 +4904,15 @@ int pipecg_b200_solver_init(pcg_solver* S, const double* b, const double* x0, do
   const double* db[4] = {S->u, S->u, S->u, S->b};
   rc = dots_any(n, 4, da, db, S->opt.dot_mode, S->dots4, S->dots_ws, st);
   if (rc) return rc;
+  if (S->engine == 3) {  // the state moves into SELL order (b stays natural)
+    const unsigned g = elementwise_grid(n);
+    gather_perm_kernel<<<g, 256, 0, st>>>(n, S->gsell.perm, S->A.inv_diag, S->dinvp);
+    double* vs[5] = {S->x, S->r, S->u, S->w[0], S->m};
+    for (double* v : vs) {
+      cudaMemcpyAsync(S->nv, v, bytes, cudaMemcpyDeviceToDevice, st);
+      gather_perm_kernel<<<g, 256, 0, st>>>(n, S->gsell.perm, S->nv, v);
+    }
+  }
   if (S->connected) {
     init_dots_exchange_kernel<<<1, 32, 0, st>>>(S->cp, S->dots4);
     S->xtarget += (unsigned long long)S->world;
@@ -4447,7 +5032,16 @@ int pipecg_b200_solver_enqueue(pcg_solver* S, int64_t count) {
   return PCG_OK;
 }
 
-double* pipecg_b200_solver_x(pcg_solver* S) { return S ? S->x : nullptr; }
+double* pipecg_b200_solver_x(pcg_solver* S) {
+  if (!S) return nullptr;
+  if (S->engine == 3 && S->initialized) {  // SELL order -> natural order (into the unused n)
+    scatter_perm_kernel<<<elementwise_grid(S->A.n_rows), 256, 0, S->stream>>>(S->A.n_rows, S->gsell.perm,
+                                                                              S->x, S->nv);
+    cudaStreamSynchronize(S->stream);
+    return S->nv;
+  }
+  return S->x;
+}
 
 void* pipecg_b200_solver_stream(pcg_solver* S) { return S ? (void*)S->stream : nullptr; }
 
@@ -4478,6 +5072,23 @@ int pipecg_b200_solver_state(pcg_solver* S, double** ptrs) {
   const long long done = c.status == PCG_STOPPED ? c.final_it : c.base_it;
   double* w = S->engine == 1 ? S->w[done & 1] : S->w[0];
   const long long n = S->A.n_rows;
+  if (S->engine == 3) {  // natural-order copies of the SELL-order state
+    if (!S->natbuf && pool_malloc(&S->natbuf, S->ld * 10 * sizeof(double)) != cudaSuccess)
+      return set_error(PCG_ENOMEM, "solver_state: natural-order copies");
+    double* src[10] = {S->x, S->r, S->u, S->w[0], nullptr, nullptr, S->z, S->q, S->s, S->p};
+    const unsigned g = elementwise_grid(n);
+    for (int k = 0; k < 10; ++k) {
+      ptrs[k] = S->natbuf + (size_t)k * S->ld;
+      if (src[k])
+        scatter_perm_kernel<<<g, 256, 0, S->stream>>>(n, S->gsell.perm, src[k], (double*)ptrs[k]);
+    }
+    int rc = pipecg_b200_jacobi_apply(n, S->A.inv_diag, (double*)ptrs[3], (double*)ptrs[4], S->stream);
+    if (!rc)
+      rc = spmv_any(n, S->A.rp64, S->A.rowptr, S->A.col, S->A.val, (double*)ptrs[4], nullptr,
+                    (double*)ptrs[5], S->long_rows, S->n_long, 0, S->stream);
+    if (rc) return rc;
+    return cuda_status(cudaStreamSynchronize(S->stream), "solver_state");
+  }
   if (!S->mn_valid) {
     int rc = pipecg_b200_jacobi_apply(n, S->A.inv_diag, w, S->m, S->stream);
     if (!rc)

@@ -414,8 +414,8 @@ class DistributedSolver:
 
         self.problem, self.group = problem, group
         opts = options or DeviceOptions()
-        if opts.engine == "two":
-            raise ValueError("the distributed path runs the fused engine")
+        if opts.engine in ("two", "fused-g"):
+            raise ValueError("the distributed path runs the fused engine (variants A-F)")
         engine = opts.engine if opts.engine.startswith("fused") else "fused"
         opts = DeviceOptions(dot_mode=opts.dot_mode, engine=engine, chunk=opts.chunk,
                              use_graphs=opts.use_graphs, max_sms=opts.max_sms)

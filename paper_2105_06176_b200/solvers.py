@@ -174,9 +174,10 @@ class DeviceOptions:
       C with a whole chunk of iterations in one persistent launch, for small
       latency-bound problems), "fused-e" / "fused-f" (A / C reading the
       matrix through its lossless row-pattern dictionary: one byte per row
-      instead of the CSR, for constant-coefficient stencil-like matrices) or
-      "two" (update kernel +
-      SpMV kernel; general matrices, very long rows).
+      instead of the CSR, for constant-coefficient stencil-like matrices),
+      "fused-g" (irregular rows: one SELL-C-sigma kernel per iteration, hub
+      rows as nnz-bounded chunks inside it) or "two" (update kernel + SpMV
+      kernel; general matrices, very long rows).
     chunk: iterations per CUDA-graph chunk (0 = sized from the problem).
     use_graphs: capture chunks as CUDA graphs.
     max_sms: size persistent grids for this many SMs (0 = all; used when
@@ -192,7 +193,7 @@ class DeviceOptions:
     def native(self) -> _lib.PcgOptions:
         eng = {"auto": 0, "fused": 1, "two": 2, "fused-a": 3, "fused-b": 4,
                "fused-c": 5, "fused-d": 6, "fused-p": 7, "fused-e": 8,
-               "fused-f": 9}[self.engine]
+               "fused-f": 9, "fused-g": 10}[self.engine]
         dm = {"tree": _lib.PCG_DOT_TREE, "seq": _lib.PCG_DOT_SEQ}[self.dot_mode]
         return _lib.PcgOptions(dm, eng, int(self.chunk), 1 if self.use_graphs else 0,
                                int(self.max_sms))

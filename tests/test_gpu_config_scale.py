@@ -42,9 +42,9 @@ GDIR = Path(__file__).resolve().parent / "golden" / "config_scale"
 CONFIGS = sorted(p.stem for p in GDIR.glob("*.json"))
 
 STENCIL_ENGINES = ["auto", "fused-e", "fused-f", "fused-a", "fused-c", "two"]
-IRREGULAR_ENGINES = ["auto", "two", "fused-d"]
+IRREGULAR_ENGINES = ["auto", "two", "fused-g", "fused-d"]
 ENGINE_NAMES = {2: "two", 3: "fused-a", 4: "fused-b", 5: "fused-c", 6: "fused-d",
-                7: "fused-p", 8: "fused-e", 9: "fused-f"}
+                7: "fused-p", 8: "fused-e", 9: "fused-f", 10: "fused-g"}
 
 
 def meta(name):
@@ -124,7 +124,10 @@ def seq_cases():
         m = meta(name)
         if m["kind"] == "powerlaw" or m["N"] > 2 ** 24:
             continue  # hub rows are tree-combined; 400^3 seq dots take minutes
-        out += [(name, e) for e in STENCIL_ENGINES]
+        # the sequential dots are one warp (~0.2 s per iteration at 256^3):
+        # the bench's own engine there, every engine below
+        engines = ["auto"] if m["N"] > 2 ** 22 else STENCIL_ENGINES
+        out += [(name, e) for e in engines]
     return out
 
 

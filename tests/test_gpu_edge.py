@@ -22,6 +22,7 @@ pytestmark = pytest.mark.gpu
 
 pb = pytest.importorskip("paper_2105_06176_b200")
 torch = pytest.importorskip("torch")
+from paper_2105_06176_b200._lib import NativeError  # noqa: E402
 
 ENGINES = ["auto", "fused-a", "fused-b", "fused-c", "fused-d", "fused-p", "fused-e", "fused-f",
            "two"]
@@ -41,8 +42,17 @@ def solve(which, A, b, x0, pc, cfg=None, dot_mode="tree"):
     name, engine = which
     if engine is None:
         return pb.pcg_solve(A, b, x0, pc, cfg, options=pb.DeviceOptions(dot_mode=dot_mode))
-    return pb.pipecg_solve(A, b, x0, pc, cfg,
-                           options=pb.DeviceOptions(engine=engine, dot_mode=dot_mode))
+    try:
+        return pb.pipecg_solve(A, b, x0, pc, cfg,
+                               options=pb.DeviceOptions(engine=engine, dot_mode=dot_mode))
+    except NativeError as e:
+        # a forced engine that does not apply to this matrix (E/F need a
+        # row-pattern dictionary; a variant's tiles may not fit shared
+        # memory): solver_create refuses it explicitly, "auto" never picks it
+        msg = str(e)
+        if "no row-pattern dictionary" in msg or "exceed shared memory" in msg:
+            pytest.skip(f"{engine} does not apply to this matrix: {msg}")
+        raise
 
 
 def identity4():

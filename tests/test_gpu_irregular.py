@@ -21,7 +21,7 @@ pytestmark = pytest.mark.gpu
 pb = pytest.importorskip("paper_2105_06176_b200")
 from test_gpu_solver import assert_within_envelope, envelope  # noqa: E402
 
-VARIANTS = ["fused-d", "two"]
+VARIANTS = ["fused-d", "two", "fused-g"]
 
 
 def _problem(A):
@@ -74,7 +74,7 @@ def test_powerlaw_seq_bitwise_balanced_tiles(cuda, monkeypatch, dcap, engine):
     np.testing.assert_array_equal(x, ref.x)
 
 
-@pytest.mark.parametrize("engine", ["auto", "fused-d", "two"])
+@pytest.mark.parametrize("engine", ["auto", "fused-d", "two", "fused-g"])
 def test_powerlaw_tree_within_envelope(cuda, engine):
     A = pb.generate_powerlaw(2**16)
     b, x0, d, tol = _problem(A)
@@ -123,8 +123,9 @@ def test_random_spd_tiles_bitwise(cuda, monkeypatch, dcap, max_len, engine):
                                envelope(A, b, x0, d, tol, 3000))
 
 
+@pytest.mark.parametrize("engine", ["two", "fused-g"])
 @pytest.mark.parametrize("n", [2**12, 3000])
-def test_sell_layout_bitwise(cuda, monkeypatch, n):
+def test_sell_layout_bitwise(cuda, monkeypatch, n, engine):
     """Engine 2's SELL-C-sigma SpMV (rows length-sorted inside 1024-row
     windows, 32-row column-major slices): every row still summed in CSR order,
     so a sequential-dot solve is bitwise the reference's (incl. a ragged
@@ -136,7 +137,7 @@ def test_sell_layout_bitwise(cuda, monkeypatch, n):
     ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=3000)
     cfg = pb.SolverConfig(tolerance=tol, max_iterations=3000, record_history=True)
     x, rep = pb.pipecg_solve(A, b, x0, pb.jacobi_setup(A), cfg,
-                             options=pb.DeviceOptions(dot_mode="seq", engine="two"))
+                             options=pb.DeviceOptions(dot_mode="seq", engine=engine))
     assert rep.history == ref.history
     np.testing.assert_array_equal(x, ref.x)
 
@@ -168,8 +169,9 @@ def _hub_spd(n, hub_rows, hub_len, seed):
     return pb.CsrMatrix(n, n, ro, cols, vals)
 
 
+@pytest.mark.parametrize("engine", ["two", "fused-g"])
 @pytest.mark.parametrize("chunk_nnz", [None, 300, 64])
-def test_hub_rows_multi_chunk(cuda, monkeypatch, chunk_nnz):
+def test_hub_rows_multi_chunk(cuda, monkeypatch, chunk_nnz, engine):
     """Engine 2's long-row path with several chunks per row (kChunkNnz =
     2,048 by default; PIPECG_B200_CHUNK_NNZ shrinks it so every row > 256
     nonzeros splits into many chunks): the last chunk to finish (atomic
@@ -185,7 +187,7 @@ def test_hub_rows_multi_chunk(cuda, monkeypatch, chunk_nnz):
     cfg = pb.SolverConfig(tolerance=tol, max_iterations=3000, record_history=True)
     env = envelope(A, b, x0, d, tol, 3000)
     for mode in ("tree", "seq"):
-        opts = pb.DeviceOptions(engine="two", dot_mode=mode)
+        opts = pb.DeviceOptions(engine=engine, dot_mode=mode)
         x, rep = pb.pipecg_solve(A, b, x0, pb.jacobi_setup(A), cfg, options=opts)
         assert_within_envelope(x, rep, ref.iterations, ref.history, ref.x, env)
         x2, rep2 = pb.pipecg_solve(A, b, x0, pb.jacobi_setup(A), cfg, options=opts)
@@ -206,3 +208,71 @@ def test_powerlaw_multi_chunk_small_chunks(cuda, monkeypatch):
                              options=pb.DeviceOptions(engine="two"))
     assert_within_envelope(x, rep, ref.iterations, ref.history, ref.x,
                            envelope(A, b, x0, d, tol, 2000))
+
+
+# ---------------------------------------------------------------------------
+# engine 3 ("fused-g"): one SELL kernel per iteration, hub rows inside it
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("case", ["powerlaw16", "hubs", "hubs-chunk64", "ragged"])
+def test_fused_g_matches_oracle(cuda, monkeypatch, case):
+    """Engine 3 in both dot modes.  Rows <= 256 nonzeros are summed by their
+    SELL position's thread in CSR order (k-blocks of the window staged in
+    shared memory): with no hub rows a seq-dot solve is the reference's bit
+    for bit.  Hub rows (warp chunks, chunk partials combined in order) are
+    graded against the oracle's reorder envelope."""
+    if case == "hubs-chunk64":
+        monkeypatch.setenv("PIPECG_B200_CHUNK_NNZ", "64")
+    A = {"powerlaw16": lambda: pb.generate_powerlaw(2**16),
+         "hubs": lambda: _hub_spd(60000, 6, 9000, seed=11),
+         "hubs-chunk64": lambda: _hub_spd(20000, 4, 3000, seed=5),
+         "ragged": lambda: _random_spd(70001, 30, seed=8)}[case]()
+    b, x0, d, tol = _problem(A)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=3000)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=3000, record_history=True)
+    hubs = A.row_nnz().max() > 256
+    env = envelope(A, b, x0, d, tol, 3000) if hubs else None
+    for mode in ("seq", "tree"):
+        x, rep = pb.pipecg_solve(A, b, x0, pb.jacobi_setup(A), cfg,
+                                 options=pb.DeviceOptions(engine="fused-g", dot_mode=mode))
+        if mode == "seq" and not hubs:
+            assert rep.history == ref.history
+            np.testing.assert_array_equal(x, ref.x)
+        else:
+            assert_within_envelope(x, rep, ref.iterations, ref.history, ref.x,
+                                   env or envelope(A, b, x0, d, tol, 3000))
+
+
+def test_fused_g_tree_deterministic_and_in_envelope(cuda):
+    """Tree mode: block partials + hub slots summed in a fixed order by the
+    last CTA -> repeated solves are bitwise identical; graded against the
+    oracle's reorder envelope."""
+    A = _hub_spd(60000, 6, 9000, seed=11)
+    b, x0, d, tol = _problem(A)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=3000)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=3000, record_history=True)
+    opts = pb.DeviceOptions(engine="fused-g")
+    x, rep = pb.pipecg_solve(A, b, x0, pb.jacobi_setup(A), cfg, options=opts)
+    assert_within_envelope(x, rep, ref.iterations, ref.history, ref.x,
+                           envelope(A, b, x0, d, tol, 3000))
+    for _ in range(2):
+        x2, rep2 = pb.pipecg_solve(A, b, x0, pb.jacobi_setup(A), cfg, options=opts)
+        assert rep2.history == rep.history
+        np.testing.assert_array_equal(x2, x)
+
+
+@pytest.mark.parametrize("pol", ["0", "1", "3", "15"])
+def test_fused_g_cache_policies_bitwise(cuda, monkeypatch, pol):
+    """The L2 policy bits (PIPECG_B200_GPOL) change only cache behaviour."""
+    monkeypatch.setenv("PIPECG_B200_GPOL", pol)
+    A = pb.generate_powerlaw(2**14)
+    b, x0, d, tol = _problem(A)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=2000)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=2000, record_history=True)
+    x, rep = pb.pipecg_solve(A, b, x0, pb.jacobi_setup(A), cfg,
+                             options=pb.DeviceOptions(engine="fused-g", dot_mode="seq"))
+    if A.row_nnz().max() <= 256:
+        assert rep.history == ref.history
+        np.testing.assert_array_equal(x, ref.x)
+    else:
+        assert_within_envelope(x, rep, ref.iterations, ref.history, ref.x,
+                               envelope(A, b, x0, d, tol, 2000))

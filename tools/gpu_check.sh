@@ -24,6 +24,7 @@ for job in "$@"; do
       case "$eng" in fused-c) kre='regex:pipecg_fused_kernel_a';; fused-a) kre='regex:pipecg_fused_kernel_a';;
                      fused-b) kre='regex:pipecg_fused_kernel[^_]';; two) kre='regex:sell_spmv|gated_spmv|pipecg_k1';;
                      fused-e|fused-f) kre='regex:pipecg_fused_kernel_s';;
+                     fused-g) kre='regex:pipecg_fused_kernel_g';;
                      *) kre='regex:pipecg_';; esac
       common="python bench.py --config $cfg --engine $eng --no-north-star --no-e2e --no-cpu --no-tts"
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
