@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-tts", action="store_true", help="skip the time-to-solution leg")
+    ap.add_argument("--no-pcg", action="store_true", help="skip the classic-PCG comparison leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--engine", default="auto",
                     help="DeviceOptions.engine (auto | fused | fused-a .. fused-f | fused-p | two)")
@@ -352,7 +353,7 @@ def time_iterations(pb, torch, A, pc_d, warmup: int, steps: int, options=None):
     ok = res.status == 0 and res.iterations == warmup + steps
     # kernels launched in the timed region: one iteration kernel per step
     # (+ the SpMV kernel(s) for engine 2) and one advance kernel per chunk
-    per_step = 1 if res.engine != 2 else 2
+    per_step = 2 if res.engine in (2, 11) else 1  # engine 2: K1 + SpMV; PCG: Q1 + Q2
     info = {"engine": res.engine, "graph_launches": res.graph_launches, "ok": bool(ok),
             "kernel_launches": steps * per_step + (res.graph_launches - g0),
             "status": res.status, "iterations_run": res.iterations,
@@ -360,6 +361,40 @@ def time_iterations(pb, torch, A, pc_d, warmup: int, steps: int, options=None):
     solver.close()
     del b, x0, x_true
     return ms, info
+
+
+def pcg_comparison(pb, torch, A, pc_d, args, peak, pipecg_ms):
+    """The paper's baseline algorithm on the same device and matrix: classic
+    PCG (solvers.py:195-273, engine 4: two kernels per iteration, the same
+    on-device control) timed exactly like the PIPECG line, plus its
+    time-to-solution at the recipe tolerance."""
+    N, nnz = A.n_rows, A.nnz
+    ms, info = time_iterations(pb, torch, A, pc_d, args.warmup, args.steps,
+                               pb.DeviceOptions(engine="pcg"))
+    t = ms / 1e3 / args.steps
+    rp = 8 if nnz >= 2**31 else 4
+    kb = 12 * 8 * N + 12 * nnz + rp * (N + 1)
+    x_true = torch.full((N,), 1.0 / math.sqrt(N), dtype=torch.float64, device="cuda")
+    b = pb.spmv(A, x_true)
+    u0 = pb.jacobi_apply(pb.JacobiPreconditioner(pc_d), b)
+    tol = 1e-8 * math.sqrt(pb.dot(u0, u0, mode="tree"))
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=20000)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    x, rep = pb.pcg_solve(A, b, torch.zeros_like(b), pb.JacobiPreconditioner(pc_d), cfg)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    return {"algorithm": "classic PCG (solvers.py:195-273) on the device, 2 kernels per iteration "
+                         "(pcg_q1_kernel: p update + SpMV + (s,p); pcg_q2_kernel: x, r, u + (u,r), (u,u))",
+            "ms_per_iter": t * 1e3, "iters_per_s": 1 / t, "pipecg_ms_per_iter": pipecg_ms,
+            "pipecg_speedup_per_iteration": (t * 1e3) / pipecg_ms,
+            "bytes_per_iteration": kb,
+            "bytes_formula": "12 vector streams x 8N + CSR (Q1: p, u read, p, s written; "
+                             "Q2: x, p, r, s, dinv read, x, r, u written)",
+            "achieved_gbs": kb / t / 1e9, "frac": kb / t / 1e9 / peak,
+            "gpu_launches": info["kernel_launches"], "timing_ok": info["ok"],
+            "time_to_solution": {"iterations": rep.iterations, "converged": rep.converged,
+                                 "seconds": dt, "verify_inf_err": float((x - x_true).abs().max())}}
 
 
 def time_to_solution(pb, torch, A, pc_d):
@@ -697,6 +732,11 @@ def run_b200(args):
         torch.cuda.empty_cache()
         A = problem_device(pb, torch, kind, n)
         line["time_to_solution"] = time_to_solution(pb, torch, A, pc_d)
+    if not args.no_pcg:
+        try:
+            line["pcg_comparison"] = pcg_comparison(pb, torch, A, pc_d, args, peak, ms / args.steps)
+        except Exception as e:  # report, do not hide
+            line["pcg_comparison"] = {"error": repr(e)}
     del A
     torch.cuda.empty_cache()
     if not args.no_north_star:

@@ -2313,6 +2313,202 @@ __global__ void __launch_bounds__(kGRows, MB) pipecg_fused_kernel_g(GParams P, i
   }
 }
 
+// ===========================================================================
+// Engine 4: classic PCG (solvers.py:195-273) on the device
+// ===========================================================================
+// Two kernels per iteration -- PCG's two global reductions are a chain
+// (delta = (s, p) needs s = A p of the updated p; alpha = gamma / delta
+// gates the update), which is what PIPECG removes:
+//   Q1(it): prologue -- (u, r) and (u, u) of iteration it-1 from Q2's
+//           partials, the gamma guard of it-1, history, the stop test,
+//           beta = gamma / gamma_prev -- then per row
+//             p_new = p * beta + u        (np.multiply(p, beta, out=p); p += u)
+//             s_i   = sum_k a_ik p_new_k  (CSR order; p_new of the neighbours
+//                                          formed on the fly from p_old, u)
+//           and the (s, p_new) partial;
+//   Q2(it): delta from Q1's partials, the delta guard, alpha = gamma / delta,
+//           x += alpha p, r -= alpha s, u = dinv r, and the (u, r), (u, u)
+//           partials.
+// Same control block, history ring, breakdown precedence, CUDA-graph chunks
+// and stop-without-host-sync as the PIPECG engines.
+template <typename RP>
+struct QParams {
+  long long n;
+  const RP* rp;
+  const int* col;
+  const double* val;
+  const double* dinv;
+  double *x, *r, *u, *s;
+  double* p[2];        // ping-pong: Q1(it) reads p[it&1], writes p[(it+1)&1]
+  Ctrl* C;
+  double* hist;
+  ReduceIn rin;        // what this kernel's prologue reduces
+  double* pout;        // this kernel's block partials [2][grid][4]
+  double* fin;         // their fixed-order sum [2][4] (last block), or null
+  unsigned* counter;   // [2]
+};
+
+template <int NT>
+__device__ __forceinline__ void reduce_partials(const ReduceIn& R, long long it_src, int lt,
+                                                double* red, double (&v)[3]) {
+  const double* P = R.pin + (size_t)(it_src & 1) * (size_t)R.n_pin * 4;
+  v[0] = v[1] = v[2] = 0.0;
+  for (int j = lt; j < R.n_pin; j += NT) {
+    v[0] = add(v[0], __ldcg(P + j * 4 + 0));
+    v[1] = add(v[1], __ldcg(P + j * 4 + 1));
+    v[2] = add(v[2], __ldcg(P + j * 4 + 2));
+  }
+  group_sum<3, NT>(v, lt, red, 1);
+}
+
+template <typename RP>
+__global__ void __launch_bounds__(256) pcg_q1_kernel(QParams<RP> P, int step) {
+  __shared__ double red[3 * 8 + 1];
+  __shared__ long long s_it;
+  Ctrl* C = P.C;
+  const int tid = threadIdx.x;
+  pdl_trigger();
+  pdl_wait();
+  const long long it = cta_iteration(C, step, &s_it);
+  if (it < 0) return;
+  const bool leader = blockIdx.x == 0 && tid == 0;
+  double gamma, norm, gamma_prev = 0.0;
+  if (it == 0) {
+    gamma = C->init.gamma;
+    norm = C->init.norm;
+  } else {
+    double v[3];
+    reduce_partials<256>(P.rin, it - 1, tid, red, v);  // Q2(it-1): (u, r), -, (u, u)
+    gamma = v[0];
+    norm = sqrt(v[2]);
+    gamma_prev = __ldcg(&C->slot[(it - 1) & 1].gamma);
+    if (gamma < 0.0 || !isfinite(gamma)) {  // solvers.py:256-257 (iteration it-1)
+      if (leader) {
+        C->bd_code = PCG_BD_GAMMA;
+        C->bd_it = it - 1;
+        C->bd_val = gamma;
+        C->status = PCG_BREAKDOWN;
+      }
+      return;
+    }
+    if (leader) P.hist[it & (kHistRing - 1)] = norm;
+  }
+  if (!(norm >= C->tol && it < C->max_it)) {  // solvers.py:241 loop condition
+    if (leader) {
+      C->final_it = it;
+      C->final_norm = norm;
+      C->status = PCG_STOPPED;
+    }
+    return;
+  }
+  const double beta = it == 0 ? 0.0 : gamma / gamma_prev;  // solvers.py:242
+  if (leader) C->slot[it & 1] = Slot{gamma, 0.0, 0.0, norm};
+  const double* p_old = P.p[it & 1];
+  double* p_new = P.p[(it + 1) & 1];
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (long long i = blockIdx.x * 256LL + tid; i < P.n; i += (long long)gridDim.x * 256) {
+    const long long lo = P.rp[i], hi = P.rp[i + 1];
+    double si = 0.0;
+    for (long long k = lo; k < hi; ++k) {  // kernels.py:64-70 on p_new
+      const int c = ldg_nc(P.col + k);
+      const double pc = add(mul(ldg_nc(p_old + c), beta), ldg_nc(P.u + c));
+      si = add(si, mul(ldg_nc(P.val + k), pc));
+    }
+    const double pi = add(mul(p_old[i], beta), P.u[i]);
+    p_new[i] = pi;
+    P.s[i] = si;
+    acc[0] = add(acc[0], mul(si, pi));  // delta = dot(s, p)
+  }
+  publish_partials<256>(acc, tid, red, 1, P.pout, P.fin, P.counter, it);
+}
+
+template <typename RP>
+__global__ void __launch_bounds__(256) pcg_q2_kernel(QParams<RP> P, int step) {
+  __shared__ double red[3 * 8 + 1];
+  __shared__ long long s_it;
+  Ctrl* C = P.C;
+  const int tid = threadIdx.x;
+  pdl_trigger();
+  pdl_wait();
+  const long long it = cta_iteration(C, step, &s_it);
+  if (it < 0) return;
+  double v[3];
+  reduce_partials<256>(P.rin, it, tid, red, v);  // Q1(it): (s, p)
+  const double delta = v[0];
+  if (delta <= 0.0 || !isfinite(delta)) {  // solvers.py:247-248
+    if (blockIdx.x == 0 && tid == 0) {
+      C->bd_code = PCG_BD_DELTA;
+      C->bd_it = it;
+      C->bd_val = delta;
+      C->status = PCG_BREAKDOWN;
+    }
+    return;
+  }
+  const double alpha = __ldcg(&C->slot[it & 1].gamma) / delta;  // solvers.py:249
+  const double* p = P.p[(it + 1) & 1];
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (long long i = blockIdx.x * 256LL + tid; i < P.n; i += (long long)gridDim.x * 256) {
+    P.x[i] = add(P.x[i], mul(alpha, p[i]));  // x += alpha * p
+    const double ri = sub(P.r[i], mul(alpha, P.s[i]));  // r -= alpha * s
+    const double ui = mul(P.dinv[i], ri);  // jacobi_apply(pc, r, out=u)
+    P.r[i] = ri;
+    P.u[i] = ui;
+    acc[0] = add(acc[0], mul(ui, ri));  // gamma = dot(u, r)
+    acc[2] = add(acc[2], mul(ui, ui));  // norm = sqrt(dot(u, u))
+  }
+  publish_partials<256>(acc, tid, red, 1, P.pout, P.fin, P.counter, it);
+}
+
+// sequential-dot mode: the reference's left-to-right dots replace the
+// partials (one partial).  which = 1 (after Q1): (s, p_new); which = 2
+// (after Q2): (u, r) and (u, u).  p_new is picked by the iteration's parity.
+__global__ void __launch_bounds__(32) pcg_seq_dots_kernel(const Ctrl* C, int step, int which,
+                                                           long long n, const double* s,
+                                                           const double* p0, const double* p1,
+                                                           const double* r, const double* u,
+                                                           double* seqbuf) {
+  constexpr int CH = 256;
+  __shared__ double prod[2][CH];
+  const long long it = cta_iteration(C, step);
+  if (it < 0) return;
+  const double* p = ((it + 1) & 1) ? p1 : p0;
+  double acc[2] = {0.0, 0.0};
+  const int lane = threadIdx.x;
+  for (long long base = 0; base < n; base += CH) {
+#pragma unroll
+    for (int j = 0; j < CH / 32; ++j) {
+      const long long i = base + j * 32 + lane;
+      double v0 = 0.0, v1 = 0.0;
+      if (i < n) {
+        if (which == 1) {
+          v0 = mul(s[i], p[i]);
+        } else {
+          v0 = mul(u[i], r[i]);
+          v1 = mul(u[i], u[i]);
+        }
+      }
+      prod[0][j * 32 + lane] = v0;
+      prod[1][j * 32 + lane] = v1;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const int cnt = (int)((n - base) < CH ? (n - base) : CH);
+      for (int j = 0; j < cnt; ++j) {
+        acc[0] = add(acc[0], prod[0][j]);
+        acc[1] = add(acc[1], prod[1][j]);
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    double* out = seqbuf + (size_t)(it & 1) * 4;
+    out[0] = acc[0];
+    out[1] = 0.0;
+    out[2] = acc[1];
+    out[3] = 0.0;
+  }
+}
+
 // SELL-order (position) <-> natural-order (row) copies of a vector
 __global__ void __launch_bounds__(256) gather_perm_kernel(long long n, const int* __restrict__ perm,
                                                           const double* __restrict__ src,
@@ -2757,6 +2953,8 @@ constexpr int kVariants = 7;  // A B C D P (= C in one persistent launch per chu
 constexpr long long kPersistMaxRows = 8LL << 20;  // P is a candidate up to this size
 // opt.engine request / result code of engine 3 (fused-g, irregular rows)
 constexpr int kReqG = 3 + kVariants;
+// ... of engine 4 (classic PCG, solvers.py:195-273)
+constexpr int kReqPCG = kReqG + 1;
 
 // a SELL-C-sigma copy of the matrix (rows sorted by length inside windows of
 // sigma rows, 32-row slices, column-major inside a slice; rows longer than
@@ -2858,8 +3056,10 @@ struct pcg_solver {
   double* hval = nullptr;
   double* dinvp = nullptr;         // inv_diag in SELL order (every init)
   double* natbuf = nullptr;        // solver_state: natural-order copies (engine 3)
+  double* qbuf = nullptr;          // engine 4: partials [2][2][grid][4] | fin [2][2][4] | seq [2][2][4]
+  unsigned* qcnt = nullptr;        // engine 4: last-block tickets [2][2]
   int g_batch = 2;                 // engine 3 SELL nonzeros per lane per load batch (2 or 4)
-  bool e2_pol = false;             // engine 2: L2 hints (streams evict-first, m evict-last)
+  bool e2_pol = true;              // engine 2: L2 hints (streams evict-first, m evict-last; -2% at 2^22)
   int g_mb = 4;                    // engine 3 CTAs per SM the kernel is compiled for (4 or 6)
   bool g_pf = false;               // engine 3 update operands loaded before the row's SpMV
   int* tile_row = nullptr;         // variant D/E tiles of the applied plan
@@ -3610,6 +3810,55 @@ void launch_g(pcg_solver* S, int k, const Record& R) {
   launch_k(kern, (unsigned)S->grid, kGRows, 0, S->stream, S->pdl, P, k);
 }
 
+// engine 4 (classic PCG): Q1 (p update + s = A p + (s,p)) and Q2 (x, r, u +
+// (u,r), (u,u)) per iteration; their partial buffers live in S->qbuf
+template <typename RP>
+void launch_q(pcg_solver* S, int k, const Record& R) {
+  const size_t G = (size_t)S->grid;
+  double* part[2] = {S->qbuf, S->qbuf + 2 * G * 4};
+  double* fin[2] = {S->qbuf + 4 * G * 4, S->qbuf + 4 * G * 4 + 8};
+  double* seq[2] = {S->qbuf + 4 * G * 4 + 16, S->qbuf + 4 * G * 4 + 24};
+  const bool seq_mode = S->opt.dot_mode == PCG_DOT_SEQ, fin_mode = S->grid > kFinGrid;
+  auto rin = [&](int j) {  // what kernel Q(j+1) reduces: the other kernel's output
+    ReduceIn r;
+    r.arrive = nullptr;
+    r.arrive_per_it = 0;
+    r.pin = seq_mode ? seq[j] : fin_mode ? fin[j] : part[j];
+    r.n_pin = seq_mode || fin_mode ? 1 : S->grid;
+    return r;
+  };
+  QParams<RP> P;
+  P.n = S->A.n_rows;
+  P.rp = static_cast<const RP*>(S->A.rowptr);
+  P.col = S->A.col;
+  P.val = S->A.val;
+  P.dinv = S->A.inv_diag;
+  P.x = S->x;
+  P.r = S->r;
+  P.u = S->u;
+  P.s = S->s;
+  P.p[0] = S->p;
+  P.p[1] = S->q;
+  P.C = R.C;
+  P.hist = R.hist;
+  cudaStream_t st = S->stream;
+  // Q1(it) reduces Q2(it-1)'s output (slot 1); Q2(it) reduces Q1(it)'s (slot 0)
+  P.rin = rin(1);
+  P.pout = part[0];
+  P.fin = fin[0];
+  P.counter = fin_mode ? S->qcnt : nullptr;
+  launch_k(pcg_q1_kernel<RP>, (unsigned)S->grid, 256, 0, st, S->pdl, P, k);
+  if (seq_mode)
+    pcg_seq_dots_kernel<<<1, 32, 0, st>>>(R.C, k, 1, P.n, S->s, S->p, S->q, S->r, S->u, seq[0]);
+  P.rin = rin(0);
+  P.pout = part[1];
+  P.fin = fin[1];
+  P.counter = fin_mode ? S->qcnt + 2 : nullptr;
+  launch_k(pcg_q2_kernel<RP>, (unsigned)S->grid, 256, 0, st, S->pdl && !seq_mode, P, k);
+  if (seq_mode)
+    pcg_seq_dots_kernel<<<1, 32, 0, st>>>(R.C, k, 2, P.n, S->s, S->p, S->q, S->r, S->u, seq[1]);
+}
+
 // enqueue graph step k (drift? -> iteration -> seq dots? -> exchange / SpMV)
 int enqueue_step(pcg_solver* S, int k) {
   Record R = record_at(S->rec_dev);
@@ -3632,6 +3881,10 @@ int enqueue_step(pcg_solver* S, int k) {
     else launch_fused<int>(S, k);
   } else if (S->engine == 3) {
     launch_g(S, k, R);
+  } else if (S->engine == 4) {
+    if (S->A.rp64) launch_q<long long>(S, k, R);
+    else launch_q<int>(S, k, R);
+    return PCG_OK;
   } else {
     TwoParams P;
     P.n = n;
@@ -3825,7 +4078,10 @@ int auto_chunk(pcg_solver* S) {
 
 void fill_result(pcg_solver* S, const Ctrl& c, pcg_result* res) {
   res->status = c.status;
-  res->engine = S->engine == 1 ? 3 + S->variant : S->engine == 3 ? kReqG : 2;
+  res->engine = S->engine == 1   ? 3 + S->variant
+                : S->engine == 3 ? kReqG
+                : S->engine == 4 ? kReqPCG
+                                 : 2;
   for (int k = 0; k < 9; ++k) res->tune_ms[k] = S->tune_ms[k];
   res->pattern_flags = S->pat.n_pat == 0 ? 0
                        : 1 | (S->n_runs > 0 ? 2 : 0) | (S->dinv_by_code ? 4 : 0) |
@@ -3912,6 +4168,8 @@ int preload_solver() {
   PCG_LOAD((pipecg_fused_kernel_g<2, 6, false>)); PCG_LOAD((pipecg_fused_kernel_g<4, 6, false>));
   PCG_LOAD(gather_perm_kernel); PCG_LOAD(scatter_perm_kernel); PCG_LOAD(iperm_kernel);
   PCG_LOAD(renumber_kernel); PCG_LOAD(hub_pack_kernel);
+  PCG_LOAD(pcg_q1_kernel<int>); PCG_LOAD(pcg_q1_kernel<long long>); PCG_LOAD(pcg_q2_kernel<int>);
+  PCG_LOAD(pcg_q2_kernel<long long>); PCG_LOAD(pcg_seq_dots_kernel);
   PCG_LOAD(iter_exchange_kernel); PCG_LOAD(vec_exchange_kernel);
   PCG_LOAD(init_dots_exchange_kernel); PCG_LOAD(snapshot_arrive_kernel); PCG_LOAD(xwait_kernel);
   PCG_LOAD(tile_span_kernel<int>); PCG_LOAD(tile_span_kernel<long long>); PCG_LOAD(max_row_kernel);
@@ -4361,7 +4619,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   // engine: 0 auto (autotuned), 1 fused (heuristic variant), 2 two-kernel,
   // 3..9 fused variant A/B/C/D/P/E/F
   const int req = S->opt.engine;
-  if (req < 0 || req > kReqG) {
+  if (req < 0 || req > kReqPCG) {
     pipecg_b200_solver_destroy(S);
     return set_error(PCG_EINVAL, "solver_create: unknown engine");
   }
@@ -4369,6 +4627,21 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   S->irregular = has_long;
   phase("stream+max_row");
   bool fused_ok = false;
+  if (req == kReqPCG) {  // classic PCG: CSR kernels only, nothing to plan or tune
+    S->engine = 4;
+    S->grid = S->n_partials = std::min<int>(kDotGrid, 4 * S->num_sms);
+    rc = alloc_state(S);
+    if (!rc && (pool_malloc(&S->qbuf, ((size_t)4 * S->grid * 4 + 32) * sizeof(double)) != cudaSuccess ||
+                pool_malloc(&S->qcnt, 4 * sizeof(unsigned)) != cudaSuccess))
+      rc = set_error(PCG_ENOMEM, "pcg workspace");
+    if (rc) {
+      pipecg_b200_solver_destroy(S);
+      return rc;
+    }
+    cudaMemsetAsync(S->qcnt, 0, 4 * sizeof(unsigned), S->stream);
+    *out = S;
+    return cuda_status(cudaStreamSynchronize(S->stream), "pcg workspace");
+  }
   if (req == 0 || req == 1 || req == 8 || req == 9) {
     // lossless row-pattern dictionary (variants E/F); none for irregular
     // matrices or when the rows are too diverse (patterns.cu)
@@ -4596,6 +4869,8 @@ int pipecg_b200_solver_destroy(pcg_solver* S) {
   pool_free(S->hval);
   pool_free(S->dinvp);
   pool_free(S->natbuf);
+  pool_free(S->qbuf);
+  pool_free(S->qcnt);
   pool_free(S->gchunk_part);
   pool_free(S->gchunk_ticket);
   for (Sell* c : {&S->sell2, &S->gsell}) {
@@ -4865,6 +5140,19 @@ int pipecg_b200_solver_init(pcg_solver* S, const double* b, const double* x0, do
   if (rc) return rc;
   rc = pipecg_b200_jacobi_apply(n, S->A.inv_diag, S->r, S->u, st);  // u = M^-1 r
   if (rc) return rc;
+  if (S->engine == 4) {  // classic PCG (solvers.py:223-231): p = 0, gamma, norm, b_norm
+    cudaMemsetAsync(S->p, 0, bytes, st);
+    cudaMemsetAsync(S->qcnt, 0, 4 * sizeof(unsigned), st);
+    const double* qa[4] = {S->r, S->u, S->u, S->b};
+    const double* qb[4] = {S->u, S->u, S->u, S->b};
+    rc = dots_any(n, 4, qa, qb, S->opt.dot_mode, S->dots4, S->dots_ws, st);
+    if (rc) return rc;
+    init_ctrl_kernel<<<1, 256, 0, st>>>(R.C, S->dots4, 1, tolerance, max_iterations,
+                                        drift_check_interval, R.hist, R.dit, nullptr);
+    S->host_base = 0;
+    S->initialized = true;
+    return cuda_status(cudaGetLastError(), "solver_init");
+  }
   if (S->connected) {  // u halo (w = A u reads it)
     vec_exchange_kernel<<<kXchgBlocks, 256, 0, st>>>(S->cp, 6, S->u);
     S->xtarget += (unsigned long long)S->world * kXchgBlocks;

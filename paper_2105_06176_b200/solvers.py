@@ -193,7 +193,7 @@ class DeviceOptions:
     def native(self) -> _lib.PcgOptions:
         eng = {"auto": 0, "fused": 1, "two": 2, "fused-a": 3, "fused-b": 4,
                "fused-c": 5, "fused-d": 6, "fused-p": 7, "fused-e": 8,
-               "fused-f": 9, "fused-g": 10}[self.engine]
+               "fused-f": 9, "fused-g": 10, "pcg": 11}[self.engine]
         dm = {"tree": _lib.PCG_DOT_TREE, "seq": _lib.PCG_DOT_SEQ}[self.dot_mode]
         return _lib.PcgOptions(dm, eng, int(self.chunk), 1 if self.use_graphs else 0,
                                int(self.max_sms))
@@ -487,61 +487,57 @@ def true_residual_norm(A, x, b) -> float:
 
 def pcg_solve(A, b, x0, pc, cfg: SolverConfig | None = None, *,
               options: DeviceOptions | None = None):
-    """Classic PCG (solvers.py:195-273) composed from the device operators.
+    """Classic PCG (solvers.py:195-273) on the device.
 
-    The reference's baseline algorithm; each
-    iteration synchronises once for its dot products.  ``options.dot_mode``
-    as in :func:`pipecg_solve`: "tree" (default) or "seq" (the reference's
-    order: bitwise-identical history)."""
+    The reference's baseline algorithm, run like
+    :func:`pipecg_solve`: the whole loop on the GPU (csrc/solver.cu engine 4:
+    two kernels per iteration -- p update + SpMV + (s, p), then x / r / u
+    updates + (u, r), (u, u) -- on-device stop test and breakdown checks,
+    CUDA-graph chunks, no per-iteration host synchronisation).  Same
+    contract: convergence when sqrt((u, u)) < cfg.tolerance at the top of an
+    iteration, ``history`` of iterations + 1 norms, drift every k
+    iterations, :class:`SolverBreakdown` ("delta" / "gamma").
+    ``options.dot_mode``: "tree" (default) or "seq" (the reference's order:
+    bitwise-identical history and x)."""
     cfg = cfg or SolverConfig()
     mode = (options or DeviceOptions()).dot_mode
     t_start = time.perf_counter()
     _check_system(A, b, x0)
+    n = int(A.n_rows)
     on_dev = is_device_tensor(b)
+    if n == 0:
+        x = torch.zeros(0, dtype=torch.float64, device="cuda") if on_dev else np.zeros(0)
+        return x, SolveReport(converged=0.0 < cfg.tolerance, iterations=0, final_norm=0.0,
+                              strategy="pcg", history=[0.0] if cfg.record_history else None,
+                              phase_times={"setup": 0.0, "iterations": 0.0},
+                              drift_history=[] if cfg.drift_check_interval > 0 else None)
     require_cuda()
-    bd = to_device_f64(b)
-    x = to_device_f64(x0).clone()
-    r = residual(A, x, bd)
-    u = jacobi_apply(pc, r)
-    p = torch.zeros_like(u)
-    s = torch.empty_like(u)
-    gamma = dot(r, u, mode)
-    gamma_prev = 0.0
-    norm = math.sqrt(dot(u, u, mode))
-    b_norm = norm2(bd, mode)
-    history = [norm] if cfg.record_history else None
-    drift = [] if cfg.drift_check_interval > 0 else None
-    t_setup = time.perf_counter()
-    it = 0
-    while norm >= cfg.tolerance and it < cfg.max_iterations:
-        beta = 0.0 if it == 0 else gamma / gamma_prev
-        p.mul_(beta)  # np.multiply(p, beta, out=p)
-        p.add_(u)
-        spmv(A, p, out=s)
-        delta = dot(s, p, mode)
-        if delta <= 0.0 or not math.isfinite(delta):
-            raise SolverBreakdown("delta", it, delta)
-        alpha = gamma / delta
-        x.add_(alpha * p)
-        r.sub_(alpha * s)
-        jacobi_apply(pc, r, out=u)
-        gamma_prev = gamma
-        gamma, uu = dots([(u, r), (u, u)], mode=mode)
-        if gamma < 0.0 or not math.isfinite(gamma):
-            raise SolverBreakdown("gamma", it, gamma)
-        norm = math.sqrt(uu)
-        it += 1
-        if history is not None:
-            history.append(norm)
-        if drift is not None and it % cfg.drift_check_interval == 0:
-            resid = residual(A, x, bd)
-            dv = norm2(resid - r, mode)
-            drift.append([it, dv / b_norm if b_norm > 0 else dv])
-    t_end = time.perf_counter()
+    solver, cached = _solver_for(A, pc, DeviceOptions(dot_mode=mode, engine="pcg"))
+    try:
+        bd, x0d = to_device_f64(b), to_device_f64(x0)
+        solver.init(bd, x0d, cfg.tolerance, cfg.max_iterations, cfg.drift_check_interval)
+        torch.cuda.ExternalStream(solver.stream).synchronize()
+        t_setup = time.perf_counter()
+        res, hist, d_it, d_val = solver.run(cfg.record_history, cfg.max_iterations,
+                                            cfg.drift_check_interval)
+        t_end = time.perf_counter()
+        if res.status == _lib.PCG_BREAKDOWN:
+            raise SolverBreakdown(_lib.BREAKDOWN_QUANTITY[res.breakdown_quantity],
+                                  int(res.breakdown_iteration), float(res.breakdown_value))
+        history = hist[: res.n_history].tolist() if hist is not None else None
+        drift = None
+        if cfg.drift_check_interval > 0:
+            drift = [[int(d_it[k]), float(d_val[k])] for k in range(res.n_drift)]
+        x = solver.x_tensor() if on_dev else solver.x_host()
+    finally:
+        solver.lock.release()
+        if not cached:
+            solver.close()
     report = SolveReport(
-        converged=norm < cfg.tolerance, iterations=it, final_norm=norm, strategy="pcg",
-        history=history, phase_times={"setup": t_setup - t_start, "iterations": t_end - t_setup},
+        converged=bool(res.converged), iterations=int(res.iterations),
+        final_norm=float(res.final_norm), strategy="pcg", history=history,
+        phase_times={"setup": t_setup - t_start, "iterations": t_end - t_setup},
         drift_history=drift,
     )
-    return (x if on_dev else x.cpu().numpy()), report
+    return x, report
 

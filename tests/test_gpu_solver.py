@@ -380,3 +380,67 @@ def test_pcg_solve_tree_vs_oracle_and_pipecg(cuda, kind, n):
     _, rp = pb.pipecg_solve(A, b, x0, pb.JacobiPreconditioner(d), cfg)
     h1, h2 = np.array(rep.history[:20]), np.array(rp.history[:20])
     assert np.max(np.abs(h1 - h2) / h1) <= 1e-6
+
+
+def _pcg_cases():
+    from test_gpu_irregular import _random_spd
+    return {
+        "3d7-20": lambda: pb.stencil_host("3d7", 20),
+        "2d5-64": lambda: pb.stencil_host("2d5", 64),
+        "powerlaw-12": lambda: pb.generate_powerlaw(2 ** 12),
+        "ragged": lambda: _random_spd(3001, 20, seed=3),
+    }
+
+
+@pytest.mark.parametrize("case", ["3d7-20", "2d5-64", "powerlaw-12", "ragged"])
+def test_pcg_device_seq_bitwise_vs_oracle(cuda, case):
+    """Device PCG (engine 4: two kernels per iteration, on-device stop test,
+    graph chunks) in seq-dot mode is the reference's PCG bit for bit: the
+    whole history, the iteration count and x (oracle.pcg_solve restates
+    solvers.py:195-273)."""
+    A = _pcg_cases()[case]()
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    ref = oracle.pcg_solve(A, b, x0, d, tol=tol, max_iterations=5000)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=5000, record_history=True)
+    x, rep = pb.pcg_solve(A, b, x0, pb.JacobiPreconditioner(d), cfg,
+                          options=pb.DeviceOptions(dot_mode="seq"))
+    assert rep.strategy == "pcg" and rep.converged == ref.converged
+    assert rep.iterations == ref.iterations
+    assert rep.history == ref.history
+    np.testing.assert_array_equal(x, ref.x)
+
+
+@pytest.mark.parametrize("max_it", [1, 2, 7, 64, 65])
+def test_pcg_device_budget_and_chunks(cuda, max_it):
+    """max_iterations across CUDA-graph chunk boundaries: exactly max_it
+    iterations, history of max_it + 1 norms, identical prefix."""
+    A = pb.stencil_host("3d7", 16)
+    _, b, x0, d = oracle.manufactured(A)
+    ref = oracle.pcg_solve(A, b, x0, d, tol=1e-300, max_iterations=max_it)
+    cfg = pb.SolverConfig(tolerance=1e-300, max_iterations=max_it, record_history=True)
+    x, rep = pb.pcg_solve(A, b, x0, pb.JacobiPreconditioner(d), cfg,
+                          options=pb.DeviceOptions(dot_mode="seq"))
+    assert rep.iterations == max_it and not rep.converged
+    assert rep.history == ref.history
+    np.testing.assert_array_equal(x, ref.x)
+
+
+def test_pcg_device_breakdown_matches_oracle(cuda):
+    """An indefinite matrix: PCG's delta <= 0 guard (solvers.py:247-248)
+    fires at the oracle's iteration with the oracle's value."""
+    g = load_golden("solve_indefinite.npz")
+    A = golden_matrix(g)
+    b, x0, d = g["b"], g["x0"], g["inv_diag"]
+    ref = oracle.pcg_solve(A, b, x0, d, tol=1e-8, max_iterations=50)
+    cfg = pb.SolverConfig(tolerance=1e-8, max_iterations=50)
+    if ref.breakdown is None:
+        x, rep = pb.pcg_solve(A, b, x0, pb.JacobiPreconditioner(d), cfg,
+                              options=pb.DeviceOptions(dot_mode="seq"))
+        assert rep.iterations == ref.iterations
+        return
+    with pytest.raises(pb.SolverBreakdown) as exc:
+        pb.pcg_solve(A, b, x0, pb.JacobiPreconditioner(d), cfg,
+                     options=pb.DeviceOptions(dot_mode="seq"))
+    assert (exc.value.quantity, exc.value.iteration) == ref.breakdown[:2]
+    assert exc.value.value == ref.breakdown[2]

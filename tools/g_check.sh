@@ -8,7 +8,7 @@ if [ "${G_TESTS:-1}" = 1 ]; then
 timeout 900 python -m pytest tests/test_gpu_irregular.py tests/test_gpu_config_scale.py tests/test_gpu_edge.py -q -m gpu -k "irregular or powerlaw or fused_g or sell or hub or edge" > $OUT/g_tests.txt 2>&1
 echo "tests rc=$?" >> $OUT/g_tests.txt; tail -5 $OUT/g_tests.txt
 fi
-B="python bench.py --config ${G_CONFIG:-powerlaw-22} --no-north-star --no-e2e --no-cpu --no-tts --steps 200 --warmup 10"
+B="python bench.py --config ${G_CONFIG:-powerlaw-22} --no-north-star --no-e2e --no-cpu --no-tts --no-pcg --steps 200 --warmup 10"
 one() {  # tag engine env-list
   local tag=$1 eng=$2 envs=$3
   env $(echo "$envs" | tr ',' ' ') timeout 300 $B --engine $eng > $OUT/g_bench_$tag.json 2>/dev/null

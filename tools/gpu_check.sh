@@ -26,7 +26,7 @@ for job in "$@"; do
                      fused-e|fused-f) kre='regex:pipecg_fused_kernel_s';;
                      fused-g) kre='regex:pipecg_fused_kernel_g';;
                      *) kre='regex:pipecg_';; esac
-      common="python bench.py --config $cfg --engine $eng --no-north-star --no-e2e --no-cpu --no-tts"
+      common="python bench.py --config $cfg --engine $eng --no-north-star --no-e2e --no-cpu --no-tts --no-pcg"
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
          --log-file $OUT/launches_${cfg}_${eng}.csv $common --steps 20 --warmup 3 > $OUT/ncu_launch_${cfg}_${eng}.json 2>&1
       echo "ncu launches $cfg $eng rc=$?"
