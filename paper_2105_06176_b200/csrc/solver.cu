@@ -942,11 +942,13 @@ template <int TR>
 struct FusedLayoutS {
   static constexpr int kVecBytes = TR * 8;
   static constexpr int kHeader = 1024;
-  // F+WIN: 7 vectors | w_old | dinv | codes | m windows
+  // F+WIN: w_old | dinv | codes | m windows (the 7 streamed vectors are
+  //        loaded by the consumers themselves: a smaller stage -> more
+  //        stages -> more window bytes in flight)
   // E+WIN: 7 vectors | w_old windows | code windows
   // gathers: 7 vectors | codes
   __host__ __device__ static int stage_bytes(bool mg, bool win, int elems, int celems) {
-    if (win && mg) return 9 * kVecBytes + TR + elems * 8;
+    if (win && mg) return 2 * kVecBytes + TR + elems * 8;
     if (win) return 7 * kVecBytes + elems * 8 + celems;
     return 7 * kVecBytes + TR;
   }
@@ -997,6 +999,10 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
   const int SB = L::stage_bytes(MG, WIN, W.elems, W.celems);
   const int S = P.stages;
   const bool dbc = W.dinv_by_code != 0;
+  // DV (F with windows): the consumers load the 7 streamed vectors; the
+  // stage holds w_old | dinv | codes | m windows
+  constexpr bool DV = MG && WIN;
+  constexpr int OFF_W = DV ? 0 : 7 * VB, OFF_D = DV ? VB : 8 * VB, OFF_C = DV ? 2 * VB : 9 * VB;
 
   Ctrl* C = P.C;
   const int tid = threadIdx.x;
@@ -1015,7 +1021,21 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
   // the dictionary is constant: load it before waiting on the previous grid
   for (int k = tid; k <= P.n_pat; k += blockDim.x) pst[k] = P.pstart[k];
   for (int k = tid; k < P.n_pat; k += blockDim.x) pdv[k] = dbc ? P.pdinv[k] : 0.0;
-  for (int k = tid; k < P.n_pat_e; k += blockDim.x) {
+  // DV (F with windows): entries as one 16-byte record {value, window
+  // index} in the space of pix | pcx | pva -- one shared load per nonzero
+  // instead of two
+  struct PEnt {
+    double v;
+    int ix, pad;
+  };
+  PEnt* pent = reinterpret_cast<PEnt*>(pix);
+  if (DV) {
+    for (int k = tid; k < P.n_pat_e; k += blockDim.x) {
+      const int w = P.pwin[k];
+      pent[k] = PEnt{P.pval[k], W.base[w] + P.poff[k] - W.lo[w], 0};
+    }
+  }
+  for (int k = tid; k < P.n_pat_e && !DV; k += blockDim.x) {
     if (WIN) {
       const int w = P.pwin[k];
       pix[k] = W.base[w] + P.poff[k] - W.lo[w];
@@ -1054,7 +1074,7 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
     const uint32_t b_vec = (uint32_t)((rows * 8 + 15) / 16 * 16);
     const uint32_t b_code = (uint32_t)((rows + 15) / 16 * 16);
     unsigned char* sb = stage0 + (size_t)s * SB;
-    uint32_t tx = (skip_x ? 6 : 7) * b_vec;
+    uint32_t tx = DV ? 0 : (skip_x ? 6 : 7) * b_vec;
     if (WIN && MG) {
       tx += b_vec + (dbc ? 0 : b_vec) + b_code;
       for (int w = 0; w < W.n; ++w)
@@ -1071,12 +1091,14 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
       tx += b_code;
     }
     mbar_arrive_expect_tx(&full[s], tx);
+    if (!DV) {
 #pragma unroll
-    for (int k = 0; k < 7; ++k)
-      if (k != 4 || !skip_x) bulk_g2s(sb + k * VB, P.vec[k] + t0, b_vec, &full[s], pol);
+      for (int k = 0; k < 7; ++k)
+        if (k != 4 || !skip_x) bulk_g2s(sb + k * VB, P.vec[k] + t0, b_vec, &full[s], pol);
+    }
     if (WIN && MG) {
-      if (!dbc) bulk_g2s_nohint(sb + 8 * VB, P.dinv + t0, b_vec, &full[s]);
-      bulk_g2s_nohint(sb + 9 * VB, P.pcode + t0, b_code, &full[s]);
+      if (!dbc) bulk_g2s_nohint(sb + OFF_D, P.dinv + t0, b_vec, &full[s]);
+      bulk_g2s_nohint(sb + OFF_C, P.pcode + t0, b_code, &full[s]);
     } else if (WIN) {
       unsigned char* carea = sb + 7 * VB + (size_t)W.elems * 8;
       for (int w = 0; w < W.n; ++w)
@@ -1096,10 +1118,10 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
     const long long t0 = (t_lo + j * t_step) * TR;
     const long long rows = min((long long)TR, P.n - t0);
     unsigned char* sb = stage0 + (size_t)s * SB;
-    unsigned char* area = sb + (MG ? 9 * VB + TR : 7 * VB);
+    unsigned char* area = sb + (MG ? OFF_C + TR : 7 * VB);
     const unsigned char* src = reinterpret_cast<const unsigned char*>(MG ? m_src : w_src);
     if (MG && part != 1)
-      bulk_g2s_nohint(sb + 7 * VB, w_src + t0, (uint32_t)((rows * 8 + 15) / 16 * 16), &full[s]);
+      bulk_g2s_nohint(sb + OFF_W, w_src + t0, (uint32_t)((rows * 8 + 15) / 16 * 16), &full[s]);
     for (int w = 0; w < W.n; ++w) {
       const bool halo = XG && t0 + W.lo[w] + W.len[w] > P.n;
       if (((msk >> w) & 1) && (part == 2 || halo == (part == 1)))
@@ -1214,6 +1236,13 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
       wi = ldg_nc(w_old + i);
       di = ldg_nc(P.dinv + i);
     }
+    // DV: this row's streamed vectors, in flight while the stage lands (a
+    // one-tile register look-ahead measured 3% slower at 27-pt)
+    double dv[7];
+    if (DV && lt < rows) {
+#pragma unroll
+      for (int k = 0; k < 7; ++k) dv[k] = (k == 4 && skip_x) ? 0.0 : ld_stream(P.vec[k] + i);
+    }
     // the tile's send range, loaded now so its latency hides under the tile
     // (loaded after the tile it stalled every tile: +0.085 ms per iteration
     // for 2 virtual ranks at 256^3)
@@ -1226,12 +1255,15 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
     if (lt < rows) {
       double nacc = 0.0;
       if (WIN && MG) {
-        const double* win = reinterpret_cast<const double*>(sb + 9 * VB + TR);
-        const int code = sb[9 * VB + lt];
-        wi = v_s[7 * TR + lt];
-        di = dbc ? pdv[code] : v_s[8 * TR + lt];
+        const double* win = reinterpret_cast<const double*>(sb + OFF_C + TR);
+        const int code = sb[OFF_C + lt];
+        wi = v_s[OFF_W / 8 + lt];
+        di = dbc ? pdv[code] : v_s[OFF_D / 8 + lt];
         const int lo = pst[code], hi = pst[code + 1];
-        for (int k = lo; k < hi; ++k) nacc = add(nacc, mul(pva[k], win[pix[k] + lt]));
+        for (int k = lo; k < hi; ++k) {
+          const PEnt e = pent[k];
+          nacc = add(nacc, mul(e.v, win[e.ix + lt]));
+        }
       } else if (WIN) {
         const double* win = reinterpret_cast<const double*>(sb + 7 * VB);
         const unsigned char* cwin = sb + 7 * VB + (size_t)W.elems * 8;
@@ -1278,19 +1310,19 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
             if (k0 + t < hi) nacc = add(nacc, mul(av[t], mv[t]));
         }
       }
+      auto vec = [&](int k) { return DV ? dv[k] : v_s[k * TR + lt]; };
       const double mi = mul(di, wi);
-      const double zi = add(nacc, mul(beta, v_s[0 * TR + lt]));
-      const double qi = add(mi, mul(beta, v_s[1 * TR + lt]));
-      const double si = add(wi, mul(beta, v_s[2 * TR + lt]));
-      const double ui = v_s[6 * TR + lt];
-      const double p_old = v_s[3 * TR + lt];
+      const double zi = add(nacc, mul(beta, vec(0)));
+      const double qi = add(mi, mul(beta, vec(1)));
+      const double si = add(wi, mul(beta, vec(2)));
+      const double ui = vec(6);
+      const double p_old = vec(3);
       const double pi = add(ui, mul(beta, p_old));
       // (deferred x: odd iterations first apply iteration it-1's update)
       const double xi = skip_x ? 0.0
-                        : add(P.defer_x ? add(v_s[4 * TR + lt], mul(alpha_prev, p_old))
-                                        : v_s[4 * TR + lt],
+                        : add(P.defer_x ? add(vec(4), mul(alpha_prev, p_old)) : vec(4),
                               mul(alpha, pi));
-      const double ri = sub(v_s[5 * TR + lt], mul(alpha, si));
+      const double ri = sub(vec(5), mul(alpha, si));
       const double un = sub(ui, mul(alpha, qi));
       const double wn = sub(wi, mul(alpha, zi));
       st_stream(P.vec[0] + i, zi);
@@ -3400,7 +3432,8 @@ int plan_one_s(pcg_solver* S, int bps, FusedPlan* out) {
                      (size_t)round_up(pat_smem_bytes(S->pat.n_pat, S->pat.n_entries), 128);
   const size_t sm_budget = 228 * 1024, cta_max = 227 * 1024;
   const char* e_st = getenv("PIPECG_B200_STAGES");
-  for (int st = e_st ? atoi(e_st) : 3; st >= 2; --st) {
+  // F stages no longer carry the streamed vectors: up to 4 fit at 2 CTAs/SM
+  for (int st = e_st ? atoi(e_st) : (MG && win ? 4 : 3); st >= 2; --st) {
     const size_t need = hdr + st * sb;
     if (need <= cta_max && (need + 1024) * bps <= sm_budget) {
       p.stages = st;
