@@ -1047,102 +1047,117 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
   }
   pdl_wait();
 
-  // ---- producer ------------------------------------------------------------
-  // range [a, a + len) of an array of `esz`-byte elements, clamped to [0, lim)
-  auto range_copy = [&](unsigned char* dst, const unsigned char* src, long long a, int len,
-                        long long lim, int esz, uint64_t* bar, bool count_only) -> uint32_t {
-    const long long b = a + len;
-    const long long ca = a < 0 ? 0 : a, cb = b > lim ? lim : b;
-    if (cb <= ca) return 0;
-    const uint32_t bytes = (uint32_t)((cb - ca) * esz);
-    if (!count_only) bulk_g2s_nohint(dst + (ca - a) * esz, src + ca * esz, bytes, bar);
-    return bytes;
-  };
-  uint64_t pol = 0;
-  // static part: expect the whole stage; copy what does not depend on the
-  // iteration (vectors, codes / code windows, F's dinv rows)
+  // ---- producer (warp 0: the copies of a tile are spread over its lanes) --
+  // One thread issuing a tile's ~12-20 bulk copies (address math, clamps,
+  // masks) was the kernel's critical path; each lane now describes and
+  // issues at most two of them.  Copy c of tile j:
+  //   0-6  the streamed vectors (not with DV)     static
+  //   7    F's dinv rows (dinv not by code)       static
+  //   8    the tile's codes (F with windows, or no windows)  static
+  //   9    F's w_old rows                         written this iteration
+  //   10.. value windows (w_old for E, m_old for F): this iteration's own
+  //        rows, or -- distributed -- rows reaching into the halo (the peers')
+  //   10 + kMaxWin.. E's code windows            static
+  // category bits: 1 static, 2 own rows of this iteration, 4 halo rows.
   // msk: the runs the tile's rows use -- distributed only (a shard's halo
-  // runs are used by its boundary tiles alone); P.tile_runs is loaded
-  // ahead: a global load in front of each tile's copies stalled the
-  // producer (measured 0.366 -> 0.460 ms at 256^3).  On one GPU every run
-  // is copied (costs less than the mask bookkeeping, measured)
-  // skip_x: x is neither read nor written this iteration (deferred update)
-  auto issue_static = [&](long long j, unsigned msk, bool skip_x) {
+  // runs are used by its boundary tiles alone); on one GPU every run is
+  // copied.  skip_x: x is neither read nor written this iteration.
+  constexpr int kCopies = 10 + 2 * kMaxWin;
+  const int lane = tid & 31;
+  uint64_t pol = 0;
+  struct Cp {
+    unsigned char* dst;
+    const unsigned char* src;
+    uint32_t bytes;
+    int cat;
+    bool hint;
+  };
+  auto copy_desc = [&](int c, long long j, unsigned msk, bool skip_x, const double* w_src,
+                       const double* m_src) -> Cp {
+    Cp d{nullptr, nullptr, 0u, 0, false};
+    if (c >= kCopies) return d;
     const int s = (int)(j % S);
     const long long t0 = (t_lo + j * t_step) * TR;
     const long long rows = min((long long)TR, P.n - t0);
     const uint32_t b_vec = (uint32_t)((rows * 8 + 15) / 16 * 16);
     const uint32_t b_code = (uint32_t)((rows + 15) / 16 * 16);
     unsigned char* sb = stage0 + (size_t)s * SB;
-    uint32_t tx = DV ? 0 : (skip_x ? 6 : 7) * b_vec;
-    if (WIN && MG) {
-      tx += b_vec + (dbc ? 0 : b_vec) + b_code;
-      for (int w = 0; w < W.n; ++w)
-        if ((msk >> w) & 1)
-          tx += range_copy(nullptr, nullptr, t0 + W.lo[w], W.len[w], W.ld, 8, nullptr, true);
-    } else if (WIN) {
-      for (int w = 0; w < W.n; ++w) {
-        if ((msk >> w) & 1)
-          tx += range_copy(nullptr, nullptr, t0 + W.lo[w], W.len[w], W.ld, 8, nullptr, true);
-        if (!W.dinv_uniform || w == W.w0)
-          tx += range_copy(nullptr, nullptr, t0 + W.clo[w], W.clen[w], W.code_ld, 1, nullptr, true);
+    // range [a, a + len) of an array of `esz`-byte elements, clamped to [0, lim)
+    auto range = [&](unsigned char* dst, const void* src, long long a, int len, long long lim,
+                     int esz, int cat) {
+      const long long e = a + len;
+      const long long ca = a < 0 ? 0 : a, ce = e > lim ? lim : e;
+      if (ce > ca) {
+        d.dst = dst + (ca - a) * esz;
+        d.src = static_cast<const unsigned char*>(src) + ca * esz;
+        d.bytes = (uint32_t)((ce - ca) * esz);
+        d.cat = cat;
+      }
+    };
+    if (c < 7) {
+      if (!DV && (c != 4 || !skip_x)) {
+        d = Cp{sb + c * VB, reinterpret_cast<const unsigned char*>(P.vec[c] + t0), b_vec, 1, true};
+      }
+    } else if (c == 7) {
+      if (WIN && MG && !dbc)
+        d = Cp{sb + OFF_D, reinterpret_cast<const unsigned char*>(P.dinv + t0), b_vec, 1, false};
+    } else if (c == 8) {
+      if (!WIN || MG) d = Cp{sb + (WIN ? OFF_C : 7 * VB), P.pcode + t0, b_code, 1, false};
+    } else if (c == 9) {
+      if (WIN && MG)
+        d = Cp{sb + OFF_W, reinterpret_cast<const unsigned char*>(w_src + t0), b_vec, 2, false};
+    } else if (c < 10 + kMaxWin) {
+      const int w = c - 10;
+      if (WIN && w < W.n && ((msk >> w) & 1)) {
+        const bool halo = XG && t0 + W.lo[w] + W.len[w] > P.n;
+        range(sb + (MG ? OFF_C + TR : 7 * VB) + (size_t)W.base[w] * 8, MG ? m_src : w_src,
+              t0 + W.lo[w], W.len[w], W.ld, 8, halo ? 4 : 2);
       }
     } else {
-      tx += b_code;
+      const int w = c - 10 - kMaxWin;
+      if (WIN && !MG && w < W.n && (!W.dinv_uniform || w == W.w0))
+        range(sb + 7 * VB + (size_t)W.elems * 8 + W.cbase[w], P.pcode, t0 + W.clo[w], W.clen[w],
+              W.code_ld, 1, 1);
     }
-    mbar_arrive_expect_tx(&full[s], tx);
-    if (!DV) {
-#pragma unroll
-      for (int k = 0; k < 7; ++k)
-        if (k != 4 || !skip_x) bulk_g2s(sb + k * VB, P.vec[k] + t0, b_vec, &full[s], pol);
-    }
-    if (WIN && MG) {
-      if (!dbc) bulk_g2s_nohint(sb + OFF_D, P.dinv + t0, b_vec, &full[s]);
-      bulk_g2s_nohint(sb + OFF_C, P.pcode + t0, b_code, &full[s]);
-    } else if (WIN) {
-      unsigned char* carea = sb + 7 * VB + (size_t)W.elems * 8;
-      for (int w = 0; w < W.n; ++w)
-        if (!W.dinv_uniform || w == W.w0)
-          range_copy(carea + W.cbase[w], P.pcode, t0 + W.clo[w], W.clen[w], W.code_ld, 1, &full[s],
-                   false);
-    } else {
-      bulk_g2s_nohint(sb + 7 * VB, P.pcode + t0, b_code, &full[s]);
-    }
+    return d;
   };
-  // iteration part: F: w_old rows + m_old windows; E: w_old windows.
-  // part 0: what this rank wrote itself (own rows), 1: windows reaching
-  // into the halo (written by the peers; distributed only), 2: both
-  auto issue_dyn = [&](long long j, const double* w_src, const double* m_src, int part,
-                       unsigned msk) {
+  // warp 0 issues tile j's copies of categories `cats`; with `expect`, lane 0
+  // first arms the stage's barrier with ALL of the tile's bytes
+  auto produce = [&](long long j, unsigned msk, bool skip_x, const double* w_src,
+                     const double* m_src, int cats, bool expect) {
     const int s = (int)(j % S);
-    const long long t0 = (t_lo + j * t_step) * TR;
-    const long long rows = min((long long)TR, P.n - t0);
-    unsigned char* sb = stage0 + (size_t)s * SB;
-    unsigned char* area = sb + (MG ? OFF_C + TR : 7 * VB);
-    const unsigned char* src = reinterpret_cast<const unsigned char*>(MG ? m_src : w_src);
-    if (MG && part != 1)
-      bulk_g2s_nohint(sb + OFF_W, w_src + t0, (uint32_t)((rows * 8 + 15) / 16 * 16), &full[s]);
-    for (int w = 0; w < W.n; ++w) {
-      const bool halo = XG && t0 + W.lo[w] + W.len[w] > P.n;
-      if (((msk >> w) & 1) && (part == 2 || halo == (part == 1)))
-        range_copy(area + (size_t)W.base[w] * 8, src, t0 + W.lo[w], W.len[w], W.ld, 8, &full[s],
-                   false);
+    Cp cp[2] = {copy_desc(lane, j, msk, skip_x, w_src, m_src),
+                copy_desc(lane + 32, j, msk, skip_x, w_src, m_src)};
+    if (expect) {
+      const uint32_t tx = __reduce_add_sync(0xffffffffu, cp[0].bytes + cp[1].bytes);
+      if (lane == 0) mbar_arrive_expect_tx(&full[s], tx);
+      __syncwarp();
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (cp[q].bytes && (cp[q].cat & cats)) {
+        if (cp[q].hint) bulk_g2s(cp[q].dst, cp[q].src, cp[q].bytes, &full[s], pol);
+        else bulk_g2s_nohint(cp[q].dst, cp[q].src, cp[q].bytes, &full[s]);
+      }
     }
   };
   // Deferred x (defer_x): x_{it+1} = x_it + alpha_it p_it only feeds the
   // result, so even iterations skip it and odd iterations apply both
   // updates in order, x = (x + alpha_{it-1} p_{it-1}) + alpha_it p_it (p_{it-1}
   // is the staged p_old) -- the reference's roundings, one x read + write
-  // saved every other iteration.  The kernel whose prologue stops the solve
-  // applies a pending update.  The producer reads the iteration itself so
+  // saved every other iteration.  The producer reads the iteration itself so
   // the first stages know whether to copy x.
-  if (tid == 0) {
+  if (producer) {
     pol = policy_evict_first();
     const long long it0 = read_status(C) == PCG_RUNNING ? C->base_it + step : -1;
     const bool skip0 = P.defer_x && it0 >= 0 && (it0 & 1) == 0;
-    for (long long j = 0; j < my_tiles && j < S; ++j)  // the masks first: one latency
-      s_msk[j] = XG && WIN ? tile_mask(P.tile_runs, t_lo + j * t_step) : ~0u;
-    for (long long j = 0; j < my_tiles && j < S; ++j) issue_static(j, XG ? s_msk[j] : ~0u, skip0);
+    for (long long j = 0; j < my_tiles && j < S; ++j) {  // the masks first: one latency
+      const unsigned m = XG && WIN ? tile_mask(P.tile_runs, t_lo + j * t_step) : ~0u;
+      if (lane == 0) s_msk[j] = m;
+    }
+    __syncwarp();
+    for (long long j = 0; j < my_tiles && j < S; ++j)
+      produce(j, s_msk[j], skip0, nullptr, nullptr, 1, true);
   }
   if (tid == 32) *s_it = read_status(C) == PCG_RUNNING ? C->base_it + step : -1;
   __syncthreads();
@@ -1151,16 +1166,16 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
   const long long par = it < 0 ? 0 : it;
   const double* w_old = P.w[par & 1];
   const double* m_old = P.m[par & 1];
-  // completes the first stages (before the prologue on one GPU; after it
-  // -- the peers' halo rows have arrived -- when distributed)
-  auto issue_first_dyn = [&](int part) {
-    if (WIN && tid == 0)
+  // completes the first stages (before the prologue on one GPU; the halo
+  // part after it -- the peers' halo rows have arrived -- when distributed)
+  auto produce_first = [&](int cats) {
+    if (producer)
       for (long long j = 0; j < my_tiles && j < S; ++j)
-        issue_dyn(j, w_old, m_old, part, XG ? s_msk[j] : ~0u);
+        produce(j, s_msk[j], skip_x, w_old, m_old, cats, false);
   };
-  issue_first_dyn(XG ? 0 : 2);
+  produce_first(XG ? 2 : 6);
   if (it < 0) {
-    if (XG) issue_first_dyn(1);  // (stale data, never read: lets the stages complete)
+    if (XG) produce_first(4);  // (stale data, never read: lets the stages complete)
     if (tid == 0)
       for (long long j = 0; j < my_tiles && j < S; ++j) mbar_wait(&full[j], 0);
     return;
@@ -1177,9 +1192,9 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
     }
   }
   __syncthreads();
-  if (XG && WIN && tid == 0)  // peers' halo stores (acquired in the prologue) before TMA reads
+  if (XG && WIN && producer)  // peers' halo stores (acquired in the prologue) before TMA reads
     asm volatile("fence.proxy.async.global;" ::: "memory");
-  if (XG) issue_first_dyn(1);
+  if (XG) produce_first(4);
   if (!*decision) {
     if (tid == 0)
       for (long long j = 0; j < my_tiles && j < S; ++j) mbar_wait(&full[j], 0);
@@ -1192,31 +1207,28 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
   }
   const double alpha = sc[0], beta = sc[1], alpha_prev = sc[2];
   if (producer) {
-    if (tid == 0) {
-      unsigned nmsk = XG && WIN && S < my_tiles ? tile_mask(P.tile_runs, t_lo + S * t_step) : ~0u;
-      for (long long j = S; j < my_tiles; ++j) {
-        const unsigned msk = nmsk;
-        if (XG && WIN && j + 1 < my_tiles)  // in flight while the stage drains
-          nmsk = tile_mask(P.tile_runs, t_lo + (j + 1) * t_step);
-        if (P.l2_prefetch && j + P.l2_prefetch < my_tiles) {
-          // HBM -> L2 for a tile that is loaded l2_prefetch stages from now:
-          // more bytes in flight than the shared-memory ring holds
-          const long long tp = (t_lo + (j + P.l2_prefetch) * t_step) * TR;
-          const uint32_t bp = (uint32_t)((min((long long)TR, P.n - tp) * 8 + 15) / 16 * 16);
+    unsigned nmsk = XG && WIN && S < my_tiles ? tile_mask(P.tile_runs, t_lo + S * t_step) : ~0u;
+    for (long long j = S; j < my_tiles; ++j) {
+      const unsigned msk = nmsk;
+      if (XG && WIN && j + 1 < my_tiles)  // in flight while the stage drains
+        nmsk = tile_mask(P.tile_runs, t_lo + (j + 1) * t_step);
+      if (P.l2_prefetch && lane == 0 && j + P.l2_prefetch < my_tiles) {
+        // HBM -> L2 for a tile that is loaded l2_prefetch stages from now:
+        // more bytes in flight than the shared-memory ring holds
+        const long long tp = (t_lo + (j + P.l2_prefetch) * t_step) * TR;
+        const uint32_t bp = (uint32_t)((min((long long)TR, P.n - tp) * 8 + 15) / 16 * 16);
 #pragma unroll
-          for (int k = 0; k < 7; ++k) l2_prefetch_bulk(P.vec[k] + tp, bp);
-          if (MG) l2_prefetch_bulk(w_old + tp, bp);
-          if (WIN) {  // the leading run: the only window not yet in L2
-            const int w = W.n - 1;
-            const long long a = tp + W.lo[w], b = min(a + W.len[w], W.ld);
-            if (b > a && a >= 0)
-              l2_prefetch_bulk((MG ? m_old : w_old) + a, (uint32_t)((b - a) * 8));
-          }
+        for (int k = 0; k < 7; ++k) l2_prefetch_bulk(P.vec[k] + tp, bp);
+        if (MG) l2_prefetch_bulk(w_old + tp, bp);
+        if (WIN) {  // the leading run: the only window not yet in L2
+          const int w = W.n - 1;
+          const long long a = tp + W.lo[w], e = min(a + W.len[w], W.ld);
+          if (e > a && a >= 0)
+            l2_prefetch_bulk((MG ? m_old : w_old) + a, (uint32_t)((e - a) * 8));
         }
-        mbar_wait(&empty[j % S], (uint32_t)((j / S - 1) & 1));
-        issue_static(j, msk, skip_x);
-        if (WIN) issue_dyn(j, w_old, m_old, 2, msk);
       }
+      mbar_wait(&empty[j % S], (uint32_t)((j / S - 1) & 1));
+      produce(j, msk, skip_x, w_old, m_old, 7, true);
     }
     return;
   }
