@@ -58,7 +58,11 @@ def run_virtual(world, make_problem, cfg, chunk=0, engine="fused"):
                                                  (3, "3d27", 20, "fused-c"), (2, "3d7", 30, "fused-d"),
                                                  (2, "3d7", 40, "fused-e"), (3, "3d7", 33, "fused-f"),
                                                  (2, "2d5", 200, "fused-e"), (4, "3d7", 36, "fused-e"),
-                                                 (3, "3d27", 20, "fused-f")])
+                                                 (3, "3d27", 20, "fused-f"),
+                                                 # world = kMaxRanks (solver.cu): the comm-block
+                                                 # slot layout and arrival counts at their limit
+                                                 (8, "3d7", 48, "fused-e"), (8, "3d7", 40, "fused-a"),
+                                                 (8, "3d27", 24, "fused-f"), (8, "3d7", 40, "fused-c")])
 def test_virtual_ranks_match_single_gpu(cuda, world, kind, n, engine):
     A = oracle.stencil(kind, n)
     x_true, b, x0, d = oracle.manufactured(A)
@@ -247,4 +251,29 @@ def test_pipecg_solve_devices_custom_preconditioner(cuda):
     ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=20000)
     x, rep = pb.pipecg_solve(A, b, x0, pb.JacobiPreconditioner(d), cfg, devices=[0, 0, 0])
     assert abs(rep.iterations - ref.iterations) <= 1
+    assert np.max(np.abs(x - ref.x)) / np.max(np.abs(ref.x)) <= 1e-8
+
+
+def test_virtual_ranks_config5_shaped(cuda):
+    """BASELINE configs[4] in miniature: the 7-pt Poisson matrix sharded 8
+    ways with every shard generated on the device from its own row block
+    (shard_stencil -> pipecg_b200_stencil_fill; the 1.5B-row case cannot
+    exist on the host), solved to the recipe tolerance; iterations, history
+    and x against the single-matrix oracle."""
+    kind, n, world = "3d7", 56, 8
+    A = oracle.stencil(kind, n)
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=20000, record_history=True)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=20000)
+    out = run_virtual(world, lambda g: D.shard_stencil(kind, n, g), cfg)
+    plans = [o[2] for o in out]
+    assert sum(p.n_local for p in plans) == n ** 3
+    assert all(p.cuts == plans[0].cuts for p in plans) and len(plans[0].cuts) == world + 1
+    x = np.concatenate([o[0] for o in out])
+    reps = [o[1] for o in out]
+    assert len({r.iterations for r in reps}) == 1
+    assert all(r.history == reps[0].history for r in reps)
+    assert abs(reps[0].iterations - ref.iterations) <= 1
+    assert oracle.history_gap(reps[0].history, ref.history) <= 1e-10
     assert np.max(np.abs(x - ref.x)) / np.max(np.abs(ref.x)) <= 1e-8
