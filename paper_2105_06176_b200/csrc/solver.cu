@@ -86,6 +86,8 @@ struct Ctrl {
   unsigned long long diag_target;  // value waited for
   int x_final;                     // deferred x: pending update applied after the stop
   int pad_;
+  unsigned long long darrive_base;  // distributed drift: x-halo pushes before this solve
+  unsigned long long dsum_base;     // ... and drift partials before this solve
 };
 static_assert(sizeof(Ctrl) <= 256, "Ctrl must fit its 256-byte record slot");
 
@@ -285,11 +287,13 @@ __device__ Step prologue(Ctrl* C, double* hist, const ReduceIn& R, long long it,
 }
 
 // Distributed comm buffer layout (identical on every rank, IPC-exported):
-//   [0] u64 arrive, [8] u64 xarrive, [256] slots[2][kMaxRanks][4],
-//   [768] islots[kMaxRanks][4]  (see the exchange section below)
-constexpr size_t kCommBytes = 1024;
+//   [0] u64 arrive, [8] u64 xarrive, [16] u64 darrive, [24] u64 dsum,
+//   [256] slots[2][kMaxRanks][4], [768] islots[kMaxRanks][4],
+//   [1024] dslots[2][kMaxRanks]  (see the exchange section below)
+constexpr size_t kCommBytes = 2048;
 constexpr size_t kCommSlots = 256;
 constexpr size_t kCommISlots = 768;
+constexpr size_t kCommDSlots = 1024;
 
 // Peer-memory exchange fused into the iteration kernel (distributed mode,
 // fused variants A/C/D): after a tile's rows are final the CTA stores the
@@ -2648,16 +2652,41 @@ __global__ void __launch_bounds__(256) drift_partial_kernel(const Ctrl* C, int s
                                                              const double* __restrict__ b,
                                                              const double* __restrict__ r,
                                                              double* __restrict__ dpart,
-                                                             const int* __restrict__ ip) {
+                                                             const int* __restrict__ ip,
+                                                             const double* xh0, const double* xh1,
+                                                             const unsigned long long* darrive,
+                                                             unsigned long long per_sample) {
+  // xh0 / xh1 (distributed): halo columns (>= n) of x for sample parity 0 / 1
+  // (see drift_push_kernel), read L2-coherently after the peers' pushes of
+  // this sample have been acquired
   __shared__ double red[8];
+  __shared__ int ok;
   const long long it = cta_iteration(C, step);
   if (it < 0) return;
   if (it < 1 || C->drift_k <= 0 || it % C->drift_k != 0) return;
+  const double* xhs = nullptr;
+  if (xh0) {
+    const long long smp = it / C->drift_k;
+    if (threadIdx.x == 0) {
+      Ctrl* Cw = const_cast<Ctrl*>(C);
+      ok = spin_until(darrive, C->darrive_base + (unsigned long long)smp * per_sample, Cw, 3) ? 1 : 0;
+      if (!ok) {  // a peer stalled: stop the solve with the exchange error
+        Cw->bd_it = it;
+        Cw->status = PCG_ECOMM_STATUS;
+      }
+    }
+    __syncthreads();
+    if (!ok) return;
+    xhs = (smp & 1) ? xh1 : xh0;
+  }
   double v[1] = {0.0};
   for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
     double acc = 0.0;
-    for (long long k = rp[i]; k < rp[i + 1]; ++k)
-      acc = add(acc, mul(val[k], x[ip ? ip[col[k]] : col[k]]));
+    for (long long k = rp[i]; k < rp[i + 1]; ++k) {
+      const int c = col[k];
+      const double xc = ip ? x[ip[c]] : (xhs && c >= n ? __ldcg(xhs + c) : x[c]);
+      acc = add(acc, mul(val[k], xc));
+    }
     const double e = sub(sub(b[i], acc), r[ip ? ip[i] : i]);
     v[0] = add(v[0], mul(e, e));
   }
@@ -2839,8 +2868,90 @@ __global__ void init_dots_exchange_kernel(CommParams CP, const double* dots4) {
 // arrivals for this solve until this rank's first setup push): snapshot the
 // iteration-arrival counter as this solve's base.
 __global__ void snapshot_arrive_kernel(Ctrl* C, const char* comm) {
+  if (threadIdx.x == 0) {
+    const volatile unsigned long long* c = reinterpret_cast<const volatile unsigned long long*>(comm);
+    C->arrive_base = c[0];
+    C->darrive_base = c[2];
+    C->dsum_base = c[3];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Drift samples on a row-sharded solve (solvers.py:190-192,371-372):
+// ||(b - A x) - r|| / ||b|| at entry of iteration it (it % k == 0), every
+// rank's rows.  Sample s = it / k:
+//   drift_push_kernel:   this rank's boundary rows of x -> the peers' halo
+//                        of a spare vector (n for even s, b for odd s: the
+//                        halo part of both is otherwise unused), then
+//                        signal darrive on every rank;
+//   drift_partial_kernel (ip = nullptr, xh = that spare vector): waits for
+//                        every peer's push of sample s, sums e_i^2 over the
+//                        own rows with halo columns read from xh;
+//   drift_dist_finish_kernel: this rank's sum -> dslots[s&1][rank] of every
+//                        rank, signal dsum, wait for all ranks, sum the
+//                        slots in rank order (the same number on every rank).
+// Double-buffering by s parity: a rank at most one iteration ahead cannot
+// overwrite what a slower rank still reads.
+__device__ __forceinline__ bool drift_step(const Ctrl* C, long long it) {
+  return it >= 1 && C->drift_k > 0 && it % C->drift_k == 0;
+}
+
+__global__ void __launch_bounds__(256) drift_push_kernel(CommParams CP, const Ctrl* C, int step,
+                                                         const double* x) {
+  const long long it = cta_iteration(C, step);
+  if (it < 0 || !drift_step(C, it)) return;
+  const int vec = ((it / C->drift_k) & 1) ? 11 : 10;  // b or n of the peer's block
+  for (long long e = blockIdx.x * 256LL + threadIdx.x; e < CP.n_send; e += (long long)gridDim.x * 256) {
+    const int q = CP.send_peer[e];
+    double* dst = reinterpret_cast<double*>(CP.peer_vbuf[q]) + (size_t)vec * CP.peer_ld[q];
+    dst[CP.send_dst[e]] = x[CP.send_row[e]];
+  }
+  __threadfence_system();
+  __syncthreads();
   if (threadIdx.x == 0)
-    C->arrive_base = *reinterpret_cast<const volatile unsigned long long*>(comm);
+    for (int q = 0; q < CP.world; ++q)
+      atomicAdd_system(reinterpret_cast<unsigned long long*>(CP.peer_comm[q] + 16), 1ull);
+}
+
+__global__ void __launch_bounds__(256) drift_dist_finish_kernel(CommParams CP, Ctrl* C, int step,
+                                                                const double* dpart, int count,
+                                                                double* dval, long long* dit,
+                                                                char* comm) {
+  __shared__ double red[8];
+  __shared__ int ok;
+  const long long it = cta_iteration(C, step);
+  if (it < 0 || !drift_step(C, it)) return;
+  const long long smp = it / C->drift_k;
+  double v[1] = {0.0};
+  for (int j = threadIdx.x; j < count; j += 256) v[0] = add(v[0], dpart[j]);
+  group_sum<1, 256>(v, threadIdx.x, red, 1);
+  if (threadIdx.x < CP.world) {
+    double* slot = reinterpret_cast<double*>(CP.peer_comm[threadIdx.x] + kCommDSlots) +
+                   (size_t)(smp & 1) * kMaxRanks + CP.rank;
+    *slot = v[0];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < CP.world; ++q)
+      atomicAdd_system(reinterpret_cast<unsigned long long*>(CP.peer_comm[q] + 24), 1ull);
+    ok = spin_until(reinterpret_cast<const unsigned long long*>(comm + 24),
+                    C->dsum_base + (unsigned long long)smp * CP.world, C, 3);
+    if (!ok) {  // a peer stalled: stop the solve with the exchange error
+      C->bd_it = it;
+      C->status = PCG_ECOMM_STATUS;
+    }
+    if (ok) {
+      const volatile double* ds =
+          reinterpret_cast<const volatile double*>(comm + kCommDSlots) + (size_t)(smp & 1) * kMaxRanks;
+      double sum = 0.0;
+      for (int q = 0; q < CP.world; ++q) sum = add(sum, ds[q]);  // rank order
+      const double nn = sqrt(sum);
+      const double bn = C->b_norm;
+      dval[it & (kHistRing - 1)] = bn > 0 ? nn / bn : nn;
+      dit[it & (kHistRing - 1)] = it;
+    }
+  }
 }
 
 // setup: wait until xarrive >= target (sets an error status on timeout)
@@ -3910,16 +4021,28 @@ int enqueue_step(pcg_solver* S, int k) {
   cudaStream_t st = S->stream;
   const long long n = S->A.n_rows;
   if (S->drift_k > 0) {
+    // distributed: x halo of this sample into the spare n / b vectors first
+    const bool dist = S->connected;
+    if (dist) drift_push_kernel<<<kXchgBlocks, 256, 0, st>>>(S->cp, R.C, k, S->x);
+    const double* xh0 = dist ? S->nv : nullptr;
+    const double* xh1 = dist ? S->b : nullptr;
+    const unsigned long long* darr = reinterpret_cast<const unsigned long long*>(S->comm + 16);
+    const unsigned long long per = (unsigned long long)S->world * kXchgBlocks;
+    const int* ip = S->engine == 3 ? S->iperm : nullptr;
     if (S->A.rp64)
       drift_partial_kernel<long long><<<kDotGrid, 256, 0, st>>>(
           R.C, k, n, static_cast<const long long*>(S->A.rowptr), S->A.col, S->A.val, S->x, S->b,
-          S->r, S->dpart, S->engine == 3 ? S->iperm : nullptr);
+          S->r, S->dpart, ip, xh0, xh1, darr, per);
     else
       drift_partial_kernel<int><<<kDotGrid, 256, 0, st>>>(R.C, k, n,
                                                            static_cast<const int*>(S->A.rowptr),
                                                            S->A.col, S->A.val, S->x, S->b, S->r,
-                                                           S->dpart, S->engine == 3 ? S->iperm : nullptr);
-    drift_finish_kernel<<<1, 256, 0, st>>>(R.C, k, S->dpart, kDotGrid, R.dval, R.dit);
+                                                           S->dpart, ip, xh0, xh1, darr, per);
+    if (dist)
+      drift_dist_finish_kernel<<<1, 256, 0, st>>>(S->cp, R.C, k, S->dpart, kDotGrid, R.dval, R.dit,
+                                                  S->comm);
+    else
+      drift_finish_kernel<<<1, 256, 0, st>>>(R.C, k, S->dpart, kDotGrid, R.dval, R.dit);
   }
   if (S->engine == 1) {
     if (S->A.rp64) launch_fused<long long>(S, k);
@@ -4207,6 +4330,7 @@ int preload_solver() {
   PCG_LOAD(gated_spmv_chunks); PCG_LOAD(seq_dots_kernel);
   PCG_LOAD(drift_partial_kernel<int>); PCG_LOAD(drift_partial_kernel<long long>);
   PCG_LOAD(drift_finish_kernel); PCG_LOAD(advance_kernel); PCG_LOAD(init_ctrl_kernel);
+  PCG_LOAD(drift_push_kernel); PCG_LOAD(drift_dist_finish_kernel);
   PCG_LOAD(finalize_x_kernel); PCG_LOAD(finalize_mark_kernel);
   PCG_LOAD((pipecg_fused_kernel_g<4, 3, true>)); PCG_LOAD((pipecg_fused_kernel_g<2, 4, true>));
   PCG_LOAD((pipecg_fused_kernel_g<2, 4, false>)); PCG_LOAD((pipecg_fused_kernel_g<4, 4, false>));
@@ -4269,7 +4393,8 @@ int comm_failed(const Ctrl& c) {
   snprintf(buf, sizeof(buf),
            "distributed exchange timed out (a peer rank stalled): %s wait at iteration %lld saw "
            "%llu of %llu arrivals (arrive_base %llu)",
-           c.diag_where == 1 ? "iteration" : "setup", c.bd_it, c.diag_seen, c.diag_target,
+           c.diag_where == 1 ? "iteration" : c.diag_where == 3 ? "drift" : "setup", c.bd_it,
+           c.diag_seen, c.diag_target,
            c.arrive_base);
   return set_error(PCG_ECOMM, buf);
 }
@@ -5122,8 +5247,6 @@ int pipecg_b200_solver_init(pcg_solver* S, const double* b, const double* x0, do
                             int64_t max_iterations, int64_t drift_check_interval, void* stream) {
   if (!S || !b || !x0) return set_error(PCG_EINVAL, "solver_init: bad arguments");
   if (max_iterations < 1) return set_error(PCG_EINVAL, "solver_init: max_iterations < 1");
-  if (S->connected && drift_check_interval > 0)
-    return set_error(PCG_EINVAL, "solver_init: drift samples are single-GPU only");
   cudaStream_t st = S->stream;
   cudaEventRecord(S->ev_in, (cudaStream_t)stream);
   cudaStreamWaitEvent(st, S->ev_in, 0);

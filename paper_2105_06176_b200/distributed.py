@@ -506,7 +506,8 @@ class DistributedSolver:
         self._opened = []
         self.solver.close()
 
-    def init(self, b_local, x0_local, tolerance: float, max_iterations: int):
+    def init(self, b_local, x0_local, tolerance: float, max_iterations: int,
+             drift_check_interval: int = 0):
         import torch
 
         # every rank's previous GPU work (including exchanges still landing
@@ -514,10 +515,14 @@ class DistributedSolver:
         torch.cuda.current_stream().synchronize()
         self.solver.poll()
         self.group.barrier()
-        self.solver.init(b_local, x0_local, tolerance, max_iterations, 0)
+        self.solver.init(b_local, x0_local, tolerance, max_iterations, drift_check_interval)
 
-    def run(self, record_history: bool, max_iterations: int):
-        return self.solver.run(record_history, max_iterations, 0)
+    def run(self, record_history: bool, max_iterations: int, drift_check_interval: int = 0):
+        """Drift samples (drift_check_interval > 0): every rank's rows, summed
+        over the ranks in rank order in-kernel (csrc/solver.cu
+        drift_push_kernel / drift_dist_finish_kernel): the same values on
+        every rank, solvers.py:190-192,371-372."""
+        return self.solver.run(record_history, max_iterations, drift_check_interval)
 
     @property
     def stream(self) -> int:
@@ -549,12 +554,10 @@ def pipecg_solve_distributed(problem: ShardedProblem, b_local, x0_local, cfg, gr
     from .solvers import SolveReport, SolverBreakdown, SolverConfig
 
     cfg = cfg or SolverConfig()
-    if cfg.drift_check_interval:
-        raise NotImplementedError("drift samples are single-GPU only")
     own = solver is None
     solver = solver or DistributedSolver(problem, group, options)
     t0 = time.perf_counter()
-    solver.init(b_local, x0_local, cfg.tolerance, cfg.max_iterations)
+    solver.init(b_local, x0_local, cfg.tolerance, cfg.max_iterations, cfg.drift_check_interval)
     import torch
 
     # the solver's own stream, not the device: another rank sharing this GPU
@@ -562,7 +565,8 @@ def pipecg_solve_distributed(problem: ShardedProblem, b_local, x0_local, cfg, gr
     # device-wide synchronize would invalidate that capture
     torch.cuda.ExternalStream(solver.stream).synchronize()
     t1 = time.perf_counter()
-    res, hist, _, _ = solver.run(cfg.record_history, cfg.max_iterations)
+    res, hist, d_it, d_val = solver.run(cfg.record_history, cfg.max_iterations,
+                                        cfg.drift_check_interval)
     t2 = time.perf_counter()
     x = solver.x_local()
     if own:
@@ -575,6 +579,8 @@ def pipecg_solve_distributed(problem: ShardedProblem, b_local, x0_local, cfg, gr
         final_norm=float(res.final_norm), strategy="pipecg",
         history=hist[: res.n_history].tolist() if hist is not None else None,
         phase_times={"setup": t1 - t0, "iterations": t2 - t1},
+        drift_history=([[int(d_it[k]), float(d_val[k])] for k in range(res.n_drift)]
+                       if cfg.drift_check_interval > 0 else None),
         partition=problem.plan.summary(),
     )
     return x, rep

@@ -277,3 +277,31 @@ def test_virtual_ranks_config5_shaped(cuda):
     assert abs(reps[0].iterations - ref.iterations) <= 1
     assert oracle.history_gap(reps[0].history, ref.history) <= 1e-10
     assert np.max(np.abs(x - ref.x)) / np.max(np.abs(ref.x)) <= 1e-8
+
+
+@pytest.mark.parametrize("world,engine,k", [(2, "fused-e", 3), (3, "fused-a", 1), (2, "fused-f", 2),
+                                            (4, "fused-c", 5)])
+def test_virtual_ranks_drift_samples(cuda, world, engine, k):
+    """Drift samples on a row-sharded solve (solvers.py:190-192,371-372):
+    every k iterations each rank pushes its boundary rows of x to the peers
+    (double-buffered spare halo), sums ((b - A x) - r)^2 over its rows and
+    the ranks' sums are combined in rank order in-kernel.  Same sample
+    iterations as the oracle, identical values on every rank, the reference
+    test's bound, and close to the oracle's own samples."""
+    kind, n = "3d7", 24
+    A = oracle.stencil(kind, n)
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=20000, record_history=True,
+                          drift_check_interval=k)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=20000, drift_check_interval=k)
+    out = run_virtual(world, lambda g: D.shard_stencil(kind, n, g), cfg, engine=engine)
+    reps = [o[1] for o in out]
+    dh = reps[0].drift_history
+    assert dh and all(r.drift_history == dh for r in reps)
+    assert [it for it, _ in dh] == [it for it, _ in ref.drift_history][: len(dh)]
+    assert abs(len(dh) - len(ref.drift_history)) <= 1
+    bn = float(np.linalg.norm(b))
+    for (it, v), (_, vr) in zip(dh, ref.drift_history):
+        assert v <= 1e-10 * max(1.0, bn)
+        assert abs(v - vr) <= 1e-12 * max(1.0, bn), (it, v, vr)
