@@ -1013,6 +1013,16 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
   const bool producer = tid < 32;
   const long long t_lo = blockIdx.x, t_step = gridDim.x;
   const long long my_tiles = P.n_tiles > t_lo ? (P.n_tiles - t_lo + t_step - 1) / t_step : 0;
+  // XG: every CTA starts in the middle of its tile list (the sweep order
+  // rotated; the tile -> CTA map, hence the partials, unchanged): a
+  // z-slab's first tiles are the ones next to the lower halo, and the first
+  // tile's SpMV runs before the prologue's wait for the peers (see below)
+  const long long rot = XG && my_tiles > 1 ? my_tiles / 2 : 0;
+  auto tile_of = [&](long long j) {
+    long long jj = j + rot;
+    if (jj >= my_tiles) jj -= my_tiles;
+    return t_lo + jj * t_step;
+  };
 
   pdl_trigger();
   if (tid == 0) {
@@ -1081,7 +1091,7 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
     Cp d{nullptr, nullptr, 0u, 0, false};
     if (c >= kCopies) return d;
     const int s = (int)(j % S);
-    const long long t0 = (t_lo + j * t_step) * TR;
+    const long long t0 = tile_of(j) * TR;
     const long long rows = min((long long)TR, P.n - t0);
     const uint32_t b_vec = (uint32_t)((rows * 8 + 15) / 16 * 16);
     const uint32_t b_code = (uint32_t)((rows + 15) / 16 * 16);
@@ -1156,7 +1166,7 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
     const long long it0 = read_status(C) == PCG_RUNNING ? C->base_it + step : -1;
     const bool skip0 = P.defer_x && it0 >= 0 && (it0 & 1) == 0;
     for (long long j = 0; j < my_tiles && j < S; ++j) {  // the masks first: one latency
-      const unsigned m = XG && WIN ? tile_mask(P.tile_runs, t_lo + j * t_step) : ~0u;
+      const unsigned m = XG && WIN ? tile_mask(P.tile_runs, tile_of(j)) : ~0u;
       if (lane == 0) s_msk[j] = m;
     }
     __syncwarp();
@@ -1185,6 +1195,96 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
     return;
   }
   double* w_new = P.w[(it + 1) & 1];
+  const int lt = tid - 32;
+  // n_i = sum_k a_ik m_k (CSR order) of row lt of a landed stage, and the
+  // row's w_old / dinv
+  auto row_spmv = [&](const unsigned char* sb, long long i, double& wi, double& di) -> double {
+    const double* v_s = reinterpret_cast<const double*>(sb);
+    double nacc = 0.0;
+    if (WIN && MG) {
+      const double* win = reinterpret_cast<const double*>(sb + OFF_C + TR);
+      const int code = sb[OFF_C + lt];
+      wi = v_s[OFF_W / 8 + lt];
+      di = dbc ? pdv[code] : v_s[OFF_D / 8 + lt];
+      const int lo = pst[code], hi = pst[code + 1];
+      for (int k = lo; k < hi; ++k) {
+        const PEnt e = pent[k];
+        nacc = add(nacc, mul(e.v, win[e.ix + lt]));
+      }
+    } else if (WIN) {
+      const double* win = reinterpret_cast<const double*>(sb + 7 * VB);
+      const unsigned char* cwin = sb + 7 * VB + (size_t)W.elems * 8;
+      wi = win[W.own + lt];
+      const int code = cwin[W.cown + lt];
+      if (W.dinv_uniform) {  // one dinv for every row: only the own-row code window
+        di = W.dinv0;
+        const int lo = pst[code], hi = pst[code + 1];
+        // a plain loop: batching the loads 8 at a time measured 8% slower
+        // at 256^3 (0.369 vs 0.339 ms, same box) and 15% at 27-pt
+        for (int k = lo; k < hi; ++k)
+          nacc = add(nacc, mul(pva[k], mul(di, win[pix[k] + lt])));  // m = M^-1 w
+      } else {
+        di = pdv[code];
+        const int lo = pst[code], hi = pst[code + 1];
+        for (int k = lo; k < hi; ++k) {
+          const double mc = mul(pdv[cwin[pcx[k] + lt]], win[pix[k] + lt]);  // m = M^-1 w
+          nacc = add(nacc, mul(pva[k], mc));
+        }
+      }
+    } else {
+      // per-nonzero gathers, three explicit phases per batch as in A (wi, di
+      // were loaded by the caller before the stage wait)
+      const int code = sb[7 * VB + lt];
+      const int lo = pst[code], hi = pst[code + 1];
+      const int ii = (int)i;
+      for (int k0 = lo; k0 < hi; k0 += 8) {
+        double av[8], mv[8];
+        int cc[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int k = k0 + t < hi ? k0 + t : lo;
+          cc[t] = ii + pix[k];
+          av[t] = pva[k];
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if (k0 + t < hi) {
+            const int c = cc[t];
+            mv[t] = MG ? ldg_nc(m_old + c) : mul(ldg_nc(P.dinv + c), ldg_nc(w_old + c));
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if (k0 + t < hi) nacc = add(nacc, mul(av[t], mv[t]));
+      }
+    }
+    return nacc;
+  };
+  // PIPECG's overlap (Ghysels-Vanroose): n = A m_old needs no
+  // alpha, so when this CTA's first tile reads no halo rows its SpMV runs
+  // BEFORE the prologue waits for the peers' arrivals -- the rendezvous
+  // overlaps it.  (Distributed only; on one GPU the wait is trivial.)
+  bool pre = false;
+  double pre_n = 0.0, pre_w = 0.0, pre_d = 0.0;
+  double pre_dv[7];
+  if (XG && WIN && !producer && my_tiles > 0) {
+    const long long t0 = tile_of(0) * TR;
+    const unsigned m0 = s_msk[0];
+    bool halo = false;
+    for (int w = 0; w < W.n; ++w)
+      halo = halo || (((m0 >> w) & 1) && t0 + W.lo[w] + W.len[w] > P.n);
+    if (!halo) {
+      pre = true;
+      const long long rows = min((long long)TR, P.n - t0);
+      const long long i = t0 + lt;
+      if (DV && lt < rows) {
+#pragma unroll
+        for (int k = 0; k < 7; ++k) pre_dv[k] = (k == 4 && skip_x) ? 0.0 : ld_stream(P.vec[k] + i);
+      }
+      mbar_wait(&full[0], 0u);
+      if (lt < rows) pre_n = row_spmv(stage0, i, pre_w, pre_d);
+    }
+  }
   if (!producer) {
     const Step stp = prologue<NT>(C, P.hist, P.rin, it, tid - 32, red, 1,
                                   blockIdx.x == 0 && tid == 32);
@@ -1211,15 +1311,15 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
   }
   const double alpha = sc[0], beta = sc[1], alpha_prev = sc[2];
   if (producer) {
-    unsigned nmsk = XG && WIN && S < my_tiles ? tile_mask(P.tile_runs, t_lo + S * t_step) : ~0u;
+    unsigned nmsk = XG && WIN && S < my_tiles ? tile_mask(P.tile_runs, tile_of(S)) : ~0u;
     for (long long j = S; j < my_tiles; ++j) {
       const unsigned msk = nmsk;
       if (XG && WIN && j + 1 < my_tiles)  // in flight while the stage drains
-        nmsk = tile_mask(P.tile_runs, t_lo + (j + 1) * t_step);
+        nmsk = tile_mask(P.tile_runs, tile_of(j + 1));
       if (P.l2_prefetch && lane == 0 && j + P.l2_prefetch < my_tiles) {
         // HBM -> L2 for a tile that is loaded l2_prefetch stages from now:
         // more bytes in flight than the shared-memory ring holds
-        const long long tp = (t_lo + (j + P.l2_prefetch) * t_step) * TR;
+        const long long tp = tile_of(j + P.l2_prefetch) * TR;
         const uint32_t bp = (uint32_t)((min((long long)TR, P.n - tp) * 8 + 15) / 16 * 16);
 #pragma unroll
         for (int k = 0; k < 7; ++k) l2_prefetch_bulk(P.vec[k] + tp, bp);
@@ -1238,15 +1338,15 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
   }
 
   // ---- consumers -----------------------------------------------------------
-  const int lt = tid - 32;
   double acc[3] = {0.0, 0.0, 0.0};
   for (long long j = 0; j < my_tiles; ++j) {
     const int s = (int)(j % S);
-    const long long t0 = (t_lo + j * t_step) * TR;
+    const long long t0 = tile_of(j) * TR;
     const long long rows = min((long long)TR, P.n - t0);
     const unsigned char* sb = stage0 + (size_t)s * SB;
     const double* v_s = reinterpret_cast<const double*>(sb);
     const long long i = t0 + lt;
+    const bool done = pre && j == 0;  // SpMV already run before the prologue
     double wi = 0.0, di = 0.0;
     if (!WIN && lt < rows) {
       wi = ldg_nc(w_old + i);
@@ -1257,7 +1357,8 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
     double dv[7];
     if (DV && lt < rows) {
 #pragma unroll
-      for (int k = 0; k < 7; ++k) dv[k] = (k == 4 && skip_x) ? 0.0 : ld_stream(P.vec[k] + i);
+      for (int k = 0; k < 7; ++k)
+        dv[k] = done ? pre_dv[k] : (k == 4 && skip_x) ? 0.0 : ld_stream(P.vec[k] + i);
     }
     // the tile's send range, loaded now so its latency hides under the tile
     // (loaded after the tile it stalled every tile: +0.085 ms per iteration
@@ -1267,64 +1368,15 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
       xe0 = ldg_nc(P.X.ptr + t0 / TR);
       xe1 = ldg_nc(P.X.ptr + t0 / TR + 1);
     }
-    mbar_wait(&full[s], (uint32_t)((j / S) & 1));
+    if (!done) mbar_wait(&full[s], (uint32_t)((j / S) & 1));
     if (lt < rows) {
-      double nacc = 0.0;
-      if (WIN && MG) {
-        const double* win = reinterpret_cast<const double*>(sb + OFF_C + TR);
-        const int code = sb[OFF_C + lt];
-        wi = v_s[OFF_W / 8 + lt];
-        di = dbc ? pdv[code] : v_s[OFF_D / 8 + lt];
-        const int lo = pst[code], hi = pst[code + 1];
-        for (int k = lo; k < hi; ++k) {
-          const PEnt e = pent[k];
-          nacc = add(nacc, mul(e.v, win[e.ix + lt]));
-        }
-      } else if (WIN) {
-        const double* win = reinterpret_cast<const double*>(sb + 7 * VB);
-        const unsigned char* cwin = sb + 7 * VB + (size_t)W.elems * 8;
-        wi = win[W.own + lt];
-        const int code = cwin[W.cown + lt];
-        if (W.dinv_uniform) {  // one dinv for every row: only the own-row code window
-          di = W.dinv0;
-          const int lo = pst[code], hi = pst[code + 1];
-          // a plain loop: batching the loads 8 at a time measured 8% slower
-          // at 256^3 (0.369 vs 0.339 ms, same box) and 15% at 27-pt
-          for (int k = lo; k < hi; ++k)
-            nacc = add(nacc, mul(pva[k], mul(di, win[pix[k] + lt])));  // m = M^-1 w
-        } else {
-          di = pdv[code];
-          const int lo = pst[code], hi = pst[code + 1];
-          for (int k = lo; k < hi; ++k) {
-            const double mc = mul(pdv[cwin[pcx[k] + lt]], win[pix[k] + lt]);  // m = M^-1 w
-            nacc = add(nacc, mul(pva[k], mc));
-          }
-        }
+      double nacc;
+      if (done) {
+        nacc = pre_n;
+        wi = pre_w;
+        di = pre_d;
       } else {
-        // per-nonzero gathers, three explicit phases per batch as in A
-        const int code = sb[7 * VB + lt];
-        const int lo = pst[code], hi = pst[code + 1];
-        const int ii = (int)i;
-        for (int k0 = lo; k0 < hi; k0 += 8) {
-          double av[8], mv[8];
-          int cc[8];
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const int k = k0 + t < hi ? k0 + t : lo;
-            cc[t] = ii + pix[k];
-            av[t] = pva[k];
-          }
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            if (k0 + t < hi) {
-              const int c = cc[t];
-              mv[t] = MG ? ldg_nc(m_old + c) : mul(ldg_nc(P.dinv + c), ldg_nc(w_old + c));
-            }
-          }
-#pragma unroll
-          for (int t = 0; t < 8; ++t)
-            if (k0 + t < hi) nacc = add(nacc, mul(av[t], mv[t]));
-        }
+        nacc = row_spmv(sb, i, wi, di);
       }
       auto vec = [&](int k) { return DV ? dv[k] : v_s[k * TR + lt]; };
       const double mi = mul(di, wi);
@@ -2653,32 +2705,18 @@ __global__ void __launch_bounds__(256) drift_partial_kernel(const Ctrl* C, int s
                                                              const double* __restrict__ r,
                                                              double* __restrict__ dpart,
                                                              const int* __restrict__ ip,
-                                                             const double* xh0, const double* xh1,
-                                                             const unsigned long long* darrive,
-                                                             unsigned long long per_sample) {
+                                                             const double* xh0, const double* xh1) {
   // xh0 / xh1 (distributed): halo columns (>= n) of x for sample parity 0 / 1
   // (see drift_push_kernel), read L2-coherently after the peers' pushes of
   // this sample have been acquired
   __shared__ double red[8];
-  __shared__ int ok;
   const long long it = cta_iteration(C, step);
   if (it < 0) return;
   if (it < 1 || C->drift_k <= 0 || it % C->drift_k != 0) return;
-  const double* xhs = nullptr;
-  if (xh0) {
-    const long long smp = it / C->drift_k;
-    if (threadIdx.x == 0) {
-      Ctrl* Cw = const_cast<Ctrl*>(C);
-      ok = spin_until(darrive, C->darrive_base + (unsigned long long)smp * per_sample, Cw, 3) ? 1 : 0;
-      if (!ok) {  // a peer stalled: stop the solve with the exchange error
-        Cw->bd_it = it;
-        Cw->status = PCG_ECOMM_STATUS;
-      }
-    }
-    __syncthreads();
-    if (!ok) return;
-    xhs = (smp & 1) ? xh1 : xh0;
-  }
+  // distributed: drift_wait_kernel (one block, stream-ordered before this
+  // grid) has acquired every peer's push of this sample -- a full grid
+  // spinning here could keep a peer sharing the GPU from ever pushing
+  const double* xhs = xh0 ? (((it / C->drift_k) & 1) ? xh1 : xh0) : nullptr;
   double v[1] = {0.0};
   for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
     double acc = 0.0;
@@ -2911,6 +2949,17 @@ __global__ void __launch_bounds__(256) drift_push_kernel(CommParams CP, const Ct
   if (threadIdx.x == 0)
     for (int q = 0; q < CP.world; ++q)
       atomicAdd_system(reinterpret_cast<unsigned long long*>(CP.peer_comm[q] + 16), 1ull);
+}
+
+__global__ void drift_wait_kernel(Ctrl* C, int step, const unsigned long long* darrive,
+                                  unsigned long long per_sample) {
+  __shared__ long long s_it;
+  const long long it = cta_iteration(C, step, &s_it);
+  if (it < 0 || !drift_step(C, it) || threadIdx.x != 0) return;
+  if (!spin_until(darrive, C->darrive_base + (unsigned long long)(it / C->drift_k) * per_sample, C, 3)) {
+    C->bd_it = it;  // a peer stalled: stop the solve with the exchange error
+    C->status = PCG_ECOMM_STATUS;
+  }
 }
 
 __global__ void __launch_bounds__(256) drift_dist_finish_kernel(CommParams CP, Ctrl* C, int step,
@@ -4023,21 +4072,24 @@ int enqueue_step(pcg_solver* S, int k) {
   if (S->drift_k > 0) {
     // distributed: x halo of this sample into the spare n / b vectors first
     const bool dist = S->connected;
-    if (dist) drift_push_kernel<<<kXchgBlocks, 256, 0, st>>>(S->cp, R.C, k, S->x);
     const double* xh0 = dist ? S->nv : nullptr;
     const double* xh1 = dist ? S->b : nullptr;
     const unsigned long long* darr = reinterpret_cast<const unsigned long long*>(S->comm + 16);
     const unsigned long long per = (unsigned long long)S->world * kXchgBlocks;
+    if (dist) {
+      drift_push_kernel<<<kXchgBlocks, 256, 0, st>>>(S->cp, R.C, k, S->x);
+      drift_wait_kernel<<<1, 32, 0, st>>>(R.C, k, darr, per);
+    }
     const int* ip = S->engine == 3 ? S->iperm : nullptr;
     if (S->A.rp64)
       drift_partial_kernel<long long><<<kDotGrid, 256, 0, st>>>(
           R.C, k, n, static_cast<const long long*>(S->A.rowptr), S->A.col, S->A.val, S->x, S->b,
-          S->r, S->dpart, ip, xh0, xh1, darr, per);
+          S->r, S->dpart, ip, xh0, xh1);
     else
       drift_partial_kernel<int><<<kDotGrid, 256, 0, st>>>(R.C, k, n,
                                                            static_cast<const int*>(S->A.rowptr),
                                                            S->A.col, S->A.val, S->x, S->b, S->r,
-                                                           S->dpart, ip, xh0, xh1, darr, per);
+                                                           S->dpart, ip, xh0, xh1);
     if (dist)
       drift_dist_finish_kernel<<<1, 256, 0, st>>>(S->cp, R.C, k, S->dpart, kDotGrid, R.dval, R.dit,
                                                   S->comm);
@@ -4330,7 +4382,7 @@ int preload_solver() {
   PCG_LOAD(gated_spmv_chunks); PCG_LOAD(seq_dots_kernel);
   PCG_LOAD(drift_partial_kernel<int>); PCG_LOAD(drift_partial_kernel<long long>);
   PCG_LOAD(drift_finish_kernel); PCG_LOAD(advance_kernel); PCG_LOAD(init_ctrl_kernel);
-  PCG_LOAD(drift_push_kernel); PCG_LOAD(drift_dist_finish_kernel);
+  PCG_LOAD(drift_push_kernel); PCG_LOAD(drift_dist_finish_kernel); PCG_LOAD(drift_wait_kernel);
   PCG_LOAD(finalize_x_kernel); PCG_LOAD(finalize_mark_kernel);
   PCG_LOAD((pipecg_fused_kernel_g<4, 3, true>)); PCG_LOAD((pipecg_fused_kernel_g<2, 4, true>));
   PCG_LOAD((pipecg_fused_kernel_g<2, 4, false>)); PCG_LOAD((pipecg_fused_kernel_g<4, 4, false>));
