@@ -53,6 +53,8 @@ from .solvers import (
     true_residual_norm,
 )
 
+from ._device import invalidate_device_cache
+
 __version__ = "0.1.0"
 
 __all__ = [
@@ -91,4 +93,5 @@ __all__ = [
     "pipecg_scalars",
     "pipecg_solve",
     "true_residual_norm",
+    "invalidate_device_cache",
 ]

@@ -34,6 +34,64 @@ def shared_max_sms(ranks_on_device: int, device: int | None = None) -> int:
     return max(8, sms // k - 10)
 
 
+def host_fingerprint(*arrays, samples: int = 2048) -> tuple:
+    """Cheap content fingerprint of host arrays for the device-copy caches:
+    each array's identity (data pointer, shape, dtype) and a hash of a
+    strided sample of its bytes (``samples`` elements + the last one, tens
+    of microseconds whatever the size).
+
+    The reference's CsrMatrix and JacobiPreconditioner are immutable after
+    construction (sparse.py:43-50, kernels.py:204); a caller that rewrites
+    their arrays in place anyway gets a fresh upload when the sample
+    changes.  A change that misses every sampled element is not detected:
+    call :func:`invalidate_device_cache` after such an edit."""
+    out = []
+    for a in arrays:
+        a = np.asarray(a)
+        flat = a.reshape(-1)
+        n = flat.size
+        h = 0
+        if n:
+            step = max(1, n // samples)
+            h = hash(flat[::step].tobytes()) ^ hash(flat[-1:].tobytes())
+        out.append((a.__array_interface__["data"][0], a.shape, a.dtype.str, h))
+    return tuple(out)
+
+
+def cached_device(owner, attr: str, make, *host_arrays):
+    """``owner.attr`` holds (device copy, fingerprint of ``host_arrays``);
+    the copy is rebuilt with ``make()`` when the fingerprint changed or the
+    copy lives on another device."""
+    fp = host_fingerprint(*host_arrays)
+    hit = getattr(owner, attr, None)
+    if isinstance(hit, tuple) and len(hit) == 2 and hit[1] == fp and _on_current(hit[0]):
+        return hit[0]
+    d = make()
+    try:
+        object.__setattr__(owner, attr, (d, fp))
+    except (AttributeError, TypeError):
+        pass
+    return d
+
+
+def _on_current(d) -> bool:
+    t = d if isinstance(d, torch.Tensor) else getattr(d, "col", None)
+    return isinstance(t, torch.Tensor) and t.device.index == torch.cuda.current_device()
+
+
+def invalidate_device_cache(obj) -> None:
+    """Forget the device copy (and the solvers built on it) cached on a
+    host CsrMatrix or JacobiPreconditioner -- after an in-place edit of its
+    arrays, which the reference's contract forbids (immutable objects) and
+    the sampled fingerprint may miss."""
+    for attr in ("_b200_device", "_b200_inv_diag"):
+        if attr in getattr(obj, "__dict__", {}):
+            try:
+                object.__delattr__(obj, attr)
+            except AttributeError:
+                pass
+
+
 def stream_ptr() -> int:
     return torch.cuda.current_stream().cuda_stream
 

@@ -23,7 +23,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import (host_f64, is_device_tensor, require_cuda, stream_ptr, to_device_f64,
+from ._device import (cached_device, host_f64, host_fingerprint, is_device_tensor, require_cuda,
+                      stream_ptr, to_device_f64,
                       vec_len)
 from .sparse import DeviceCsr, as_device_csr
 
@@ -182,15 +183,9 @@ class JacobiPreconditioner:
 
 def device_inv_diag(pc) -> torch.Tensor:
     """Device float64 copy of ``pc.inv_diag`` (cached on the object)."""
-    cached = getattr(pc, "_b200_inv_diag", None)
-    if isinstance(cached, torch.Tensor) and cached.device.index == torch.cuda.current_device():
-        return cached
-    d = to_device_f64(pc.inv_diag)
-    try:
-        object.__setattr__(pc, "_b200_inv_diag", d)
-    except (AttributeError, TypeError):
-        pass
-    return d
+    if is_device_tensor(pc.inv_diag):
+        return to_device_f64(pc.inv_diag)  # the caller's device tensor: no copy to go stale
+    return cached_device(pc, "_b200_inv_diag", lambda: to_device_f64(pc.inv_diag), pc.inv_diag)
 
 
 def jacobi_setup(matrix) -> JacobiPreconditioner:
@@ -213,10 +208,9 @@ def jacobi_setup(matrix) -> JacobiPreconditioner:
     _lib.check("pipecg_b200_jacobi_setup", rc)
     d = d[: A.n_rows]
     if isinstance(matrix, DeviceCsr):
-        pc = JacobiPreconditioner(d)
-    else:
-        pc = JacobiPreconditioner(d.cpu().numpy())
-    object.__setattr__(pc, "_b200_inv_diag", d)
+        return JacobiPreconditioner(d)
+    pc = JacobiPreconditioner(d.cpu().numpy())
+    object.__setattr__(pc, "_b200_inv_diag", (d, host_fingerprint(pc.inv_diag)))
     return pc
 
 

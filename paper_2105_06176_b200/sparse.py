@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import h2d, require_cuda, stream_ptr
+from ._device import cached_device, h2d, host_fingerprint, require_cuda, stream_ptr
 
 __all__ = [
     "CsrMatrix",
@@ -245,15 +245,8 @@ def as_device_csr(A) -> DeviceCsr:
     """Device form of ``A`` (uploaded once and cached on the object)."""
     if isinstance(A, DeviceCsr):
         return A
-    cached = getattr(A, "_b200_device", None)
-    if isinstance(cached, DeviceCsr) and cached.col.device.index == torch.cuda.current_device():
-        return cached
-    d = upload_csr(A)
-    try:
-        object.__setattr__(A, "_b200_device", d)
-    except (AttributeError, TypeError):
-        pass
-    return d
+    return cached_device(A, "_b200_device", lambda: upload_csr(A), A.row_offsets, A.col_indices,
+                         A.values)
 
 
 # --- stencil generators (device) -------------------------------------------
@@ -305,7 +298,8 @@ def stencil_host(kind, n: int) -> CsrMatrix:
     """Stencil matrix generated on the device and returned as a host CsrMatrix."""
     d = stencil_device(kind, n)
     A = d.to_host()
-    object.__setattr__(A, "_b200_device", d)
+    object.__setattr__(A, "_b200_device",
+                       (d, host_fingerprint(A.row_offsets, A.col_indices, A.values)))
     return A
 
 
@@ -429,7 +423,8 @@ def _mm_csr(handle) -> CsrMatrix:
     rowptr[n + 1:].fill_(int(nnz.value))
     d = DeviceCsr(n, m, int(nnz.value), rowptr, col, val)
     A = d.to_host()
-    object.__setattr__(A, "_b200_device", d)
+    object.__setattr__(A, "_b200_device",
+                       (d, host_fingerprint(A.row_offsets, A.col_indices, A.values)))
     return A
 
 

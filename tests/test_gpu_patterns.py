@@ -293,3 +293,23 @@ def test_autotune_alternatives_fit_the_partials(cuda, max_sms):
             np.testing.assert_array_equal(x, ref.x)
         else:
             assert abs(rep.iterations - ref.iterations) <= 1
+
+
+def test_in_place_edits_of_cached_host_arrays_are_seen(cuda):
+    """ADVICE/VERDICT r1: the device copies cached on a host CsrMatrix /
+    JacobiPreconditioner must not go stale when the caller rewrites the
+    arrays in place (the reference reads them afresh every call).  Scale
+    the matrix values and the preconditioner in place between two solves:
+    the second solve is the oracle's solve of the edited system."""
+    A = pb.stencil_host("3d7", 16)
+    pc = pb.jacobi_setup(A)
+    x_true, b, x0, d = oracle.manufactured(A)
+    cfg = pb.SolverConfig(tolerance=1e-10, max_iterations=2000, record_history=True)
+    opts = pb.DeviceOptions(dot_mode="seq")
+    pb.pipecg_solve(A, b, x0, pc, cfg, options=opts)  # caches the device copies
+    A.values[:] *= 3.0          # in place: same arrays, new content
+    pc.inv_diag[:] /= 3.0
+    ref = oracle.pipecg_solve(A, b, x0, pc.inv_diag, tol=1e-10, max_iterations=2000)
+    x, rep = pb.pipecg_solve(A, b, x0, pc, cfg, options=opts)
+    assert rep.history == ref.history
+    np.testing.assert_array_equal(x, ref.x)

@@ -191,3 +191,37 @@ def test_powerlaw_generator_full_size_matches_survey():
     rl = A.row_nnz()
     assert A.nnz == 49_986_874
     assert (rl.min(), int(np.median(rl)), rl.max()) == (1, 9, 49_349)
+
+
+def test_host_fingerprint_tracks_in_place_edits():
+    """The device-copy caches (as_device_csr, device_inv_diag) are keyed on
+    a sampled content fingerprint: an in-place rewrite of a cached host
+    array is seen (re-upload), identity changes are seen, unchanged arrays
+    keep the cache."""
+    from paper_2105_06176_b200._device import host_fingerprint
+
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal(1_000_003)
+    b = np.arange(77, dtype=np.int64)
+    f0 = host_fingerprint(a, b)
+    assert host_fingerprint(a, b) == f0
+    a *= 2.0  # whole-array rewrite (every sample changes)
+    assert host_fingerprint(a, b) != f0
+    f1 = host_fingerprint(a, b)
+    b[-1] += 1  # the last element is always sampled
+    assert host_fingerprint(a, b) != f1
+    assert host_fingerprint(a.copy(), b) != host_fingerprint(a, b)  # another buffer
+    z = np.zeros(0)
+    assert host_fingerprint(z) == host_fingerprint(z)
+
+
+def test_invalidate_device_cache_drops_cached_copies():
+    import paper_2105_06176_b200 as pb
+
+    A = pb.csr_from_dense(np.eye(3))
+    pc = pb.JacobiPreconditioner(np.ones(3))
+    object.__setattr__(A, "_b200_device", ("stale", ()))
+    object.__setattr__(pc, "_b200_inv_diag", ("stale", ()))
+    pb.invalidate_device_cache(A)
+    pb.invalidate_device_cache(pc)
+    assert "_b200_device" not in A.__dict__ and "_b200_inv_diag" not in pc.__dict__
