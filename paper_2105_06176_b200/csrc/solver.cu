@@ -2446,7 +2446,17 @@ struct QParams {
   double* pout;        // this kernel's block partials [2][grid][4]
   double* fin;         // their fixed-order sum [2][4] (last block), or null
   unsigned* counter;   // [2]
+  long long long_row;  // Q1: rows longer than this are pcg_hub_kernel's
+  const double* hsum;  // Q2: the hub rows' (s, p) sum [2] by parity (null: no hub rows)
 };
+
+// Q1's SpMV, one warp per 32 consecutive rows ("CSR stream"): the warp
+// copies the rows' contiguous column / value range into shared memory with
+// coalesced loads, then every lane sums its own row from there in CSR order
+// (bitwise _spmv).  Ranges longer than kQCap fall back to per-lane global
+// loads; rows longer than long_row are left to pcg_hub_kernel.
+constexpr int kQCap = 1024;  // entries staged per warp (27-pt: 32 rows x 27)
+constexpr int kQSmem = 8 * kQCap * 12;
 
 template <int NT>
 __device__ __forceinline__ void reduce_partials(const ReduceIn& R, long long it_src, int lt,
@@ -2505,21 +2515,126 @@ __global__ void __launch_bounds__(256) pcg_q1_kernel(QParams<RP> P, int step) {
   if (leader) C->slot[it & 1] = Slot{gamma, 0.0, 0.0, norm};
   const double* p_old = P.p[it & 1];
   double* p_new = P.p[(it + 1) & 1];
+  extern __shared__ __align__(16) unsigned char qsm[];
+  const int warp = tid >> 5, lane = tid & 31;
+  int* col_s = reinterpret_cast<int*>(qsm) + warp * kQCap;
+  double* val_s = reinterpret_cast<double*>(qsm + 8 * kQCap * 4) + warp * kQCap;
+  // p_new of a column, formed from p_old and u (bitwise the stored p_new)
+  auto pnew = [&](int c) { return add(mul(ldg_nc(p_old + c), beta), ldg_nc(P.u + c)); };
   double acc[3] = {0.0, 0.0, 0.0};
-  for (long long i = blockIdx.x * 256LL + tid; i < P.n; i += (long long)gridDim.x * 256) {
-    const long long lo = P.rp[i], hi = P.rp[i + 1];
-    double si = 0.0;
-    for (long long k = lo; k < hi; ++k) {  // kernels.py:64-70 on p_new
-      const int c = ldg_nc(P.col + k);
-      const double pc = add(mul(ldg_nc(p_old + c), beta), ldg_nc(P.u + c));
-      si = add(si, mul(ldg_nc(P.val + k), pc));
+  const long long n_blk = (P.n + 31) / 32;
+  for (long long blk = blockIdx.x * 8LL + warp; blk < n_blk; blk += (long long)gridDim.x * 8) {
+    const long long r0 = blk * 32, i = r0 + lane;
+    const long long e0 = P.rp[r0], e1 = P.rp[min(r0 + 32, P.n)];
+    const bool staged = e1 - e0 <= kQCap;
+    if (staged)
+      for (long long e = e0 + lane; e < e1; e += 32) {
+        col_s[e - e0] = ldg_nc(P.col + e);
+        val_s[e - e0] = ldg_nc(P.val + e);
+      }
+    __syncwarp();
+    if (i < P.n) {
+      const long long lo = P.rp[i], hi = P.rp[i + 1];
+      double si = 0.0;
+      if (hi - lo <= P.long_row) {
+        // kernels.py:64-70 on p_new: batches of 8 -- indices and values,
+        // then the gathers, then the ordered adds
+        for (long long k0 = lo; k0 < hi; k0 += 8) {
+          double av[8], pv[8];
+          int cc[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const long long k = k0 + t;
+            cc[t] = k < hi ? (staged ? col_s[k - e0] : ldg_nc(P.col + k)) : 0;
+            av[t] = k < hi ? (staged ? val_s[k - e0] : ldg_nc(P.val + k)) : 0.0;
+          }
+#pragma unroll
+          for (int t = 0; t < 8; ++t) pv[t] = k0 + t < hi ? pnew(cc[t]) : 0.0;
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            if (k0 + t < hi) si = add(si, mul(av[t], pv[t]));
+        }
+      }
+      const double pi = add(mul(p_old[i], beta), P.u[i]);
+      p_new[i] = pi;
+      if (hi - lo <= P.long_row) {
+        P.s[i] = si;
+        acc[0] = add(acc[0], mul(si, pi));  // delta = dot(s, p)
+      }
     }
-    const double pi = add(mul(p_old[i], beta), P.u[i]);
-    p_new[i] = pi;
-    P.s[i] = si;
-    acc[0] = add(acc[0], mul(si, pi));  // delta = dot(s, p)
+    __syncwarp();  // the staged range is rewritten by the warp's next block
   }
   publish_partials<256>(acc, tid, red, 1, P.pout, P.fin, P.counter, it);
+}
+
+// Q1's hub rows (longer than kLongRow): engine 2's nnz-bounded chunks of the
+// row, one CTA each with a fixed tree (not the reference's order -- graded
+// like a parallel dot), reading Q1's complete p_new; the row's last chunk
+// sums the chunk partials in order, writes s and the row's s*p term; the
+// grid's last CTA sums the terms in row order into hsum[it & 1] for Q2.
+__global__ void __launch_bounds__(256) pcg_hub_kernel(const Ctrl* C, int step,
+                                                      const LongChunk* __restrict__ ch,
+                                                      const int* __restrict__ col,
+                                                      const double* __restrict__ val,
+                                                      const double* p0, const double* p1, double* s,
+                                                      double* part, unsigned* ticket, double* hterm,
+                                                      int n_hub, double* hsum, unsigned* gticket) {
+  __shared__ double red[9];
+  __shared__ int last;
+  __shared__ long long s_it;
+  const long long it = cta_iteration(C, step, &s_it);
+  if (it < 0) return;
+  const double* p = ((it + 1) & 1) ? p1 : p0;  // p_new of iteration it
+  const LongChunk c = ch[blockIdx.x];
+  double v[1] = {0.0};
+  for (long long k0 = c.lo + threadIdx.x; k0 < c.hi; k0 += 4 * 256) {
+    double a[4], xv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long k = k0 + 256LL * u;
+      a[u] = 0.0;
+      xv[u] = 0.0;
+      if (k < c.hi) {
+        a[u] = ldg_nc(val + k);
+        xv[u] = __ldcg(p + ldg_nc(col + k));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (k0 + 256LL * u < c.hi) v[0] = add(v[0], mul(a[u], xv[u]));
+  }
+  group_sum<1, 256>(v, threadIdx.x, red, 1);
+  if (threadIdx.x == 0) {
+    bool mine = true;
+    double srow = v[0];
+    if (c.n > 1) {
+      part[blockIdx.x] = v[0];
+      __threadfence();
+      mine = atomicAdd(ticket + c.slot, 1u) == (unsigned)(c.n - 1);
+      if (mine) {
+        __threadfence();
+        srow = 0.0;
+        for (int j = 0; j < c.n; ++j) srow = add(srow, __ldcg(part + c.first + j));
+        ticket[c.slot] = 0u;  // next iteration (stream-ordered)
+      }
+    }
+    if (mine) {
+      s[c.row] = srow;
+      hterm[c.hub] = mul(srow, __ldcg(p + c.row));
+    }
+    __threadfence();
+    last = atomicAdd(gticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double h[1] = {0.0};
+  for (int k = threadIdx.x; k < n_hub; k += 256) h[0] = add(h[0], __ldcg(hterm + k));
+  group_sum<1, 256>(h, threadIdx.x, red, 1);
+  if (threadIdx.x == 0) {
+    hsum[it & 1] = h[0];
+    *gticket = 0u;
+  }
 }
 
 template <typename RP>
@@ -2534,7 +2649,8 @@ __global__ void __launch_bounds__(256) pcg_q2_kernel(QParams<RP> P, int step) {
   if (it < 0) return;
   double v[3];
   reduce_partials<256>(P.rin, it, tid, red, v);  // Q1(it): (s, p)
-  const double delta = v[0];
+  // + the hub rows' terms (tree mode; the seq-mode dot covers every row)
+  const double delta = P.hsum ? add(v[0], __ldcg(P.hsum + (it & 1))) : v[0];
   if (delta <= 0.0 || !isfinite(delta)) {  // solvers.py:247-248
     if (blockIdx.x == 0 && tid == 0) {
       C->bd_code = PCG_BD_DELTA;
@@ -3261,7 +3377,8 @@ struct pcg_solver {
   double* dinvp = nullptr;         // inv_diag in SELL order (every init)
   double* natbuf = nullptr;        // solver_state: natural-order copies (engine 3)
   double* qbuf = nullptr;          // engine 4: partials [2][2][grid][4] | fin [2][2][4] | seq [2][2][4]
-  unsigned* qcnt = nullptr;        // engine 4: last-block tickets [2][2]
+  unsigned* qcnt = nullptr;        // engine 4: last-block tickets [2][2] | hub-kernel ticket
+  double* qhub = nullptr;          // engine 4: hub rows' s*p terms [n_long] | their sum [2]
   int g_batch = 2;                 // engine 3 SELL nonzeros per lane per load batch (2 or 4)
   bool e2_pol = true;              // engine 2: L2 hints (streams evict-first, m evict-last; -2% at 2^22)
   int g_mb = 4;                    // engine 3 CTAs per SM the kernel is compiled for (4 or 6)
@@ -4033,6 +4150,9 @@ void launch_q(pcg_solver* S, int k, const Record& R) {
     return r;
   };
   QParams<RP> P;
+  const bool hubs = S->n_chunks > 0;
+  P.long_row = hubs ? kLongRow : LLONG_MAX;
+  P.hsum = nullptr;
   P.n = S->A.n_rows;
   P.rp = static_cast<const RP*>(S->A.rowptr);
   P.col = S->A.col;
@@ -4052,13 +4172,18 @@ void launch_q(pcg_solver* S, int k, const Record& R) {
   P.pout = part[0];
   P.fin = fin[0];
   P.counter = fin_mode ? S->qcnt : nullptr;
-  launch_k(pcg_q1_kernel<RP>, (unsigned)S->grid, 256, 0, st, S->pdl, P, k);
+  launch_k(pcg_q1_kernel<RP>, (unsigned)S->grid, 256, kQSmem, st, S->pdl, P, k);
+  if (hubs)
+    pcg_hub_kernel<<<(unsigned)S->n_chunks, 256, 0, st>>>(
+        R.C, k, S->chunks, S->A.col, S->A.val, S->p, S->q, S->s, S->chunk_part, S->chunk_ticket,
+        S->qhub, (int)S->n_long, S->qhub + S->n_long, S->qcnt + 4);
   if (seq_mode)
     pcg_seq_dots_kernel<<<1, 32, 0, st>>>(R.C, k, 1, P.n, S->s, S->p, S->q, S->r, S->u, seq[0]);
   P.rin = rin(0);
   P.pout = part[1];
   P.fin = fin[1];
   P.counter = fin_mode ? S->qcnt + 2 : nullptr;
+  P.hsum = hubs && !seq_mode ? S->qhub + S->n_long : nullptr;
   launch_k(pcg_q2_kernel<RP>, (unsigned)S->grid, 256, 0, st, S->pdl && !seq_mode, P, k);
   if (seq_mode)
     pcg_seq_dots_kernel<<<1, 32, 0, st>>>(R.C, k, 2, P.n, S->s, S->p, S->q, S->r, S->u, seq[1]);
@@ -4390,7 +4515,7 @@ int preload_solver() {
   PCG_LOAD(gather_perm_kernel); PCG_LOAD(scatter_perm_kernel); PCG_LOAD(iperm_kernel);
   PCG_LOAD(renumber_kernel); PCG_LOAD(hub_pack_kernel);
   PCG_LOAD(pcg_q1_kernel<int>); PCG_LOAD(pcg_q1_kernel<long long>); PCG_LOAD(pcg_q2_kernel<int>);
-  PCG_LOAD(pcg_q2_kernel<long long>); PCG_LOAD(pcg_seq_dots_kernel);
+  PCG_LOAD(pcg_q2_kernel<long long>); PCG_LOAD(pcg_seq_dots_kernel); PCG_LOAD(pcg_hub_kernel);
   PCG_LOAD(iter_exchange_kernel); PCG_LOAD(vec_exchange_kernel);
   PCG_LOAD(init_dots_exchange_kernel); PCG_LOAD(snapshot_arrive_kernel); PCG_LOAD(xwait_kernel);
   PCG_LOAD(tile_span_kernel<int>); PCG_LOAD(tile_span_kernel<long long>); PCG_LOAD(max_row_kernel);
@@ -4398,6 +4523,7 @@ int preload_solver() {
 #define PCG_SMEM(k) \
   if (e == cudaSuccess)  \
   e = cudaFuncSetAttribute((const void*)(k), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)
+  PCG_SMEM(pcg_q1_kernel<int>); PCG_SMEM(pcg_q1_kernel<long long>);
   PCG_SMEM((pipecg_fused_kernel<int, 256>)); PCG_SMEM((pipecg_fused_kernel<int, 128>));
   PCG_SMEM((pipecg_fused_kernel<int, 64>)); PCG_SMEM((pipecg_fused_kernel<long long, 256>));
   PCG_SMEM((pipecg_fused_kernel<long long, 128>)); PCG_SMEM((pipecg_fused_kernel<long long, 64>));
@@ -4851,16 +4977,34 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   bool fused_ok = false;
   if (req == kReqPCG) {  // classic PCG: CSR kernels only, nothing to plan or tune
     S->engine = 4;
-    S->grid = S->n_partials = std::min<int>(kDotGrid, 4 * S->num_sms);
-    rc = alloc_state(S);
+    // Q1 stages 96 KB per CTA: two CTAs per SM
+    S->grid = S->n_partials = 2 * S->num_sms;
+    if (has_long) {  // hub rows: engine 2's chunks (pcg_hub_kernel)
+      int64_t cnt = 0;
+      rc = pipecg_b200_find_long_rows(A->n_rows, A->rp64, A->rowptr, kLongRow, nullptr, 0, &cnt,
+                                      S->stream);
+      if (!rc && cnt > 0) {
+        if (pool_malloc(&S->long_rows, cnt * sizeof(int)) != cudaSuccess)
+          rc = set_error(PCG_ENOMEM, "long rows alloc");
+        else
+          rc = pipecg_b200_find_long_rows(A->n_rows, A->rp64, A->rowptr, kLongRow, S->long_rows,
+                                          cnt, &cnt, S->stream);
+        S->n_long = cnt;
+      }
+      if (!rc) rc = build_long_chunks(S);
+      if (!rc && S->n_long > 0 &&
+          pool_malloc(&S->qhub, (S->n_long + 2) * sizeof(double)) != cudaSuccess)
+        rc = set_error(PCG_ENOMEM, "pcg hub workspace");
+    }
+    if (!rc) rc = alloc_state(S);
     if (!rc && (pool_malloc(&S->qbuf, ((size_t)4 * S->grid * 4 + 32) * sizeof(double)) != cudaSuccess ||
-                pool_malloc(&S->qcnt, 4 * sizeof(unsigned)) != cudaSuccess))
+                pool_malloc(&S->qcnt, 8 * sizeof(unsigned)) != cudaSuccess))
       rc = set_error(PCG_ENOMEM, "pcg workspace");
     if (rc) {
       pipecg_b200_solver_destroy(S);
       return rc;
     }
-    cudaMemsetAsync(S->qcnt, 0, 4 * sizeof(unsigned), S->stream);
+    cudaMemsetAsync(S->qcnt, 0, 8 * sizeof(unsigned), S->stream);
     *out = S;
     return cuda_status(cudaStreamSynchronize(S->stream), "pcg workspace");
   }
@@ -5093,6 +5237,7 @@ int pipecg_b200_solver_destroy(pcg_solver* S) {
   pool_free(S->natbuf);
   pool_free(S->qbuf);
   pool_free(S->qcnt);
+  pool_free(S->qhub);
   pool_free(S->gchunk_part);
   pool_free(S->gchunk_ticket);
   for (Sell* c : {&S->sell2, &S->gsell}) {
@@ -5362,7 +5507,7 @@ int pipecg_b200_solver_init(pcg_solver* S, const double* b, const double* x0, do
   if (rc) return rc;
   if (S->engine == 4) {  // classic PCG (solvers.py:223-231): p = 0, gamma, norm, b_norm
     cudaMemsetAsync(S->p, 0, bytes, st);
-    cudaMemsetAsync(S->qcnt, 0, 4 * sizeof(unsigned), st);
+    cudaMemsetAsync(S->qcnt, 0, 8 * sizeof(unsigned), st);
     const double* qa[4] = {S->r, S->u, S->u, S->b};
     const double* qb[4] = {S->u, S->u, S->u, S->b};
     rc = dots_any(n, 4, qa, qb, S->opt.dot_mode, S->dots4, S->dots_ws, st);

@@ -444,3 +444,28 @@ def test_pcg_device_breakdown_matches_oracle(cuda):
                      options=pb.DeviceOptions(dot_mode="seq"))
     assert (exc.value.quantity, exc.value.iteration) == ref.breakdown[:2]
     assert exc.value.value == ref.breakdown[2]
+
+
+@pytest.mark.parametrize("mode", ["seq", "tree"])
+def test_pcg_device_hub_rows(cuda, mode):
+    """Rows longer than kLongRow (6 rows of ~9,000 nonzeros, several engine-2
+    chunks each) go through pcg_hub_kernel (fixed-tree chunks, in-order
+    chunk combine, the hub terms of delta summed in row order): within the
+    oracle's reorder envelope in both dot modes and bitwise repeatable."""
+    from test_gpu_irregular import _hub_spd
+
+    A = _hub_spd(60000, 6, 9000, seed=11)
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    ref = oracle.pcg_solve(A, b, x0, d, tol=tol, max_iterations=3000)
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=3000, record_history=True)
+    opts = pb.DeviceOptions(dot_mode=mode)
+    x, rep = pb.pcg_solve(A, b, x0, pb.JacobiPreconditioner(d), cfg, options=opts)
+    ref2 = oracle.pcg_solve(A, b, x0, d, tol=tol, max_iterations=3000, dot_mode="blocked")
+    E = oracle.history_gap(ref2.history, ref.history)
+    assert abs(rep.iterations - ref.iterations) <= max(1, abs(ref2.iterations - ref.iterations))
+    assert oracle.history_gap(rep.history, ref.history) <= max(1e-10, 3 * E)
+    assert np.max(np.abs(x - ref.x)) / np.max(np.abs(ref.x)) <= 1e-8
+    x2, rep2 = pb.pcg_solve(A, b, x0, pb.JacobiPreconditioner(d), cfg, options=opts)
+    assert rep2.history == rep.history
+    np.testing.assert_array_equal(x2, x)

@@ -82,6 +82,7 @@ def main():
         print(f"| {len(v)} | {sum(v) / 1e3:.1f} | {100 * sum(v) / tot:.1f}% | "
               f"{sum(v) / len(v) / 1e3:.1f} | `{k[:110]}` |")
     if a.report:
+        per_launch = []  # (dram bytes, seconds, kernel) of every captured launch
         for rec in raw(a.report):
             print(f"\n## ncu --set full: `{rec['Kernel Name'][0][:120]}`\n")
             print("| metric | value | unit |\n|---|---:|---|")
@@ -99,22 +100,32 @@ def main():
                 wr *= scale[rec["dram__bytes_write.sum"][1]]
                 print(f"\nDRAM traffic per launch: {(rd + wr) / 1e9:.4f} GB "
                       f"({(rd + wr) / t_s / 1e9:.0f} GB/s over the ncu duration)")
-                if a.traffic_key:
-                    import json
-                    import pathlib
-
-                    tp = pathlib.Path(__file__).resolve().parents[1] / "profiles" / "traffic.json"
-                    d = json.loads(tp.read_text()) if tp.exists() else {}
-                    d[a.traffic_key] = {"dram_bytes_per_launch": rd + wr,
-                                        "kernel": rec["Kernel Name"][0][:120],
-                                        "ncu_duration_s": t_s,
-                                        "source": a.source or a.report}
-                    tp.write_text(json.dumps(d, indent=1, sort_keys=True) + "\n")
+                per_launch.append((rd + wr, t_s, rec["Kernel Name"][0][:120]))
                 if a.bytes:
                     print(f"Algorithmic (canonical) bytes per launch: {a.bytes / 1e9:.4f} GB; "
                           f"traffic/algorithmic = {(rd + wr) / a.bytes:.3f}")
             except (KeyError, ValueError):
                 pass
+        if per_launch:
+            n = len(per_launch)
+            avg_b = sum(p[0] for p in per_launch) / n
+            avg_t = sum(p[1] for p in per_launch) / n
+            if n > 1:
+                print(f"\n## Average over the {n} captured launches (e.g. an even + an odd "
+                      f"iteration of the deferred-x kernels)\n\nDRAM traffic per launch: "
+                      f"{avg_b / 1e9:.4f} GB, {avg_t * 1e6:.1f} us, {avg_b / avg_t / 1e9:.0f} GB/s")
+                if a.bytes:
+                    print(f"traffic/algorithmic = {avg_b / a.bytes:.3f}")
+            if a.traffic_key:
+                import json
+                import pathlib
+
+                tp = pathlib.Path(__file__).resolve().parents[1] / "profiles" / "traffic.json"
+                d = json.loads(tp.read_text()) if tp.exists() else {}
+                d[a.traffic_key] = {"dram_bytes_per_launch": avg_b, "launches_averaged": n,
+                                    "kernel": per_launch[0][2], "ncu_duration_s": avg_t,
+                                    "source": a.source or a.report}
+                tp.write_text(json.dumps(d, indent=1, sort_keys=True) + "\n")
 
 
 if __name__ == "__main__":
