@@ -2450,13 +2450,9 @@ struct QParams {
   const double* hsum;  // Q2: the hub rows' (s, p) sum [2] by parity (null: no hub rows)
 };
 
-// Q1's SpMV, one warp per 32 consecutive rows ("CSR stream"): the warp
-// copies the rows' contiguous column / value range into shared memory with
-// coalesced loads, then every lane sums its own row from there in CSR order
-// (bitwise _spmv).  Ranges longer than kQCap fall back to per-lane global
-// loads; rows longer than long_row are left to pcg_hub_kernel.
-constexpr int kQCap = 1024;  // entries staged per warp (27-pt: 32 rows x 27)
-constexpr int kQSmem = 8 * kQCap * 12;
+// (A warp-cooperative variant staging each 32-row block's CSR range in
+// shared memory measured 2.4x slower at 3D 7-pt 256^3: 96 KB per CTA
+// left two CTAs per SM for a latency-bound gather kernel.)
 
 template <int NT>
 __device__ __forceinline__ void reduce_partials(const ReduceIn& R, long long it_src, int lt,
@@ -2515,54 +2511,34 @@ __global__ void __launch_bounds__(256) pcg_q1_kernel(QParams<RP> P, int step) {
   if (leader) C->slot[it & 1] = Slot{gamma, 0.0, 0.0, norm};
   const double* p_old = P.p[it & 1];
   double* p_new = P.p[(it + 1) & 1];
-  extern __shared__ __align__(16) unsigned char qsm[];
-  const int warp = tid >> 5, lane = tid & 31;
-  int* col_s = reinterpret_cast<int*>(qsm) + warp * kQCap;
-  double* val_s = reinterpret_cast<double*>(qsm + 8 * kQCap * 4) + warp * kQCap;
   // p_new of a column, formed from p_old and u (bitwise the stored p_new)
   auto pnew = [&](int c) { return add(mul(ldg_nc(p_old + c), beta), ldg_nc(P.u + c)); };
   double acc[3] = {0.0, 0.0, 0.0};
-  const long long n_blk = (P.n + 31) / 32;
-  for (long long blk = blockIdx.x * 8LL + warp; blk < n_blk; blk += (long long)gridDim.x * 8) {
-    const long long r0 = blk * 32, i = r0 + lane;
-    const long long e0 = P.rp[r0], e1 = P.rp[min(r0 + 32, P.n)];
-    const bool staged = e1 - e0 <= kQCap;
-    if (staged)
-      for (long long e = e0 + lane; e < e1; e += 32) {
-        col_s[e - e0] = ldg_nc(P.col + e);
-        val_s[e - e0] = ldg_nc(P.val + e);
-      }
-    __syncwarp();
-    if (i < P.n) {
-      const long long lo = P.rp[i], hi = P.rp[i + 1];
-      double si = 0.0;
-      if (hi - lo <= P.long_row) {
-        // kernels.py:64-70 on p_new: batches of 8 -- indices and values,
-        // then the gathers, then the ordered adds
-        for (long long k0 = lo; k0 < hi; k0 += 8) {
-          double av[8], pv[8];
-          int cc[8];
+  for (long long i = blockIdx.x * 256LL + tid; i < P.n; i += (long long)gridDim.x * 256) {
+    const long long lo = P.rp[i], hi = P.rp[i + 1];
+    const double pi = add(mul(p_old[i], beta), P.u[i]);
+    p_new[i] = pi;
+    if (hi - lo > P.long_row) continue;  // pcg_hub_kernel's row
+    // kernels.py:64-70 on p_new, batches of 8: indices and values, then
+    // the gathers, then the ordered adds (independent loads in flight)
+    double si = 0.0;
+    for (long long k0 = lo; k0 < hi; k0 += 8) {
+      double av[8], pv[8];
+      int cc[8];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const long long k = k0 + t;
-            cc[t] = k < hi ? (staged ? col_s[k - e0] : ldg_nc(P.col + k)) : 0;
-            av[t] = k < hi ? (staged ? val_s[k - e0] : ldg_nc(P.val + k)) : 0.0;
-          }
-#pragma unroll
-          for (int t = 0; t < 8; ++t) pv[t] = k0 + t < hi ? pnew(cc[t]) : 0.0;
-#pragma unroll
-          for (int t = 0; t < 8; ++t)
-            if (k0 + t < hi) si = add(si, mul(av[t], pv[t]));
-        }
+      for (int t = 0; t < 8; ++t) {
+        const long long k = k0 + t;
+        cc[t] = k < hi ? ldg_nc(P.col + k) : 0;
+        av[t] = k < hi ? ldg_nc(P.val + k) : 0.0;
       }
-      const double pi = add(mul(p_old[i], beta), P.u[i]);
-      p_new[i] = pi;
-      if (hi - lo <= P.long_row) {
-        P.s[i] = si;
-        acc[0] = add(acc[0], mul(si, pi));  // delta = dot(s, p)
-      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t) pv[t] = k0 + t < hi ? pnew(cc[t]) : 0.0;
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        if (k0 + t < hi) si = add(si, mul(av[t], pv[t]));
     }
-    __syncwarp();  // the staged range is rewritten by the warp's next block
+    P.s[i] = si;
+    acc[0] = add(acc[0], mul(si, pi));  // delta = dot(s, p)
   }
   publish_partials<256>(acc, tid, red, 1, P.pout, P.fin, P.counter, it);
 }
@@ -4172,7 +4148,7 @@ void launch_q(pcg_solver* S, int k, const Record& R) {
   P.pout = part[0];
   P.fin = fin[0];
   P.counter = fin_mode ? S->qcnt : nullptr;
-  launch_k(pcg_q1_kernel<RP>, (unsigned)S->grid, 256, kQSmem, st, S->pdl, P, k);
+  launch_k(pcg_q1_kernel<RP>, (unsigned)S->grid, 256, 0, st, S->pdl, P, k);
   if (hubs)
     pcg_hub_kernel<<<(unsigned)S->n_chunks, 256, 0, st>>>(
         R.C, k, S->chunks, S->A.col, S->A.val, S->p, S->q, S->s, S->chunk_part, S->chunk_ticket,
@@ -4523,7 +4499,6 @@ int preload_solver() {
 #define PCG_SMEM(k) \
   if (e == cudaSuccess)  \
   e = cudaFuncSetAttribute((const void*)(k), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)
-  PCG_SMEM(pcg_q1_kernel<int>); PCG_SMEM(pcg_q1_kernel<long long>);
   PCG_SMEM((pipecg_fused_kernel<int, 256>)); PCG_SMEM((pipecg_fused_kernel<int, 128>));
   PCG_SMEM((pipecg_fused_kernel<int, 64>)); PCG_SMEM((pipecg_fused_kernel<long long, 256>));
   PCG_SMEM((pipecg_fused_kernel<long long, 128>)); PCG_SMEM((pipecg_fused_kernel<long long, 64>));
@@ -4977,8 +4952,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   bool fused_ok = false;
   if (req == kReqPCG) {  // classic PCG: CSR kernels only, nothing to plan or tune
     S->engine = 4;
-    // Q1 stages 96 KB per CTA: two CTAs per SM
-    S->grid = S->n_partials = 2 * S->num_sms;
+    S->grid = S->n_partials = std::min<int>(kDotGrid, 4 * S->num_sms);
     if (has_long) {  // hub rows: engine 2's chunks (pcg_hub_kernel)
       int64_t cnt = 0;
       rc = pipecg_b200_find_long_rows(A->n_rows, A->rp64, A->rowptr, kLongRow, nullptr, 0, &cnt,
