@@ -626,7 +626,10 @@ def run_distributed(args):
         peak, peak_src = measured_peak()
         B = canonical_bytes(N, nnz) + 4 * (ws - 1)  # one row-pointer sentinel per extra block
         t_iter = ms / 1e3 / steps
-        achieved = B / t_iter / 1e9
+        # the variant's algorithmic bytes over all ranks (its own layout, as
+        # the N = 1 line); the halo bytes cross NVLink, not HBM
+        kb, kb_formula = engine_bytes(res.engine, res.pattern_flags, N, nnz)
+        achieved = kb / t_iter / 1e9
         line = {
             "metric": METRIC, "value": steps / (ms / 1e3), "unit": UNIT, "n_gpus": ws,
             "steps": steps, "warmup": warm, "ms_per_step": ms / steps, "higher_is_better": True,
@@ -640,8 +643,15 @@ def run_distributed(args):
                        "l2": "inputs >> L2; no flush needed"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * ws, "unit": "GB/s",
                          "frac": achieved / (peak * ws), "traffic": None,
-                         "bytes_per_iteration": B, "peak_source": peak_src + f" x {ws} GPUs",
-                         "note": "aggregate over ranks"},
+                         "bytes_per_iteration": kb, "bytes_formula": kb_formula,
+                         "canonical_equivalent": {
+                             "bytes_per_iteration": B,
+                             "achieved": B / t_iter / 1e9, "frac": B / t_iter / 1e9 / (peak * ws)},
+                         "peak_source": peak_src + f" x {ws} GPUs",
+                         "note": "aggregate over ranks" + (
+                             "; every rank shares ONE GPU (PIPECG_B200_TEST_SAME_GPU): a protocol "
+                             "check, not a scaling number" if same else "")},
+            "engine": ENGINES.get(res.engine, "?"),
             "gpu_launches": launches,
             "timing_ok": ok,
             "clocks": clk.summary(),
