@@ -949,11 +949,12 @@ struct FusedLayoutS {
   // F+WIN: w_old | dinv | codes | m windows (the 7 streamed vectors are
   //        loaded by the consumers themselves: a smaller stage -> more
   //        stages -> more window bytes in flight)
-  // E+WIN: 7 vectors | w_old windows | code windows
+  // E+WIN: [7 vectors |] w_old windows | code windows (dv: the streamed
+  //        vectors loaded by the consumers, as F -- the autotuner times both)
   // gathers: 7 vectors | codes
-  __host__ __device__ static int stage_bytes(bool mg, bool win, int elems, int celems) {
+  __host__ __device__ static int stage_bytes(bool mg, bool win, int elems, int celems, bool dv) {
     if (win && mg) return 2 * kVecBytes + TR + elems * 8;
-    if (win) return 7 * kVecBytes + elems * 8 + celems;
+    if (win) return (dv ? 0 : 7 * kVecBytes) + elems * 8 + celems;
     return 7 * kVecBytes + TR;
   }
 };
@@ -979,7 +980,7 @@ __host__ __device__ __forceinline__ int pat_smem_bytes(int n_pat, int n_e) {
 // rows of w (E) / m (F) are pushed to the peers after each tile, and the
 // windows of the first stages are requested only after the prologue has
 // seen every peer's previous iteration (they may cover halo rows).
-template <int TR, bool MG, bool WIN, bool XG = false>
+template <int TR, bool MG, bool WIN, bool XG = false, bool DVT = false>
 __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128 ? 6 : 8))
     pipecg_fused_kernel_s(FusedParams<int> P, WinTable W, int step) {
   using L = FusedLayoutS<TR>;
@@ -1000,13 +1001,15 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
   double* pva = reinterpret_cast<double*>(pcx + n_e4);
   double* pdv = pva + P.n_pat_e;  // per-code dinv
   unsigned char* stage0 = smem + L::kHeader + round_up(pat_smem_bytes(P.n_pat, P.n_pat_e), 128);
-  const int SB = L::stage_bytes(MG, WIN, W.elems, W.celems);
+  // DV: the consumers load the 7 streamed vectors (F with windows always;
+  // E with windows when the plan says so)
+  constexpr bool DV = MG ? WIN : (WIN && DVT);
+  const int SB = L::stage_bytes(MG, WIN, W.elems, W.celems, DV);
   const int S = P.stages;
   const bool dbc = W.dinv_by_code != 0;
-  // DV (F with windows): the consumers load the 7 streamed vectors; the
-  // stage holds w_old | dinv | codes | m windows
-  constexpr bool DV = MG && WIN;
+  // F: the stage holds w_old | dinv | codes | m windows
   constexpr int OFF_W = DV ? 0 : 7 * VB, OFF_D = DV ? VB : 8 * VB, OFF_C = DV ? 2 * VB : 9 * VB;
+  constexpr int OFF_E = DV ? 0 : 7 * VB;  // E: start of the w_old windows
 
   Ctrl* C = P.C;
   const int tid = threadIdx.x;
@@ -1035,7 +1038,7 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
   // the dictionary is constant: load it before waiting on the previous grid
   for (int k = tid; k <= P.n_pat; k += blockDim.x) pst[k] = P.pstart[k];
   for (int k = tid; k < P.n_pat; k += blockDim.x) pdv[k] = dbc ? P.pdinv[k] : 0.0;
-  // DV (F with windows): entries as one 16-byte record {value, window
+  // F with windows: entries as one 16-byte record {value, window
   // index} in the space of pix | pcx | pva -- one shared load per nonzero
   // instead of two
   struct PEnt {
@@ -1043,13 +1046,14 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
     int ix, pad;
   };
   PEnt* pent = reinterpret_cast<PEnt*>(pix);
-  if (DV) {
+  constexpr bool PE = MG && WIN;  // F reads PEnt records, E pix / pcx / pva
+  if (PE) {
     for (int k = tid; k < P.n_pat_e; k += blockDim.x) {
       const int w = P.pwin[k];
       pent[k] = PEnt{P.pval[k], W.base[w] + P.poff[k] - W.lo[w], 0};
     }
   }
-  for (int k = tid; k < P.n_pat_e && !DV; k += blockDim.x) {
+  for (int k = tid; k < P.n_pat_e && !PE; k += blockDim.x) {
     if (WIN) {
       const int w = P.pwin[k];
       pix[k] = W.base[w] + P.poff[k] - W.lo[w];
@@ -1124,13 +1128,13 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
       const int w = c - 10;
       if (WIN && w < W.n && ((msk >> w) & 1)) {
         const bool halo = XG && t0 + W.lo[w] + W.len[w] > P.n;
-        range(sb + (MG ? OFF_C + TR : 7 * VB) + (size_t)W.base[w] * 8, MG ? m_src : w_src,
+        range(sb + (MG ? OFF_C + TR : OFF_E) + (size_t)W.base[w] * 8, MG ? m_src : w_src,
               t0 + W.lo[w], W.len[w], W.ld, 8, halo ? 4 : 2);
       }
     } else {
       const int w = c - 10 - kMaxWin;
       if (WIN && !MG && w < W.n && (!W.dinv_uniform || w == W.w0))
-        range(sb + 7 * VB + (size_t)W.elems * 8 + W.cbase[w], P.pcode, t0 + W.clo[w], W.clen[w],
+        range(sb + OFF_E + (size_t)W.elems * 8 + W.cbase[w], P.pcode, t0 + W.clo[w], W.clen[w],
               W.code_ld, 1, 1);
     }
     return d;
@@ -1212,8 +1216,8 @@ __global__ void __launch_bounds__(TR + 32, TR == 256 ? (MG ? 2 : 3) : (TR == 128
         nacc = add(nacc, mul(e.v, win[e.ix + lt]));
       }
     } else if (WIN) {
-      const double* win = reinterpret_cast<const double*>(sb + 7 * VB);
-      const unsigned char* cwin = sb + 7 * VB + (size_t)W.elems * 8;
+      const double* win = reinterpret_cast<const double*>(sb + OFF_E);
+      const unsigned char* cwin = sb + OFF_E + (size_t)W.elems * 8;
       wi = win[W.own + lt];
       const int code = cwin[W.cown + lt];
       if (W.dinv_uniform) {  // one dinv for every row: only the own-row code window
@@ -3237,6 +3241,7 @@ struct FusedPlan {
   int variant = 0;  // 0: consumer gathers dinv,w (A); 1: gather warps (B); 2: stored m (C);
                     // 3: nnz-balanced tiles + cooperative gathers of the stored m (D)
   int tr = 0, stages = 0, bps = 0, cap_val = 0, cap_col = 0, grid = 0, score = 0;
+  int dv = 0;  // E: consumers load the streamed vectors (smaller stages)
   size_t smem = 0;
   long long n_tiles = 0;  // variants D/E: tiles built for this plan (owned by the solver)
   long long cap = 0, hub_len = 0;
@@ -3369,6 +3374,7 @@ struct pcg_solver {
   unsigned char* pwin = nullptr;   // [n_entries] run of each dictionary entry
   double* pdinv = nullptr;         // [n_pat] dinv of each code's first row
   unsigned short* tile_runs[3] = {nullptr, nullptr, nullptr};  // per tile height 256/128/64
+  int dv = 0;                      // E plan: streamed vectors loaded by the consumers
   bool dinv_by_code = false;       // dinv[i] == pdinv[code[i]] for every row (checked at init)
   bool dinv_uniform = false;       // ... and all pdinv equal (dinv0)
   double dinv0 = 0.0;
@@ -3686,19 +3692,21 @@ inline bool s_windows(const pcg_solver* S, bool mg) {
 // One E/F plan: tile height TR with exactly `bps` CTAs per SM (3 stages if
 // they fit, else 2).  stages == 0: does not fit.
 template <int TR, bool MG>
-int plan_one_s(pcg_solver* S, int bps, FusedPlan* out) {
+int plan_one_s(pcg_solver* S, int bps, FusedPlan* out, bool dv_e = false, int max_st = 0) {
   FusedPlan p;
   p.variant = MG ? 6 : 5;
   p.tr = TR;
   const bool win = s_windows(S, MG);
   const WinTable W = win_table(S, TR);
-  const size_t sb = FusedLayoutS<TR>::stage_bytes(MG, win, W.elems, W.celems);
+  const bool dv = MG ? win : (win && dv_e);
+  p.dv = dv && !MG;
+  const size_t sb = FusedLayoutS<TR>::stage_bytes(MG, win, W.elems, W.celems, dv);
   const size_t hdr = FusedLayoutS<TR>::kHeader +
                      (size_t)round_up(pat_smem_bytes(S->pat.n_pat, S->pat.n_entries), 128);
   const size_t sm_budget = 228 * 1024, cta_max = 227 * 1024;
   const char* e_st = getenv("PIPECG_B200_STAGES");
-  // F stages no longer carry the streamed vectors: up to 4 fit at 2 CTAs/SM
-  for (int st = e_st ? atoi(e_st) : (MG && win ? 4 : 3); st >= 2; --st) {
+  // stages without the streamed vectors are small: up to 4 (or max_st)
+  for (int st = e_st ? atoi(e_st) : (max_st ? max_st : (dv ? 4 : 3)); st >= 2; --st) {
     const size_t need = hdr + st * sb;
     if (need <= cta_max && (need + 1024) * bps <= sm_budget) {
       p.stages = st;
@@ -3714,7 +3722,9 @@ int plan_one_s(pcg_solver* S, int bps, FusedPlan* out) {
   }
   int occ = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &occ, win ? pipecg_fused_kernel_s<TR, MG, true> : pipecg_fused_kernel_s<TR, MG, false>,
+      &occ,
+      win ? (p.dv ? pipecg_fused_kernel_s<TR, MG, true, false, true> : pipecg_fused_kernel_s<TR, MG, true>)
+          : pipecg_fused_kernel_s<TR, MG, false>,
       TR + 32, p.smem);
   if (e != cudaSuccess) return cuda_status(e, "pattern occupancy");
   if (occ < bps) {  // registers do not allow this many CTAs
@@ -3750,6 +3760,17 @@ int plan_variant_s(pcg_solver* S, FusedPlan* best, std::vector<FusedPlan>* alts)
     if (rc) return rc;
     if (p.stages) alts->push_back(p);
     if (e_bps) break;
+  }
+  // E with windows: also the stages without the streamed vectors (the
+  // consumers load them), 2 stages at 3 and 2 CTAs per SM (3D 7-pt 256^3:
+  // 0.322 vs 0.333 ms; slower at 27-pt -- the autotuner decides)
+  if (!MG && s_windows(S, false) && !e_bps && (!tr_pick || tr_pick == 256)) {
+    for (int bps : {3, 2}) {
+      FusedPlan p;
+      int rc = plan_one_s<256, MG>(S, bps, &p, true, 2);
+      if (rc) return rc;
+      if (p.stages) alts->push_back(p);
+    }
   }
   *best = alts->empty() ? FusedPlan() : alts->front();
   return PCG_OK;
@@ -3802,6 +3823,7 @@ void apply_plan(pcg_solver* S, const FusedPlan& p) {
   S->smem = p.smem;
   S->grid = p.grid;
   S->n_partials = p.grid;
+  S->dv = p.dv;
 }
 
 // pinned kRecBytes records, recycled across solvers (page-locking memory
@@ -4010,26 +4032,29 @@ void launch_fused(pcg_solver* S, int k) {
   if (variant == 5 || variant == 6) {
     const FusedParams<int> PS = fused_params<int>(S);  // E/F never read the row pointers
     const WinTable W = win_table(S, S->tr);
-#define PCG_LS(MGV, WV)                                                                                \
-  switch (S->tr) {                                                                                     \
-    case 256: launch_k(pipecg_fused_kernel_s<256, MGV, WV>, g, 256 + 32, sm, st, pdl, PS, W, k); break; \
-    case 128: launch_k(pipecg_fused_kernel_s<128, MGV, WV>, g, 128 + 32, sm, st, pdl, PS, W, k); break; \
-    default: launch_k(pipecg_fused_kernel_s<64, MGV, WV>, g, 64 + 32, sm, st, pdl, PS, W, k); break;    \
+#define PCG_LS(MGV, WV, DVV)                                                                                      \
+  switch (S->tr) {                                                                                                \
+    case 256: launch_k(pipecg_fused_kernel_s<256, MGV, WV, false, DVV>, g, 256 + 32, sm, st, pdl, PS, W, k); break; \
+    case 128: launch_k(pipecg_fused_kernel_s<128, MGV, WV, false, DVV>, g, 128 + 32, sm, st, pdl, PS, W, k); break; \
+    default: launch_k(pipecg_fused_kernel_s<64, MGV, WV, false, DVV>, g, 64 + 32, sm, st, pdl, PS, W, k); break;    \
   }
     const bool win = s_windows(S, variant == 6);
     if (S->fused_xchg) {  // connect keeps E/F only with windows
-#define PCG_LSX(MGV)                                                                                         \
-  switch (S->tr) {                                                                                           \
-    case 256: launch_k(pipecg_fused_kernel_s<256, MGV, true, true>, g, 256 + 32, sm, st, pdl, PS, W, k); break; \
-    case 128: launch_k(pipecg_fused_kernel_s<128, MGV, true, true>, g, 128 + 32, sm, st, pdl, PS, W, k); break; \
-    default: launch_k(pipecg_fused_kernel_s<64, MGV, true, true>, g, 64 + 32, sm, st, pdl, PS, W, k); break;    \
+#define PCG_LSX(MGV, DVV)                                                                                          \
+  switch (S->tr) {                                                                                                 \
+    case 256: launch_k(pipecg_fused_kernel_s<256, MGV, true, true, DVV>, g, 256 + 32, sm, st, pdl, PS, W, k); break; \
+    case 128: launch_k(pipecg_fused_kernel_s<128, MGV, true, true, DVV>, g, 128 + 32, sm, st, pdl, PS, W, k); break; \
+    default: launch_k(pipecg_fused_kernel_s<64, MGV, true, true, DVV>, g, 64 + 32, sm, st, pdl, PS, W, k); break;    \
   }
-      if (variant == 6) { PCG_LSX(true) } else { PCG_LSX(false) }
+      if (variant == 6) { PCG_LSX(true, false) }
+      else if (S->dv) { PCG_LSX(false, true) }
+      else { PCG_LSX(false, false) }
 #undef PCG_LSX
-    } else if (variant == 6 && win) { PCG_LS(true, true) }
-    else if (variant == 6) { PCG_LS(true, false) }
-    else if (win) { PCG_LS(false, true) }
-    else { PCG_LS(false, false) }
+    } else if (variant == 6 && win) { PCG_LS(true, true, false) }
+    else if (variant == 6) { PCG_LS(true, false, false) }
+    else if (win && S->dv) { PCG_LS(false, true, true) }
+    else if (win) { PCG_LS(false, true, false) }
+    else { PCG_LS(false, false, false) }
 #undef PCG_LS
   } else if (variant == 1) {
     switch (S->tr) {
@@ -4473,6 +4498,12 @@ int preload_solver() {
   PCG_LOAD((pipecg_fused_kernel_s<256, false, true, true>)); PCG_LOAD((pipecg_fused_kernel_s<128, false, true, true>));
   PCG_LOAD((pipecg_fused_kernel_s<64, false, true, true>)); PCG_LOAD((pipecg_fused_kernel_s<256, true, true, true>));
   PCG_LOAD((pipecg_fused_kernel_s<128, true, true, true>)); PCG_LOAD((pipecg_fused_kernel_s<64, true, true, true>));
+  PCG_LOAD((pipecg_fused_kernel_s<256, false, true, false, true>));
+  PCG_LOAD((pipecg_fused_kernel_s<128, false, true, false, true>));
+  PCG_LOAD((pipecg_fused_kernel_s<64, false, true, false, true>));
+  PCG_LOAD((pipecg_fused_kernel_s<256, false, true, true, true>));
+  PCG_LOAD((pipecg_fused_kernel_s<128, false, true, true, true>));
+  PCG_LOAD((pipecg_fused_kernel_s<64, false, true, true, true>));
   PCG_LOAD(tile_runs_kernel); PCG_LOAD(uniform_check_kernel);
 
   PCG_LOAD(pipecg_k1_kernel<false>); PCG_LOAD(pipecg_k1_kernel<true>); PCG_LOAD(gated_spmv_rows<int>); PCG_LOAD(gated_spmv_rows<long long>);
@@ -4532,6 +4563,12 @@ int preload_solver() {
   PCG_SMEM((pipecg_fused_kernel_s<256, false, true, true>)); PCG_SMEM((pipecg_fused_kernel_s<128, false, true, true>));
   PCG_SMEM((pipecg_fused_kernel_s<64, false, true, true>)); PCG_SMEM((pipecg_fused_kernel_s<256, true, true, true>));
   PCG_SMEM((pipecg_fused_kernel_s<128, true, true, true>)); PCG_SMEM((pipecg_fused_kernel_s<64, true, true, true>));
+  PCG_SMEM((pipecg_fused_kernel_s<256, false, true, false, true>));
+  PCG_SMEM((pipecg_fused_kernel_s<128, false, true, false, true>));
+  PCG_SMEM((pipecg_fused_kernel_s<64, false, true, false, true>));
+  PCG_SMEM((pipecg_fused_kernel_s<256, false, true, true, true>));
+  PCG_SMEM((pipecg_fused_kernel_s<128, false, true, true, true>));
+  PCG_SMEM((pipecg_fused_kernel_s<64, false, true, true, true>));
 #undef PCG_SMEM
   if (e != cudaSuccess) return cuda_status(e, "preload solver kernels");
   rc = preload_patterns();
@@ -5462,6 +5499,15 @@ int pipecg_b200_solver_init(pcg_solver* S, const double* b, const double* x0, do
       S->dinv_by_code = dbc;
       S->dinv_uniform = uni;
       S->dinv0 = d0;
+      // an E plan without the streamed vectors in its stages only fits the
+      // window layout: without windows (dinv no longer by code) take E's
+      // plan that stages them
+      if (S->engine == 1 && S->variant == 5 && S->dv && !s_windows(S, false))
+        for (const FusedPlan& q : S->alts[5])
+          if (!q.dv) {
+            apply_plan(S, q);
+            break;
+          }
       for (int k = 0; k < 2; ++k) {  // graphs bake the kernel choice in
         for (auto& kv : S->graphs[k]) cudaGraphExecDestroy(kv.second);
         S->graphs[k].clear();
