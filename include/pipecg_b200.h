@@ -219,7 +219,9 @@ typedef struct {
                           (0 = not run) */
   int pattern_flags;   /* row-pattern dictionary in use by E/F: 1 dictionary, 2 windows,
                           4 dinv a function of the row's code, 8 ... one dinv for all rows,
-                          16 deferred x update (x read + written every other iteration) */
+                          16 deferred x update (x read + written every other iteration),
+                          32 E's stages without the streamed vectors (the consumers
+                          load them) */
 } pcg_result;
 
 int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_solver** out);

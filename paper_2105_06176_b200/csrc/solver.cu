@@ -3764,7 +3764,13 @@ int plan_variant_s(pcg_solver* S, FusedPlan* best, std::vector<FusedPlan>* alts)
   // E with windows: also the stages without the streamed vectors (the
   // consumers load them), 2 stages at 3 and 2 CTAs per SM (3D 7-pt 256^3:
   // 0.322 vs 0.333 ms; slower at 27-pt -- the autotuner decides)
-  if (!MG && s_windows(S, false) && !e_bps && (!tr_pick || tr_pick == 256)) {
+  // (PIPECG_B200_DV=0 / 1: only the staged / only the consumer-loaded
+  // layout -- to pin the layout for ncu captures, whose replays mislead
+  // the autotuner)
+  const char* e_dv = getenv("PIPECG_B200_DV");
+  if (e_dv && atoi(e_dv) == 1 && !MG) alts->clear();
+  if (!MG && s_windows(S, false) && !e_bps && (!tr_pick || tr_pick == 256) &&
+      !(e_dv && atoi(e_dv) == 0)) {
     for (int bps : {3, 2}) {
       FusedPlan p;
       int rc = plan_one_s<256, MG>(S, bps, &p, true, 2);
@@ -4432,7 +4438,8 @@ void fill_result(pcg_solver* S, const Ctrl& c, pcg_result* res) {
   res->pattern_flags = S->pat.n_pat == 0 ? 0
                        : 1 | (S->n_runs > 0 ? 2 : 0) | (S->dinv_by_code ? 4 : 0) |
                              (S->dinv_by_code && S->dinv_uniform ? 8 : 0) |
-                             (defer_x_active(S) ? 16 : 0);
+                             (defer_x_active(S) ? 16 : 0) |
+                             (S->engine == 1 && S->variant == 5 && S->dv ? 32 : 0);
   res->graph_launches = S->graph_launches;
   res->norm0 = c.init.norm;
   res->breakdown_quantity = c.bd_code;
