@@ -123,6 +123,11 @@ int pipecg_b200_narrow_i64(int64_t n, const int64_t* src, int32_t* dst, int* ove
 enum { PCG_H2D_COPY64 = 0, PCG_H2D_I64_TO_I32 = 1 };
 int pipecg_b200_h2d(void* dst_dev, const void* src_host, int64_t count, int kind, void* stream);
 int pipecg_b200_d2h(void* dst_host, const void* src_dev, int64_t bytes, void* stream);
+/* Touch every page of a freshly allocated host buffer (host threads): the
+ * first-touch page faults of a new numpy array otherwise cap a following
+ * pipecg_b200_d2h at ~15 GB/s (~38 GB/s into touched pages).  Run while the
+ * GPU solves.  Contents become unspecified. */
+int pipecg_b200_host_prefault(void* host, int64_t bytes);
 
 /* Matrix Market ingestion (replaces sparse.py:195-326
  * parse_matrix_market / load_matrix_market).  Same accepted subset

@@ -233,6 +233,23 @@ extern "C" int pipecg_b200_h2d(void* dst_dev, const void* src_host, int64_t coun
   return overflow ? set_error(PCG_ERANGE, "h2d: index outside int32 range") : PCG_OK;
 }
 
+extern "C" int pipecg_b200_host_prefault(void* host, int64_t bytes) {
+  if (bytes < 0 || (bytes > 0 && !host)) return set_error(PCG_EINVAL, "host_prefault: bad arguments");
+  if (bytes == 0) return PCG_OK;
+  Ring& R = ring();
+  std::lock_guard<std::mutex> lk(R.mu);  // the pool serves one transfer at a time
+  Pool& pool = Pool::get();
+  constexpr int64_t kPage = 4096;
+  const int64_t pages = (bytes + kPage - 1) / kPage;
+  const int parts = (int)std::min<int64_t>(pool.size() * 4, std::max<int64_t>(1, pages / 64));
+  char* base = static_cast<char*>(host);
+  pool.run(parts, [&](int p) {
+    const int64_t lo = pages * p / parts, hi = pages * (p + 1) / parts;
+    for (int64_t g = lo; g < hi; ++g) reinterpret_cast<volatile char*>(base)[g * kPage] = 0;
+  });
+  return PCG_OK;
+}
+
 extern "C" int pipecg_b200_d2h(void* dst_host, const void* src_dev, int64_t bytes, void* stream) {
   if (bytes < 0 || (bytes > 0 && (!dst_host || !src_dev)) || bytes % 8)
     return set_error(PCG_EINVAL, "d2h: bad arguments");

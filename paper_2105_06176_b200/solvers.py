@@ -290,10 +290,11 @@ class PipecgSolver:
         _cuda_memcpy_d2d(out.data_ptr(), ptr, self.n * 8)
         return out
 
-    def x_host(self) -> np.ndarray:
-        """The iterate x downloaded into a new host array (native pinned
-        pipeline, on the solver's stream)."""
-        out = np.empty(self.n, dtype=np.float64)
+    def x_host(self, out: np.ndarray | None = None) -> np.ndarray:
+        """The iterate x downloaded into a new host array (or ``out``; native
+        pinned pipeline, on the solver's stream)."""
+        if out is None:
+            out = np.empty(self.n, dtype=np.float64)
         if self.n:
             _lib.call("pipecg_b200_d2h", out.ctypes.data, _lib.load().pipecg_b200_solver_x(self._h),
                       self.n * 8, self.stream)
@@ -327,6 +328,27 @@ def _cuda_memcpy_d2d(dst: int, src: int, nbytes: int) -> None:
     d = torch.as_tensor(_Raw(dst, n), device="cuda")
     d.copy_(s)
     torch.cuda.current_stream().synchronize()
+
+
+class _PrefaultedHost:
+    """A new float64 host array whose pages host threads touch in the
+    background while the GPU solves (``pipecg_b200_host_prefault``): the
+    x download then runs at ~38 GB/s instead of the ~15 GB/s that the
+    first-touch page faults of a fresh array allow."""
+
+    def __init__(self, n: int):
+        self.out = np.empty(n, dtype=np.float64)
+        self._t = None
+        if n:
+            self._t = threading.Thread(target=_lib.call, daemon=True,
+                                       args=("pipecg_b200_host_prefault", self.out.ctypes.data,
+                                             self.out.nbytes))
+            self._t.start()
+
+    def get(self) -> np.ndarray:
+        if self._t is not None:
+            self._t.join()
+        return self.out
 
 
 _CACHE_LOCK = threading.Lock()
@@ -450,6 +472,7 @@ def pipecg_solve(A, b, x0, pc, cfg: SolverConfig | None = None, *,
         nvtx.range_pop()
         t_setup = time.perf_counter()
         nvtx.range_push("pipecg.iterations")
+        x_out = None if on_dev else _PrefaultedHost(n)  # pages touched while the GPU solves
         res, hist, d_it, d_val = solver.run(cfg.record_history, cfg.max_iterations,
                                             cfg.drift_check_interval)
         nvtx.range_pop()
@@ -461,7 +484,7 @@ def pipecg_solve(A, b, x0, pc, cfg: SolverConfig | None = None, *,
         drift = None
         if cfg.drift_check_interval > 0:
             drift = [[int(d_it[k]), float(d_val[k])] for k in range(res.n_drift)]
-        x = solver.x_tensor() if on_dev else solver.x_host()
+        x = solver.x_tensor() if on_dev else solver.x_host(out=x_out.get())
     finally:
         solver.lock.release()
         if not cached:
@@ -518,6 +541,7 @@ def pcg_solve(A, b, x0, pc, cfg: SolverConfig | None = None, *,
         solver.init(bd, x0d, cfg.tolerance, cfg.max_iterations, cfg.drift_check_interval)
         torch.cuda.ExternalStream(solver.stream).synchronize()
         t_setup = time.perf_counter()
+        x_out = None if on_dev else _PrefaultedHost(n)
         res, hist, d_it, d_val = solver.run(cfg.record_history, cfg.max_iterations,
                                             cfg.drift_check_interval)
         t_end = time.perf_counter()
@@ -528,7 +552,7 @@ def pcg_solve(A, b, x0, pc, cfg: SolverConfig | None = None, *,
         drift = None
         if cfg.drift_check_interval > 0:
             drift = [[int(d_it[k]), float(d_val[k])] for k in range(res.n_drift)]
-        x = solver.x_tensor() if on_dev else solver.x_host()
+        x = solver.x_tensor() if on_dev else solver.x_host(out=x_out.get())
     finally:
         solver.lock.release()
         if not cached:
