@@ -4832,8 +4832,13 @@ int autotune(pcg_solver* S, int grid2, int grid3, bool with_engine2, bool irregu
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   // timed as the solve runs: graph chunks (built before the timed chunk),
-  // kTuneIters iterations after a 2-iteration warm-up
+  // kTuneIters iterations after a 2-iteration warm-up.  When an iteration
+  // moves more than ~0.5 GB (>= ~80 us) the launch overhead a graph saves is
+  // noise and its capture + instantiation per candidate is not: direct
+  // launches then (first-call cost)
   constexpr int kTuneIters = 8;
+  const int saved_graphs = S->opt.use_graphs;
+  if (136.0 * S->A.n_rows + 12.0 * S->A.nnz > 0.5e9) S->opt.use_graphs = 0;
   int best = -1;
   float best_ms = 0.f;
   int rc = PCG_OK;
@@ -4841,7 +4846,14 @@ int autotune(pcg_solver* S, int grid2, int grid3, bool with_engine2, bool irregu
   // (kVariants + 1: irregular rows, when its SELL copy exists)
   const bool g_ok = irregular && S->g_built;
   const int n_cand = with_engine2 ? (g_ok ? kVariants + 2 : kVariants + 1) : kVariants;
+  // a row-pattern dictionary read through windows (E/F): the CSR variants
+  // A/C/D and the two-kernel engine were 1.7-2.3x slower at every stencil
+  // size measured (7/27-pt 128^3-400^3, 2D 512^2) -- not timed (P is: it
+  // wins the launch-bound sizes)
+  const bool dict = (S->plans[5].stages && s_windows(S, false)) ||
+                    (S->plans[6].stages && s_windows(S, true));
   for (int cand = 0; cand < n_cand && !rc; ++cand) {
+    if (dict && (cand == 0 || cand == 2 || cand == 3 || cand == kVariants)) continue;
     if (cand < kVariants) {
       // B (gather warps) never won a measurement; D only pays for irregular rows
       if (!S->plans[cand].stages || cand == 1 || (cand == 3 && !irregular)) continue;
@@ -4894,6 +4906,7 @@ int autotune(pcg_solver* S, int grid2, int grid3, bool with_engine2, bool irregu
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  S->opt.use_graphs = saved_graphs;
   S->initialized = false;
   S->host_base = 0;
   if (rc) return rc;
