@@ -4823,7 +4823,8 @@ std::mutex& tune_cache_mu() {
   return mu;
 }
 
-int autotune(pcg_solver* S, int grid2, int grid3, bool with_engine2, bool irregular) {
+// only >= 0: time just that fused variant's alternatives (a forced E / F)
+int autotune(pcg_solver* S, int grid2, int grid3, bool with_engine2, bool irregular, int only = -1) {
   const long long n = S->A.n_rows;
   cudaStream_t st = S->stream;
   fill_kernel<<<elementwise_grid(n), 256, 0, st>>>(S->nv, n, 1.0);
@@ -4853,7 +4854,8 @@ int autotune(pcg_solver* S, int grid2, int grid3, bool with_engine2, bool irregu
   const bool dict = (S->plans[5].stages && s_windows(S, false)) ||
                     (S->plans[6].stages && s_windows(S, true));
   for (int cand = 0; cand < n_cand && !rc; ++cand) {
-    if (dict && (cand == 0 || cand == 2 || cand == 3 || cand == kVariants)) continue;
+    if (only >= 0 && cand != only) continue;
+    if (only < 0 && dict && (cand == 0 || cand == 2 || cand == 3 || cand == kVariants)) continue;
     if (cand < kVariants) {
       // B (gather warps) never won a measurement; D only pays for irregular rows
       if (!S->plans[cand].stages || cand == 1 || (cand == 3 && !irregular)) continue;
@@ -5161,6 +5163,30 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   } else if (req >= 3) {
     S->engine = 1;
     apply_plan(S, S->plans[req - 3]);
+    // a forced E / F still picks the fastest of its own occupancy / stage
+    // alternatives (process-cached like the full autotune)
+    if (A->n_rows >= kTuneRows && S->alts[req - 3].size() > 1) {
+      const TuneKey key{dev, A->n_rows, A->n_cols, A->nnz, A->rp64, (long long)max_row,
+                        S->num_sms, S->opt.dot_mode, req, S->pat.n_pat,
+                        (S->dinv_by_code ? 1 : 0) + (S->dinv_uniform ? 2 : 0)};
+      int cached = -1, cached_alt = 0;
+      if (!getenv("PIPECG_B200_NO_TUNE_CACHE")) {
+        std::lock_guard<std::mutex> lk(tune_cache_mu());
+        auto it = tune_cache().find(key);
+        if (it != tune_cache().end()) std::tie(cached, cached_alt) = it->second;
+      }
+      if (cached == req - 3 && cached_alt < (int)S->alts[cached].size()) {
+        apply_plan(S, S->alts[cached][cached_alt]);
+      } else {
+        rc = autotune(S, grid2, grid3, false, has_long, req - 3);
+        if (rc) {
+          pipecg_b200_solver_destroy(S);
+          return rc;
+        }
+        std::lock_guard<std::mutex> lk(tune_cache_mu());
+        tune_cache()[key] = std::make_pair(S->variant, S->alt_pick[S->variant]);
+      }
+    }
   } else if (A->n_rows < kTuneRows) {
     // small: no autotune.  Irregular rows -> D (balanced tiles); else P, then
     // C for wide rows (> 12 nnz/row, one gather per nonzero) or A
