@@ -8,12 +8,16 @@ import sys, math
 sys.path.insert(0, ".")
 import numpy as np, paper_2105_06176_b200 as pb
 eng = sys.argv[1]
+def solve(A, b, cfg):
+    if eng == "pcg":  # the device PCG (engine 4)
+        return pb.pcg_solve(A, b, np.zeros(A.n_rows), pb.jacobi_setup(A), cfg,
+                            options=pb.DeviceOptions(chunk=8))
+    return pb.pipecg_solve(A, b, np.zeros(A.n_rows), pb.jacobi_setup(A), cfg,
+                           options=pb.DeviceOptions(engine=eng, chunk=8))
 for kind, n in (("3d7", 20), ("2d5", 64)):
     A = pb.stencil_host(kind, n)
     xt = np.full(A.n_rows, 1 / math.sqrt(A.n_rows)); b = pb.spmv(A, xt)
-    x, rep = pb.pipecg_solve(A, b, np.zeros(A.n_rows), pb.jacobi_setup(A),
-                             pb.SolverConfig(tolerance=1e-9, max_iterations=400),
-                             options=pb.DeviceOptions(engine=eng, chunk=8))
+    x, rep = solve(A, b, pb.SolverConfig(tolerance=1e-9, max_iterations=400))
     print(eng, kind, n, rep.iterations, float(np.abs(x - xt).max()))
 P = pb.generate_powerlaw(2**13)
 xt = np.full(P.n_rows, 1 / math.sqrt(P.n_rows)); b = pb.spmv(P, xt)
@@ -29,14 +33,12 @@ if eng in ("fused-e", "fused-f"):  # diagonal varies by row class: E's code wind
                              pb.SolverConfig(tolerance=1e-9, max_iterations=400),
                              options=pb.DeviceOptions(engine=eng, chunk=8))
     print(eng, "perturbed 3d7", rep.iterations, float(np.abs(x - xt).max()))
-if eng in ("fused-d", "two"):
-    x, rep = pb.pipecg_solve(P, b, np.zeros(P.n_rows), pb.jacobi_setup(P),
-                             pb.SolverConfig(tolerance=1e-9, max_iterations=100),
-                             options=pb.DeviceOptions(engine=eng, chunk=8))
+if eng in ("fused-d", "two", "fused-g", "pcg"):  # hub rows: chunks / warp chunks / pcg_hub_kernel
+    x, rep = solve(P, b, pb.SolverConfig(tolerance=1e-9, max_iterations=100))
     print(eng, "powerlaw", rep.iterations)
 PY
 for tool in memcheck racecheck synccheck; do
-  for eng in ${ENGINES:-fused-a fused-b fused-c fused-d fused-p fused-e fused-f two}; do
+  for eng in ${ENGINES:-fused-a fused-b fused-c fused-d fused-p fused-e fused-f two fused-g pcg}; do
     timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python /tmp/san_case.py $eng > $OUT/san_${tool}_${eng}.log 2>&1
     echo "$tool $eng rc=$? $(grep -c 'ERROR SUMMARY: 0 errors\|RACECHECK SUMMARY: 0 hazards' $OUT/san_${tool}_${eng}.log) $(grep 'SUMMARY' $OUT/san_${tool}_${eng}.log | tail -1)"
   done
