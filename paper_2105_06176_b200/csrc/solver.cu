@@ -1970,7 +1970,7 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(const Ctrl* C, long long
                                                          const int* __restrict__ col,
                                                          const double* __restrict__ val,
                                                          const double* __restrict__ x,
-                                                         double* __restrict__ y) {
+                                                         double* __restrict__ y, int gld) {
   pdl_wait();     // m from K1
   pdl_trigger();  // ... then the hub-row chunks may start beside this kernel
   if (C && read_status(C) != PCG_RUNNING) return;
@@ -1999,7 +1999,10 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(const Ctrl* C, long long
       }
 #pragma unroll
       for (int u = 0; u < SB; ++u)
-        xv[u] = k0 + u < len ? (POL ? ld_gather(x + c[u], pl) : ldg_nc(x + c[u])) : 0.0;
+        xv[u] = k0 + u < len ? (POL ? (gld == 1 ? __ldca(x + c[u]) : gld == 2 ? __ldcg(x + c[u])
+                                                     : ld_gather(x + c[u], pl))
+                                    : ldg_nc(x + c[u]))
+                             : 0.0;
 #pragma unroll
       for (int u = 0; u < SB; ++u)
         if (k0 + u < len) acc = add(acc, mul(a[u], xv[u]));
@@ -3329,7 +3332,8 @@ struct pcg_solver {
   unsigned long long* gbar = nullptr;  // variant P grid-barrier counter
   // engine-2 K2 in SELL-C-sigma layout (irregular matrices)
   bool sell = false;
-  int sell_batch = 2;              // nonzeros per lane per load batch in the SELL K2 (2 ~ 4 > 8, measured)
+  int sell_batch = 4;              // nonzeros per lane per load batch in the SELL K2 (4 with the L2
+                                   // hints: 2% over 2; 8 spills)
   Sell sell2;                      // engine 2's copy (rows <= kLongRow, sigma kSellSigma)
   Sell gsell;                      // engine 3's copy (rows <= g_thr, sigma kGRows)
   int* x_ptr = nullptr;            // its per-tile send lists (sorted by row)
@@ -3361,7 +3365,9 @@ struct pcg_solver {
   unsigned* qcnt = nullptr;        // engine 4: last-block tickets [2][2] | hub-kernel ticket
   double* qhub = nullptr;          // engine 4: hub rows' s*p terms [n_long] | their sum [2]
   int g_batch = 2;                 // engine 3 SELL nonzeros per lane per load batch (2 or 4)
-  bool e2_pol = true;              // engine 2: L2 hints (streams evict-first, m evict-last; -2% at 2^22)
+  bool e2_pol = true;
+  int sell_gld = 1;                // engine 2 SELL gathers: 0 evict-last hint, 1 ld.ca (L1 + L2, default:
+                                   // +0.5%), 2 ld.cg (L2 only: 33% slower -- hub columns hit L1)              // engine 2: L2 hints (streams evict-first, m evict-last; -2% at 2^22)
   int g_mb = 4;                    // engine 3 CTAs per SM the kernel is compiled for (4 or 6)
   bool g_pf = false;               // engine 3 update operands loaded before the row's SpMV
   int* tile_row = nullptr;         // variant D/E tiles of the applied plan
@@ -4268,7 +4274,7 @@ int enqueue_step(pcg_solver* S, int k) {
     launch_k(sk, elementwise_grid(S->sell2.slices * 32), 256, 0, st, S->pdl, (const Ctrl*)R.C, n,
              S->sell2.slices, (const long long*)S->sell2.ptr, (const int*)S->sell2.perm,
              (const int*)S->sell2.len, (const int*)S->sell2.col, (const double*)S->sell2.val,
-             (const double*)S->m, S->nv);
+             (const double*)S->m, S->nv, S->sell_gld);
     if (S->n_chunks > 0) {
       launch_k(gated_spmv_chunks, (unsigned)S->n_chunks, 256, 0, st, S->pdl, (const Ctrl*)R.C,
                (const LongChunk*)S->chunks, (const int*)S->A.col, (const double*)S->A.val,
@@ -4577,6 +4583,14 @@ int preload_solver() {
   PCG_SMEM((pipecg_fused_kernel_s<128, false, true, true, true>));
   PCG_SMEM((pipecg_fused_kernel_s<64, false, true, true, true>));
 #undef PCG_SMEM
+  // engine 2's SELL SpMV uses no shared memory and lives on L1 hits of its
+  // gathers (hub columns recur): ask for the largest L1 carveout
+  if (!getenv("PIPECG_B200_NO_L1PREF"))
+    for (auto ks : {sell_spmv_kernel<2, true>, sell_spmv_kernel<4, true>, sell_spmv_kernel<2, false>,
+                    sell_spmv_kernel<4, false>, sell_spmv_kernel<8, false>})
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute((const void*)ks, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 (int)cudaSharedmemCarveoutMaxL1);
   if (e != cudaSuccess) return cuda_status(e, "preload solver kernels");
   rc = preload_patterns();
   if (rc) return rc;
@@ -4953,6 +4967,7 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   if (const char* e = getenv("PIPECG_B200_G_BATCH")) S->g_batch = atoi(e);         // experiment
   if (const char* e = getenv("PIPECG_B200_G_MB")) S->g_mb = atoi(e);               // experiment
   if (const char* e = getenv("PIPECG_B200_E2POL")) S->e2_pol = atoi(e) != 0;      // experiment
+  if (const char* e = getenv("PIPECG_B200_E2GLD")) S->sell_gld = atoi(e);          // experiment
   if (const char* e = getenv("PIPECG_B200_G_PF")) S->g_pf = atoi(e) != 0;          // experiment
   if (const char* e = getenv("PIPECG_B200_G_THR")) S->g_thr = std::max(8LL, atoll(e)); // experiment
   if (const char* e = getenv("PIPECG_B200_PA")) S->p_mg = atoi(e) == 0;  // experiment switch
