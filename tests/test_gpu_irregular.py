@@ -260,19 +260,29 @@ def test_fused_g_tree_deterministic_and_in_envelope(cuda):
         np.testing.assert_array_equal(x2, x)
 
 
-@pytest.mark.parametrize("pol", ["0", "1", "3", "15"])
-def test_fused_g_cache_policies_bitwise(cuda, monkeypatch, pol):
-    """The L2 policy bits (PIPECG_B200_GPOL) change only cache behaviour."""
-    monkeypatch.setenv("PIPECG_B200_GPOL", pol)
-    A = pb.generate_powerlaw(2**14)
+@pytest.mark.parametrize("engine,env", [
+    ("two", {"PIPECG_B200_E2POL": "0"}), ("two", {"PIPECG_B200_E2GLD": "0"}),
+    ("two", {"PIPECG_B200_E2GLD": "2"}), ("two", {"PIPECG_B200_SELL_BATCH": "2"}),
+    ("fused-g", {"PIPECG_B200_G_BATCH": "4"}), ("fused-g", {"PIPECG_B200_G_MB": "6"}),
+    ("fused-g", {"PIPECG_B200_G_PF": "1"}), ("fused-g", {"PIPECG_B200_G_THR": "128"})])
+def test_irregular_kernel_switches_bitwise(cuda, monkeypatch, engine, env):
+    """The experiment switches of the irregular engines (L2 hints, gather
+    cache mode, batch depth, CTAs per SM, operand prefetch, lane-row
+    threshold up to 128) change only speed: a seq-dot solve is still the
+    reference's bit for bit when no row is longer than 256 nonzeros, and
+    within the reorder envelope otherwise."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    A = pb.generate_powerlaw(2**13)
+    mx = int(A.row_nnz().max())
     b, x0, d, tol = _problem(A)
     ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=2000)
     cfg = pb.SolverConfig(tolerance=tol, max_iterations=2000, record_history=True)
     x, rep = pb.pipecg_solve(A, b, x0, pb.jacobi_setup(A), cfg,
-                             options=pb.DeviceOptions(engine="fused-g", dot_mode="seq"))
-    if A.row_nnz().max() <= 256:
+                             options=pb.DeviceOptions(engine=engine, dot_mode="seq"))
+    if mx <= 256:
         assert rep.history == ref.history
         np.testing.assert_array_equal(x, ref.x)
-    else:
+    else:  # rows > 256: the init SpMVs (and engine 2) combine them with a tree
         assert_within_envelope(x, rep, ref.iterations, ref.history, ref.x,
                                envelope(A, b, x0, d, tol, 2000))
