@@ -316,6 +316,32 @@ def engine_bytes(engine: int, flags: int, N: int, nnz: int):
     return canonical_bytes(N, nnz), "two kernels: 22 vector streams x 8N + CSR (canonical)"
 
 
+# Random fp64 gathers from an L2-resident vector: 269.3 G/s = 0.95 per
+# clock per SM (one 128 B line per clock through the L1TEX data stage),
+# measured with tools/gather_mb.cu on a B200 (profiles/r02_gather_mb.txt).
+GATHER_RATE = 269.28e9
+
+
+def gather_floor(engine: int, N: int, nnz: int, peak_gbs: float, t_iter: float):
+    """Second roofline for the irregular engines, whose SpMV is bound by
+    random gathers (one L1TEX line per gather), not by HBM: the iteration
+    floor is the HBM time of the streams plus, for the SpMV, the larger of
+    its HBM time and nnz gathers at GATHER_RATE.  None for other engines."""
+    bw = peak_gbs * 1e9
+    if engine == 2:  # K1 (20 streams, HBM) then the SELL SpMV (max of both bounds)
+        t1 = 160 * N / bw
+        t2 = max((12 * nnz + 12 * N) / bw, nnz / GATHER_RATE)
+        floor, how = t1 + t2, "K1 20x8N / HBM + max(SELL 12nnz+12N / HBM, nnz / gather rate)"
+    elif engine == 10:  # one pass: both bounds overlap at best
+        floor = max((152 * N + 12 * nnz) / bw, nnz / GATHER_RATE)
+        how = "max((18x8N + 8N + 12nnz) / HBM, nnz / gather rate)"
+    else:
+        return None
+    return {"bound": "hbm + l1tex gathers", "gathers_per_iteration": nnz,
+            "gather_rate_per_s": GATHER_RATE, "gather_rate_source": "profiles/r02_gather_mb.txt",
+            "floor_us": floor * 1e6, "formula": how, "frac": floor / t_iter}
+
+
 def committed_traffic(config: str, engine: int):
     """DRAM bytes per launch of the dominant kernel from the committed ncu
     --set full capture (profiles/traffic.json, written by tools/ncu_summary.py)."""
@@ -737,6 +763,9 @@ def run_b200(args):
         "timing_ok": info["ok"],
         "clocks": clk.summary(),
     }
+    gf = gather_floor(info["engine"], N, nnz, peak, t_iter)
+    if gf:
+        line["roofline"]["gather_floor"] = gf
     if not args.no_tts:
         del A
         torch.cuda.empty_cache()
