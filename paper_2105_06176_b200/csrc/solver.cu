@@ -5275,6 +5275,44 @@ int pipecg_b200_solver_create(const pcg_matrix* A, const pcg_options* opts, pcg_
   return PCG_OK;
 }
 
+// cudaFree synchronises the whole device.  While a connected solver of
+// this process may be running, its kernels can be spinning on a peer
+// rank's arrival -- and that peer's host thread may be the one that would
+// block in cudaFree (a virtual rank sharing the GPU, or a thread of
+// pipecg_solve_devices collecting garbage), which stalls the exchange until
+// the spin timeout.  So the IPC-exported buffers (plain cudaMalloc, no
+// stream-ordered free) of a destroyed solver are parked here while any
+// connected solver is alive and freed when the last one goes.
+struct DeferredFrees {
+  std::mutex mu;
+  std::vector<std::pair<int, void*>> ptrs;  // (device, pointer)
+  int connected = 0;
+};
+DeferredFrees& deferred_frees() {
+  static DeferredFrees d;
+  return d;
+}
+void free_exported(pcg_solver* S) {
+  DeferredFrees& D = deferred_frees();
+  std::lock_guard<std::mutex> lk(D.mu);
+  if (S->connected) --D.connected;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (D.connected > 0) {
+    if (S->vbuf) D.ptrs.emplace_back(dev, S->vbuf);
+    if (S->comm) D.ptrs.emplace_back(dev, S->comm);
+    return;
+  }
+  cudaFree(S->vbuf);
+  cudaFree(S->comm);
+  for (auto& dp : D.ptrs) {
+    cudaSetDevice(dp.first);
+    cudaFree(dp.second);
+  }
+  D.ptrs.clear();
+  cudaSetDevice(dev);
+}
+
 int pipecg_b200_solver_destroy(pcg_solver* S) {
   if (!S) return PCG_OK;
   if (S->stream) cudaStreamSynchronize(S->stream);
@@ -5284,7 +5322,7 @@ int pipecg_b200_solver_destroy(pcg_solver* S) {
     if (S->rec_host[k]) pinned_record_release(S->rec_host[k]);
     if (S->ev_rec[k]) cudaEventDestroy(S->ev_rec[k]);
   }
-  cudaFree(S->vbuf);
+  free_exported(S);  // vbuf, comm
   pool_free(S->partials);
   pool_free(S->fin);
   pool_free(S->gbar);
@@ -5294,7 +5332,6 @@ int pipecg_b200_solver_destroy(pcg_solver* S) {
   pool_free(S->dots_ws);
   pool_free(S->dots4);
   pool_free(S->rec_dev);
-  cudaFree(S->comm);
   pool_free(S->long_rows);
   pool_free(S->chunks);
   pool_free(S->chunk_part);
@@ -5478,6 +5515,10 @@ int pipecg_b200_solver_connect(pcg_solver* S, int rank, int world, void* const* 
   cp.send_peer = send_peer;
   cp.send_dst = reinterpret_cast<const long long*>(send_dst);
   S->cp = cp;
+  if (!S->connected) {
+    std::lock_guard<std::mutex> lk(deferred_frees().mu);
+    ++deferred_frees().connected;
+  }
   S->connected = true;
   AllocStream alloc_on(S->stream);
   // The shard's row-pattern dictionary is valid in its [owned | halo]

@@ -26,6 +26,22 @@ from paper_2105_06176_b200 import distributed as D  # noqa: E402
 from paper_2105_06176_b200._device import shared_max_sms  # noqa: E402
 
 
+@pytest.fixture(autouse=True)
+def _quiesce():
+    """Virtual ranks share one GPU from threads of this process: a
+    device-wide synchronisation in one rank's thread (a cudaFree from
+    collecting an earlier test's objects, the caching allocator releasing
+    blocks) while a peer's kernel spins on its arrival stalls the exchange.
+    Collect and release before the ranks start (the library itself defers
+    its own device-synchronising frees while connected solvers live)."""
+    import gc
+
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    yield
+
+
 def run_virtual(world, make_problem, cfg, chunk=0, engine="fused"):
     G = D.LocalGroup(world)
     out = [None] * world
@@ -49,6 +65,8 @@ def run_virtual(world, make_problem, cfg, chunk=0, engine="fused"):
         t.start()
     for t in ts:
         t.join(timeout=300)
+    for r, e in errs:  # full messages (the assertion repr truncates them)
+        print(f"rank {r}: {e}")
     assert not errs, errs
     return out
 
