@@ -5298,7 +5298,7 @@ void free_exported(pcg_solver* S) {
   if (S->connected) --D.connected;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (D.connected > 0) {
+  if (D.connected > 0 && !getenv("PIPECG_B200_EAGER_FREE")) {  // (env: regression check)
     if (S->vbuf) D.ptrs.emplace_back(dev, S->vbuf);
     if (S->comm) D.ptrs.emplace_back(dev, S->comm);
     return;

@@ -323,3 +323,53 @@ def test_virtual_ranks_drift_samples(cuda, world, engine, k):
     for (it, v), (_, vr) in zip(dh, ref.drift_history):
         assert v <= 1e-10 * max(1.0, bn)
         assert abs(v - vr) <= 1e-12 * max(1.0, bn), (it, v, vr)
+
+
+def test_destroy_while_peer_waits_does_not_stall(cuda):
+    """A rank's thread destroys an unrelated solver while its peer's kernel
+    already waits for this rank's first arrival (virtual ranks, one GPU).
+    cudaFree synchronises the whole device, so an immediate free would block
+    this thread until the peer's spin timed out (10 s, 'exchange timed
+    out'); the library parks such frees while connected solvers live."""
+    import time
+
+    kind, n, world = "3d7", 24, 2
+    G = D.LocalGroup(world)
+    other = pb.PipecgSolver(pb.stencil_device("3d7", 16),
+                            pb.jacobi_setup(pb.stencil_device("3d7", 16)).inv_diag,
+                            pb.DeviceOptions(max_sms=20))
+    started = threading.Event()
+    res, errs, waited = [None] * world, [], []
+
+    def work(r):
+        try:
+            torch.cuda.set_device(0)
+            g = G.view(r)
+            prob = D.shard_stencil(kind, n, g)
+            solver = D.DistributedSolver(prob, g, pb.DeviceOptions(max_sms=shared_max_sms(world)))
+            xt, b = D.manufactured_local(prob)
+            solver.init(b, torch.zeros_like(b), 1e-10, 2000)
+            torch.cuda.ExternalStream(solver.stream).synchronize()
+            if r == 0:
+                started.set()
+            else:
+                started.wait(30)
+                time.sleep(0.3)  # rank 0's iteration-1 kernel now spins on our arrival
+                t = time.perf_counter()
+                other.close()
+                waited.append(time.perf_counter() - t)
+            out = solver.run(False, 2000)
+            res[r] = out[0]
+            solver.close()
+        except BaseException as e:  # noqa: BLE001
+            errs.append((r, repr(e)))
+            G._barrier.abort()
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=120)
+    assert not errs, errs
+    assert waited and waited[0] < 2.0, waited
+    assert res[0].converged and res[0].iterations == res[1].iterations
