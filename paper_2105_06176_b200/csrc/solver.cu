@@ -5299,8 +5299,13 @@ void free_exported(pcg_solver* S) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (D.connected > 0 && !getenv("PIPECG_B200_EAGER_FREE")) {  // (env: regression check)
-    if (S->vbuf) D.ptrs.emplace_back(dev, S->vbuf);
-    if (S->comm) D.ptrs.emplace_back(dev, S->comm);
+    for (void* p : {static_cast<void*>(S->vbuf), static_cast<void*>(S->comm)}) {
+      if (!p) continue;
+      cudaPointerAttributes a{};
+      const bool known = cudaPointerGetAttributes(&a, p) == cudaSuccess;
+      D.ptrs.emplace_back(known ? a.device : dev, p);  // freed on its own device later
+    }
+    cudaGetLastError();
     return;
   }
   cudaFree(S->vbuf);
