@@ -122,6 +122,11 @@ int pipecg_b200_narrow_i64(int64_t n, const int64_t* src, int32_t* dst, int* ove
  * source may be reused then); d2h returns when dst_host holds the data. */
 enum { PCG_H2D_COPY64 = 0, PCG_H2D_I64_TO_I32 = 1 };
 int pipecg_b200_h2d(void* dst_dev, const void* src_host, int64_t count, int kind, void* stream);
+/* Several arrays in one pass (e.g. a CSR's row offsets, column indices and
+ * values), their chunks interleaved so that host-bound narrowing overlaps
+ * PCIe-bound copies; same kinds and semantics as pipecg_b200_h2d. */
+int pipecg_b200_h2d_multi(int n_arrays, void* const* dst_dev, const void* const* src_host,
+                          const int64_t* count, const int* kind, void* stream);
 int pipecg_b200_d2h(void* dst_host, const void* src_dev, int64_t bytes, void* stream);
 /* Touch every page of a freshly allocated host buffer (host threads): the
  * first-touch page faults of a new numpy array otherwise cap a following

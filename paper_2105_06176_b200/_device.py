@@ -145,6 +145,27 @@ def h2d(dst: torch.Tensor, src: np.ndarray, narrow: bool = False) -> None:
     # orders the copies before any kernel that reads dst
 
 
+def h2d_multi(items) -> None:
+    """Several host -> device transfers in one pass of the pinned pipeline,
+    their chunks interleaved (host-bound narrowing overlaps PCIe-bound
+    copies).  ``items``: (dst tensor, contiguous int64 / float64 host array,
+    narrow) triples, as for :func:`h2d`."""
+    import ctypes
+
+    from . import _lib
+
+    items = [(d, np.ascontiguousarray(a), bool(nw)) for d, a, nw in items if np.asarray(a).size]
+    k = len(items)
+    if not k:
+        return
+    dst = (ctypes.c_void_p * k)(*[d.data_ptr() for d, _, _ in items])
+    src = (ctypes.c_void_p * k)(*[a.ctypes.data for _, a, _ in items])
+    cnt = (ctypes.c_int64 * k)(*[a.size for _, a, _ in items])
+    kinds = (ctypes.c_int * k)(*[_lib.PCG_H2D_I64_TO_I32 if nw else _lib.PCG_H2D_COPY64
+                                 for _, _, nw in items])
+    _lib.call("pipecg_b200_h2d_multi", k, dst, src, cnt, kinds, stream_ptr())
+
+
 def d2h(src: torch.Tensor) -> np.ndarray:
     """Device float64 vector -> new host ndarray (native pinned pipeline)."""
     from . import _lib

@@ -81,6 +81,8 @@ _SIGS = {
     "pipecg_b200_dots_workspace_bytes": ([], _i64),
     "pipecg_b200_narrow_i64": ([_i64, _vp, _vp, ctypes.POINTER(_int), _vp], _int),
     "pipecg_b200_h2d": ([_vp, _vp, _i64, _int, _vp], _int),
+    "pipecg_b200_h2d_multi": ([_int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _p_i64,
+                               ctypes.POINTER(_int), _vp], _int),
     "pipecg_b200_d2h": ([_vp, _vp, _i64, _vp], _int),
     "pipecg_b200_host_prefault": ([_vp, _i64], _int),
     "pipecg_b200_mm_parse": ([ctypes.c_char_p, _i64, _int, ctypes.POINTER(_vp)], _int),

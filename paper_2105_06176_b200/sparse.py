@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import cached_device, h2d, host_fingerprint, require_cuda, stream_ptr
+from ._device import cached_device, h2d_multi, host_fingerprint, require_cuda, stream_ptr
 
 __all__ = [
     "CsrMatrix",
@@ -229,15 +229,18 @@ def upload_csr(A) -> DeviceCsr:
     # host-side narrowing in the native pinned pipeline (csrc/hostio.cu):
     # 12 bytes per nonzero cross PCIe instead of the host layout's 16
     rowptr = torch.empty(n + 1 + PAD, dtype=torch.int64 if rp64 else torch.int32, device=dev)
-    h2d(rowptr[: n + 1], ro, narrow=not rp64)
     rowptr[n + 1:].fill_(nnz)
     col = torch.empty(nnz + PAD, dtype=torch.int32, device=dev)
     val = torch.empty(nnz + PAD, dtype=torch.float64, device=dev)
     col[nnz:].zero_()
     val[nnz:].zero_()
+    # one interleaved pass: the column narrowing (host-bound) overlaps the
+    # value copies (PCIe-bound)
+    items = [(rowptr[: n + 1], ro, not rp64)]
     if nnz:
-        h2d(col[:nnz], np.ascontiguousarray(A.col_indices, dtype=np.int64), narrow=True)
-        h2d(val[:nnz], np.ascontiguousarray(A.values, dtype=np.float64))
+        items += [(col[:nnz], np.ascontiguousarray(A.col_indices, dtype=np.int64), True),
+                  (val[:nnz], np.ascontiguousarray(A.values, dtype=np.float64), False)]
+    h2d_multi(items)
     return DeviceCsr(n, m, nnz, rowptr, col, val, host=A)
 
 

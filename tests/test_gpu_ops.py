@@ -200,3 +200,31 @@ def test_host_transfer_pipeline(cuda):
     with pytest.raises(_lib.NativeError) as e:
         h2d(dst, bad, narrow=True)
     assert e.value.code == _lib.PCG_ERANGE
+
+
+def test_host_transfer_pipeline_interleaved(cuda):
+    """pipecg_b200_h2d_multi: several arrays of mixed kinds (narrowed
+    indices, copied values, an empty one) interleaved chunk by chunk land
+    exactly where single transfers would; an out-of-range index anywhere
+    still raises PCG_ERANGE."""
+    from paper_2105_06176_b200._device import h2d_multi
+
+    rng = np.random.default_rng(9)
+    n1, n2, n3 = (8 << 20) // 4 * 5 + 321, (8 << 20) // 8 * 3 + 17, 1000
+    a1 = rng.integers(-2**31, 2**31, size=n1, dtype=np.int64)
+    a2 = rng.standard_normal(n2)
+    a3 = rng.integers(0, 100, size=n3, dtype=np.int64)
+    d1 = torch.empty(n1, dtype=torch.int32, device="cuda")
+    d2 = torch.empty(n2, dtype=torch.float64, device="cuda")
+    d3 = torch.empty(n3, dtype=torch.int32, device="cuda")
+    d0 = torch.empty(0, dtype=torch.float64, device="cuda")
+    h2d_multi([(d1, a1, True), (d0, np.zeros(0), False), (d2, a2, False), (d3, a3, True)])
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(d1.cpu().numpy(), a1.astype(np.int32))
+    np.testing.assert_array_equal(d2.cpu().numpy(), a2)
+    np.testing.assert_array_equal(d3.cpu().numpy(), a3.astype(np.int32))
+    bad = a3.copy()
+    bad[-1] = -2**31 - 1
+    with pytest.raises(_lib.NativeError) as e:
+        h2d_multi([(d2, a2, False), (d3, bad, True)])
+    assert e.value.code == _lib.PCG_ERANGE
