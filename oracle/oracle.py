@@ -303,7 +303,7 @@ def stencil(kind: str, n: int) -> Csr:
     return Csr(N, N, ro, ci, va)
 
 
-def row_patterns(A, max_pat=256, max_entries=2048):
+def row_patterns(A, max_pat=256, max_entries=8192):
     """Checker for the device row-pattern dictionary (csrc/patterns.cu): the
     distinct rows of A written relative to their own index -- (col - i,
     value bits) in CSR order -- numbered by first occurrence.  Returns

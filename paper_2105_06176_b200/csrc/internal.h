@@ -48,7 +48,8 @@ int preload_ops();
 // (i + off[k], val[k]) for k in [start[code[i]], start[code[i] + 1]), in
 // the CSR order, bit for bit.  n_pat == 0: the matrix has no dictionary.
 constexpr int kPatMax = 256;          // codes are one byte
-constexpr int kPatMaxEntries = 2048;  // dictionary entries (shared memory: 16 B each)
+constexpr int kPatMaxEntries = 8192;  // dictionary entries (shared memory: 16 B each; the
+                                      // plans check what fits -- 125-pt: 6,859)
 struct RowPatterns {
   int n_pat = 0, n_entries = 0, max_len = 0;
   unsigned char* code = nullptr;  // [n + 256]

@@ -3597,16 +3597,29 @@ int build_runs(pcg_solver* S) {
   d.push_back(0);  // E reads each row's own w / dinv from the windows
   std::sort(d.begin(), d.end());
   d.erase(std::unique(d.begin(), d.end()), d.end());
+  // bridge gaps of up to kWinGap; when that leaves more than kMaxWin runs
+  // (the 125-point stencil: 25 lines), bridge wider gaps -- the lines of a
+  // plane, which overlap anyway once the tile height exceeds the line
+  // length -- before giving up on windows
   int lo[kMaxWin], hi[kMaxWin], n = 0;
-  for (size_t k = 0; k < d.size(); ++k) {
-    if (n > 0 && d[k] - hi[n - 1] <= kWinGap) {
-      hi[n - 1] = d[k];
-      continue;
+  for (int gap : {kWinGap, 64, 256, 1024}) {
+    n = 0;
+    bool fits = true;
+    for (size_t k = 0; k < d.size() && fits; ++k) {
+      if (n > 0 && d[k] - hi[n - 1] <= gap) {
+        hi[n - 1] = d[k];
+        continue;
+      }
+      if (n == kMaxWin) fits = false;
+      else {
+        lo[n] = hi[n] = d[k];
+        ++n;
+      }
     }
-    if (n == kMaxWin) return PCG_OK;  // too many runs: gathers
-    lo[n] = hi[n] = d[k];
-    ++n;
+    if (fits) break;
+    n = -1;
   }
+  if (n < 0) return PCG_OK;  // too many runs: gathers
   std::vector<unsigned char> run(ne);
   int w0 = 0;
   for (int w = 0; w < n; ++w)
@@ -3767,6 +3780,16 @@ int plan_variant_s(pcg_solver* S, FusedPlan* best, std::vector<FusedPlan>* alts)
     if (p.stages) alts->push_back(p);
     if (e_bps) break;
   }
+  // a large dictionary (125-point stencils: ~110 KB of shared memory) can
+  // leave room for one CTA per SM only
+  if (alts->empty() && !e_bps) {
+    FusedPlan p;
+    int rc = PCG_OK;
+    if (!tr_pick || tr_pick == 256) rc = plan_one_s<256, MG>(S, 1, &p);
+    if (!rc && !p.stages && (!tr_pick || tr_pick == 128)) rc = plan_one_s<128, MG>(S, 1, &p);
+    if (rc) return rc;
+    if (p.stages) alts->push_back(p);
+  }
   // E with windows: also the stages without the streamed vectors (the
   // consumers load them), 2 stages at 3 and 2 CTAs per SM (3D 7-pt 256^3:
   // 0.322 vs 0.333 ms; slower at 27-pt -- the autotuner decides)
@@ -3777,7 +3800,8 @@ int plan_variant_s(pcg_solver* S, FusedPlan* best, std::vector<FusedPlan>* alts)
   if (e_dv && atoi(e_dv) == 1 && !MG) alts->clear();
   if (!MG && s_windows(S, false) && !e_bps && (!tr_pick || tr_pick == 256) &&
       !(e_dv && atoi(e_dv) == 0)) {
-    for (int bps : {3, 2}) {
+    for (int bps : {3, 2, 1}) {
+      if (bps == 1 && !alts->empty() && alts->front().bps > 1) break;  // (large dictionaries only)
       FusedPlan p;
       int rc = plan_one_s<256, MG>(S, bps, &p, true, 2);
       if (rc) return rc;
@@ -4865,8 +4889,10 @@ int autotune(pcg_solver* S, int grid2, int grid3, bool with_engine2, bool irregu
   // A/C/D and the two-kernel engine were 1.7-2.3x slower at every stencil
   // size measured (7/27-pt 128^3-400^3, 2D 512^2) -- not timed (P is: it
   // wins the launch-bound sizes)
-  const bool dict = (S->plans[5].stages && s_windows(S, false)) ||
-                    (S->plans[6].stages && s_windows(S, true));
+  // (a dictionary so large that one CTA per SM is all that fits is timed
+  // against everything)
+  const bool dict = (S->plans[5].stages && S->plans[5].bps > 1 && s_windows(S, false)) ||
+                    (S->plans[6].stages && S->plans[6].bps > 1 && s_windows(S, true));
   for (int cand = 0; cand < n_cand && !rc; ++cand) {
     if (only >= 0 && cand != only) continue;
     if (only < 0 && dict && (cand == 0 || cand == 2 || cand == 3 || cand == kVariants)) continue;

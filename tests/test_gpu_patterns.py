@@ -65,8 +65,24 @@ def test_dictionary_perturbed_rows_and_rp64(cuda):
         np.testing.assert_array_equal(codes.cpu().numpy(), r_codes)
 
 
-@pytest.mark.parametrize("make", [lambda: pb.stencil_host("p125", 7),
-                                  lambda: _random_spd(3000, 12, 5)])
+def _wide_band(n=2000, half=40, kinds=100):
+    """Band matrix (not symmetric -- never solved) whose interior rows come
+    in `kinds` value sets: <= 256 row patterns but > 8,192 dictionary
+    entries."""
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        for d in range(-half, half + 1):
+            j = i + d
+            if 0 <= j < n:
+                rows.append(i)
+                cols.append(j)
+                vals.append(4.0 * half if d == 0 else -1.0 - (i % kinds) / 1000.0)
+    ro = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(ro, np.asarray(rows) + 1, 1)
+    return pb.CsrMatrix(n, n, np.cumsum(ro), np.asarray(cols, dtype=np.int64), np.asarray(vals))
+
+
+@pytest.mark.parametrize("make", [_wide_band, lambda: _random_spd(3000, 12, 5)])
 def test_no_dictionary_when_rows_are_diverse(cuda, make):
     A = make()
     assert oracle.row_patterns(A)[0] == 0
@@ -98,7 +114,10 @@ def _seq_vs_oracle(A, engine, max_it=5000, device_matrix=None):
 
 
 @pytest.mark.parametrize("engine", ["fused-e", "fused-f"])
-@pytest.mark.parametrize("kind,n", [("2d5", 40), ("3d7", 20), ("3d27", 12), ("3d7", 13), ("3d7", 2)])
+@pytest.mark.parametrize("kind,n", [("2d5", 40), ("3d7", 20), ("3d27", 12), ("3d7", 13), ("3d7", 2),
+                                    # 125 row patterns / 6,859 entries; 25 lines of
+                                    # offsets bridged into 5 plane windows
+                                    ("p125", 40)])
 def test_stencil_seq_bitwise(cuda, kind, n, engine):
     _seq_vs_oracle(pb.stencil_host(kind, n), engine)
 

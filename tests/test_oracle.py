@@ -161,12 +161,14 @@ def test_threaded_baseline_same_iterations():
 
 
 @pytest.mark.parametrize("kind,n,expect", [("2d5", 10, 9), ("3d7", 6, 27), ("3d27", 5, 27),
-                                           ("3d7", 2, 8), ("p125", 6, 0)])
+                                           ("3d7", 2, 8), ("p125", 6, 125)])
 def test_row_pattern_checker(kind, n, expect):
     """oracle.row_patterns (the checker of csrc/patterns.cu): the boundary
     classes of each stencil, codes by first occurrence, and every row
-    rebuilt from its dictionary entry is the CSR row bit for bit.  p125
-    (125 classes x up to 125 entries) exceeds the 2048-entry dictionary."""
+    rebuilt from its dictionary entry is the CSR row bit for bit.  p125:
+    125 classes x up to 125 entries = 6,859 entries (<= 8,192)."""
+    if kind == "p125":
+        assert oracle.row_patterns(oracle.stencil(kind, n), max_entries=6858)[0] == 0
     A = oracle.stencil(kind, n)
     n_pat, n_e, codes = oracle.row_patterns(A)
     assert n_pat == expect
