@@ -58,6 +58,9 @@ CONFIGS = {
     "3d7-256": ("3d7", 256, True),
     "3d7-400": ("3d7", 400, False),
     "3d27-400": ("3d27", 400, False),
+    # the paper's own 125-point Poisson matrices (Table II: n = 165-185)
+    "p125-64": ("p125", 64, True),
+    "p125-185": ("p125", 185, False),
 }
 
 
