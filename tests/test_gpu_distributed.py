@@ -80,7 +80,10 @@ def run_virtual(world, make_problem, cfg, chunk=0, engine="fused"):
                                                  # world = kMaxRanks (solver.cu): the comm-block
                                                  # slot layout and arrival counts at their limit
                                                  (8, "3d7", 48, "fused-e"), (8, "3d7", 40, "fused-a"),
-                                                 (8, "3d27", 24, "fused-f"), (8, "3d7", 40, "fused-c")])
+                                                 (8, "3d27", 24, "fused-f"), (8, "3d7", 40, "fused-c"),
+                                                 # 125-point: bridged plane windows,
+                                                 # 6,859-entry dictionary, 1 CTA/SM
+                                                 (2, "p125", 30, "fused-f"), (3, "p125", 30, "fused-e")])
 def test_virtual_ranks_match_single_gpu(cuda, world, kind, n, engine):
     A = oracle.stencil(kind, n)
     x_true, b, x0, d = oracle.manufactured(A)
