@@ -11,11 +11,17 @@ The B200 generalisation of the reference's Hybrid-3 split
   a row is untouched -- unlike the reference's local/remote in-row reorder
   (partition.py:67-90), which reassociates row sums (hybrid.py:17-18) -- so
   every row's SpMV stays bitwise equal to the single-device product.
-* Per iteration: the fused kernel (csrc/solver.cu) runs on the local rows,
-  then an exchange kernel stores the boundary rows of w into the
-  neighbours' halo and the rank's dot partial into every rank's slot
-  directly over NVLink (CUDA IPC-mapped peer memory) and signals; the next
-  iteration waits for that signal inside its prologue.  No host sync, no
+* Per iteration ONE fused kernel (csrc/solver.cu) runs on the local rows
+  and does the exchange itself: as each tile's rows are final, its CTA
+  stores that tile's halo rows of the vector the peers gather next (w for
+  A/E, the stored m for C/D/F) straight into the neighbours' HBM over
+  NVLink (CUDA IPC-mapped peer memory); the grid's last block writes the
+  rank's dot partial into every rank's slot and bumps every rank's arrival
+  counter.  The next iteration's prologue waits for those arrivals -- after
+  running the SpMV of a first tile that needs no halo rows, so the
+  rendezvous overlaps it (PIPECG's SpMV / reduction overlap).  Only variant
+  B keeps a separate exchange kernel.  Drift samples (every k iterations)
+  are summed over the ranks in rank order in-kernel.  No host sync, no
   NCCL on the data path; torch.distributed is used only at setup (plan and
   IPC-handle exchange) and to time max-over-ranks.
 
