@@ -160,7 +160,7 @@ int pipecg_b200_find_long_rows(int64_t n_rows, int rp64, const void* rowptr, int
 /* Lossless row-pattern dictionary (csrc/patterns.cu; what fused variants
  * E/F read instead of the CSR): row i's entries are (i + off_k, v_k) for one
  * of *n_pat distinct lists, *n_entries entries in all.  *n_pat = 0: the rows
- * are too diverse (> 256 lists or > 2048 entries).  codes (device uint8[n_rows],
+ * are too diverse (> 256 lists or > 8192 entries).  codes (device uint8[n_rows],
  * optional) receives each row's list index, lists numbered by first row.
  * Synchronous.  No reference counterpart (a storage format of sparse.py's CSR). */
 int pipecg_b200_row_patterns(int64_t n_rows, int rp64, const void* rowptr, const int32_t* col,

@@ -182,7 +182,7 @@ def test_fused_update_pc_dots(cuda):
 
 def test_host_transfer_pipeline(cuda):
     """csrc/hostio.cu: chunked pinned-ring uploads (with int64 -> int32
-    narrowing) and downloads, across several 32 MB slots."""
+    narrowing) and downloads, across several 8 MB ring slots."""
     from paper_2105_06176_b200._device import d2h, h2d
 
     n = (32 << 20) // 4 * 3 + 12345  # > 2 ring slots of narrowed data
