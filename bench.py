@@ -279,7 +279,8 @@ KERNELS = {2: "gated_spmv_rows + pipecg_k1_kernel", 3: "pipecg_fused_kernel_a<in
 CONFIG_NAMES = {"3d7-256": "BASELINE.json configs[1]", "2d5-512": "BASELINE.json configs[0]",
                 "3d27-400": "BASELINE.json configs[2], single-GPU leg",
                 "3d7-400": "north_star headline (>= 64M rows)",
-                "powerlaw-22": "BASELINE.json configs[3]"}
+                "powerlaw-22": "BASELINE.json configs[3]",
+                "p125-185": "the paper's Table II 125-point Poisson, largest size (SURVEY.md §8(f) row 1)"}
 
 
 def engine_bytes(engine: int, flags: int, N: int, nnz: int):
