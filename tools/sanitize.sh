@@ -33,6 +33,11 @@ if eng in ("fused-e", "fused-f"):  # diagonal varies by row class: E's code wind
                              pb.SolverConfig(tolerance=1e-9, max_iterations=400),
                              options=pb.DeviceOptions(engine=eng, chunk=8))
     print(eng, "perturbed 3d7", rep.iterations, float(np.abs(x - xt).max()))
+    # 125-point: 6,859-entry dictionary, 25 lines bridged into 5 plane windows
+    A = pb.stencil_host("p125", 24)
+    xt = np.full(A.n_rows, 1 / math.sqrt(A.n_rows)); b = pb.spmv(A, xt)
+    x, rep = solve(A, b, pb.SolverConfig(tolerance=1e-9, max_iterations=400))
+    print(eng, "p125 24", rep.iterations, float(np.abs(x - xt).max()))
 if eng in ("fused-d", "two", "fused-g", "pcg"):  # hub rows: chunks / warp chunks / pcg_hub_kernel
     x, rep = solve(P, b, pb.SolverConfig(tolerance=1e-9, max_iterations=100))
     print(eng, "powerlaw", rep.iterations)
