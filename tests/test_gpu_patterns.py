@@ -43,7 +43,7 @@ def _perturbed(kind, n, rows):
     return pb.CsrMatrix(A.n_rows, A.n_cols, ro, ci, va)
 
 
-DICT_CASES = [("2d5", 20), ("3d7", 12), ("3d27", 9), ("3d7", 3)]
+DICT_CASES = [("2d5", 20), ("3d7", 12), ("3d27", 9), ("3d7", 3), ("p125", 9)]
 
 
 @pytest.mark.parametrize("kind,n", DICT_CASES)
@@ -52,7 +52,9 @@ def test_dictionary_matches_oracle(cuda, kind, n):
     n_pat, n_e, codes = pb.as_device_csr(A).row_patterns(codes=True)
     r_pat, r_e, r_codes = oracle.row_patterns(A)
     assert (n_pat, n_e) == (r_pat, r_e)
-    assert n_pat == (9 if kind == "2d5" else 27)
+    assert n_pat == {"2d5": 9, "p125": 125}.get(kind, 27)
+    if kind == "p125":
+        assert n_e == 6859  # (3 + 4 + 5 + 4 + 3)^3 entries, <= the 8192 limit
     np.testing.assert_array_equal(codes.cpu().numpy(), r_codes)
 
 
