@@ -469,3 +469,31 @@ def test_pcg_device_hub_rows(cuda, mode):
     x2, rep2 = pb.pcg_solve(A, b, x0, pb.JacobiPreconditioner(d), cfg, options=opts)
     assert rep2.history == rep.history
     np.testing.assert_array_equal(x2, x)
+
+
+@pytest.mark.parametrize("kind,n", [("3d7", 128), ("p125", 40)])
+def test_pcg_device_config_scale_vs_oracle(cuda, kind, n):
+    """Device PCG at a realistic size (3D 7-pt 128^3: 2.1M rows, ~300
+    iterations; 125-point 40^3: 7.3M nonzeros): seq dots bit for bit the
+    oracle's PCG (history, count, x); tree dots within the oracle's
+    blocked-dot envelope (BASELINE.md gates)."""
+    A = oracle.stencil(kind, n)
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    ref = oracle.pcg_solve(A, b, x0, d, tol=tol, max_iterations=5000)
+    ref2 = oracle.pcg_solve(A, b, x0, d, tol=tol, max_iterations=5000, dot_mode="blocked")
+    E = oracle.history_gap(ref2.history, ref.history)
+    Ad = pb.stencil_device(kind, n)
+    bd = torch.as_tensor(b, device="cuda")
+    pc = pb.JacobiPreconditioner(torch.as_tensor(d, device="cuda"))
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=5000, record_history=True)
+    x, rep = pb.pcg_solve(Ad, bd, torch.zeros_like(bd), pc, cfg,
+                          options=pb.DeviceOptions(dot_mode="seq"))
+    assert rep.iterations == ref.iterations and rep.history == ref.history
+    np.testing.assert_array_equal(x.cpu().numpy(), ref.x)
+    x, rep = pb.pcg_solve(Ad, bd, torch.zeros_like(bd), pc, cfg)
+    assert abs(rep.iterations - ref.iterations) <= 1
+    assert oracle.history_gap(rep.history, ref.history) <= max(1e-10, 3 * E)
+    xs = x.cpu().numpy()
+    assert np.max(np.abs(xs - ref.x)) / np.max(np.abs(ref.x)) <= max(
+        1e-8, 3 * np.max(np.abs(ref2.x - ref.x)) / np.max(np.abs(ref.x)))
