@@ -497,3 +497,33 @@ def test_pcg_device_config_scale_vs_oracle(cuda, kind, n):
     xs = x.cpu().numpy()
     assert np.max(np.abs(xs - ref.x)) / np.max(np.abs(ref.x)) <= max(
         1e-8, 3 * np.max(np.abs(ref2.x - ref.x)) / np.max(np.abs(ref.x)))
+
+
+def test_drift_samples_config_scale(cuda):
+    """Drift samples every 50 iterations on 3D 7-pt 128^3 (2.1M rows, the
+    autotuned engine -- E/F then update x every iteration): the sample
+    iterations are the reference's (solvers.py:371-372), every value meets
+    the reference's own bound (test_solvers.py:220-230) and sits at the
+    oracle's rounding-noise level, and the history passes the gates."""
+    A = oracle.stencil("3d7", 128)
+    x_true, b, x0, d = oracle.manufactured(A)
+    tol = oracle.recipe_tolerance(A, b, d)
+    ref = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=5000, drift_check_interval=50)
+    ref2 = oracle.pipecg_solve(A, b, x0, d, tol=tol, max_iterations=5000, dot_mode="blocked")
+    E = oracle.history_gap(ref2.history, ref.history)
+    Ad = pb.stencil_device("3d7", 128)
+    bd = torch.as_tensor(b, device="cuda")
+    pc = pb.JacobiPreconditioner(torch.as_tensor(d, device="cuda"))
+    cfg = pb.SolverConfig(tolerance=tol, max_iterations=5000, record_history=True,
+                          drift_check_interval=50)
+    x, rep = pb.pipecg_solve(Ad, bd, torch.zeros_like(bd), pc, cfg)
+    assert abs(rep.iterations - ref.iterations) <= 1
+    assert oracle.history_gap(rep.history, ref.history) <= max(1e-10, 3 * E)
+    got = [it for it, _ in rep.drift_history]
+    want = [it for it, _ in ref.drift_history]
+    assert got == want[: len(got)] and len(got) >= len(want) - 1
+    b_norm = float(np.linalg.norm(b))
+    noise = max(v for _, v in ref.drift_history)
+    for it, v in rep.drift_history:
+        assert 0 <= v <= 1e-10 * max(1.0, b_norm)
+        assert v <= 100 * noise + 1e-15, (it, v, noise)
