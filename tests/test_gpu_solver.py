@@ -527,3 +527,33 @@ def test_drift_samples_config_scale(cuda):
     for it, v in rep.drift_history:
         assert 0 <= v <= 1e-10 * max(1.0, b_norm)
         assert v <= 100 * noise + 1e-15, (it, v, noise)
+
+
+@pytest.mark.parametrize("engine", ["auto", "fused-e", "fused-f", "fused-a", "two"])
+def test_breakdown_at_scale_matches_oracle(cuda, engine):
+    """An indefinite 3D 7-pt 64^3 system (every 7th diagonal -6: Jacobi's
+    u = D^-1 r then has mixed signs and gamma = (r, u) turns negative) at
+    262K rows: the device raises the reference's SolverBreakdown
+    (solvers.py:354-357) -- same quantity and iteration, the value bit for
+    bit in seq mode and to reduction-order noise in tree mode.  The row
+    classes x diagonal sign give a 46-code dictionary, so E/F run."""
+    A = oracle.stencil("3d7", 64)
+    n = A.n_rows
+    va = np.array(A.values)
+    rows = np.repeat(np.arange(n), np.diff(A.row_offsets))
+    va[(A.col_indices == rows) & (rows % 7 == 0)] = -6.0
+    A = pb.CsrMatrix(n, n, A.row_offsets, A.col_indices, va)
+    d = oracle.jacobi_inv_diag(A)
+    b = oracle.spmv(A, np.full(n, 1 / np.sqrt(n)))
+    ref = oracle.pipecg_solve(A, b, np.zeros(n), d, tol=1e-12, max_iterations=3000)
+    q, it, val = ref.breakdown
+    cfg = pb.SolverConfig(tolerance=1e-12, max_iterations=3000)
+    for mode in ("seq", "tree"):
+        with pytest.raises(pb.SolverBreakdown) as e:
+            pb.pipecg_solve(A, b, np.zeros(n), pb.JacobiPreconditioner(d), cfg,
+                            options=pb.DeviceOptions(engine=engine, dot_mode=mode))
+        assert (e.value.quantity, e.value.iteration) == (q, it)
+        if mode == "seq":
+            assert e.value.value == val
+        else:
+            assert abs(e.value.value - val) <= 1e-9 * abs(val)
