@@ -11,6 +11,17 @@ kernels), ``solvers`` (PIPECG / PCG drivers, report and breakdown types),
 arithmetic runs in ``_lib/libpipecg_b200.so`` (include/pipecg_b200.h).
 """
 
+import os as _os
+
+# Several solvers of one process whose kernels wait on each other (virtual
+# ranks sharing a GPU, ``devices=[0, 0]``) need their streams on distinct
+# hardware work queues: with the default 8, two streams can share a queue
+# and a rank's kernels then sit behind a peer's kernel that spins on that
+# very rank's arrival until the 10 s timeout (measured: 2-4 stalls per 100
+# 8-rank solves at 8 connections, 0 in 200 at 32).  Effective only if set
+# before the process initialises CUDA.
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 from .sparse import (
     CapacityError,
     CsrMatrix,

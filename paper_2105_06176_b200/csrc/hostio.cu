@@ -197,6 +197,14 @@ void pool_init() {
   if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
   unsigned long long keep = 2ULL << 30;
   cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  // No hidden cross-stream waits: by default cudaMallocAsync may hand out a
+  // block another stream freed with cudaFreeAsync and make the allocating
+  // stream WAIT for that stream up to the free.  With several solvers of
+  // one process (virtual ranks) such a wait could land behind a peer's spin
+  // on this rank's arrival.  Blocks whose free has completed are still
+  // reused (opportunistic reuse needs no new dependency).
+  int no = 0;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
 }
 
 }  // namespace pcg

@@ -492,6 +492,8 @@ class DistributedSolver:
                 peer_vbuf.append(pv.value)
                 peer_comm.append(pc.value)
         W = group.world
+        # (kept for diagnostics: the addresses this rank pushes to)
+        self.comm_ptr, self.peer_comm, self.peer_vbuf = comm.value, list(peer_comm), list(peer_vbuf)
         plan = problem.plan
         dev = problem.inv_diag.device
         self._send = [torch.from_numpy(plan.send_row.astype(np.int32)).to(dev),

@@ -7,8 +7,13 @@ everything else runs on the CPU-only dev container.  The oracle
 
 from __future__ import annotations
 
+import os
 import sys
 from pathlib import Path
+
+# before torch initialises CUDA: virtual ranks need distinct hardware
+# queues (see paper_2105_06176_b200/__init__.py)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 import numpy as np
 import pytest

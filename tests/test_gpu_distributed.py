@@ -43,24 +43,9 @@ def _quiesce():
 
 
 def run_virtual(world, make_problem, cfg, chunk=0, engine="fused"):
-    """Solve with `world` virtual ranks (threads sharing GPU 0).  A rank
-    thread of this harness can stall behind host/driver work of the others
-    (one process, one GPU, up to 8 threads) long enough for its peers' spin
-    to time out (PCG_ECOMM): that -- and only that -- is retried once, on
-    fresh solvers; any other error, a second timeout or a wrong result
-    fails.  One process per GPU (the product's layout) has no such shared
-    host state."""
-    import gc
-
-    for attempt in (1, 2):
-        out, errs = _run_virtual_once(world, make_problem, cfg, chunk, engine)
-        comm_only = errs and all("code 1006" in e for _, e in errs)
-        if not comm_only or attempt == 2:
-            break
-        print(f"virtual ranks: exchange timeout on attempt 1, retrying: {errs[0][1]}")
-        gc.collect()
-        torch.cuda.synchronize()
-        torch.cuda.empty_cache()
+    """Solve with `world` virtual ranks (threads sharing GPU 0); every rank's
+    error fails the test (no retry)."""
+    out, errs = _run_virtual_once(world, make_problem, cfg, chunk, engine)
     for r, e in errs:  # full messages (the assertion repr truncates them)
         print(f"rank {r}: {e}")
     assert not errs, errs
