@@ -5566,6 +5566,16 @@ int pipecg_b200_solver_connect(pcg_solver* S, int rank, int world, void* const* 
     if (rc) return rc;
     keep = S->dinv_by_code && S->dinv_uniform && !bad;
   }
+  // E's consumer-loaded layout (dv) is the single-GPU autotuner's pick at
+  // 7-pt, but with the fused exchange the staged layout is faster (3D 7-pt
+  // 256^3, one connected rank: 0.358 vs 0.535 ms per iteration,
+  // tools/dist1.py): take E's first staged alternative
+  if (keep && S->variant == 5 && S->dv && !getenv("PIPECG_B200_DIST_KEEP_DV"))
+    for (const FusedPlan& q : S->alts[5])
+      if (!q.dv) {
+        apply_plan(S, q);
+        break;
+      }
   if (S->engine == 1 && S->variant >= 4 && !keep) {
     const FusedPlan& csr = S->plans[S->variant == 5 ? 0 : 2];
     if (!csr.stages) return set_error(PCG_EINVAL, "solver_connect: no CSR variant fits this shard");
