@@ -445,14 +445,15 @@ class DistributedSolver:
         mine = int(self.solver.poll().engine)
         mine = 5 if mine == 7 else mine  # P runs as C once connected
         chosen = group.all_gather_object(mine)[0]
-        # Ranks sharing one GPU (max_sms > 0: virtual ranks, tests): E trails
-        # F there (2 ranks on one B200 at 256^3: F 0.55, E 0.59-0.60
-        # ms/iteration, tools/dist1.py) -> F.  With a GPU per rank the
-        # shard's own autotuning stands (one connected rank at 256^3: E 0.387,
-        # F 0.445 ms/iteration).
-        if (chosen == 8 and engine != "fused-e" and opts.max_sms > 0
-                and not os.environ.get("PIPECG_B200_DIST_KEEP_E")):
-            chosen = 9
+        # Connected, E (staged layout, csrc/solver.cu solver_connect) beats F
+        # wherever measured (tools/dist1.py, one B200): 3D 7-pt 256^3 one
+        # rank E 0.339 / F 0.412 ms per iteration, two virtual ranks 0.389 /
+        # 1.242, 27-pt 300^3 one rank 0.694 / 1.290 -- F's consumer-loaded
+        # streams do not mix with the fused exchange.  So an autotuned F
+        # (rank 0's single-GPU pick) runs as E once connected.
+        if (chosen == 9 and engine != "fused-f"
+                and not os.environ.get("PIPECG_B200_DIST_KEEP_F")):
+            chosen = 8
         if mine != chosen:
             self.solver.close()
             opts = DeviceOptions(dot_mode=opts.dot_mode, engine=names[chosen], chunk=opts.chunk,
