@@ -383,3 +383,22 @@ def test_destroy_while_peer_waits_does_not_stall(cuda):
     assert not errs, errs
     assert waited and waited[0] < 2.0, waited
     assert res[0].converged and res[0].iterations == res[1].iterations
+
+
+def test_connected_e_runs_the_staged_layout(cuda):
+    """A connected E never keeps the consumer-loaded stage layout (pattern
+    flag 32) the single-GPU autotuner may pick: with the fused exchange it
+    measured 1.5-1.6x slower (tools/dist1.py; csrc/solver.cu
+    solver_connect).  And an autotuned engine runs as E, not F, once
+    connected (distributed.py)."""
+    for engine in ("fused-e", "fused"):
+        G = D.LocalGroup(1)
+        g = G.view(0)
+        prob = D.shard_stencil("3d7", 128, g)
+        s = D.DistributedSolver(prob, g, pb.DeviceOptions(engine=engine))
+        xt, b = D.manufactured_local(prob)
+        s.init(b, torch.zeros_like(b), 1e-9, 50)
+        res = s.run(False, 50)[0]
+        assert res.engine == 8, (engine, res.engine)
+        assert not (res.pattern_flags & 32), (engine, res.pattern_flags)
+        s.close()
